@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DG hot path (arXiv 1805.11930): dg_apply + block-Jacobi sweeps.
+
+Workload (BASELINE.json configs[1], the config its metric is quoted on; fits one GPU):
+  C2 = 32^3 hexahedra, DG Q3 (64 DoF/cell, 2,097,152 DoF), Poisson K=1, alpha=2, Dirichlet;
+  one STEP = 100 dg_apply + 10 block-Jacobi sweeps (omega=1, local Jacobi-PCG to 1e-12),
+  the config's own unit of work, on seeded U[-1,1) u and f (synth/). With --gpus N the same
+  mesh is split into N z-slabs (strong scaling, NCCL face-layer halo per apply/sweep).
+
+Prints ONE JSON line (rank 0). `value` = DoF processed per second over the whole job
+(global DoF x 110 calls x steps / max-over-ranks device time). Timing: CUDA events on the
+launching stream, W warm-up steps, L2 flushed (512 MiB write) before every timed step, u reset
+to the seeded input before every step (outside the timed region).
+`--impl reference` times the CPU oracle (oracle/, numpy fp64) on a bounded cell sample of the
+same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_APPLY, N_SWEEP = 100, 10
+METRIC = "fp64 DoF/s and GFLOP/s (fraction of fp64 peak) for DG apply + block-Jacobi sweep"
+SM_COUNT, DFMA_PER_CLK_PER_SM = 148, 64   # B200: 148 SMs, 64 fp64 FMA lanes per SM per clock
+
+
+def flops_model(p: int):
+    """SURVEY.md §8(d) canonical sum-factorised model, flops per DoF (FMA = 2 flops)."""
+    n = p + 1
+    vol = 24 * n ** 4 + 8 * n ** 3
+    self_face = 8 * n ** 3 + 12 * n ** 2
+    nbr_face = 10 * n ** 3
+    apply = (vol + 6 * self_face + 6 * nbr_face) / n ** 3
+    dt = (vol + 6 * self_face) / n ** 3
+    return {"apply": apply, "D_T": dt, "cg_iter": dt + 12, "bicgstab_iter": 2 * dt + 20}
+
+
+def describe(P, local_solver):
+    return (f"{P.name}: {P.nx}x{P.ny}x{P.nz} hex, DG Q{P.p} ({P.nd} DoF/cell, {P.n_dof} DoF), "
+            f"step = {N_APPLY} dg_apply + {N_SWEEP} block-Jacobi sweeps (omega=1, local "
+            f"{local_solver} to 1e-12)")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def init_dist(gpus):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        raise SystemExit(f"--gpus {gpus} but WORLD_SIZE={world}")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def cpu_oracle_sample(P, u, f, seconds: float, kind: str):
+    """Times the oracle (tier B, as it stands) on a bounded sample of cells of the workload and
+    projects the time of one full step; one thread (threadpoolctl)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+    from oracle.tier_b import TierB
+    tb = TierB(P)
+    rng = np.random.default_rng(0)
+    t_apply, t_sweep, n_a, n_s = 0.0, 0.0, 0, 0
+    with threadpool_limits(limits=1):
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end or n_s == 0:
+            c = [int(rng.integers(0, P.n_cells))]
+            t0 = time.perf_counter()
+            tb.apply_cells(u, c)
+            t1 = time.perf_counter()
+            tb.sweep_cells(u, f, 1.0, c)
+            t2 = time.perf_counter()
+            t_apply += t1 - t0
+            t_sweep += t2 - t1
+            n_a += 1
+            n_s += 1
+    per_cell_apply, per_cell_sweep = t_apply / n_a, t_sweep / n_s
+    step_s = P.n_cells * (N_APPLY * per_cell_apply + N_SWEEP * per_cell_sweep)
+    value = P.n_dof * (N_APPLY + N_SWEEP) / step_s
+    return {"value": value, "unit": "DoF/s", "cores": 1, "kind": kind,
+            "sample": (f"{n_a} random cells of {P.name}: oracle dg_apply (dense per-cell blocks) and "
+                       f"sweep (defect + LU of D_T) timed per cell ({t_apply + t_sweep:.1f} s, 1 thread), "
+                       f"projected to one step of {P.n_cells} cells x ({N_APPLY} applies + "
+                       f"{N_SWEEP} sweeps)"),
+            "apply_s_per_cell": per_cell_apply, "sweep_s_per_cell": per_cell_sweep,
+            "projected_step_s": step_s}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from synth import make_config, make_vectors
+    P = make_config(args.config)
+    u, f = make_vectors(P)
+    solver = "CG" if P.local_solver == "cg" else "BiCGStab"
+    per_step = []
+    base = None
+    for s in range(args.warmup + args.steps):
+        r = cpu_oracle_sample(P, u, f, args.ref_seconds, "oracle")
+        if s >= args.warmup:
+            per_step.append(r["projected_step_s"])
+            base = r
+    step_s = statistics.mean(per_step)
+    value = P.n_dof * (N_APPLY + N_SWEEP) / step_s
+    base["value"] = value
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded SplitMix64, synth/)",
+            "config": {"workload": describe(P, solver), "n_dof": P.n_dof, "p": P.p},
+            "cpu_baseline": base,
+            "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import paper_1805_11930_b200 as dg
+    from synth import make_config, make_vectors
+
+    rank, world, local = init_dist(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    P = make_config(args.config)
+    nid = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [dg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = dg.DGContext(P, rank=rank, nranks=world, device=local, nccl_id=nid)
+    solver = "CG" if P.local_solver == "cg" else "BiCGStab"
+    u_h, f_h = make_vectors(P, cell_begin=ctx.cell_begin, cell_end=ctx.cell_end)
+    u0 = torch.from_numpy(u_h).to(dev)
+    f0 = torch.from_numpy(f_h).to(dev)
+    u = u0.clone()
+    Au = torch.empty_like(u0)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(record=None):
+        launches = 0
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(N_APPLY):
+            ctx.apply(u, Au)
+            launches += ctx.launch_count()
+        e1.record(stream)
+        sweeps = []
+        for _ in range(N_SWEEP):
+            a, b = ev(), ev()
+            a.record(stream)
+            ctx.sweep(u, f0, 1.0, 1e-12)
+            b.record(stream)
+            launches += ctx.launch_count()
+            sweeps.append((a, b))
+        if record is not None:
+            record.append(((e0, e1), sweeps))
+        return launches
+
+    # warm-up
+    for _ in range(args.warmup):
+        u.copy_(u0)
+        step()
+    torch.cuda.synchronize()
+    # timed
+    clocks = Clocks() if rank == 0 else None
+    if clocks:
+        clocks.start()
+    total_ms, t_apply_ms, sweep_ms, launches = 0.0, 0.0, [], 0
+    for _ in range(args.steps):
+        u.copy_(u0)
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        s0, s1 = ev(), ev()
+        rec = []
+        s0.record(stream)
+        launches += step(rec)
+        s1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms += s0.elapsed_time(s1)
+        (a0, a1), sw = rec[0]
+        t_apply_ms += a0.elapsed_time(a1)
+        sweep_ms += [a.elapsed_time(b) for a, b in sw]
+    clk = clocks.stop() if clocks else None
+    # iteration counts of the (deterministic) sweeps, replayed untimed
+    u.copy_(u0)
+    it_sums, it_stats = [], []
+    for _ in range(N_SWEEP):
+        ctx.sweep(u, f0, 1.0, 1e-12)
+        st = ctx.stats()
+        it_sums.append(st["it_sum"])
+        it_stats.append(st)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, t_apply_ms, sum(sweep_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, t_apply_ms, tsw = t.tolist()
+        its = torch.tensor([float(sum(it_sums))], dtype=torch.float64, device=dev)
+        dist.all_reduce(its)
+        it_sum_total = its.item()
+    else:
+        tsw = sum(sweep_ms)
+        it_sum_total = float(sum(it_sums))
+
+    # ---- e2e: the same step through the C ABI with host buffers (H2D/D2H inside the region)
+    u_pin = torch.from_numpy(u_h).pin_memory()
+    f_pin = torch.from_numpy(f_h).pin_memory()
+    out_pin = torch.empty_like(u_pin).pin_memory()
+    f_dev = torch.empty_like(f0)
+    e2e_ms = 0.0
+    e2e_steps = max(1, min(args.steps, 3))
+    for _ in range(e2e_steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        barrier()
+        a, b = ev(), ev()
+        a.record(stream)
+        u.copy_(u_pin, non_blocking=True)
+        f_dev.copy_(f_pin, non_blocking=True)
+        for _ in range(N_APPLY):
+            ctx.apply(u, Au)
+        for _ in range(N_SWEEP):
+            ctx.sweep(u, f_dev, 1.0, 1e-12)
+        out_pin.copy_(u, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms += a.elapsed_time(b)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = t.item()
+
+    # ---- fp64 peak: derived and measured (DFMA microbenchmark)
+    sink = torch.empty(148 * 8 * 256, dtype=torch.float64, device=dev)
+    dg.microbench_dfma(sink, 148 * 8, 1000)
+    a, b = ev(), ev()
+    a.record(stream)
+    fl = dg.microbench_dfma(sink, 148 * 8, 20000)
+    b.record(stream)
+    torch.cuda.synchronize()
+    dfma_tflops = fl / (a.elapsed_time(b) * 1e-3) / 1e12
+
+    if rank != 0:
+        ctx.close()
+        return
+    steps = args.steps
+    dof = P.n_dof
+    value = dof * (N_APPLY + N_SWEEP) * steps / (total_ms * 1e-3)
+    fm = flops_model(P.p)
+    iter_key = "cg_iter" if P.local_solver == "cg" else "bicgstab_iter"
+    apply_flops = dof * fm["apply"]
+    sweep_flops_all = N_SWEEP * dof * (fm["apply"] + 4) + it_sum_total * P.nd * fm[iter_key]
+    step_flops = N_APPLY * apply_flops + sweep_flops_all
+    sweep_launch_flops = sweep_flops_all / N_SWEEP
+    sweep_launch_s = tsw * 1e-3 / (steps * N_SWEEP)
+    apply_launch_s = t_apply_ms * 1e-3 / (steps * N_APPLY)
+    sm_clock = (clk or {}).get("sm_max_mhz") or 1965.0
+    peak_derived = SM_COUNT * DFMA_PER_CLK_PER_SM * 2 * 1965e6 / 1e12
+    dominant = "sweep" if tsw >= t_apply_ms else "apply"
+    if dominant == "sweep":
+        achieved = sweep_launch_flops / sweep_launch_s / 1e12
+    else:
+        achieved = apply_flops / apply_launch_s / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            tj = json.load(open(tpath))
+            traffic = tj.get(P.name, {}).get(dominant)
+        except Exception:
+            traffic = None
+    e2e_value = dof * (N_APPLY + N_SWEEP) * e2e_steps / (e2e_ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 u, f ~ U[-1,1), synth/)",
+        "config": {"workload": describe(P, solver), "n_dof": dof, "p": P.p,
+                   "mesh": [P.nx, P.ny, P.nz], "decomposition": f"{world} z-slab(s)",
+                   "l2": "flushed before every timed step (512 MiB write); u reset outside timing"},
+        "gflops_model": step_flops * steps / (total_ms * 1e-3) / 1e9,
+        "frac_fp64_peak_model": step_flops * steps / (total_ms * 1e-3) / 1e12 / peak_derived,
+        "apply": {"dof_per_s": dof / apply_launch_s, "us_per_call": apply_launch_s * 1e6,
+                  "gflops_model": apply_flops / apply_launch_s / 1e9,
+                  "frac_fp64_peak": apply_flops / apply_launch_s / 1e12 / peak_derived},
+        "sweep": {"dof_per_s": dof / sweep_launch_s, "us_per_call": sweep_launch_s * 1e6,
+                  "gflops_model": sweep_launch_flops / sweep_launch_s / 1e9,
+                  "frac_fp64_peak": sweep_launch_flops / sweep_launch_s / 1e12 / peak_derived,
+                  "local_iterations_mean": it_stats[0]["it_mean"], "local_iterations_max": it_stats[0]["it_max"],
+                  "local_nonconverged": it_stats[0]["n_nonconverged"]},
+        "roofline": {"bound": "alu", "kernel": "k_cg<4,true> (fused defect + local CG + update)"
+                     if dominant == "sweep" else "k_apply<4>",
+                     "achieved": achieved, "peak": peak_derived, "unit": "TFLOP/s",
+                     "frac": achieved / peak_derived, "traffic": traffic,
+                     "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1965 MHz (DESIGN.md)",
+                     "dfma_microbench_tflops": dfma_tflops},
+        "e2e": {"value": e2e_value, "unit": "DoF/s",
+                "h2d_bytes_per_step": int(world * 2 * u_h.nbytes), "d2h_bytes_per_step": int(world * u_h.nbytes)},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_oracle_sample(P, u_h, f_h, args.cpu_seconds, "oracle")
+    print(json.dumps(line), flush=True)
+    ctx.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * dg.h — C ABI of the B200-native matrix-free DG hot path of arXiv 1805.11930.
+ *
+ * Problem: find u in V_h^p with a_h(u, v) = l_h(v), i.e. A u = f with
+ * A_ij = a_h(psi_j, psi_i) (P:328-330, P:427-430 eq. linear_equation), a_h the WSIPG
+ * form with upwind flux (P:333-360 eq. bilinear_form_split), on a
+ * structured box of hexahedral cells with the nodal Gauss-Lobatto Q_p basis
+ * (P:436-440). The library applies A matrix-free with sum factorisation
+ * (§3.1) and runs the block-Jacobi smoother of Alg. 2 whose
+ * diagonal blocks D_T = A_{T,T} (P:893-903 eq. block_diag_apply) are inverted
+ * iteratively by a cell-local preconditioned Krylov solve (§2.2.1,
+ * P:904-911 §3.2).
+ *
+ * Layout of every vector (u, f, Au, d, du): fp64, cell-major. Cell
+ * c = cx + nx*(cy + ny*cz) (x fastest), DoF inside a cell I = i + n*j + n*n*k with
+ * n = p+1 (x fastest), i.e. u[c*n^3 + I]. With nranks > 1 a rank holds the z-slab
+ * cz in [z_begin, z_end) (dg_local_range), a contiguous range of the global vector,
+ * and its pointers address that local range only.
+ *
+ * Pointers named u/f/Au/d/du are DEVICE pointers (e.g. torch CUDA tensors) on
+ * desc.device, owned by the caller. Calls are stream ordered on `cuda_stream`
+ * (a cudaStream_t, NULL = legacy default stream) and return before the GPU work
+ * completes; statistics are valid after dg_get_stats (which synchronises).
+ * The library owns all scratch, halo buffers and the NCCL communicator.
+ * Errors: a dg_status; no exception crosses the ABI. dg_last_error() returns a
+ * thread-local message for the last failing call on the calling thread.
+ */
+#ifndef DG_B200_H
+#define DG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dg_ctx dg_ctx; /* opaque, owned by the library */
+
+typedef enum {
+  DG_OK = 0,
+  DG_ERR_INVALID = 1,     /* bad sizes, p outside 1..7, non-positive L, negative K or c, NULL */
+  DG_ERR_NOMEM = 2,       /* device allocation failed */
+  DG_ERR_CUDA = 3,        /* CUDA runtime error (message in dg_last_error) */
+  DG_ERR_NCCL = 4,        /* NCCL unavailable or failed */
+  DG_ERR_STATE = 5,       /* call not valid in this context state */
+  DG_ERR_UNSUPPORTED = 6  /* valid request outside this build (e.g. no sm_100a device) */
+} dg_status;
+
+enum { DG_BC_DIRICHLET = 0, DG_BC_NEUMANN = 1 };
+enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2 };
+enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
+
+typedef struct {
+  int32_t nx, ny, nz;        /* GLOBAL cells per axis (uniform cells, D2 of SURVEY §2.1) */
+  double Lx, Ly, Lz;         /* box [0,Lx]x[0,Ly]x[0,Lz], > 0 */
+  int32_t bc[6];             /* x-, x+, y-, y+, z-, z+ : DG_BC_DIRICHLET / DG_BC_NEUMANN */
+  int32_t p;                 /* polynomial degree 1..7 (n = p+1 GL nodes, m = p+1 Gauss points) */
+  double alpha;              /* penalty parameter of gamma_F; configs use 2.0 */
+  int32_t k_components;      /* 1: scalar K per cell; 3: diagonal (Kx,Ky,Kz) per cell */
+  const double* K;           /* HOST, GLOBAL [nx*ny*nz][k_components], >= 0; copied at create */
+  double b[3];               /* constant advection field b */
+  const double* c;           /* HOST, GLOBAL [nx*ny*nz] reaction >= 0, or NULL (c = 0) */
+  int32_t rank, nranks;      /* z-slab decomposition; nranks = 1 for a single GPU */
+  int32_t halo_mode;         /* DG_HALO_NCCL or DG_HALO_EXTERNAL (caller fills ghost layers) */
+  const void* nccl_id;       /* HOST, 128-byte ncclUniqueId (same on all ranks) if NCCL mode and
+                                nranks > 1, else NULL */
+  int32_t device;            /* CUDA device ordinal of this rank */
+} dg_desc;
+
+typedef struct {
+  double it_mean, it_std;    /* local Krylov iterations per cell of the last sweep / solve */
+  int32_t it_max, it_min;
+  int64_t n_cells;           /* local cells */
+  int64_t n_nonconverged;    /* cells that hit max_it before ||r|| <= tol ||d|| (not fatal) */
+  int64_t it_sum;
+} dg_stats;
+
+/* Validates desc, builds the 1D tables (GL nodes, Gauss rule), copies this
+ * rank's slice of K / c plus one ghost z-layer to the device, allocates scratch and
+ * (NCCL mode, nranks > 1) creates the communicator. *out = NULL on failure. */
+dg_status dg_create(const dg_desc* desc, dg_ctx** out);
+dg_status dg_destroy(dg_ctx* ctx);
+
+/* This rank's slab: global z-layers [z_begin, z_end) and its DoF count. */
+dg_status dg_local_range(const dg_ctx* ctx, int32_t* z_begin, int32_t* z_end, int64_t* n_local_dof);
+
+/* Au = A u, matrix-free: sum-factorised volume terms (Stages 1-3)
+ * plus interior/boundary face terms. u, Au: device [n_local_dof], must not alias.
+ * With nranks > 1 the z-boundary layers of u are exchanged first (NCCL or external). */
+dg_status dg_apply(dg_ctx* ctx, const double* u, double* Au, void* cuda_stream);
+
+/* One block-Jacobi sweep, Alg. 2 lines 2-4: d = f - A u; for every cell solve
+ * D_T du_T = d_T by Jacobi-preconditioned CG (b = 0) or BiCGStab from du = 0 until
+ * ||d_T - D_T du_T||_2 <= local_tol ||d_T||_2 or max_it; u <- u + omega du.
+ * u: device [n_local_dof] in/out; f: device [n_local_dof]. */
+dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double omega,
+                                double local_tol, void* cuda_stream);
+
+/* Alg. 2 line 3 alone: du_T = (iterative) D_T^{-1} d_T for every local cell. */
+dg_status dg_local_block_solve(dg_ctx* ctx, const double* d, double* du, double local_tol,
+                               void* cuda_stream);
+
+/* Local Krylov method (DG_LOCAL_AUTO: CG if b == 0 else BiCGStab) and iteration cap
+ * (default 1000; reading #13 of SURVEY §8(c)). */
+dg_status dg_set_local_solver(dg_ctx* ctx, int32_t method, int32_t max_it);
+
+/* Synchronises the last sweep/solve stream and reduces its per-cell iteration counts. */
+dg_status dg_get_stats(dg_ctx* ctx, dg_stats* st);
+
+/* Component hooks for parity tests:
+ *  dg_apply_parts: mask 1 = volume terms a^v, 2 = interior-face terms a^if,
+ *                  4 = boundary-face terms a^bf (sums of the selected parts of A u);
+ *  dg_block_diag_apply: Du_T = D_T u_T for every cell. */
+dg_status dg_apply_parts(dg_ctx* ctx, const double* u, double* out, uint32_t mask, void* cuda_stream);
+dg_status dg_block_diag_apply(dg_ctx* ctx, const double* u, double* Du, void* cuda_stream);
+
+/* External halo mode: device pointers of the ghost layers (nx*ny cells, n^3 DoF each, same
+ * layout as u) that hold the neighbouring ranks' adjacent z-layer of u. Filled by the
+ * caller before dg_apply / dg_block_jacobi_sweep; NULL where the slab touches the domain. */
+dg_status dg_ghost_layers(dg_ctx* ctx, double** ghost_lo, double** ghost_hi, int64_t* layer_dof);
+
+/* External halo mode: copies caller device buffers (each one layer: nx*ny cells, n^3 DoF) into
+ * the ghost layers, stream ordered. lo / hi may be NULL when the slab has no such neighbour. */
+dg_status dg_fill_ghosts(dg_ctx* ctx, const double* lo, const double* hi, void* cuda_stream);
+
+/* The 1D tables used by the kernels, for parity with the oracle's own: out receives
+ * z[n], xq[n], wq[n], A[n*n], D[n*n], M[n*n], d0[n], d1[n] (5n + 3n^2 doubles). */
+dg_status dg_tables(int32_t p, double* out);
+
+/* Writes a fresh 128-byte ncclUniqueId (rank 0 broadcasts it to the other ranks). */
+dg_status dg_nccl_unique_id(void* out128);
+
+/* fp64 FMA-throughput microbenchmark: launches `blocks` x 256 threads,
+ * each running 16 independent DFMA chains for `iters` steps on `cuda_stream`; *flops receives
+ * the flop count (2 per DFMA). sink: device buffer of blocks*256 doubles (defeats DCE). */
+dg_status dg_microbench_dfma(double* sink, int32_t blocks, int32_t iters, int64_t* flops,
+                             void* cuda_stream);
+
+/* Kernel launches issued by the last call on ctx (for launch accounting). */
+int32_t dg_last_launch_count(const dg_ctx* ctx);
+
+const char* dg_last_error(void);
+const char* dg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_B200_H */

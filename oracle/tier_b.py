@@ -173,6 +173,24 @@ class TierB:
     def apply(self, u):
         return self.apply_cells(u, range(self.P.n_cells)).reshape(-1)
 
+    def apply_parts_cells(self, u, cells, mask):
+        """Selected parts of (A u)_T: mask 1 = a^v, 2 = a^if (self + neighbour), 4 = a^bf."""
+        nd = self.nd
+        U = np.asarray(u).reshape(-1, nd)
+        out = np.zeros((len(cells), nd))
+        for r, c in enumerate(cells):
+            if mask & 1:
+                out[r] += self.volume_block(c) @ U[c]
+            for axis in range(3):
+                for hi in (False, True):
+                    interior = self.neighbour(c, axis, hi) is not None
+                    if (interior and mask & 2) or (not interior and mask & 4):
+                        out[r] += self.embed(axis, self.self_face_1d(c, axis, hi)) @ U[c]
+                    if interior and mask & 2:
+                        nb, B = self.nbr_face_1d(c, axis, hi)
+                        out[r] += self.embed(axis, B) @ U[nb]
+        return out
+
     def block_diag_apply(self, u, cells=None):
         cells = range(self.P.n_cells) if cells is None else cells
         U = np.asarray(u).reshape(-1, self.nd)

@@ -1,0 +1,460 @@
+// C ABI of the matrix-free DG hot path (include/dg.h): validation, the z-slab
+// partition, coefficient upload with ghost layers, the halo exchange (NCCL loaded
+// at run time, or caller-filled ghost layers) and kernel dispatch.
+#include "dg.h"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dg_kernels.h"
+#include "dg_tables.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+dg_status fail(dg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+dg_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(DG_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// ---- minimal NCCL binding, resolved with dlopen so single-GPU use needs no NCCL ----
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclFloat64 = 8 };
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* why) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) { *why = std::string("dlopen libnccl failed: ") + dlerror(); return false; }
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    send = (decltype(send))dlsym(h, "ncclSend");
+    recv = (decltype(recv))dlsym(h, "ncclRecv");
+    groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
+    groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
+    getErrorString = (decltype(getErrorString))dlsym(h, "ncclGetErrorString");
+    if (!commInitRank || !commDestroy || !send || !recv || !groupStart || !groupEnd) {
+      *why = "libnccl is missing required symbols";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+
+}  // namespace
+
+struct dg_ctx {
+  dg_desc desc{};
+  int n = 0, nd = 0;
+  int z_begin = 0, z_end = 0, nzl = 0;
+  int64_t ncells = 0, ndof = 0, layer_dof = 0;
+  dg::Tables1D tab{};
+  dg::KParams kp{};
+  double* d_K = nullptr;
+  double* d_c = nullptr;
+  double* d_ghost_lo = nullptr;
+  double* d_ghost_hi = nullptr;
+  double* d_unew = nullptr;
+  int32_t* d_its = nullptr;
+  int method = 0;  // resolved local method
+  int32_t max_it = 1000;
+  ncclComm_t comm = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool have_stats = false;
+  int32_t launches = 0;
+};
+
+namespace {
+
+dg_status validate(const dg_desc* d) {
+  if (!d) return fail(DG_ERR_INVALID, "desc is NULL");
+  if (d->nx < 1 || d->ny < 1 || d->nz < 1) return fail(DG_ERR_INVALID, "nx, ny, nz must be >= 1");
+  if (!(d->Lx > 0) || !(d->Ly > 0) || !(d->Lz > 0)) return fail(DG_ERR_INVALID, "Lx, Ly, Lz must be > 0");
+  if (d->p < 1 || d->p > 7) return fail(DG_ERR_INVALID, "p must be in 1..7");
+  if (!(d->alpha >= 0) || !std::isfinite(d->alpha)) return fail(DG_ERR_INVALID, "alpha must be >= 0");
+  for (int i = 0; i < 6; ++i)
+    if (d->bc[i] != DG_BC_DIRICHLET && d->bc[i] != DG_BC_NEUMANN)
+      return fail(DG_ERR_INVALID, "bc[i] must be DG_BC_DIRICHLET or DG_BC_NEUMANN");
+  if (d->k_components != 1 && d->k_components != 3)
+    return fail(DG_ERR_INVALID, "k_components must be 1 or 3");
+  if (!d->K) return fail(DG_ERR_INVALID, "K is NULL");
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(d->b[i])) return fail(DG_ERR_INVALID, "b must be finite");
+  if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
+    return fail(DG_ERR_INVALID, "need 0 <= rank < nranks");
+  if (d->nranks > d->nz) return fail(DG_ERR_INVALID, "nranks must not exceed nz (empty slab)");
+  if (d->halo_mode != DG_HALO_NCCL && d->halo_mode != DG_HALO_EXTERNAL)
+    return fail(DG_ERR_INVALID, "halo_mode must be DG_HALO_NCCL or DG_HALO_EXTERNAL");
+  if (d->nranks > 1 && d->halo_mode == DG_HALO_NCCL && !d->nccl_id)
+    return fail(DG_ERR_INVALID, "nccl_id required for nranks > 1 in NCCL halo mode");
+  const int64_t N = (int64_t)d->nx * d->ny * d->nz;
+  for (int64_t i = 0; i < N * d->k_components; ++i)
+    if (!(d->K[i] >= 0) || !std::isfinite(d->K[i])) return fail(DG_ERR_INVALID, "K must be finite and >= 0");
+  if (d->c)
+    for (int64_t i = 0; i < N; ++i)
+      if (!(d->c[i] >= 0) || !std::isfinite(d->c[i])) return fail(DG_ERR_INVALID, "c must be finite and >= 0");
+  return DG_OK;
+}
+
+void release(dg_ctx* c) {
+  if (!c) return;
+  if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  cudaFree(c->d_K);
+  cudaFree(c->d_c);
+  cudaFree(c->d_ghost_lo);
+  cudaFree(c->d_ghost_hi);
+  cudaFree(c->d_unew);
+  cudaFree(c->d_its);
+  delete c;
+}
+
+dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
+  if (c->desc.nranks == 1 || c->desc.halo_mode == DG_HALO_EXTERNAL) return DG_OK;
+  const int r = c->desc.rank, G = c->desc.nranks;
+  const size_t L = (size_t)c->layer_dof;
+  ncclResult_t e = g_nccl.groupStart();
+  if (r > 0) {
+    e |= g_nccl.send(u, L, ncclFloat64, r - 1, c->comm, s);
+    e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, r - 1, c->comm, s);
+  }
+  if (r < G - 1) {
+    e |= g_nccl.send(u + (size_t)(c->nzl - 1) * L, L, ncclFloat64, r + 1, c->comm, s);
+    e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, r + 1, c->comm, s);
+  }
+  e |= g_nccl.groupEnd();
+  if (e != 0) return fail(DG_ERR_NCCL, "NCCL halo exchange failed");
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dg_last_error(void) { return g_err.c_str(); }
+const char* dg_version(void) { return "dg-b200 0.1 (sm_100a, fp64)"; }
+
+dg_status dg_tables(int32_t p, double* out) {
+  dg::Tables1D t;
+  if (!out) return fail(DG_ERR_INVALID, "out is NULL");
+  if (!dg::build_tables(p, &t)) return fail(DG_ERR_INVALID, "p must be in 1..7");
+  const int n = t.n;
+  double* o = out;
+  for (int i = 0; i < n; ++i) *o++ = t.z[i];
+  for (int i = 0; i < n; ++i) *o++ = t.xq[i];
+  for (int i = 0; i < n; ++i) *o++ = t.wq[i];
+  for (int i = 0; i < n * n; ++i) *o++ = t.A[i];
+  for (int i = 0; i < n * n; ++i) *o++ = t.D[i];
+  for (int i = 0; i < n * n; ++i) *o++ = t.M[i];
+  for (int i = 0; i < n; ++i) *o++ = t.d0[i];
+  for (int i = 0; i < n; ++i) *o++ = t.d1[i];
+  return DG_OK;
+}
+
+dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
+  if (!out) return fail(DG_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  dg_status st = validate(desc);
+  if (st != DG_OK) return st;
+  cudaError_t e = cudaSetDevice(desc->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  e = cudaGetDeviceProperties(&prop, desc->device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(DG_ERR_UNSUPPORTED, "this build targets sm_100a (B200); device is sm_" +
+                                        std::to_string(prop.major) + std::to_string(prop.minor));
+  dg_ctx* c = new dg_ctx();
+  c->desc = *desc;
+  c->desc.K = nullptr;
+  c->desc.c = nullptr;
+  c->desc.nccl_id = nullptr;
+  c->n = desc->p + 1;
+  c->nd = c->n * c->n * c->n;
+  const int G = desc->nranks, r = desc->rank;
+  c->z_begin = (int)((int64_t)r * desc->nz / G);
+  c->z_end = (int)((int64_t)(r + 1) * desc->nz / G);
+  c->nzl = c->z_end - c->z_begin;
+  const int64_t nxy = (int64_t)desc->nx * desc->ny;
+  c->ncells = nxy * c->nzl;
+  c->ndof = c->ncells * c->nd;
+  c->layer_dof = nxy * c->nd;
+  dg::build_tables(desc->p, &c->tab);
+  if (!dg::upload_tables(desc->p, c->tab, &e)) { release(c); return cuda_fail(e, "upload tables"); }
+
+  // K with one ghost z-layer on each side, always 3 components
+  std::vector<double> K3((size_t)(c->nzl + 2) * nxy * 3, 0.0);
+  for (int zl = -1; zl <= c->nzl; ++zl) {
+    const int zg = c->z_begin + zl;
+    if (zg < 0 || zg >= desc->nz) continue;
+    for (int64_t col = 0; col < nxy; ++col) {
+      const int64_t gc = (int64_t)zg * nxy + col;
+      for (int a = 0; a < 3; ++a)
+        K3[((size_t)(zl + 1) * nxy + col) * 3 + a] =
+            desc->k_components == 1 ? desc->K[gc] : desc->K[gc * 3 + a];
+    }
+  }
+  auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 8); };
+  if ((e = alloc((void**)&c->d_K, K3.size() * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc K"); }
+  if ((e = cudaMemcpy(c->d_K, K3.data(), K3.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy K"); }
+  if (desc->c) {
+    if ((e = alloc((void**)&c->d_c, (size_t)c->ncells * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc c"); }
+    if ((e = cudaMemcpy(c->d_c, desc->c + (size_t)c->z_begin * nxy, (size_t)c->ncells * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy c"); }
+  }
+  if (G > 1) {
+    if (alloc((void**)&c->d_ghost_lo, (size_t)c->layer_dof * 8) != cudaSuccess ||
+        alloc((void**)&c->d_ghost_hi, (size_t)c->layer_dof * 8) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc ghosts"); }
+    cudaMemset(c->d_ghost_lo, 0, (size_t)c->layer_dof * 8);
+    cudaMemset(c->d_ghost_hi, 0, (size_t)c->layer_dof * 8);
+  }
+  if (alloc((void**)&c->d_unew, (size_t)c->ndof * 8) != cudaSuccess ||
+      alloc((void**)&c->d_its, (size_t)c->ncells * 4) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc scratch"); }
+  cudaMemset(c->d_its, 0, (size_t)c->ncells * 4);
+
+  dg::KParams& kp = c->kp;
+  kp.nx = desc->nx; kp.ny = desc->ny; kp.nzl = c->nzl; kp.ncells = (int32_t)c->ncells;
+  kp.h[0] = desc->Lx / desc->nx; kp.h[1] = desc->Ly / desc->ny; kp.h[2] = desc->Lz / desc->nz;
+  kp.pen = desc->alpha * desc->p * (desc->p + 2);
+  for (int a = 0; a < 3; ++a) kp.b[a] = desc->b[a];
+  for (int f = 0; f < 4; ++f) kp.slab_face[f] = desc->bc[f] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN;
+  kp.slab_face[4] = r > 0 ? dg::FK_GHOST : (desc->bc[4] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN);
+  kp.slab_face[5] = r < G - 1 ? dg::FK_GHOST : (desc->bc[5] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN);
+  kp.K = c->d_K;
+  kp.c = c->d_c;
+  kp.ghost_lo = r > 0 ? c->d_ghost_lo : nullptr;
+  kp.ghost_hi = r < G - 1 ? c->d_ghost_hi : nullptr;
+  kp.mask = 7u;
+  kp.its = c->d_its;
+  c->method = (desc->b[0] == 0.0 && desc->b[1] == 0.0 && desc->b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
+  c->max_it = 1000;
+
+  if (G > 1 && desc->halo_mode == DG_HALO_NCCL) {
+    std::string why;
+    if (!g_nccl.load(&why)) { release(c); return fail(DG_ERR_NCCL, why); }
+    ncclUniqueId id;
+    std::memcpy(&id, desc->nccl_id, sizeof(id));
+    ncclResult_t ne = g_nccl.commInitRank(&c->comm, G, id, r);
+    if (ne != 0) {
+      c->comm = nullptr;
+      release(c);
+      return fail(DG_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.getErrorString ? g_nccl.getErrorString(ne) : "error"));
+    }
+  }
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { release(c); return cuda_fail(e, "create"); }
+  *out = c;
+  return DG_OK;
+}
+
+dg_status dg_destroy(dg_ctx* ctx) {
+  if (!ctx) return fail(DG_ERR_INVALID, "ctx is NULL");
+  cudaSetDevice(ctx->desc.device);
+  cudaDeviceSynchronize();
+  release(ctx);
+  return DG_OK;
+}
+
+dg_status dg_local_range(const dg_ctx* c, int32_t* zb, int32_t* ze, int64_t* nd) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (zb) *zb = c->z_begin;
+  if (ze) *ze = c->z_end;
+  if (nd) *nd = c->ndof;
+  return DG_OK;
+}
+
+dg_status dg_ghost_layers(dg_ctx* c, double** lo, double** hi, int64_t* layer_dof) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (lo) *lo = (double*)c->kp.ghost_lo;
+  if (hi) *hi = (double*)c->kp.ghost_hi;
+  if (layer_dof) *layer_dof = c->layer_dof;
+  return DG_OK;
+}
+
+dg_status dg_fill_ghosts(dg_ctx* c, const double* lo, const double* hi, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (c->desc.halo_mode != DG_HALO_EXTERNAL) return fail(DG_ERR_STATE, "context is not in external halo mode");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)c->layer_dof * 8;
+  if (lo && c->kp.ghost_lo) {
+    cudaError_t e = cudaMemcpyAsync(c->d_ghost_lo, lo, bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fill ghost lo");
+  }
+  if (hi && c->kp.ghost_hi) {
+    cudaError_t e = cudaMemcpyAsync(c->d_ghost_hi, hi, bytes, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "fill ghost hi");
+  }
+  return DG_OK;
+}
+
+dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (max_it < 1) return fail(DG_ERR_INVALID, "max_it must be >= 1");
+  if (method == DG_LOCAL_AUTO) {
+    const double* b = c->desc.b;
+    c->method = (b[0] == 0.0 && b[1] == 0.0 && b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
+  } else if (method == DG_LOCAL_CG) {
+    c->method = dg::LM_CG;
+  } else if (method == DG_LOCAL_BICGSTAB) {
+    c->method = dg::LM_BICGSTAB;
+  } else {
+    return fail(DG_ERR_INVALID, "unknown local method");
+  }
+  c->max_it = max_it;
+  return DG_OK;
+}
+
+static dg_status check_vec(const void* p, const char* name) {
+  if (!p) return fail(DG_ERR_INVALID, std::string(name) + " is NULL");
+  return DG_OK;
+}
+
+dg_status dg_apply_parts(dg_ctx* c, const double* u, double* Au, uint32_t mask, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(Au, "Au")) return DG_ERR_INVALID;
+  if (u == Au) return fail(DG_ERR_INVALID, "u and Au must not alias");
+  if (mask == 0 || mask > 7) return fail(DG_ERR_INVALID, "mask must be in 1..7");
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches = 0;
+  dg_status st = halo_exchange(c, u, s);
+  if (st != DG_OK) return st;
+  dg::KParams kp = c->kp;
+  kp.mask = mask;
+  cudaError_t e = dg::launch_apply(c->desc.p, kp, u, Au, s);
+  if (e != cudaSuccess) return cuda_fail(e, "apply");
+  c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_apply(dg_ctx* c, const double* u, double* Au, void* stream) {
+  return dg_apply_parts(c, u, Au, 7u, stream);
+}
+
+dg_status dg_block_diag_apply(dg_ctx* c, const double* u, double* Du, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(Du, "Du")) return DG_ERR_INVALID;
+  if (u == Du) return fail(DG_ERR_INVALID, "u and Du must not alias");
+  cudaError_t e = dg::launch_block_diag_apply(c->desc.p, c->kp, u, Du, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "block_diag_apply");
+  c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_local_block_solve(dg_ctx* c, const double* d, double* du, double tol, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(d, "d") || check_vec(du, "du")) return DG_ERR_INVALID;
+  if (d == du) return fail(DG_ERR_INVALID, "d and du must not alias");
+  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
+  dg::KParams kp = c->kp;
+  kp.tol2 = tol * tol;
+  kp.max_it = c->max_it;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = dg::launch_local_solve(c->desc.p, c->method, kp, d, du, s);
+  if (e != cudaSuccess) return cuda_fail(e, "local_block_solve");
+  c->last_stream = s;
+  c->have_stats = true;
+  c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_block_jacobi_sweep(dg_ctx* c, double* u, const double* f, double omega, double tol,
+                                void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
+  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
+  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  cudaStream_t s = (cudaStream_t)stream;
+  c->launches = 0;
+  dg_status st = halo_exchange(c, u, s);
+  if (st != DG_OK) return st;
+  dg::KParams kp = c->kp;
+  kp.tol2 = tol * tol;
+  kp.max_it = c->max_it;
+  kp.omega = omega;
+  cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, c->d_unew, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sweep");
+  e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sweep copy-back");
+  c->last_stream = s;
+  c->have_stats = true;
+  c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_get_stats(dg_ctx* c, dg_stats* st) {
+  if (!c || !st) return fail(DG_ERR_INVALID, "NULL argument");
+  if (!c->have_stats) return fail(DG_ERR_STATE, "no sweep or local solve has run");
+  cudaError_t e = cudaStreamSynchronize(c->last_stream);
+  if (e != cudaSuccess) return cuda_fail(e, "stats sync");
+  std::vector<int32_t> its((size_t)c->ncells);
+  e = cudaMemcpy(its.data(), c->d_its, its.size() * 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "stats copy");
+  double s = 0, s2 = 0;
+  int32_t mx = 0, mn = its.empty() ? 0 : (its[0] & ~(1 << 30));
+  int64_t nonconv = 0, sum = 0;
+  for (int32_t raw : its) {
+    const int32_t v = raw & ~(1 << 30);
+    if (raw & (1 << 30)) ++nonconv;
+    s += v;
+    s2 += (double)v * v;
+    sum += v;
+    mx = v > mx ? v : mx;
+    mn = v < mn ? v : mn;
+  }
+  const double n = its.empty() ? 1.0 : (double)its.size();
+  st->it_mean = s / n;
+  st->it_std = std::sqrt(std::fmax(0.0, s2 / n - (s / n) * (s / n)));
+  st->it_max = mx;
+  st->it_min = mn;
+  st->n_cells = c->ncells;
+  st->n_nonconverged = nonconv;
+  st->it_sum = sum;
+  return DG_OK;
+}
+
+int32_t dg_last_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+dg_status dg_nccl_unique_id(void* out128) {
+  if (!out128) return fail(DG_ERR_INVALID, "out is NULL");
+  std::string why;
+  if (!g_nccl.load(&why)) return fail(DG_ERR_NCCL, why);
+  auto get = (ncclResult_t(*)(ncclUniqueId*))dlsym(g_nccl.h, "ncclGetUniqueId");
+  if (!get) return fail(DG_ERR_NCCL, "ncclGetUniqueId missing");
+  ncclUniqueId id;
+  if (get(&id) != 0) return fail(DG_ERR_NCCL, "ncclGetUniqueId failed");
+  std::memcpy(out128, &id, sizeof(id));
+  return DG_OK;
+}
+
+dg_status dg_microbench_dfma(double* sink, int32_t blocks, int32_t iters, int64_t* flops, void* stream) {
+  if (!sink || !flops || blocks < 1 || iters < 1) return fail(DG_ERR_INVALID, "bad microbench arguments");
+  cudaError_t e = dg::launch_dfma_bench(sink, blocks, iters, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "dfma bench");
+  *flops = (int64_t)blocks * 256 * 16 * 2 * (int64_t)iters;
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,49 @@
+// Internal (non-ABI) launch interface of the fp64 sm_100a kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "dg_tables.h"
+
+namespace dg {
+
+enum FaceKind : int32_t { FK_DIRICHLET = 0, FK_NEUMANN = 1, FK_GHOST = 2 };
+
+// Everything a kernel needs about the local slab (passed by value).
+struct KParams {
+  int32_t nx, ny, nzl, ncells;   // local slab: nzl z-layers, ncells = nx*ny*nzl
+  double h[3];                   // cell sizes
+  double pen;                    // alpha * p * (p + d - 1), d = 3
+  double b[3];                   // constant advection
+  int32_t slab_face[6];          // x-,x+,y-,y+,z-,z+ of the slab: FaceKind
+  const double* K;               // [(nzl+2)*nx*ny][3] diagonal K, z-shifted by one ghost layer
+  const double* c;               // [ncells] reaction or nullptr
+  const double* ghost_lo;        // [nx*ny*n^3] neighbour rank's last layer (or nullptr)
+  const double* ghost_hi;        // [nx*ny*n^3] neighbour rank's first layer
+  uint32_t mask;                 // 1 volume, 2 interior faces, 4 boundary faces
+  int32_t max_it;
+  double tol2;                   // local_tol^2
+  double omega;
+  int32_t* its;                  // [ncells] iterations of the last solve
+};
+
+enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2 };
+
+bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
+
+// Au (or selected parts) for all local cells.
+cudaError_t launch_apply(int p, const KParams& kp, const double* u, double* out, cudaStream_t s);
+// D_T u_T for all local cells.
+cudaError_t launch_block_diag_apply(int p, const KParams& kp, const double* u, double* out,
+                                    cudaStream_t s);
+// du = D^{-1} d (iterative, per cell).
+cudaError_t launch_local_solve(int p, int method, const KParams& kp, const double* d, double* du,
+                               cudaStream_t s);
+// u_new = u + omega D^{-1}(f - A u).
+cudaError_t launch_sweep(int p, int method, const KParams& kp, const double* u, const double* f,
+                         double* u_new, cudaStream_t s);
+
+// fp64 FMA peak microbenchmark: blocks x 256 threads, 16 chains x iters DFMA each.
+cudaError_t launch_dfma_bench(double* sink, int blocks, int iters, cudaStream_t s);
+
+}  // namespace dg

@@ -1,0 +1,238 @@
+"""Thin ctypes binding of the C ABI in include/dg.h (argument marshalling only).
+
+Every step of the hot path runs in libdg_b200.so; this module only converts a
+`synth.Problem` into a `dg_desc`, passes torch CUDA tensors as raw device
+pointers plus the current CUDA stream, and maps error codes to exceptions. There
+is no CPU fallback: if the library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+
+DG_OK, DG_ERR_INVALID, DG_ERR_NOMEM, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_STATE, DG_ERR_UNSUPPORTED = range(7)
+DG_LOCAL_AUTO, DG_LOCAL_CG, DG_LOCAL_BICGSTAB = 0, 1, 2
+DG_HALO_NCCL, DG_HALO_EXTERNAL = 0, 1
+MASK_VOLUME, MASK_INTERIOR_FACES, MASK_BOUNDARY_FACES = 1, 2, 4
+
+# every symbol include/dg.h declares (checked by the CPU tests)
+EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_jacobi_sweep",
+           "dg_local_block_solve", "dg_set_local_solver", "dg_get_stats", "dg_apply_parts",
+           "dg_block_diag_apply", "dg_ghost_layers", "dg_fill_ghosts", "dg_tables",
+           "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
+           "dg_microbench_dfma"]
+
+
+class DGError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"dg error {code}: {msg}")
+        self.code = code
+
+
+class dg_desc(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+                ("Lx", ctypes.c_double), ("Ly", ctypes.c_double), ("Lz", ctypes.c_double),
+                ("bc", ctypes.c_int32 * 6), ("p", ctypes.c_int32), ("alpha", ctypes.c_double),
+                ("k_components", ctypes.c_int32), ("K", ctypes.POINTER(ctypes.c_double)),
+                ("b", ctypes.c_double * 3), ("c", ctypes.POINTER(ctypes.c_double)),
+                ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("halo_mode", ctypes.c_int32),
+                ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32)]
+
+
+class dg_stats(ctypes.Structure):
+    _fields_ = [("it_mean", ctypes.c_double), ("it_std", ctypes.c_double),
+                ("it_max", ctypes.c_int32), ("it_min", ctypes.c_int32),
+                ("n_cells", ctypes.c_int64), ("n_nonconverged", ctypes.c_int64),
+                ("it_sum", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Loads libdg_b200.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    P, i32, i64, u32, dbl = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_double
+    sig = {
+        "dg_create": ([ctypes.POINTER(dg_desc), ctypes.POINTER(P)], i32),
+        "dg_destroy": ([P], i32),
+        "dg_local_range": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i64)], i32),
+        "dg_apply": ([P, P, P, P], i32),
+        "dg_apply_parts": ([P, P, P, u32, P], i32),
+        "dg_block_diag_apply": ([P, P, P, P], i32),
+        "dg_block_jacobi_sweep": ([P, P, P, dbl, dbl, P], i32),
+        "dg_local_block_solve": ([P, P, P, dbl, P], i32),
+        "dg_set_local_solver": ([P, i32, i32], i32),
+        "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
+        "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
+        "dg_fill_ghosts": ([P, P, P, P], i32),
+        "dg_tables": ([i32, ctypes.POINTER(dbl)], i32),
+        "dg_last_launch_count": ([P], i32),
+        "dg_last_error": ([], ctypes.c_char_p),
+        "dg_version": ([], ctypes.c_char_p),
+        "dg_nccl_unique_id": ([P], i32),
+        "dg_microbench_dfma": ([P, i32, i32, ctypes.POINTER(i64), P], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def _check(code):
+    if code != DG_OK:
+        raise DGError(code, _lib.dg_last_error().decode())
+
+
+def tables(p: int):
+    """The 1D tables the kernels use: dict of z, xq, wq, A, D, M, d0, d1 (numpy)."""
+    import numpy as np
+    lib = load_library()
+    n = p + 1
+    buf = (ctypes.c_double * (5 * n + 3 * n * n))()
+    _check(lib.dg_tables(p, buf))
+    a = np.frombuffer(buf, dtype=np.float64).copy()
+    out, o = {}, 0
+    for name, size in (("z", n), ("xq", n), ("wq", n), ("A", n * n), ("D", n * n), ("M", n * n),
+                       ("d0", n), ("d1", n)):
+        out[name] = a[o:o + size].reshape((n, n) if size == n * n else (n,))
+        o += size
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(lib.dg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def microbench_dfma(sink, blocks: int, iters: int, stream=None) -> int:
+    """Launches the DFMA-throughput kernel; returns its flop count (time it with CUDA events)."""
+    lib = load_library()
+    flops = ctypes.c_int64()
+    _check(lib.dg_microbench_dfma(_ptr(sink), blocks, iters, ctypes.byref(flops), _stream(stream)))
+    return flops.value
+
+
+def _ptr(t):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class DGContext:
+    """One rank's view of the DG operator / smoother on its z-slab (dg_create ... dg_destroy)."""
+
+    def __init__(self, problem, rank: int = 0, nranks: int = 1, device: Optional[int] = None,
+                 halo_mode: int = DG_HALO_NCCL, nccl_id: Optional[bytes] = None):
+        import numpy as np
+        import torch
+        lib = load_library()
+        self.lib = lib
+        self.problem = problem
+        P = problem
+        if device is None:
+            device = torch.cuda.current_device()
+        K = np.ascontiguousarray(np.asarray(P.K, dtype=np.float64))
+        kc = 1 if K.ndim == 1 else 3
+        c = None if P.c is None else np.ascontiguousarray(np.asarray(P.c, dtype=np.float64))
+        self._keep = (K, c)
+        d = dg_desc()
+        d.nx, d.ny, d.nz = P.nx, P.ny, P.nz
+        d.Lx, d.Ly, d.Lz = P.Lx, P.Ly, P.Lz
+        d.bc[:] = list(P.bc)
+        d.p = P.p
+        d.alpha = P.alpha
+        d.k_components = kc
+        d.K = K.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        d.b[:] = list(P.b)
+        d.c = c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if c is not None else None
+        d.rank, d.nranks, d.halo_mode = rank, nranks, halo_mode
+        self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        d.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
+        d.device = device
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(lib.dg_create(ctypes.byref(d), ctypes.byref(h)))
+        self.h = h
+        zb, ze, nd = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+        _check(lib.dg_local_range(h, ctypes.byref(zb), ctypes.byref(ze), ctypes.byref(nd)))
+        self.z_begin, self.z_end, self.n_local_dof = zb.value, ze.value, nd.value
+        nxy = P.nx * P.ny
+        self.cell_begin, self.cell_end = self.z_begin * nxy, self.z_end * nxy
+
+    def close(self):
+        if getattr(self, "h", None):
+            _check(self.lib.dg_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- calls ---------------------------------------------------------------
+    def apply(self, u, out, stream=None):
+        _check(self.lib.dg_apply(self.h, _ptr(u), _ptr(out), _stream(stream)))
+        return out
+
+    def apply_parts(self, u, out, mask: int, stream=None):
+        _check(self.lib.dg_apply_parts(self.h, _ptr(u), _ptr(out), mask, _stream(stream)))
+        return out
+
+    def block_diag_apply(self, u, out, stream=None):
+        _check(self.lib.dg_block_diag_apply(self.h, _ptr(u), _ptr(out), _stream(stream)))
+        return out
+
+    def local_block_solve(self, d, du, tol: float, stream=None):
+        _check(self.lib.dg_local_block_solve(self.h, _ptr(d), _ptr(du), float(tol), _stream(stream)))
+        return du
+
+    def sweep(self, u, f, omega: float = 1.0, tol: float = 1e-12, stream=None):
+        _check(self.lib.dg_block_jacobi_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
+                                              _stream(stream)))
+        return u
+
+    def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000):
+        _check(self.lib.dg_set_local_solver(self.h, method, max_it))
+
+    def stats(self) -> dict:
+        st = dg_stats()
+        _check(self.lib.dg_get_stats(self.h, ctypes.byref(st)))
+        return st.as_dict()
+
+    def fill_ghosts(self, lo=None, hi=None, stream=None):
+        _check(self.lib.dg_fill_ghosts(self.h, _ptr(lo) if lo is not None else None,
+                                       _ptr(hi) if hi is not None else None, _stream(stream)))
+
+    def launch_count(self) -> int:
+        return int(self.lib.dg_last_launch_count(self.h))

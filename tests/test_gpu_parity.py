@@ -1,0 +1,270 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): relative L2 <= 1e-12 for dg_apply and its parts,
+<= 1e-9 after a block-Jacobi sweep with local solves converged to 1e-12; local solves vs
+dense LU <= 1e-10 per cell."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+from oracle.kron1d import separable_apply, to_cell_major          # noqa: E402
+from oracle.tier_b import TierB                                    # noqa: E402
+from synth import (DIRICHLET, NEUMANN, Problem, make_config, make_vectors,  # noqa: E402
+                   random_problem, uniform_pm1)
+import paper_1805_11930_b200 as dg                                  # noqa: E402
+
+APPLY_TOL = 1e-12
+SWEEP_TOL = 1e-9
+MIXED = (DIRICHLET, NEUMANN, DIRICHLET, DIRICHLET, NEUMANN, DIRICHLET)
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def vec(P, seed):
+    return uniform_pm1(seed, 0, P.n_dof), uniform_pm1(seed + 1, 0, P.n_dof)
+
+
+def problems():
+    out = []
+    for p in range(1, 8):
+        # sizes span several CTAs' cell groups and a ragged last group
+        nx, ny, nz = {1: (9, 7, 5), 2: (7, 5, 4), 3: (5, 4, 3), 4: (4, 3, 3), 5: (3, 3, 2),
+                      6: (3, 2, 2), 7: (3, 2, 1)}[p]
+        out.append(("poisson", random_problem(nx, ny, nz, p, seed=200 + p, spread=1.5)))
+        out.append(("conv", random_problem(nx, ny, nz, p, seed=300 + p, b=(1.0, -0.5, 0.25), c=True,
+                                           bc=MIXED, L=(1.0, 0.6, 1.4))))
+    return out
+
+
+PROBS = problems()
+IDS = [f"{k}-p{P.p}" for k, P in PROBS]
+
+
+@pytest.mark.parametrize("kind,P", PROBS, ids=IDS)
+def test_apply_matches_oracle(kind, P):
+    u, _ = vec(P, 11)
+    ref = TierB(P).apply(u)
+    with dg.DGContext(P) as ctx:
+        out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.apply(cuda(u), out)
+        got = host(out)
+    assert rel(got, ref) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("kind,P", PROBS[::3], ids=IDS[::3])
+@pytest.mark.parametrize("mask", [1, 2, 4, 3, 6])
+def test_apply_parts_match_oracle(kind, P, mask):
+    u, _ = vec(P, 12)
+    ref = TierB(P).apply_parts_cells(u, range(P.n_cells), mask).reshape(-1)
+    with dg.DGContext(P) as ctx:
+        out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.apply_parts(cuda(u), out, mask)
+        got = host(out)
+    assert rel(got, ref) <= APPLY_TOL * 10 if np.linalg.norm(ref) > 0 else np.abs(got).max() == 0
+
+
+@pytest.mark.parametrize("kind,P", PROBS, ids=IDS)
+def test_block_diag_apply_matches_oracle(kind, P):
+    u, _ = vec(P, 13)
+    ref = TierB(P).block_diag_apply(u).reshape(-1)
+    with dg.DGContext(P) as ctx:
+        out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.block_diag_apply(cuda(u), out)
+        got = host(out)
+    assert rel(got, ref) <= APPLY_TOL
+
+
+@pytest.mark.parametrize("kind,P", PROBS, ids=IDS)
+def test_local_solve_matches_lu(kind, P):
+    d, _ = vec(P, 14)
+    tb = TierB(P)
+    ref = tb.local_solve(d)
+    with dg.DGContext(P) as ctx:
+        out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.local_block_solve(cuda(d), out, 1e-12)
+        got = host(out).reshape(P.n_cells, P.nd)
+        st = ctx.stats()
+    assert st["n_nonconverged"] == 0
+    for c in range(P.n_cells):
+        assert rel(got[c], ref[c]) <= 1e-10, (c, rel(got[c], ref[c]))
+
+
+@pytest.mark.parametrize("kind,P", PROBS, ids=IDS)
+def test_sweep_matches_oracle(kind, P):
+    u, f = vec(P, 15)
+    ref = TierB(P).sweep(u, f, 0.8)
+    with dg.DGContext(P) as ctx:
+        ut = cuda(u)
+        ctx.sweep(ut, cuda(f), omega=0.8, tol=1e-12)
+        got = host(ut)
+        st = ctx.stats()
+    assert st["n_nonconverged"] == 0
+    assert rel(got, ref) <= SWEEP_TOL
+
+
+def test_zero_defect_gives_zero_and_no_iterations():
+    P = random_problem(3, 3, 2, 3, seed=5)
+    with dg.DGContext(P) as ctx:
+        out = torch.full((P.n_dof,), 7.0, dtype=torch.float64, device="cuda")
+        ctx.local_block_solve(torch.zeros(P.n_dof, dtype=torch.float64, device="cuda"), out, 1e-12)
+        assert float(out.abs().max()) == 0.0
+        st = ctx.stats()
+        assert st["it_max"] == 0 and st["n_nonconverged"] == 0
+
+
+def test_single_cell_mesh_sweep_solves_system():
+    """1-cell mesh: D_T = A, so one sweep with omega = 1 gives A u = f to ~tol."""
+    P = random_problem(1, 1, 1, 3, seed=8, b=(0.4, -0.2, 0.1), c=True)
+    u, f = vec(P, 16)
+    with dg.DGContext(P) as ctx:
+        ut = cuda(u)
+        ctx.sweep(ut, cuda(f), 1.0, 1e-13)
+        Au = torch.empty_like(ut)
+        ctx.apply(ut, Au)
+        assert rel(host(Au), f) < 1e-10
+
+
+def test_symmetry_on_gpu():
+    P = random_problem(4, 3, 3, 3, seed=9, spread=1.0)
+    u, w = vec(P, 17)
+    with dg.DGContext(P) as ctx:
+        Au, Aw = (torch.empty(P.n_dof, dtype=torch.float64, device="cuda") for _ in range(2))
+        ctx.apply(cuda(u), Au)
+        ctx.apply(cuda(w), Aw)
+        a, b = float(host(Au) @ w), float(u @ host(Aw))
+    assert abs(a - b) <= 1e-12 * abs(a)
+
+
+def test_determinism():
+    P = random_problem(5, 4, 3, 3, seed=10, b=(0.3, 0.1, 0.0))
+    u, f = vec(P, 18)
+    with dg.DGContext(P) as ctx:
+        outs = []
+        for _ in range(2):
+            ut = cuda(u)
+            ctx.sweep(ut, cuda(f), 1.0, 1e-12)
+            outs.append(host(ut))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_c1_full_apply_and_sweep():
+    """BASELINE configs[0] at full size: every DoF against the oracle."""
+    P = make_config("C1")
+    u, f = make_vectors(P)
+    tb = TierB(P)
+    with dg.DGContext(P) as ctx:
+        ut, ft = cuda(u), cuda(f)
+        Au = torch.empty_like(ut)
+        ctx.apply(ut, Au)
+        assert rel(host(Au), tb.apply(u)) <= APPLY_TOL
+        ctx.sweep(ut, ft, 1.0, 1e-12)
+        assert rel(host(ut), tb.sweep(u, f, 1.0)) <= SWEEP_TOL
+        st = ctx.stats()
+        assert st["n_nonconverged"] == 0 and st["it_max"] > 0
+
+
+def test_c2_full_apply_separable():
+    """BASELINE configs[1] (32^3, p=3) at full size, every DoF: for a separable u the exact A u
+    is the Kronecker sum of independently assembled 1D SIPG operators (oracle/kron1d.py)."""
+    P = make_config("C2")
+    n = P.p + 1
+    rng = np.random.default_rng(0)
+    ux, uy, uz = (rng.uniform(-1, 1, k * n) for k in (P.nx, P.ny, P.nz))
+    u = to_cell_major(P, ux, uy, uz)
+    ref = separable_apply(P, ux, uy, uz)
+    with dg.DGContext(P) as ctx:
+        Au = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.apply(cuda(u), Au)
+        assert rel(host(Au), ref) <= APPLY_TOL
+
+
+SAMPLE = 24
+
+
+def sample_cells(P, seed):
+    rng = np.random.default_rng(seed)
+    N = P.n_cells
+    corners = [0, P.nx - 1, N - 1, N - P.nx, P.nx * P.ny * (P.nz // 2) + P.nx * (P.ny // 2)]
+    return sorted(set(corners) | set(rng.integers(0, N, SAMPLE).tolist()))
+
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_full_config_sampled_parity(name):
+    """Full BASELINE sizes in the bench's launch configuration: sampled cells (incl. corners)
+    of dg_apply and of one sweep against the oracle, cell by cell."""
+    P = make_config(name)
+    u, f = make_vectors(P)
+    cells = sample_cells(P, 1)
+    tb = TierB(P)
+    nd = P.nd
+    with dg.DGContext(P) as ctx:
+        ut, ft = cuda(u), cuda(f)
+        Au = torch.empty_like(ut)
+        ctx.apply(ut, Au)
+        A_h = host(Au).reshape(-1, nd)
+        ref = tb.apply_cells(u, cells)
+        assert rel(A_h[cells], ref) <= APPLY_TOL
+        ctx.sweep(ut, ft, 1.0, 1e-12)
+        S_h = host(ut).reshape(-1, nd)
+        st = ctx.stats()
+    ref = tb.sweep_cells(u, f, 1.0, cells)
+    assert rel(S_h[cells], ref) <= SWEEP_TOL
+    assert st["n_nonconverged"] == 0
+    del ut, ft, Au
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_partition_invariance_external_halo(G):
+    """z-slab decomposition: G virtual ranks on one GPU, ghost layers filled from
+    the neighbouring slabs' boundary layers, reproduce the G=1 apply and sweep bit for bit."""
+    P = random_problem(4, 3, 7, 2, seed=21, spread=1.0, b=(0.2, 0.0, 0.3), c=True)
+    u, f = vec(P, 19)
+    with dg.DGContext(P) as one:
+        ut = cuda(u)
+        ref_A = torch.empty_like(ut)
+        one.apply(ut, ref_A)
+        one.sweep(ut, cuda(f), 0.9, 1e-12)
+        ref_A, ref_S = host(ref_A), host(ut)
+    nd, nxy = P.nd, P.nx * P.ny
+    ctxs = [dg.DGContext(P, rank=r, nranks=G, halo_mode=dg.DG_HALO_EXTERNAL) for r in range(G)]
+    try:
+        parts_u = [cuda(u[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+        parts_f = [cuda(f[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+
+        def exchange():
+            for r, c in enumerate(ctxs):
+                lo = parts_u[r - 1][-nxy * nd:] if r > 0 else None
+                hi = parts_u[r + 1][:nxy * nd] if r < G - 1 else None
+                c.fill_ghosts(lo, hi)
+
+        exchange()
+        outs = []
+        for r, c in enumerate(ctxs):
+            o = torch.empty_like(parts_u[r])
+            c.apply(parts_u[r], o)
+            outs.append(host(o))
+        assert np.array_equal(np.concatenate(outs), ref_A)
+        exchange()
+        torch.cuda.synchronize()
+        for r, c in enumerate(ctxs):
+            c.sweep(parts_u[r], parts_f[r], 0.9, 1e-12)
+        got = np.concatenate([host(x) for x in parts_u])
+        assert np.array_equal(got, ref_S)
+    finally:
+        for c in ctxs:
+            c.close()
