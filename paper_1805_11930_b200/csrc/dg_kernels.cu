@@ -28,8 +28,9 @@ namespace dg {
 namespace {
 
 struct DevTab {
-  double A[64], D[64], M[64];
+  double A[64], D[64], M[64], G[64];
   double w[8], d0[8], d1[8], Sd[8], Cd[8], Md[8];
+  double E0[8], E1[8], F0[8], F1[8];  // A^-T e0, A^-T e1, A^-T d0, A^-T d1 (trace/derivative at 0/1 from Gauss values)
 };
 __constant__ DevTab c_tab[kMaxN + 1];
 
@@ -129,27 +130,24 @@ template <int N> __device__ __forceinline__ void dir_term(const double* U, doubl
 }
 
 // ---- group setup: coefficients, face parameters, neighbour pointers ------------
-template <int N>
-__device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const double* u) {
-  using G = Geo<N>;
-  constexpr int C = G::C;
+// Per cell of the group: volume scalings vc, face coefficients fc, neighbour pointers nb
+// (nullptr when u == nullptr, i.e. for D_T-only operators). Ends with __syncthreads.
+template <int N, int C, int NT>
+__device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6][6],
+                            const double* (*nb_)[6], int* cellv, int cell0, const double* u) {
+  constexpr int N3 = N * N * N;
   const int t = threadIdx.x;
-  if (t < N) {
-    g.tw[t] = c_tab[N].w[t];
-    g.td0[t] = c_tab[N].d0[t];
-    g.td1[t] = c_tab[N].d1[t];
-  }
   const int nxy = kp.nx * kp.ny;
   const double vol = kp.h[0] * kp.h[1] * kp.h[2];
-  for (int it = t; it < C * 6; it += G::NT) {
+  for (int it = t; it < C * 6; it += NT) {
     const int cs = it / 6, f = it % 6, axis = f >> 1, hi = f & 1;
     const int cell = cell0 + cs;
     const bool valid = cell < kp.ncells;
     double co[6] = {0, 0, 0, 0, 0, 0};
     const double* nbp = nullptr;
     if (f == 0) {
-      g.cell[cs] = valid ? cell : -1;
-      double* vc = g.vc[cs];
+      if (cellv) cellv[cs] = valid ? cell : -1;
+      double* vc = vc_[cs];
       if (valid && (kp.mask & 1u)) {
         const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
         vc[0] = vol * Kc[0] / (kp.h[0] * kp.h[0]);
@@ -173,14 +171,14 @@ __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const dou
         kind = 0;
         const long nb = cell + (hi ? dstep[axis] : -dstep[axis]);
         kidx = nb + nxy;
-        if (u) nbp = u + (size_t)nb * G::N3;
+        if (u) nbp = u + (size_t)nb * N3;
       } else {
         const int sk = kp.slab_face[f];
         if (sk == FK_GHOST) {
           kind = 0;
           const int col = coord[0] + kp.nx * coord[1];
           kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
-          if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * G::N3;
+          if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * N3;
         } else {
           kind = (sk == FK_DIRICHLET) ? 1 : 2;
         }
@@ -208,10 +206,22 @@ __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const dou
       if (kind != 0) nbp = nullptr;
     }
 #pragma unroll
-    for (int e = 0; e < 6; ++e) g.fc[cs][f][e] = co[e];
-    g.nb[cs][f] = nbp;
+    for (int e = 0; e < 6; ++e) fc_[cs][f][e] = co[e];
+    nb_[cs][f] = nbp;
   }
   __syncthreads();
+}
+
+template <int N>
+__device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const double* u) {
+  using G = Geo<N>;
+  const int t = threadIdx.x;
+  if (t < N) {
+    g.tw[t] = c_tab[N].w[t];
+    g.td0[t] = c_tab[N].d0[t];
+    g.td1[t] = c_tab[N].d1[t];
+  }
+  setup_cells<N, G::C, G::NT>(kp, g.vc, g.fc, g.nb, g.cell, cell0, u);
 }
 
 // ---- tiles ---------------------------------------------------------------------
@@ -923,6 +933,12 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] ? g.its[tid] : (g.its[tid] | (1 << 30));
 }
 
+}  // namespace
+
+#include "dg_plane.cuh"
+
+namespace {
+
 // ---- host-side launch helpers ------------------------------------------------------
 template <int N> constexpr size_t smem_bytes(int tensors) {
   return sizeof(double) * ((size_t)tensors * Geo<N>::TENSOR + Geo<N>::FACE);
@@ -939,25 +955,46 @@ cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, c
 
 template <int N>
 cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
-  using G = Geo<N>;
-  const int grid = (kp.ncells + G::C - 1) / G::C;
-  if (grid == 0) return cudaSuccess;
-  const size_t smem = smem_bytes<N>(3);
-  cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
-  return cudaGetLastError();
+  if constexpr (N <= 5) {
+    using G = pk::Geo<N>;
+    const int grid = (kp.ncells + G::C - 1) / G::C;
+    if (grid == 0) return cudaSuccess;
+    const size_t smem = pk::smem_apply<N>();
+    auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, G::NT, smem, s>>>(kp, u, out);
+    return cudaGetLastError();
+  } else {
+    using G = Geo<N>;
+    const int grid = (kp.ncells + G::C - 1) / G::C;
+    if (grid == 0) return cudaSuccess;
+    const size_t smem = smem_bytes<N>(3);
+    cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
+    return cudaGetLastError();
+  }
 }
 
 template <int N, bool SWEEP>
 cudaError_t solve_n(int method, const KParams& kp, const double* in, const double* f, double* out,
                     cudaStream_t s) {
-  using G = Geo<N>;
-  const int grid = (kp.ncells + G::C - 1) / G::C;
-  if (grid == 0) return cudaSuccess;
-  if (method == LM_BICGSTAB)
-    return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
-  return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
+  if constexpr (N <= 5) {
+    using G = pk::Geo<N>;
+    const int grid = (kp.ncells + G::C - 1) / G::C;
+    if (grid == 0) return cudaSuccess;
+    if (method == LM_BICGSTAB)
+      return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+    return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
+  } else {
+    using G = Geo<N>;
+    const int grid = (kp.ncells + G::C - 1) / G::C;
+    if (grid == 0) return cudaSuccess;
+    if (method == LM_BICGSTAB)
+      return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
+    return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
+  }
 }
 
 #define DG_DISPATCH(p, CALL)             \
@@ -997,10 +1034,11 @@ cudaError_t launch_dfma_bench(double* sink, int blocks, int iters, cudaStream_t 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
   DevTab d{};
   const int n = t.n;
-  for (int i = 0; i < n * n; ++i) { d.A[i] = t.A[i]; d.D[i] = t.D[i]; d.M[i] = t.M[i]; }
+  for (int i = 0; i < n * n; ++i) { d.A[i] = t.A[i]; d.D[i] = t.D[i]; d.M[i] = t.M[i]; d.G[i] = t.G[i]; }
   for (int i = 0; i < n; ++i) {
     d.w[i] = t.wq[i]; d.d0[i] = t.d0[i]; d.d1[i] = t.d1[i];
     d.Sd[i] = t.Sdiag[i]; d.Cd[i] = t.Cdiag[i]; d.Md[i] = t.Mdiag[i];
+    d.E0[i] = t.E0[i]; d.E1[i] = t.E1[i]; d.F0[i] = t.F0[i]; d.F1[i] = t.F1[i];
   }
   *err = cudaMemcpyToSymbol(c_tab, &d, sizeof(DevTab), sizeof(DevTab) * (p + 1));
   return *err == cudaSuccess;

@@ -1,0 +1,977 @@
+// Plane-per-thread fp64 kernels for n = p+1 <= 5 (included by dg_kernels.cu).
+//
+// Each cell is owned by n consecutive lanes of one warp; lane t holds one n x n plane of
+// the cell in registers, so two of the three 1D contractions of every sum-factorisation
+// stage run in registers and only the third goes through shared memory. One operator
+// application (A or D_T) is three register phases separated by two transposes:
+//
+//   Q1 (lane = z node k, plane (j,i)):  a = A_x u;  t2 = A_y a;  t2y = G_y a     (Stage 1)
+//        y-face traces of the nodal plane -> S/T arrays, interpolated along x
+//   Q2 (lane = y Gauss point qy, plane (qz,qx)):  U = A_z t2, Uy = A_z t2y;
+//        Stage 2 at the Gauss points; x- and z-direction terms D^T(W(K D U - b U));
+//        x- and z-face traces straight from the Gauss values (E/F end-point vectors),
+//        face fluxes injected back through A^-T (so the later A^T contractions give the
+//        tangential face mass); then A_z^T on R and on F_y                     (Stage 3, part)
+//   Q3 (lane = z node k, plane (qy,qx)):  V' = A_y^T R + G_y^T F_y;  y-face terms with the
+//        z face mass;  V = A_x^T V'                                              (Stage 3)
+//
+// The output plane has the same ownership as the input plane, so the per-cell Krylov
+// vectors of the local solves stay in registers; dot products are n-lane shuffles.
+// Neighbour traces (A only) are staged tile by tile through shared memory with coalesced
+// loads in a prologue and enter Q1/Q2 as extra face arrays.
+
+namespace pk {
+
+template <int N> struct PL;
+template <> struct PL<2> { static constexpr int WARPS = 4, KS = 5, CTB = 22; };
+template <> struct PL<3> { static constexpr int WARPS = 4, KS = 19, CTB = 121; };
+template <> struct PL<4> { static constexpr int WARPS = 4, KS = 20, CTB = 161; };
+template <> struct PL<5> { static constexpr int WARPS = 2, KS = 25, CTB = 253; };
+
+template <int N_> struct Geo {
+  static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
+  static constexpr int CPW = 32 / N, WARPS = PL<N>::WARPS, C = CPW * WARPS, NT = 32 * WARPS;
+  static constexpr int KS = PL<N>::KS, ARR = N * KS, CTB = PL<N>::CTB;
+  static constexpr int FS = 4 * N2 + 1;   // per-cell stride of a block of 4 face arrays
+  static constexpr int PS = (N3 > 4 * N2 ? N3 : 4 * N2) + 1;  // per-cell plane storage (X, Dg, ...)
+  // dynamic shared memory (doubles)
+  static constexpr int TB = C * CTB;      // transposes / tile staging
+  static constexpr int FY = C * FS;       // y-face arrays (k, qx)
+  static constexpr int FX = C * FS;       // x-neighbour arrays (k, qy)
+  static constexpr int FZ = C * FS;       // z-neighbour arrays (j, qx)
+};
+
+template <int N> struct Cells {
+  static constexpr int C = Geo<N>::C;
+  double vc[C][4];
+  double fc[C][6][6];
+  const double* nb[C][6];
+  int cell[C];
+};
+
+// per-lane identity
+struct Lane {
+  int lane, cs, t;
+  bool active;
+};
+template <int N> __device__ __forceinline__ Lane lane_id() {
+  using G = Geo<N>;
+  Lane L;
+  L.lane = threadIdx.x & 31;
+  L.active = L.lane < G::CPW * N;
+  L.cs = (threadIdx.x >> 5) * G::CPW + (L.active ? L.lane / N : 0);
+  L.t = L.lane % N;
+  return L;
+}
+
+// sum over the n lanes of the cell (identical order, hence identical result, in every lane)
+template <int N> __device__ __forceinline__ double cell_sum(double v, int lane) {
+  const int base = (lane / N) * N;
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) s += __shfl_sync(0xffffffffu, v, base + m);
+  return s;
+}
+
+template <int N> __device__ __forceinline__ double T_A(int i) { return c_tab[N].A[i]; }
+template <int N> __device__ __forceinline__ double T_G(int i) { return c_tab[N].G[i]; }
+template <int N> __device__ __forceinline__ double T_D(int i) { return c_tab[N].D[i]; }
+template <int N> __device__ __forceinline__ double T_W(int i) { return c_tab[N].w[i]; }
+
+// runtime-indexed rows held in registers
+template <int N> struct Rows {
+  double wt;        // w[t]
+  double Arow[N];   // A[t][.]
+  double Mrow[N];   // Mhat[t][.]
+  double Md, Sd, Cd;
+  double d0t, d1t;  // d0[t], d1[t]
+};
+template <int N> __device__ __forceinline__ void load_rows(Rows<N>& r, int t) {
+  r.wt = c_tab[N].w[t];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    r.Arow[j] = c_tab[N].A[t * N + j];
+    r.Mrow[j] = c_tab[N].M[t * N + j];
+  }
+  r.Md = c_tab[N].Md[t];
+  r.Sd = c_tab[N].Sd[t];
+  r.Cd = c_tab[N].Cd[t];
+  r.d0t = c_tab[N].d0[t];
+  r.d1t = c_tab[N].d1[t];
+}
+
+struct Scal {
+  double h[3], ih[3], sb[3];
+};
+__device__ __forceinline__ Scal make_scal(const KParams& kp) {
+  Scal s;
+  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    s.h[a] = kp.h[a];
+    s.ih[a] = 1.0 / kp.h[a];
+    s.sb[a] = T3 * kp.b[a] / kp.h[a];
+  }
+  return s;
+}
+
+// ---- coalesced tile staging: C cells x n^3 (contiguous in global) -> TB layout ---------
+// element (k, j, i) of cell slot cs at cs*CTB + k*KS + j*N + i
+template <int N>
+__device__ __forceinline__ void stage_tile(double* TB, const double* __restrict__ src, int nvalid) {
+  using G = Geo<N>;
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = (cs < nvalid) ? src[e] : 0.0;
+  }
+}
+// neighbour tile: per-cell base pointers (nullptr -> zeros)
+template <int N>
+__device__ __forceinline__ void stage_nbr(double* TB, const Cells<N>& cl, int f) {
+  using G = Geo<N>;
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    const double* p = cl.nb[cs][f];
+    TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = p ? p[r] : 0.0;
+  }
+}
+template <int N>
+__device__ __forceinline__ void unstage_tile(const double* TB, double* __restrict__ dst, int nvalid) {
+  using G = Geo<N>;
+  for (int e = threadIdx.x; e < nvalid * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    dst[e] = TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)];
+  }
+}
+template <int N>
+__device__ __forceinline__ void read_plane(const double* TB, const Lane& L, double (&p)[N][N]) {
+  using G = Geo<N>;
+  const double* b = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) p[j][i] = b[j * N + i];
+}
+template <int N>
+__device__ __forceinline__ void write_plane(double* TB, const Lane& L, const double (&p)[N][N]) {
+  using G = Geo<N>;
+  double* b = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[j * N + i] = p[j][i];
+}
+
+// ---- neighbour prologue: traces of the 6 face neighbours -> FY (nodal), FX, FZ ----------
+// Must be called by all threads; leaves TB free. Face order f = 2*axis + hi.
+template <int N>
+__device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, double* TB,
+                             double* FY, double* FX, double* FZ) {
+  using G = Geo<N>;
+  const int k = L.t;
+  for (int f = 0; f < 6; ++f) {
+    __syncthreads();
+    stage_nbr<N>(TB, cl, f);
+    __syncthreads();
+    if (!L.active) continue;
+    const double* c = cl.fc[L.cs][f];
+    const double cna = c[2], cng = c[3], ctn = c[5];
+    const int axis = f >> 1, hi = f & 1;
+    const double* nb = TB + L.cs * G::CTB;   // neighbour cell, layout k*KS + j*N + i
+    if (axis == 0) {
+      // lane k: rows j of the neighbour's plane k; lo face sees the neighbour's x=1 end
+      double S[N], T[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double row[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) row[i] = nb[k * G::KS + j * N + i];
+        double g = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) g = fma(hi ? c_tab[N].d0[i] : c_tab[N].d1[i], row[i], g);
+        const double a = hi ? row[0] : row[N - 1];
+        S[j] = cna * a + cng * g * sc.ih[0];
+        T[j] = ctn * a;
+      }
+      // interpolate along y: (k, qy)
+      double* fx = FX + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double s = 0.0, tt = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          s = fma(T_A<N>(q * N + j), S[j], s);
+          tt = fma(T_A<N>(q * N + j), T[j], tt);
+        }
+        fx[q] = s;
+        fx[G::N2 + q] = tt;
+      }
+    } else if (axis == 1) {
+      // lane k: columns i of the neighbour's plane k (nodal in i; interpolated in Q1)
+      double* fy = FY + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double g = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+          g = fma(hi ? c_tab[N].d0[j] : c_tab[N].d1[j], nb[k * G::KS + j * N + i], g);
+        const double a = nb[k * G::KS + (hi ? 0 : N - 1) * N + i];
+        fy[i] = cna * a + cng * g * sc.ih[1];
+        fy[G::N2 + i] = ctn * a;
+      }
+    } else {
+      // lane t = y node j: the neighbour's z-lines (kk, i) at fixed j
+      const int j = L.t;
+      double S[N], T[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double g = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk)
+          g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
+        const double a = nb[(hi ? 0 : N - 1) * G::KS + j * N + i];
+        S[i] = cna * a + cng * g * sc.ih[2];
+        T[i] = ctn * a;
+      }
+      double* fz = FZ + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + j * N;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        double s = 0.0, tt = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          s = fma(T_A<N>(q * N + i), S[i], s);
+          tt = fma(T_A<N>(q * N + i), T[i], tt);
+        }
+        fz[q] = s;
+        fz[G::N2 + q] = tt;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---- the operator: out = A u (NBR) or D_T u (self faces only) on the lane's plane ---------
+// All threads must call it (two __syncthreads inside). TB must be free on entry.
+template <int N, bool NBR>
+__device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, const Rows<N>& rw,
+                                         const Scal& sc, bool vol, const double (&in)[N][N],
+                                         double (&out)[N][N], double* TB, double* FY,
+                                         const double* FX, const double* FZ) {
+  using G = Geo<N>;
+  double* tb = TB + L.cs * G::CTB;
+  double* fy = FY + L.cs * G::FS;
+  const double* fc = &cl.fc[L.cs][0][0];
+  // ---------------- Q1: lane = z node k ----------------
+  if (L.active) {
+    const int k = L.t;
+    {  // t2 is needed for the face traces even without the volume terms; t2y only with them
+      double a[N][N];
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double s = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) s = fma(T_A<N>(q * N + i), in[j][i], s);
+          a[j][q] = s;
+        }
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx)
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) {
+          double s = 0.0, sy = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            s = fma(T_A<N>(qy * N + j), a[j][qx], s);
+            sy = fma(T_G<N>(qy * N + j), a[j][qx], sy);
+          }
+          tb[k * G::KS + qy * N + qx] = s;
+          if (vol) tb[G::ARR + k * G::KS + qy * N + qx] = sy;
+        }
+    }
+    // y faces (normal y, tangential z = lane, x): nodal S/T combos, then A_x
+    const double* clo = fc + 2 * 6;
+    const double* chi = fc + 3 * 6;
+    double X0[N], X1[N], X2[N], X3[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double glo = 0.0, ghi = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        glo = fma(c_tab[N].d0[j], in[j][i], glo);
+        ghi = fma(c_tab[N].d1[j], in[j][i], ghi);
+      }
+      const double alo = in[0][i], ahi = in[N - 1][i];
+      X0[i] = clo[0] * alo + clo[1] * glo * sc.ih[1];
+      X1[i] = clo[4] * alo;
+      X2[i] = chi[0] * ahi + chi[1] * ghi * sc.ih[1];
+      X3[i] = chi[4] * ahi;
+      if (NBR) {
+        X0[i] += fy[0 * G::N2 + k * N + i];
+        X1[i] += fy[1 * G::N2 + k * N + i];
+        X2[i] += fy[2 * G::N2 + k * N + i];
+        X3[i] += fy[3 * G::N2 + k * N + i];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double A = T_A<N>(q * N + i);
+        s0 = fma(A, X0[i], s0);
+        s1 = fma(A, X1[i], s1);
+        s2 = fma(A, X2[i], s2);
+        s3 = fma(A, X3[i], s3);
+      }
+      fy[0 * G::N2 + k * N + q] = s0;
+      fy[1 * G::N2 + k * N + q] = s1;
+      fy[2 * G::N2 + k * N + q] = s2;
+      fy[3 * G::N2 + k * N + q] = s3;
+    }
+  }
+  __syncthreads();
+  // ---------------- Q2: lane = y Gauss point qy ----------------
+  if (L.active) {
+    const int qy = L.t;
+    const double* vcell = cl.vc[L.cs];
+    double U[N][N], R[N][N], Fy[N][N];   // [qz][qx]
+    if (vol) {
+      // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double c0[N], c1[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          c0[k] = tb[k * G::KS + qy * N + qx];
+          c1[k] = tb[G::ARR + k * G::KS + qy * N + qx];
+        }
+#pragma unroll
+        for (int qz = 0; qz < N; ++qz) {
+          double s = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            s = fma(T_A<N>(qz * N + k), c0[k], s);
+            s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
+          }
+          const double W = rw.wt * T_W<N>(qz) * T_W<N>(qx);
+          U[qz][qx] = s;
+          R[qz][qx] = W * vcell[3] * s;
+          Fy[qz][qx] = W * fma(vcell[1], s1, -sc.sb[1] * s);
+        }
+      }
+      // x direction: rows qz
+#pragma unroll
+      for (int qz = 0; qz < N; ++qz) {
+        double F[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double du = 0.0;
+#pragma unroll
+          for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[qz][r], du);
+          F[q] = rw.wt * T_W<N>(qz) * T_W<N>(q) * fma(vcell[0], du, -sc.sb[0] * U[qz][q]);
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          double s = R[qz][r];
+#pragma unroll
+          for (int q = 0; q < N; ++q) s = fma(T_D<N>(q * N + r), F[q], s);
+          R[qz][r] = s;
+        }
+      }
+      // z direction: columns qx
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double F[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double du = 0.0;
+#pragma unroll
+          for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[r][qx], du);
+          F[q] = rw.wt * T_W<N>(q) * T_W<N>(qx) * fma(vcell[2], du, -sc.sb[2] * U[q][qx]);
+        }
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          double s = R[r][qx];
+#pragma unroll
+          for (int q = 0; q < N; ++q) s = fma(T_D<N>(q * N + r), F[q], s);
+          R[r][qx] = s;
+        }
+      }
+    } else {
+      // faces only: U still needed for the traces
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double c0[N];
+#pragma unroll
+        for (int k = 0; k < N; ++k) c0[k] = tb[k * G::KS + qy * N + qx];
+#pragma unroll
+        for (int qz = 0; qz < N; ++qz) {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) s = fma(T_A<N>(qz * N + k), c0[k], s);
+          U[qz][qx] = s;
+          R[qz][qx] = 0.0;
+          Fy[qz][qx] = 0.0;
+        }
+      }
+    }
+    // x faces at the face Gauss points (qz, qy): traces from the x-rows of U
+    {
+      const double* clo = fc + 0 * 6;
+      const double* chi = fc + 1 * 6;
+      const double* fx = FX + L.cs * G::FS;
+#pragma unroll
+      for (int qz = 0; qz < N; ++qz) {
+        double alo = 0.0, ahi = 0.0, glo = 0.0, ghi = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          alo = fma(c_tab[N].E0[q], U[qz][q], alo);
+          ahi = fma(c_tab[N].E1[q], U[qz][q], ahi);
+          glo = fma(c_tab[N].F0[q], U[qz][q], glo);
+          ghi = fma(c_tab[N].F1[q], U[qz][q], ghi);
+        }
+        double Slo = clo[0] * alo + clo[1] * glo * sc.ih[0], Tlo = clo[4] * alo;
+        double Shi = chi[0] * ahi + chi[1] * ghi * sc.ih[0], Thi = chi[4] * ahi;
+        if (NBR) {  // neighbour traces at (k, qy) -> interpolate in z
+          double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            const double A = T_A<N>(qz * N + k);
+            n0 = fma(A, fx[0 * G::N2 + k * N + qy], n0);
+            n1 = fma(A, fx[1 * G::N2 + k * N + qy], n1);
+            n2 = fma(A, fx[2 * G::N2 + k * N + qy], n2);
+            n3 = fma(A, fx[3 * G::N2 + k * N + qy], n3);
+          }
+          Slo += n0; Tlo += n1; Shi += n2; Thi += n3;
+        }
+        const double Wf = rw.wt * T_W<N>(qz) * sc.h[1] * sc.h[2];
+        Slo *= Wf; Tlo *= Wf; Shi *= Wf; Thi *= Wf;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          R[qz][q] += c_tab[N].E0[q] * Slo + c_tab[N].F0[q] * Tlo + c_tab[N].E1[q] * Shi +
+                      c_tab[N].F1[q] * Thi;
+      }
+    }
+    // z faces at the face Gauss points (qy, qx): traces from the z-columns of U
+    {
+      const double* clo = fc + 4 * 6;
+      const double* chi = fc + 5 * 6;
+      const double* fz = FZ + L.cs * G::FS;
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double alo = 0.0, ahi = 0.0, glo = 0.0, ghi = 0.0;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          alo = fma(c_tab[N].E0[q], U[q][qx], alo);
+          ahi = fma(c_tab[N].E1[q], U[q][qx], ahi);
+          glo = fma(c_tab[N].F0[q], U[q][qx], glo);
+          ghi = fma(c_tab[N].F1[q], U[q][qx], ghi);
+        }
+        double Slo = clo[0] * alo + clo[1] * glo * sc.ih[2], Tlo = clo[4] * alo;
+        double Shi = chi[0] * ahi + chi[1] * ghi * sc.ih[2], Thi = chi[4] * ahi;
+        if (NBR) {  // neighbour traces at (j, qx) -> interpolate in y (row qy of A)
+          double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            const double A = rw.Arow[j];
+            n0 = fma(A, fz[0 * G::N2 + j * N + qx], n0);
+            n1 = fma(A, fz[1 * G::N2 + j * N + qx], n1);
+            n2 = fma(A, fz[2 * G::N2 + j * N + qx], n2);
+            n3 = fma(A, fz[3 * G::N2 + j * N + qx], n3);
+          }
+          Slo += n0; Tlo += n1; Shi += n2; Thi += n3;
+        }
+        const double Wf = rw.wt * T_W<N>(qx) * sc.h[0] * sc.h[1];
+        Slo *= Wf; Tlo *= Wf; Shi *= Wf; Thi *= Wf;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          R[q][qx] += c_tab[N].E0[q] * Slo + c_tab[N].F0[q] * Tlo + c_tab[N].E1[q] * Shi +
+                      c_tab[N].F1[q] * Thi;
+      }
+    }
+    // A_z^T on R and F_y, stored in place of t2 / t2y (same index set (., qy, .))
+#pragma unroll
+    for (int qx = 0; qx < N; ++qx)
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
+        double s = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int qz = 0; qz < N; ++qz) {
+          s = fma(T_A<N>(qz * N + k), R[qz][qx], s);
+          s1 = fma(T_A<N>(qz * N + k), Fy[qz][qx], s1);
+        }
+        tb[k * G::KS + qy * N + qx] = s;
+        tb[G::ARR + k * G::KS + qy * N + qx] = s1;
+      }
+  }
+  __syncthreads();
+  // ---------------- Q3: lane = z node k ----------------
+  if (L.active) {
+    const int k = L.t;
+    double Vq[N][N];   // [j][qx]
+#pragma unroll
+    for (int qx = 0; qx < N; ++qx) {
+      double r[N], f[N];
+#pragma unroll
+      for (int qy = 0; qy < N; ++qy) {
+        r[qy] = tb[k * G::KS + qy * N + qx];
+        f[qy] = tb[G::ARR + k * G::KS + qy * N + qx];
+      }
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int qy = 0; qy < N; ++qy) {
+          s = fma(T_A<N>(qy * N + j), r[qy], s);
+          s = fma(T_G<N>(qy * N + j), f[qy], s);
+        }
+        Vq[j][qx] = s;
+      }
+    }
+    // y faces: z face mass (row k of Mhat) on the (k', qx) arrays, x weights, end profiles in j
+    {
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) {
+          const double M = rw.Mrow[kk];
+          z0 = fma(M, fy[0 * G::N2 + kk * N + qx], z0);
+          z1 = fma(M, fy[1 * G::N2 + kk * N + qx], z1);
+          z2 = fma(M, fy[2 * G::N2 + kk * N + qx], z2);
+          z3 = fma(M, fy[3 * G::N2 + kk * N + qx], z3);
+        }
+        const double Wf = T_W<N>(qx) * sc.h[0] * sc.h[2];
+        z0 *= Wf; z1 *= Wf; z2 *= Wf; z3 *= Wf;
+        Vq[0][qx] += z0;
+        Vq[N - 1][qx] += z2;
+#pragma unroll
+        for (int j = 0; j < N; ++j) Vq[j][qx] += c_tab[N].d0[j] * z1 + c_tab[N].d1[j] * z3;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx) s = fma(T_A<N>(qx * N + i), Vq[j][qx], s);
+        out[j][i] = s;
+      }
+  }
+}
+
+// diag(D_T) on the lane's plane (Jacobi preconditioner), from 1D diagonals
+template <int N>
+__device__ __forceinline__ void plane_diag(const Cells<N>& cl, const Lane& L, const Rows<N>& rw,
+                                           const Scal& sc, double (&dg)[N][N]) {
+  const double* vc = cl.vc[L.cs];
+  const double* fc = &cl.fc[L.cs][0][0];
+  const int k = L.t;
+  const double area[3] = {sc.h[1] * sc.h[2], sc.h[0] * sc.h[2], sc.h[0] * sc.h[1]};
+  const double dd0 = c_tab[N].d0[0], dd1 = c_tab[N].d1[N - 1];
+  auto fd = [&](int f, double dd, double ih) {
+    const double* c = fc + f * 6;
+    return c[0] + c[1] * dd * ih + c[4] * dd;
+  };
+  const double zlo = (k == 0) ? fd(4, dd0, sc.ih[2]) : 0.0;
+  const double zhi = (k == N - 1) ? fd(5, dd1, sc.ih[2]) : 0.0;
+  const double xlo = fd(0, dd0, sc.ih[0]), xhi = fd(1, dd1, sc.ih[0]);
+  const double ylo = fd(2, dd0, sc.ih[1]), yhi = fd(3, dd1, sc.ih[1]);
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double Mi = c_tab[N].Md[i], Mj = c_tab[N].Md[j], Mk = rw.Md;
+      double d = vc[3] * Mi * Mj * Mk;
+      d += (vc[0] * c_tab[N].Sd[i] - sc.sb[0] * c_tab[N].Cd[i]) * Mj * Mk;
+      d += (vc[1] * c_tab[N].Sd[j] - sc.sb[1] * c_tab[N].Cd[j]) * Mi * Mk;
+      d += (vc[2] * rw.Sd - sc.sb[2] * rw.Cd) * Mi * Mj;
+      if (i == 0) d += area[0] * Mj * Mk * xlo;
+      if (i == N - 1) d += area[0] * Mj * Mk * xhi;
+      if (j == 0) d += area[1] * Mi * Mk * ylo;
+      if (j == N - 1) d += area[1] * Mi * Mk * yhi;
+      d += area[2] * Mi * Mj * (zlo + zhi);
+      dg[j][i] = d;
+    }
+}
+
+// =============================== kernels ================================================
+template <int N>
+__device__ __forceinline__ void setup(const KParams& kp, Cells<N>& cl, int cell0, const double* u) {
+  using G = Geo<N>;
+  setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.fc, cl.nb, cl.cell, cell0, u);
+}
+
+// out = A u (with_nbr) or D_T u, selected parts by kp.mask
+template <int N, bool NBR>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  __shared__ Cells<N> cl;
+  double* TB = sm;
+  double* FY = TB + G::TB;
+  double* FX = FY + G::FY;
+  double* FZ = FX + G::FX;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(G::C, kp.ncells - cell0);
+  const Lane L = lane_id<N>();
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  const Scal sc = make_scal(kp);
+  stage_tile<N>(TB, u + (size_t)cell0 * G::N3, nvalid);
+  setup<N>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
+  double in[N][N], o[N][N];
+  read_plane<N>(TB, L, in);
+  if (NBR) nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);  // starts and ends with a barrier
+  else __syncthreads();
+  plane_op<N, NBR>(cl, L, rw, sc, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
+  if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
+  __syncthreads();
+  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+}
+
+// Jacobi-PCG per cell; SWEEP: defect d = f - A u first, result u + omega du.
+// Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+     double* __restrict__ out) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  __shared__ Cells<N> cl;
+  double* TB = sm;
+  double* FY = TB + G::TB;
+  double* XS = FY + G::FY;          // FX / FZ (defect prologue only) alias XS / DS
+  double* DS = XS + G::C * G::PS;
+  double* FX = XS;
+  double* FZ = DS;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(G::C, kp.ncells - cell0);
+  const Lane L = lane_id<N>();
+  const bool valid = L.active && L.cs < nvalid;
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  const Scal sc = make_scal(kp);
+  KParams kq = kp;
+  kq.mask = 7u;
+  stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  setup<N>(kq, cl, cell0, SWEEP ? in : nullptr);
+  double R[N][N], P[N][N];
+  read_plane<N>(TB, L, P);
+  if (SWEEP) {
+    double Q[N][N];
+    nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);
+    plane_op<N, true>(cl, L, rw, sc, true, P, Q, TB, FY, FX, FZ);   // Q = A u
+    __syncthreads();
+    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    __syncthreads();
+    read_plane<N>(TB, L, R);
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? R[j][i] - Q[j][i] : 0.0;
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? P[j][i] : 0.0;
+  }
+  const int po = L.cs * G::PS + L.t * G::N2;
+  double* xs = XS + po;
+  double* ds = DS + po;
+  __syncthreads();   // the prologue's FX / FZ (aliasing XS / DS) are consumed
+  {
+    double dg[N][N];
+    plane_diag<N>(cl, L, rw, sc, dg);
+    if (L.active)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) ds[j * N + i] = valid ? dg[j][i] : 1.0;
+  }
+  double rr = 0.0, rz = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double z = L.active ? R[j][i] / ds[j * N + i] : 0.0;
+      P[j][i] = z;
+      rr = fma(R[j][i], R[j][i], rr);
+      rz = fma(R[j][i], z, rz);
+      if (L.active) xs[j * N + i] = 0.0;
+    }
+  const double rr0 = cell_sum<N>(rr, L.lane);
+  rz = cell_sum<N>(rz, L.lane);
+  bool conv = !valid || rr0 == 0.0;
+  int its = 0;
+  for (int iter = 0;; ++iter) {
+    const int done = __syncthreads_and(conv || !L.active);
+    if (done || iter >= kp.max_it) break;
+    double Q[N][N];
+    plane_op<N, false>(cl, L, rw, sc, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+    double pq = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) pq = fma(P[j][i], Q[j][i], pq);
+    pq = cell_sum<N>(pq, L.lane);
+    double alpha = 0.0;
+    if (!conv) {
+      if (pq > 0.0) alpha = rz / pq;
+      else conv = true;
+    }
+    double r2 = 0.0, rzn = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
+        R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
+        r2 = fma(R[j][i], R[j][i], r2);
+        if (L.active) rzn = fma(R[j][i], R[j][i] / ds[j * N + i], rzn);
+      }
+    r2 = cell_sum<N>(r2, L.lane);
+    rzn = cell_sum<N>(rzn, L.lane);
+    if (!conv) {
+      ++its;
+      if (r2 <= kp.tol2 * rr0) conv = true;
+      const double beta = rzn / rz;
+      rz = rzn;
+      if (!conv && L.active) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] / ds[j * N + i]);
+      }
+    }
+  }
+  // result: X (+ u) -> TB -> global
+  __syncthreads();
+  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  __syncthreads();
+  if (L.active) {
+    double* b = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        b[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], b[j * N + i]) : xs[j * N + i];
+  }
+  __syncthreads();
+  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
+}
+
+// Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks).
+// Registers: r and the operator input/output planes; shared: x, r^, p, v, diag planes.
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+           double* __restrict__ out) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  __shared__ Cells<N> cl;
+  double* TB = sm;
+  double* FY = TB + G::TB;
+  double* XS = FY + G::FY;          // FX / FZ (defect prologue only) alias XS / RHS
+  double* RHS = XS + G::C * G::PS;
+  double* PSM = RHS + G::C * G::PS;
+  double* VSM = PSM + G::C * G::PS;
+  double* DS = VSM + G::C * G::PS;
+  double* FX = XS;
+  double* FZ = RHS;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(G::C, kp.ncells - cell0);
+  const Lane L = lane_id<N>();
+  const bool valid = L.active && L.cs < nvalid;
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  const Scal sc = make_scal(kp);
+  KParams kq = kp;
+  kq.mask = 7u;
+  stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  setup<N>(kq, cl, cell0, SWEEP ? in : nullptr);
+  double R[N][N], W[N][N];
+  read_plane<N>(TB, L, W);
+  if (SWEEP) {
+    double T[N][N];
+    nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);
+    plane_op<N, true>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);
+    __syncthreads();
+    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    __syncthreads();
+    read_plane<N>(TB, L, R);
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? R[j][i] - T[j][i] : 0.0;
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? W[j][i] : 0.0;
+  }
+  const int po = L.cs * G::PS + L.t * G::N2;
+  double* xs = XS + po;
+  double* rh = RHS + po;
+  double* ps = PSM + po;
+  double* vs = VSM + po;
+  double* ds = DS + po;
+  __syncthreads();   // the prologue's FX / FZ (aliasing XS / RHS) are consumed
+  {
+    double dg[N][N];
+    plane_diag<N>(cl, L, rw, sc, dg);
+    if (L.active)
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) ds[j * N + i] = valid ? dg[j][i] : 1.0;
+  }
+  double rr = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      rr = fma(R[j][i], R[j][i], rr);
+      if (L.active) {
+        xs[j * N + i] = 0.0;
+        rh[j * N + i] = R[j][i];
+        ps[j * N + i] = 0.0;
+        vs[j * N + i] = 0.0;
+      }
+    }
+  const double rr0 = cell_sum<N>(rr, L.lane);
+  bool conv = !valid || rr0 == 0.0;
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  bool rst = false;
+  int its = 0;
+  for (int iter = 0;; ++iter) {
+    const int done = __syncthreads_and(conv || !L.active);
+    if (done || iter >= kp.max_it) break;
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (L.active) a = fma(rh[j * N + i], R[j][i], a);
+        b = fma(R[j][i], R[j][i], b);
+      }
+    double rhon = cell_sum<N>(a, L.lane);
+    const double r2 = cell_sum<N>(b, L.lane);
+    if (fabs(rhon) <= 1e-24 * r2) rst = true;   // breakdown: restart with r^ = r
+    if (rst) rhon = r2;
+    const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
+    // p = r + beta (p - omega v);  W = M^-1 p
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double p = 0.0;
+        if (L.active) {
+          p = ps[j * N + i];
+          if (!conv) {
+            p = rst ? R[j][i] : fma(beta, fma(-omega, vs[j * N + i], p), R[j][i]);
+            ps[j * N + i] = p;
+            if (rst) rh[j * N + i] = R[j][i];
+          }
+          p /= ds[j * N + i];
+        }
+        W[j][i] = p;
+      }
+    rst = false;
+    double T[N][N];
+    plane_op<N, false>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
+    double rv = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        if (L.active) {
+          vs[j * N + i] = T[j][i];
+          rv = fma(rh[j * N + i], T[j][i], rv);
+        }
+    rv = cell_sum<N>(rv, L.lane);
+    alpha = 0.0;
+    if (!conv) {
+      if (rv != 0.0) alpha = rhon / rv;
+      else rst = true;
+    }
+    // x += alpha p^;  s = r - alpha v (in R);  W = M^-1 s
+    double ss = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (L.active) xs[j * N + i] = fma(alpha, W[j][i], xs[j * N + i]);
+        R[j][i] = fma(-alpha, T[j][i], R[j][i]);
+        ss = fma(R[j][i], R[j][i], ss);
+        W[j][i] = L.active ? R[j][i] / ds[j * N + i] : 0.0;
+      }
+    ss = cell_sum<N>(ss, L.lane);
+    if (!conv && ss <= kp.tol2 * rr0) {
+      conv = true;
+      ++its;
+    }
+    plane_op<N, false>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
+    double ts = 0.0, tt = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        ts = fma(T[j][i], R[j][i], ts);
+        tt = fma(T[j][i], T[j][i], tt);
+      }
+    ts = cell_sum<N>(ts, L.lane);
+    tt = cell_sum<N>(tt, L.lane);
+    const double om = (!conv && tt > 0.0) ? ts / tt : 0.0;
+    double r2n = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        if (L.active) xs[j * N + i] = fma(om, W[j][i], xs[j * N + i]);
+        R[j][i] = fma(-om, T[j][i], R[j][i]);
+        r2n = fma(R[j][i], R[j][i], r2n);
+      }
+    r2n = cell_sum<N>(r2n, L.lane);
+    if (!conv) {
+      ++its;
+      if (r2n <= kp.tol2 * rr0) conv = true;
+      rho = rhon;
+      omega = om;
+      if (omega == 0.0) {
+        rst = true;
+        omega = 1.0;
+      }
+    }
+  }
+  __syncthreads();
+  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  __syncthreads();
+  if (L.active) {
+    double* bb = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        bb[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], bb[j * N + i]) : xs[j * N + i];
+  }
+  __syncthreads();
+  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
+}
+
+template <int N> constexpr size_t smem_apply() {
+  using G = Geo<N>;
+  return sizeof(double) * (size_t)(G::TB + G::FY + G::FX + G::FZ);
+}
+template <int N> constexpr size_t smem_solve(int planes) {
+  using G = Geo<N>;
+  static_assert(G::FS == G::PS || G::FS < G::PS, "face block must fit a plane block");
+  return sizeof(double) * (size_t)(G::TB + G::FY + planes * G::C * G::PS);
+}
+
+}  // namespace pk

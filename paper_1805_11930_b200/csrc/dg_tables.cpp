@@ -115,6 +115,10 @@ bool build_tables(int p, Tables1D* t) {
     t->Sdiag[i] = sd;
     t->Cdiag[i] = cd;
     t->Mdiag[i] = t->M[i * n + i];
+    t->E0[i] = lagrange(t->xq, n, i, 0.0);
+    t->E1[i] = lagrange(t->xq, n, i, 1.0);
+    t->F0[i] = lagrange_d(t->xq, n, i, 0.0);
+    t->F1[i] = lagrange_d(t->xq, n, i, 1.0);
   }
   return true;
 }

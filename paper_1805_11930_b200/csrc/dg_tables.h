@@ -23,6 +23,10 @@ struct Tables1D {
   double Sdiag[kMaxN];         // diag of Shat = G^T W G
   double Cdiag[kMaxN];         // diag of Chat = G^T W A (test derivative)
   double Mdiag[kMaxN];
+  // Gauss-point Lagrange polynomials l_q evaluated at the cell ends: E0[q] = l_q(0), E1[q] = l_q(1),
+  // F0[q] = l_q'(0), F1[q] = l_q'(1). Trace / normal derivative of a polynomial from its Gauss
+  // values U: u(0) = E0.U, u'(0) = F0.U; and A^T E0 = e0, A^T F0 = d0 (used to inject face terms).
+  double E0[kMaxN], E1[kMaxN], F0[kMaxN], F1[kMaxN];
 };
 
 // Fills t for degree p (1..7). Returns false on invalid p.
