@@ -238,6 +238,14 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   dg::KParams& kp = c->kp;
   kp.nx = desc->nx; kp.ny = desc->ny; kp.nzl = c->nzl; kp.ncells = (int32_t)c->ncells;
   kp.h[0] = desc->Lx / desc->nx; kp.h[1] = desc->Ly / desc->ny; kp.h[2] = desc->Lz / desc->nz;
+  for (int a = 0; a < 3; ++a) kp.ih[a] = 1.0 / kp.h[a];
+  {
+    const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
+    for (int a = 0; a < 3; ++a) kp.sb[a] = T3 * desc->b[a] / kp.h[a];
+    kp.fa[0] = kp.h[1] * kp.h[2];
+    kp.fa[1] = kp.h[0] * kp.h[2];
+    kp.fa[2] = kp.h[0] * kp.h[1];
+  }
   kp.pen = desc->alpha * desc->p * (desc->p + 2);
   for (int a = 0; a < 3; ++a) kp.b[a] = desc->b[a];
   for (int f = 0; f < 4; ++f) kp.slab_face[f] = desc->bc[f] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN;

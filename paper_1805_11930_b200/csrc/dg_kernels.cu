@@ -31,6 +31,10 @@ struct DevTab {
   double A[64], D[64], M[64], G[64];
   double w[8], d0[8], d1[8], Sd[8], Cd[8], Md[8];
   double E0[8], E1[8], F0[8], F1[8];  // A^-T e0, A^-T e1, A^-T d0, A^-T d1 (trace/derivative at 0/1 from Gauss values)
+  // weight-folded variants for the unweighted quadrature residual of the plane kernels:
+  double AW[64], GW[64];              // A[q][j] w_q, G[q][j] w_q
+  double DW[64];                      // D[q][r] w_q / w_r
+  double E0W[8], E1W[8], F0W[8], F1W[8];  // E0/w, E1/w, F0/w, F1/w
 };
 __constant__ DevTab c_tab[kMaxN + 1];
 
@@ -1039,7 +1043,15 @@ bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
     d.w[i] = t.wq[i]; d.d0[i] = t.d0[i]; d.d1[i] = t.d1[i];
     d.Sd[i] = t.Sdiag[i]; d.Cd[i] = t.Cdiag[i]; d.Md[i] = t.Mdiag[i];
     d.E0[i] = t.E0[i]; d.E1[i] = t.E1[i]; d.F0[i] = t.F0[i]; d.F1[i] = t.F1[i];
+    d.E0W[i] = t.E0[i] / t.wq[i]; d.E1W[i] = t.E1[i] / t.wq[i];
+    d.F0W[i] = t.F0[i] / t.wq[i]; d.F1W[i] = t.F1[i] / t.wq[i];
   }
+  for (int q = 0; q < n; ++q)
+    for (int j = 0; j < n; ++j) {
+      d.AW[q * n + j] = t.A[q * n + j] * t.wq[q];
+      d.GW[q * n + j] = t.G[q * n + j] * t.wq[q];
+      d.DW[q * n + j] = t.D[q * n + j] * t.wq[q] / t.wq[j];
+    }
   *err = cudaMemcpyToSymbol(c_tab, &d, sizeof(DevTab), sizeof(DevTab) * (p + 1));
   return *err == cudaSuccess;
 }
@@ -1055,13 +1067,17 @@ cudaError_t launch_block_diag_apply(int p, const KParams& kp, const double* u, d
   DG_DISPATCH(p, (apply_n<N>(k2, u, out, s, 0)));
 }
 
-cudaError_t launch_local_solve(int p, int method, const KParams& kp, const double* d, double* du,
+cudaError_t launch_local_solve(int p, int method, const KParams& kp0, const double* d, double* du,
                                cudaStream_t s) {
+  KParams kp = kp0;
+  kp.mask = 7u;
   DG_DISPATCH(p, (solve_n<N, false>(method, kp, d, nullptr, du, s)));
 }
 
-cudaError_t launch_sweep(int p, int method, const KParams& kp, const double* u, const double* f,
+cudaError_t launch_sweep(int p, int method, const KParams& kp0, const double* u, const double* f,
                          double* u_new, cudaStream_t s) {
+  KParams kp = kp0;
+  kp.mask = 7u;
   DG_DISPATCH(p, (solve_n<N, true>(method, kp, u, f, u_new, s)));
 }
 

@@ -13,6 +13,9 @@ enum FaceKind : int32_t { FK_DIRICHLET = 0, FK_NEUMANN = 1, FK_GHOST = 2 };
 struct KParams {
   int32_t nx, ny, nzl, ncells;   // local slab: nzl z-layers, ncells = nx*ny*nzl
   double h[3];                   // cell sizes
+  double ih[3];                  // 1 / h
+  double sb[3];                  // |T| b_k / h_k  (volume advection scaling)
+  double fa[3];                  // face areas |F| of x-, y-, z-faces: hy*hz, hx*hz, hx*hy
   double pen;                    // alpha * p * (p + d - 1), d = 3
   double b[3];                   // constant advection
   int32_t slab_face[6];          // x-,x+,y-,y+,z-,z+ of the slab: FaceKind

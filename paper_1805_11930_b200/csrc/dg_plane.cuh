@@ -23,17 +23,21 @@
 namespace pk {
 
 template <int N> struct PL;
-template <> struct PL<2> { static constexpr int WARPS = 4, KS = 5, CTB = 22; };
-template <> struct PL<3> { static constexpr int WARPS = 4, KS = 19, CTB = 121; };
-template <> struct PL<4> { static constexpr int WARPS = 4, KS = 20, CTB = 161; };
-template <> struct PL<5> { static constexpr int WARPS = 2, KS = 25, CTB = 253; };
+// KS/CTB: transpose-buffer plane / cell strides; QS/PS: plane / cell strides of the per-lane
+// plane storage (X, diag, ...). All chosen by an offline search for conflict-free lane patterns.
+template <> struct PL<2> { static constexpr int WARPS = 4, KS = 5, CTB = 22, QS = 8, PS = 17; };
+template <> struct PL<3> { static constexpr int WARPS = 4, KS = 19, CTB = 121, QS = 13, PS = 39; };
+template <> struct PL<4> { static constexpr int WARPS = 4, KS = 20, CTB = 161, QS = 17, PS = 68; };
+template <> struct PL<5> { static constexpr int WARPS = 2, KS = 25, CTB = 253, QS = 25, PS = 125; };
 
 template <int N_> struct Geo {
   static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
   static constexpr int CPW = 32 / N, WARPS = PL<N>::WARPS, C = CPW * WARPS, NT = 32 * WARPS;
   static constexpr int KS = PL<N>::KS, ARR = N * KS, CTB = PL<N>::CTB;
   static constexpr int FS = 4 * N2 + 1;   // per-cell stride of a block of 4 face arrays
-  static constexpr int PS = (N3 > 4 * N2 ? N3 : 4 * N2) + 1;  // per-cell plane storage (X, Dg, ...)
+  static constexpr int QS = PL<N>::QS, PS = PL<N>::PS;  // plane storage (X, Dg, ...)
+  static_assert(PS >= N * QS && PS >= FS, "plane storage must hold a cell and a face block");
+  static constexpr int PER = (C * N3 + NT - 1) / NT;      // tile elements per thread
   // dynamic shared memory (doubles)
   static constexpr int TB = C * CTB;      // transposes / tile staging
   static constexpr int FY = C * FS;       // y-face arrays (k, qx)
@@ -80,14 +84,11 @@ template <int N> __device__ __forceinline__ double T_W(int i) { return c_tab[N].
 
 // runtime-indexed rows held in registers
 template <int N> struct Rows {
-  double wt;        // w[t]
-  double Arow[N];   // A[t][.]
-  double Mrow[N];   // Mhat[t][.]
+  double Arow[N];   // A[t][.]   (y interpolation of z-neighbour traces)
+  double Mrow[N];   // Mhat[t][.] (z face mass of the y faces)
   double Md, Sd, Cd;
-  double d0t, d1t;  // d0[t], d1[t]
 };
 template <int N> __device__ __forceinline__ void load_rows(Rows<N>& r, int t) {
-  r.wt = c_tab[N].w[t];
 #pragma unroll
   for (int j = 0; j < N; ++j) {
     r.Arow[j] = c_tab[N].A[t * N + j];
@@ -96,43 +97,45 @@ template <int N> __device__ __forceinline__ void load_rows(Rows<N>& r, int t) {
   r.Md = c_tab[N].Md[t];
   r.Sd = c_tab[N].Sd[t];
   r.Cd = c_tab[N].Cd[t];
-  r.d0t = c_tab[N].d0[t];
-  r.d1t = c_tab[N].d1[t];
 }
-
-struct Scal {
-  double h[3], ih[3], sb[3];
-};
-__device__ __forceinline__ Scal make_scal(const KParams& kp) {
-  Scal s;
-  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    s.h[a] = kp.h[a];
-    s.ih[a] = 1.0 / kp.h[a];
-    s.sb[a] = T3 * kp.b[a] / kp.h[a];
-  }
-  return s;
-}
+template <int N> __device__ __forceinline__ double T_AW(int i) { return c_tab[N].AW[i]; }
+template <int N> __device__ __forceinline__ double T_GW(int i) { return c_tab[N].GW[i]; }
+template <int N> __device__ __forceinline__ double T_DW(int i) { return c_tab[N].DW[i]; }
 
 // ---- coalesced tile staging: C cells x n^3 (contiguous in global) -> TB layout ---------
 // element (k, j, i) of cell slot cs at cs*CTB + k*KS + j*N + i
 template <int N>
 __device__ __forceinline__ void stage_tile(double* TB, const double* __restrict__ src, int nvalid) {
   using G = Geo<N>;
-  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+  double v[G::PER];
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    v[m] = (e < G::C * G::N3 && e / G::N3 < nvalid) ? src[e] : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
     const int cs = e / G::N3, r = e % G::N3;
-    TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = (cs < nvalid) ? src[e] : 0.0;
+    if (e < G::C * G::N3) TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = v[m];
   }
 }
-// neighbour tile: per-cell base pointers (nullptr -> zeros)
+// neighbour tile: per-cell base pointers (nullptr -> zeros); all loads issued before the stores
 template <int N>
 __device__ __forceinline__ void stage_nbr(double* TB, const Cells<N>& cl, int f) {
   using G = Geo<N>;
-  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+  double v[G::PER];
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    const double* p = (e < G::C * G::N3) ? cl.nb[e / G::N3][f] : nullptr;
+    v[m] = p ? __ldg(p + e % G::N3) : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
     const int cs = e / G::N3, r = e % G::N3;
-    const double* p = cl.nb[cs][f];
-    TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = p ? p[r] : 0.0;
+    if (e < G::C * G::N3) TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = v[m];
   }
 }
 template <int N>
@@ -165,35 +168,39 @@ __device__ __forceinline__ void write_plane(double* TB, const Lane& L, const dou
 // ---- neighbour prologue: traces of the 6 face neighbours -> FY (nodal), FX, FZ ----------
 // Must be called by all threads; leaves TB free. Face order f = 2*axis + hi.
 template <int N>
-__device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, double* TB,
-                             double* FY, double* FX, double* FZ) {
+__device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& L, double* TB,
+                             double* FY, double* FX, double* FZ, const double* tile) {
   using G = Geo<N>;
   const int k = L.t;
-  for (int f = 0; f < 6; ++f) {
-    __syncthreads();
-    stage_nbr<N>(TB, cl, f);
-    __syncthreads();
-    if (!L.active) continue;
-    const double* c = cl.fc[L.cs][f];
-    const double cna = c[2], cng = c[3], ctn = c[5];
-    const int axis = f >> 1, hi = f & 1;
-    const double* nb = TB + L.cs * G::CTB;   // neighbour cell, layout k*KS + j*N + i
-    if (axis == 0) {
-      // lane k: rows j of the neighbour's plane k; lo face sees the neighbour's x=1 end
+  // x faces: the neighbour is usually the next / previous cell of the group, whose tile is
+  // still in TB (staged by the caller); otherwise its plane k is read from global memory.
+  if (L.active) {
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const double* c = cl.fc[L.cs][hi];
+      const double cna = c[2], cng = c[3], ctn = c[5];
+      const double* nbp = cl.nb[L.cs][hi];
+      const int ncs = L.cs + (hi ? 1 : -1);
+      const double* plane = nullptr;
+      if (nbp) {
+        if (ncs >= 0 && ncs < G::C && nbp == tile + (size_t)ncs * G::N3)
+          plane = TB + ncs * G::CTB + k * G::KS;
+        else
+          plane = nbp + k * G::N2;
+      }
       double S[N], T[N];
 #pragma unroll
       for (int j = 0; j < N; ++j) {
         double row[N];
 #pragma unroll
-        for (int i = 0; i < N; ++i) row[i] = nb[k * G::KS + j * N + i];
+        for (int i = 0; i < N; ++i) row[i] = plane ? plane[j * N + i] : 0.0;
         double g = 0.0;
 #pragma unroll
         for (int i = 0; i < N; ++i) g = fma(hi ? c_tab[N].d0[i] : c_tab[N].d1[i], row[i], g);
         const double a = hi ? row[0] : row[N - 1];
-        S[j] = cna * a + cng * g * sc.ih[0];
+        S[j] = cna * a + cng * g * kp.ih[0];
         T[j] = ctn * a;
       }
-      // interpolate along y: (k, qy)
       double* fx = FX + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
 #pragma unroll
       for (int q = 0; q < N; ++q) {
@@ -206,7 +213,18 @@ __device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, 
         fx[q] = s;
         fx[G::N2 + q] = tt;
       }
-    } else if (axis == 1) {
+    }
+  }
+  for (int f = 2; f < 6; ++f) {
+    __syncthreads();
+    stage_nbr<N>(TB, cl, f);
+    __syncthreads();
+    if (!L.active) continue;
+    const double* c = cl.fc[L.cs][f];
+    const double cna = c[2], cng = c[3], ctn = c[5];
+    const int axis = f >> 1, hi = f & 1;
+    const double* nb = TB + L.cs * G::CTB;   // neighbour cell, layout k*KS + j*N + i
+    if (axis == 1) {
       // lane k: columns i of the neighbour's plane k (nodal in i; interpolated in Q1)
       double* fy = FY + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
 #pragma unroll
@@ -216,7 +234,7 @@ __device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, 
         for (int j = 0; j < N; ++j)
           g = fma(hi ? c_tab[N].d0[j] : c_tab[N].d1[j], nb[k * G::KS + j * N + i], g);
         const double a = nb[k * G::KS + (hi ? 0 : N - 1) * N + i];
-        fy[i] = cna * a + cng * g * sc.ih[1];
+        fy[i] = cna * a + cng * g * kp.ih[1];
         fy[G::N2 + i] = ctn * a;
       }
     } else {
@@ -230,7 +248,7 @@ __device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, 
         for (int kk = 0; kk < N; ++kk)
           g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
         const double a = nb[(hi ? 0 : N - 1) * G::KS + j * N + i];
-        S[i] = cna * a + cng * g * sc.ih[2];
+        S[i] = cna * a + cng * g * kp.ih[2];
         T[i] = ctn * a;
       }
       double* fz = FZ + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + j * N;
@@ -252,9 +270,12 @@ __device__ void nbr_prologue(const Cells<N>& cl, const Lane& L, const Scal& sc, 
 
 // ---- the operator: out = A u (NBR) or D_T u (self faces only) on the lane's plane ---------
 // All threads must call it (two __syncthreads inside). TB must be free on entry.
+// The quadrature-point residual R is kept UNWEIGHTED: the Gauss weights (and |T|, face
+// areas through kp) are folded into the transposed 1D tables AW = A w, GW = G w,
+// DW = D w_q / w_r and the end-point injection vectors E/w, F/w.
 template <int N, bool NBR>
-__device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, const Rows<N>& rw,
-                                         const Scal& sc, bool vol, const double (&in)[N][N],
+__device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, const Lane& L,
+                                         const Rows<N>& rw, bool vol, const double (&in)[N][N],
                                          double (&out)[N][N], double* TB, double* FY,
                                          const double* FX, const double* FZ) {
   using G = Geo<N>;
@@ -264,7 +285,7 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
   // ---------------- Q1: lane = z node k ----------------
   if (L.active) {
     const int k = L.t;
-    {  // t2 is needed for the face traces even without the volume terms; t2y only with them
+    {  // Stage 1 in the plane: a = A_x u; t2 = A_y a (always, for the face traces); t2y = G_y a
       double a[N][N];
 #pragma unroll
       for (int j = 0; j < N; ++j)
@@ -289,7 +310,7 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
           if (vol) tb[G::ARR + k * G::KS + qy * N + qx] = sy;
         }
     }
-    // y faces (normal y, tangential z = lane, x): nodal S/T combos, then A_x
+    // y faces (normal y; tangential z = this lane, x): nodal S/T combos, then A_x
     const double* clo = fc + 2 * 6;
     const double* chi = fc + 3 * 6;
     double X0[N], X1[N], X2[N], X3[N];
@@ -302,9 +323,9 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
         ghi = fma(c_tab[N].d1[j], in[j][i], ghi);
       }
       const double alo = in[0][i], ahi = in[N - 1][i];
-      X0[i] = clo[0] * alo + clo[1] * glo * sc.ih[1];
+      X0[i] = fma(clo[0], alo, clo[1] * glo * kp.ih[1]);
       X1[i] = clo[4] * alo;
-      X2[i] = chi[0] * ahi + chi[1] * ghi * sc.ih[1];
+      X2[i] = fma(chi[0], ahi, chi[1] * ghi * kp.ih[1]);
       X3[i] = chi[4] * ahi;
       if (NBR) {
         X0[i] += fy[0 * G::N2 + k * N + i];
@@ -335,9 +356,10 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
   if (L.active) {
     const int qy = L.t;
     const double* vcell = cl.vc[L.cs];
-    double U[N][N], R[N][N], Fy[N][N];   // [qz][qx]
+    double U[N][N], R[N][N], Fy[N][N];   // [qz][qx], unweighted
     if (vol) {
       // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise
+      const double cK = vcell[1], cR = vcell[3];
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
         double c0[N], c1[N];
@@ -354,13 +376,12 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
             s = fma(T_A<N>(qz * N + k), c0[k], s);
             s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
           }
-          const double W = rw.wt * T_W<N>(qz) * T_W<N>(qx);
           U[qz][qx] = s;
-          R[qz][qx] = W * vcell[3] * s;
-          Fy[qz][qx] = W * fma(vcell[1], s1, -sc.sb[1] * s);
+          R[qz][qx] = cR * s;
+          Fy[qz][qx] = fma(cK, s1, -kp.sb[1] * s);
         }
       }
-      // x direction: rows qz
+      // x direction: rows qz;  R += DW^T (sK D U - sb U)
 #pragma unroll
       for (int qz = 0; qz < N; ++qz) {
         double F[N];
@@ -369,13 +390,13 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[qz][r], du);
-          F[q] = rw.wt * T_W<N>(qz) * T_W<N>(q) * fma(vcell[0], du, -sc.sb[0] * U[qz][q]);
+          F[q] = fma(vcell[0], du, -kp.sb[0] * U[qz][q]);
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
           double s = R[qz][r];
 #pragma unroll
-          for (int q = 0; q < N; ++q) s = fma(T_D<N>(q * N + r), F[q], s);
+          for (int q = 0; q < N; ++q) s = fma(T_DW<N>(q * N + r), F[q], s);
           R[qz][r] = s;
         }
       }
@@ -388,13 +409,13 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[r][qx], du);
-          F[q] = rw.wt * T_W<N>(q) * T_W<N>(qx) * fma(vcell[2], du, -sc.sb[2] * U[q][qx]);
+          F[q] = fma(vcell[2], du, -kp.sb[2] * U[q][qx]);
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
           double s = R[r][qx];
 #pragma unroll
-          for (int q = 0; q < N; ++q) s = fma(T_D<N>(q * N + r), F[q], s);
+          for (int q = 0; q < N; ++q) s = fma(T_DW<N>(q * N + r), F[q], s);
           R[r][qx] = s;
         }
       }
@@ -431,26 +452,24 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
           glo = fma(c_tab[N].F0[q], U[qz][q], glo);
           ghi = fma(c_tab[N].F1[q], U[qz][q], ghi);
         }
-        double Slo = clo[0] * alo + clo[1] * glo * sc.ih[0], Tlo = clo[4] * alo;
-        double Shi = chi[0] * ahi + chi[1] * ghi * sc.ih[0], Thi = chi[4] * ahi;
+        double Slo = fma(clo[0], alo, clo[1] * glo * kp.ih[0]), Tlo = clo[4] * alo;
+        double Shi = fma(chi[0], ahi, chi[1] * ghi * kp.ih[0]), Thi = chi[4] * ahi;
         if (NBR) {  // neighbour traces at (k, qy) -> interpolate in z
-          double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
 #pragma unroll
           for (int k = 0; k < N; ++k) {
             const double A = T_A<N>(qz * N + k);
-            n0 = fma(A, fx[0 * G::N2 + k * N + qy], n0);
-            n1 = fma(A, fx[1 * G::N2 + k * N + qy], n1);
-            n2 = fma(A, fx[2 * G::N2 + k * N + qy], n2);
-            n3 = fma(A, fx[3 * G::N2 + k * N + qy], n3);
+            Slo = fma(A, fx[0 * G::N2 + k * N + qy], Slo);
+            Tlo = fma(A, fx[1 * G::N2 + k * N + qy], Tlo);
+            Shi = fma(A, fx[2 * G::N2 + k * N + qy], Shi);
+            Thi = fma(A, fx[3 * G::N2 + k * N + qy], Thi);
           }
-          Slo += n0; Tlo += n1; Shi += n2; Thi += n3;
         }
-        const double Wf = rw.wt * T_W<N>(qz) * sc.h[1] * sc.h[2];
-        Slo *= Wf; Tlo *= Wf; Shi *= Wf; Thi *= Wf;
+        const double fa = kp.fa[0];
+        Slo *= fa; Tlo *= fa; Shi *= fa; Thi *= fa;
 #pragma unroll
         for (int q = 0; q < N; ++q)
-          R[qz][q] += c_tab[N].E0[q] * Slo + c_tab[N].F0[q] * Tlo + c_tab[N].E1[q] * Shi +
-                      c_tab[N].F1[q] * Thi;
+          R[qz][q] += fma(c_tab[N].E0W[q], Slo,
+                          fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
     }
     // z faces at the face Gauss points (qy, qx): traces from the z-columns of U
@@ -468,29 +487,27 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
           glo = fma(c_tab[N].F0[q], U[q][qx], glo);
           ghi = fma(c_tab[N].F1[q], U[q][qx], ghi);
         }
-        double Slo = clo[0] * alo + clo[1] * glo * sc.ih[2], Tlo = clo[4] * alo;
-        double Shi = chi[0] * ahi + chi[1] * ghi * sc.ih[2], Thi = chi[4] * ahi;
+        double Slo = fma(clo[0], alo, clo[1] * glo * kp.ih[2]), Tlo = clo[4] * alo;
+        double Shi = fma(chi[0], ahi, chi[1] * ghi * kp.ih[2]), Thi = chi[4] * ahi;
         if (NBR) {  // neighbour traces at (j, qx) -> interpolate in y (row qy of A)
-          double n0 = 0.0, n1 = 0.0, n2 = 0.0, n3 = 0.0;
 #pragma unroll
           for (int j = 0; j < N; ++j) {
             const double A = rw.Arow[j];
-            n0 = fma(A, fz[0 * G::N2 + j * N + qx], n0);
-            n1 = fma(A, fz[1 * G::N2 + j * N + qx], n1);
-            n2 = fma(A, fz[2 * G::N2 + j * N + qx], n2);
-            n3 = fma(A, fz[3 * G::N2 + j * N + qx], n3);
+            Slo = fma(A, fz[0 * G::N2 + j * N + qx], Slo);
+            Tlo = fma(A, fz[1 * G::N2 + j * N + qx], Tlo);
+            Shi = fma(A, fz[2 * G::N2 + j * N + qx], Shi);
+            Thi = fma(A, fz[3 * G::N2 + j * N + qx], Thi);
           }
-          Slo += n0; Tlo += n1; Shi += n2; Thi += n3;
         }
-        const double Wf = rw.wt * T_W<N>(qx) * sc.h[0] * sc.h[1];
-        Slo *= Wf; Tlo *= Wf; Shi *= Wf; Thi *= Wf;
+        const double fa = kp.fa[2];
+        Slo *= fa; Tlo *= fa; Shi *= fa; Thi *= fa;
 #pragma unroll
         for (int q = 0; q < N; ++q)
-          R[q][qx] += c_tab[N].E0[q] * Slo + c_tab[N].F0[q] * Tlo + c_tab[N].E1[q] * Shi +
-                      c_tab[N].F1[q] * Thi;
+          R[q][qx] += fma(c_tab[N].E0W[q], Slo,
+                          fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
     }
-    // A_z^T on R and F_y, stored in place of t2 / t2y (same index set (., qy, .))
+    // (A w)_z^T on R and F_y, stored in place of t2 / t2y (same index set (., qy, .))
 #pragma unroll
     for (int qx = 0; qx < N; ++qx)
 #pragma unroll
@@ -498,8 +515,8 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
         double s = 0.0, s1 = 0.0;
 #pragma unroll
         for (int qz = 0; qz < N; ++qz) {
-          s = fma(T_A<N>(qz * N + k), R[qz][qx], s);
-          s1 = fma(T_A<N>(qz * N + k), Fy[qz][qx], s1);
+          s = fma(T_AW<N>(qz * N + k), R[qz][qx], s);
+          s1 = fma(T_AW<N>(qz * N + k), Fy[qz][qx], s1);
         }
         tb[k * G::KS + qy * N + qx] = s;
         tb[G::ARR + k * G::KS + qy * N + qx] = s1;
@@ -523,32 +540,30 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
         double s = 0.0;
 #pragma unroll
         for (int qy = 0; qy < N; ++qy) {
-          s = fma(T_A<N>(qy * N + j), r[qy], s);
-          s = fma(T_G<N>(qy * N + j), f[qy], s);
+          s = fma(T_AW<N>(qy * N + j), r[qy], s);
+          s = fma(T_GW<N>(qy * N + j), f[qy], s);
         }
         Vq[j][qx] = s;
       }
     }
-    // y faces: z face mass (row k of Mhat) on the (k', qx) arrays, x weights, end profiles in j
-    {
+    // y faces: z face mass (row k of Mhat) on the (k', qx) arrays, end profiles in j
 #pragma unroll
-      for (int qx = 0; qx < N; ++qx) {
-        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+    for (int qx = 0; qx < N; ++qx) {
+      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
 #pragma unroll
-        for (int kk = 0; kk < N; ++kk) {
-          const double M = rw.Mrow[kk];
-          z0 = fma(M, fy[0 * G::N2 + kk * N + qx], z0);
-          z1 = fma(M, fy[1 * G::N2 + kk * N + qx], z1);
-          z2 = fma(M, fy[2 * G::N2 + kk * N + qx], z2);
-          z3 = fma(M, fy[3 * G::N2 + kk * N + qx], z3);
-        }
-        const double Wf = T_W<N>(qx) * sc.h[0] * sc.h[2];
-        z0 *= Wf; z1 *= Wf; z2 *= Wf; z3 *= Wf;
-        Vq[0][qx] += z0;
-        Vq[N - 1][qx] += z2;
-#pragma unroll
-        for (int j = 0; j < N; ++j) Vq[j][qx] += c_tab[N].d0[j] * z1 + c_tab[N].d1[j] * z3;
+      for (int kk = 0; kk < N; ++kk) {
+        const double M = rw.Mrow[kk];
+        z0 = fma(M, fy[0 * G::N2 + kk * N + qx], z0);
+        z1 = fma(M, fy[1 * G::N2 + kk * N + qx], z1);
+        z2 = fma(M, fy[2 * G::N2 + kk * N + qx], z2);
+        z3 = fma(M, fy[3 * G::N2 + kk * N + qx], z3);
       }
+      const double fa = kp.fa[1];
+      z0 *= fa; z1 *= fa; z2 *= fa; z3 *= fa;
+      Vq[0][qx] += z0;
+      Vq[N - 1][qx] += z2;
+#pragma unroll
+      for (int j = 0; j < N; ++j) Vq[j][qx] = fma(c_tab[N].d0[j], z1, fma(c_tab[N].d1[j], z3, Vq[j][qx]));
     }
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -556,44 +571,43 @@ __device__ __forceinline__ void plane_op(const Cells<N>& cl, const Lane& L, cons
       for (int i = 0; i < N; ++i) {
         double s = 0.0;
 #pragma unroll
-        for (int qx = 0; qx < N; ++qx) s = fma(T_A<N>(qx * N + i), Vq[j][qx], s);
+        for (int qx = 0; qx < N; ++qx) s = fma(T_AW<N>(qx * N + i), Vq[j][qx], s);
         out[j][i] = s;
       }
   }
 }
 
-// diag(D_T) on the lane's plane (Jacobi preconditioner), from 1D diagonals
+// 1 / diag(D_T) on the lane's plane (Jacobi preconditioner), from 1D diagonals
 template <int N>
-__device__ __forceinline__ void plane_diag(const Cells<N>& cl, const Lane& L, const Rows<N>& rw,
-                                           const Scal& sc, double (&dg)[N][N]) {
+__device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>& cl, const Lane& L,
+                                               const Rows<N>& rw, double (&dg)[N][N]) {
   const double* vc = cl.vc[L.cs];
   const double* fc = &cl.fc[L.cs][0][0];
   const int k = L.t;
-  const double area[3] = {sc.h[1] * sc.h[2], sc.h[0] * sc.h[2], sc.h[0] * sc.h[1]};
   const double dd0 = c_tab[N].d0[0], dd1 = c_tab[N].d1[N - 1];
   auto fd = [&](int f, double dd, double ih) {
     const double* c = fc + f * 6;
     return c[0] + c[1] * dd * ih + c[4] * dd;
   };
-  const double zlo = (k == 0) ? fd(4, dd0, sc.ih[2]) : 0.0;
-  const double zhi = (k == N - 1) ? fd(5, dd1, sc.ih[2]) : 0.0;
-  const double xlo = fd(0, dd0, sc.ih[0]), xhi = fd(1, dd1, sc.ih[0]);
-  const double ylo = fd(2, dd0, sc.ih[1]), yhi = fd(3, dd1, sc.ih[1]);
+  const double zlo = (k == 0) ? fd(4, dd0, kp.ih[2]) : 0.0;
+  const double zhi = (k == N - 1) ? fd(5, dd1, kp.ih[2]) : 0.0;
+  const double xlo = fd(0, dd0, kp.ih[0]), xhi = fd(1, dd1, kp.ih[0]);
+  const double ylo = fd(2, dd0, kp.ih[1]), yhi = fd(3, dd1, kp.ih[1]);
 #pragma unroll
   for (int j = 0; j < N; ++j)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const double Mi = c_tab[N].Md[i], Mj = c_tab[N].Md[j], Mk = rw.Md;
       double d = vc[3] * Mi * Mj * Mk;
-      d += (vc[0] * c_tab[N].Sd[i] - sc.sb[0] * c_tab[N].Cd[i]) * Mj * Mk;
-      d += (vc[1] * c_tab[N].Sd[j] - sc.sb[1] * c_tab[N].Cd[j]) * Mi * Mk;
-      d += (vc[2] * rw.Sd - sc.sb[2] * rw.Cd) * Mi * Mj;
-      if (i == 0) d += area[0] * Mj * Mk * xlo;
-      if (i == N - 1) d += area[0] * Mj * Mk * xhi;
-      if (j == 0) d += area[1] * Mi * Mk * ylo;
-      if (j == N - 1) d += area[1] * Mi * Mk * yhi;
-      d += area[2] * Mi * Mj * (zlo + zhi);
-      dg[j][i] = d;
+      d += (vc[0] * c_tab[N].Sd[i] - kp.sb[0] * c_tab[N].Cd[i]) * Mj * Mk;
+      d += (vc[1] * c_tab[N].Sd[j] - kp.sb[1] * c_tab[N].Cd[j]) * Mi * Mk;
+      d += (vc[2] * rw.Sd - kp.sb[2] * rw.Cd) * Mi * Mj;
+      if (i == 0) d += kp.fa[0] * Mj * Mk * xlo;
+      if (i == N - 1) d += kp.fa[0] * Mj * Mk * xhi;
+      if (j == 0) d += kp.fa[1] * Mi * Mk * ylo;
+      if (j == N - 1) d += kp.fa[1] * Mi * Mk * yhi;
+      d += kp.fa[2] * Mi * Mj * (zlo + zhi);
+      dg[j][i] = 1.0 / d;
     }
 }
 
@@ -620,14 +634,13 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   const Lane L = lane_id<N>();
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  const Scal sc = make_scal(kp);
   stage_tile<N>(TB, u + (size_t)cell0 * G::N3, nvalid);
   setup<N>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
   double in[N][N], o[N][N];
   read_plane<N>(TB, L, in);
-  if (NBR) nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);  // starts and ends with a barrier
+  if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3);
   else __syncthreads();
-  plane_op<N, NBR>(cl, L, rw, sc, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
+  plane_op<N, NBR>(kp, cl, L, rw, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
@@ -654,17 +667,14 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  const Scal sc = make_scal(kp);
-  KParams kq = kp;
-  kq.mask = 7u;
   stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
-  setup<N>(kq, cl, cell0, SWEEP ? in : nullptr);
+  setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
   double R[N][N], P[N][N];
   read_plane<N>(TB, L, P);
   if (SWEEP) {
     double Q[N][N];
-    nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);
-    plane_op<N, true>(cl, L, rw, sc, true, P, Q, TB, FY, FX, FZ);   // Q = A u
+    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    plane_op<N, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
@@ -679,13 +689,13 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
       for (int i = 0; i < N; ++i) R[j][i] = valid ? P[j][i] : 0.0;
   }
-  const int po = L.cs * G::PS + L.t * G::N2;
+  const int po = L.cs * G::PS + L.t * G::QS;
   double* xs = XS + po;
   double* ds = DS + po;
   __syncthreads();   // the prologue's FX / FZ (aliasing XS / DS) are consumed
   {
     double dg[N][N];
-    plane_diag<N>(cl, L, rw, sc, dg);
+    plane_inv_diag<N>(kp, cl, L, rw, dg);
     if (L.active)
 #pragma unroll
       for (int j = 0; j < N; ++j)
@@ -697,7 +707,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   for (int j = 0; j < N; ++j)
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      const double z = L.active ? R[j][i] / ds[j * N + i] : 0.0;
+      const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
       P[j][i] = z;
       rr = fma(R[j][i], R[j][i], rr);
       rz = fma(R[j][i], z, rz);
@@ -711,7 +721,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     const int done = __syncthreads_and(conv || !L.active);
     if (done || iter >= kp.max_it) break;
     double Q[N][N];
-    plane_op<N, false>(cl, L, rw, sc, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+    plane_op<N, false>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
     double pq = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -731,7 +741,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
         R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
         r2 = fma(R[j][i], R[j][i], r2);
-        if (L.active) rzn = fma(R[j][i], R[j][i] / ds[j * N + i], rzn);
+        if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
       }
     r2 = cell_sum<N>(r2, L.lane);
     rzn = cell_sum<N>(rzn, L.lane);
@@ -744,7 +754,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
         for (int j = 0; j < N; ++j)
 #pragma unroll
-          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] / ds[j * N + i]);
+          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
       }
     }
   }
@@ -789,17 +799,14 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  const Scal sc = make_scal(kp);
-  KParams kq = kp;
-  kq.mask = 7u;
   stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
-  setup<N>(kq, cl, cell0, SWEEP ? in : nullptr);
+  setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
   double R[N][N], W[N][N];
   read_plane<N>(TB, L, W);
   if (SWEEP) {
     double T[N][N];
-    nbr_prologue<N>(cl, L, sc, TB, FY, FX, FZ);
-    plane_op<N, true>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);
+    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    plane_op<N, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
@@ -814,7 +821,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
 #pragma unroll
       for (int i = 0; i < N; ++i) R[j][i] = valid ? W[j][i] : 0.0;
   }
-  const int po = L.cs * G::PS + L.t * G::N2;
+  const int po = L.cs * G::PS + L.t * G::QS;
   double* xs = XS + po;
   double* rh = RHS + po;
   double* ps = PSM + po;
@@ -823,7 +830,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   __syncthreads();   // the prologue's FX / FZ (aliasing XS / RHS) are consumed
   {
     double dg[N][N];
-    plane_diag<N>(cl, L, rw, sc, dg);
+    plane_inv_diag<N>(kp, cl, L, rw, dg);
     if (L.active)
 #pragma unroll
       for (int j = 0; j < N; ++j)
@@ -877,13 +884,13 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
             ps[j * N + i] = p;
             if (rst) rh[j * N + i] = R[j][i];
           }
-          p /= ds[j * N + i];
+          p *= ds[j * N + i];
         }
         W[j][i] = p;
       }
     rst = false;
     double T[N][N];
-    plane_op<N, false>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
+    plane_op<N, false>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
     double rv = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -908,14 +915,14 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
         if (L.active) xs[j * N + i] = fma(alpha, W[j][i], xs[j * N + i]);
         R[j][i] = fma(-alpha, T[j][i], R[j][i]);
         ss = fma(R[j][i], R[j][i], ss);
-        W[j][i] = L.active ? R[j][i] / ds[j * N + i] : 0.0;
+        W[j][i] = L.active ? R[j][i] * ds[j * N + i] : 0.0;
       }
     ss = cell_sum<N>(ss, L.lane);
     if (!conv && ss <= kp.tol2 * rr0) {
       conv = true;
       ++its;
     }
-    plane_op<N, false>(cl, L, rw, sc, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
+    plane_op<N, false>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
     double ts = 0.0, tt = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -970,7 +977,6 @@ template <int N> constexpr size_t smem_apply() {
 }
 template <int N> constexpr size_t smem_solve(int planes) {
   using G = Geo<N>;
-  static_assert(G::FS == G::PS || G::FS < G::PS, "face block must fit a plane block");
   return sizeof(double) * (size_t)(G::TB + G::FY + planes * G::C * G::PS);
 }
 
