@@ -120,17 +120,20 @@ __device__ __forceinline__ void stage_tile(double* TB, const double* __restrict_
     if (e < G::C * G::N3) TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = v[m];
   }
 }
-// neighbour tile: per-cell base pointers (nullptr -> zeros); all loads issued before the stores
+// neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
 template <int N>
-__device__ __forceinline__ void stage_nbr(double* TB, const Cells<N>& cl, int f) {
+__device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N>& cl, int f) {
   using G = Geo<N>;
-  double v[G::PER];
 #pragma unroll
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
     const double* p = (e < G::C * G::N3) ? cl.nb[e / G::N3][f] : nullptr;
     v[m] = p ? __ldg(p + e % G::N3) : 0.0;
   }
+}
+template <int N>
+__device__ __forceinline__ void store_tile(double* TB, const double (&v)[Geo<N>::PER]) {
+  using G = Geo<N>;
 #pragma unroll
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
@@ -215,53 +218,67 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& 
       }
     }
   }
-  for (int f = 2; f < 6; ++f) {
+  // y / z neighbours: two tiles per round (the y pair, then the z pair) staged into the two
+  // halves of TB; the z pair's global loads are in flight while the y traces are extracted.
+  double pv0[G::PER], pv1[G::PER];
+  load_nbr<N>(pv0, cl, 2);
+  load_nbr<N>(pv1, cl, 3);
+#pragma unroll 1
+  for (int axis = 1; axis < 3; ++axis) {
     __syncthreads();
-    stage_nbr<N>(TB, cl, f);
+    store_tile<N>(TB, pv0);
+    store_tile<N>(TB + G::ARR, pv1);
     __syncthreads();
-    if (!L.active) continue;
-    const double* c = cl.fc[L.cs][f];
-    const double cna = c[2], cng = c[3], ctn = c[5];
-    const int axis = f >> 1, hi = f & 1;
-    const double* nb = TB + L.cs * G::CTB;   // neighbour cell, layout k*KS + j*N + i
     if (axis == 1) {
-      // lane k: columns i of the neighbour's plane k (nodal in i; interpolated in Q1)
-      double* fy = FY + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
+      load_nbr<N>(pv0, cl, 4);
+      load_nbr<N>(pv1, cl, 5);
+    }
+    if (!L.active) continue;
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double g = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j)
-          g = fma(hi ? c_tab[N].d0[j] : c_tab[N].d1[j], nb[k * G::KS + j * N + i], g);
-        const double a = nb[k * G::KS + (hi ? 0 : N - 1) * N + i];
-        fy[i] = cna * a + cng * g * kp.ih[1];
-        fy[G::N2 + i] = ctn * a;
-      }
-    } else {
-      // lane t = y node j: the neighbour's z-lines (kk, i) at fixed j
-      const int j = L.t;
-      double S[N], T[N];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double g = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < N; ++kk)
-          g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
-        const double a = nb[(hi ? 0 : N - 1) * G::KS + j * N + i];
-        S[i] = cna * a + cng * g * kp.ih[2];
-        T[i] = ctn * a;
-      }
-      double* fz = FZ + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + j * N;
-#pragma unroll
-      for (int q = 0; q < N; ++q) {
-        double s = 0.0, tt = 0.0;
+    for (int hi = 0; hi < 2; ++hi) {
+      const int f = 2 * axis + hi;
+      const double* c = cl.fc[L.cs][f];
+      const double cna = c[2], cng = c[3], ctn = c[5];
+      const double* nb = TB + L.cs * G::CTB + hi * G::ARR;   // layout k*KS + j*N + i
+      if (axis == 1) {
+        // lane k: columns i of the neighbour's plane k (nodal in i; interpolated in Q1)
+        double* fy = FY + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + k * N;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          s = fma(T_A<N>(q * N + i), S[i], s);
-          tt = fma(T_A<N>(q * N + i), T[i], tt);
+          double g = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+            g = fma(hi ? c_tab[N].d0[j] : c_tab[N].d1[j], nb[k * G::KS + j * N + i], g);
+          const double a = nb[k * G::KS + (hi ? 0 : N - 1) * N + i];
+          fy[i] = cna * a + cng * g * kp.ih[1];
+          fy[G::N2 + i] = ctn * a;
         }
-        fz[q] = s;
-        fz[G::N2 + q] = tt;
+      } else {
+        // lane t = y node j: the neighbour's z-lines (kk, i) at fixed j
+        const int j = L.t;
+        double S[N], T[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double g = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < N; ++kk)
+            g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
+          const double a = nb[(hi ? 0 : N - 1) * G::KS + j * N + i];
+          S[i] = cna * a + cng * g * kp.ih[2];
+          T[i] = ctn * a;
+        }
+        double* fz = FZ + L.cs * G::FS + (hi ? 2 : 0) * G::N2 + j * N;
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double s = 0.0, tt = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            s = fma(T_A<N>(q * N + i), S[i], s);
+            tt = fma(T_A<N>(q * N + i), T[i], tt);
+          }
+          fz[q] = s;
+          fz[G::N2 + q] = tt;
+        }
       }
     }
   }
@@ -356,13 +373,14 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
   if (L.active) {
     const int qy = L.t;
     const double* vcell = cl.vc[L.cs];
-    double U[N][N], R[N][N], Fy[N][N];   // [qz][qx], unweighted
+    double U[N][N], R[N][N];   // [qz][qx], unweighted
     if (vol) {
-      // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise
+      // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise; the y flux
+      // column goes straight through (A w)_z^T into TB (its t2y column has just been read)
       const double cK = vcell[1], cR = vcell[3];
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
-        double c0[N], c1[N];
+        double c0[N], c1[N], fy_[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
           c0[k] = tb[k * G::KS + qy * N + qx];
@@ -378,7 +396,14 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
           }
           U[qz][qx] = s;
           R[qz][qx] = cR * s;
-          Fy[qz][qx] = fma(cK, s1, -kp.sb[1] * s);
+          fy_[qz] = fma(cK, s1, -kp.sb[1] * s);
+        }
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          double s = 0.0;
+#pragma unroll
+          for (int qz = 0; qz < N; ++qz) s = fma(T_AW<N>(qz * N + k), fy_[qz], s);
+          tb[G::ARR + k * G::KS + qy * N + qx] = s;
         }
       }
       // x direction: rows qz;  R += DW^T (sK D U - sb U)
@@ -433,8 +458,9 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
           for (int k = 0; k < N; ++k) s = fma(T_A<N>(qz * N + k), c0[k], s);
           U[qz][qx] = s;
           R[qz][qx] = 0.0;
-          Fy[qz][qx] = 0.0;
         }
+#pragma unroll
+        for (int k = 0; k < N; ++k) tb[G::ARR + k * G::KS + qy * N + qx] = 0.0;
       }
     }
     // x faces at the face Gauss points (qz, qy): traces from the x-rows of U
@@ -507,19 +533,15 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
                           fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
     }
-    // (A w)_z^T on R and F_y, stored in place of t2 / t2y (same index set (., qy, .))
+    // (A w)_z^T on R, stored in place of t2 (same index set (., qy, .))
 #pragma unroll
     for (int qx = 0; qx < N; ++qx)
 #pragma unroll
       for (int k = 0; k < N; ++k) {
-        double s = 0.0, s1 = 0.0;
+        double s = 0.0;
 #pragma unroll
-        for (int qz = 0; qz < N; ++qz) {
-          s = fma(T_AW<N>(qz * N + k), R[qz][qx], s);
-          s1 = fma(T_AW<N>(qz * N + k), Fy[qz][qx], s1);
-        }
+        for (int qz = 0; qz < N; ++qz) s = fma(T_AW<N>(qz * N + k), R[qz][qx], s);
         tb[k * G::KS + qy * N + qx] = s;
-        tb[G::ARR + k * G::KS + qy * N + qx] = s1;
       }
   }
   __syncthreads();
