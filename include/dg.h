@@ -127,6 +127,17 @@ dg_status dg_fill_ghosts(dg_ctx* ctx, const double* lo, const double* hi, void* 
  * z[n], xq[n], wq[n], A[n*n], D[n*n], M[n*n], d0[n], d1[n] (5n + 3n^2 doubles). */
 dg_status dg_tables(int32_t p, double* out);
 
+/* Host-only (no GPU): the z-slab of `rank` among `nranks` for nz global layers,
+ * [floor(rank*nz/nranks), floor((rank+1)*nz/nranks)). */
+dg_status dg_slab_range(int32_t nz, int32_t rank, int32_t nranks, int32_t* z_begin, int32_t* z_end);
+
+/* Host-only (no GPU): the halo plan of desc's rank. out[0] = DoF offset (in the local vector) of
+ * the layer sent to the lower neighbour (or -1), out[1] = offset of the layer sent to the upper
+ * neighbour (or -1), out[2] = DoF per layer (nx*ny*n^3), out[3] = lower peer rank (or -1),
+ * out[4] = upper peer rank (or -1), out[5] = local DoF count. The lower ghost layer receives the
+ * lower peer's out[1] layer and the upper ghost its out[0] layer. */
+dg_status dg_halo_plan(const dg_desc* desc, int64_t out[6]);
+
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 broadcasts it to the other ranks). */
 dg_status dg_nccl_unique_id(void* out128);
 

@@ -87,6 +87,7 @@ struct dg_ctx {
   cudaStream_t last_stream = nullptr;
   bool have_stats = false;
   int32_t launches = 0;
+  int64_t plan[6] = {-1, -1, 0, -1, -1, 0};  // dg_halo_plan
 };
 
 namespace {
@@ -135,16 +136,16 @@ void release(dg_ctx* c) {
 
 dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
   if (c->desc.nranks == 1 || c->desc.halo_mode == DG_HALO_EXTERNAL) return DG_OK;
-  const int r = c->desc.rank, G = c->desc.nranks;
-  const size_t L = (size_t)c->layer_dof;
+  const int64_t* pl = c->plan;
+  const size_t L = (size_t)pl[2];
   ncclResult_t e = g_nccl.groupStart();
-  if (r > 0) {
-    e |= g_nccl.send(u, L, ncclFloat64, r - 1, c->comm, s);
-    e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, r - 1, c->comm, s);
+  if (pl[3] >= 0) {
+    e |= g_nccl.send(u + pl[0], L, ncclFloat64, (int)pl[3], c->comm, s);
+    e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, (int)pl[3], c->comm, s);
   }
-  if (r < G - 1) {
-    e |= g_nccl.send(u + (size_t)(c->nzl - 1) * L, L, ncclFloat64, r + 1, c->comm, s);
-    e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, r + 1, c->comm, s);
+  if (pl[4] >= 0) {
+    e |= g_nccl.send(u + pl[1], L, ncclFloat64, (int)pl[4], c->comm, s);
+    e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, (int)pl[4], c->comm, s);
   }
   e |= g_nccl.groupEnd();
   if (e != 0) return fail(DG_ERR_NCCL, "NCCL halo exchange failed");
@@ -196,8 +197,8 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   c->n = desc->p + 1;
   c->nd = c->n * c->n * c->n;
   const int G = desc->nranks, r = desc->rank;
-  c->z_begin = (int)((int64_t)r * desc->nz / G);
-  c->z_end = (int)((int64_t)(r + 1) * desc->nz / G);
+  dg_slab_range(desc->nz, r, G, &c->z_begin, &c->z_end);
+  dg_halo_plan(desc, c->plan);
   c->nzl = c->z_end - c->z_begin;
   const int64_t nxy = (int64_t)desc->nx * desc->ny;
   c->ncells = nxy * c->nzl;
@@ -444,6 +445,31 @@ dg_status dg_get_stats(dg_ctx* c, dg_stats* st) {
 }
 
 int32_t dg_last_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
+
+dg_status dg_slab_range(int32_t nz, int32_t rank, int32_t nranks, int32_t* zb, int32_t* ze) {
+  if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || nranks > nz || !zb || !ze)
+    return fail(DG_ERR_INVALID, "need nz >= nranks >= 1, 0 <= rank < nranks, non-NULL outputs");
+  *zb = (int32_t)((int64_t)rank * nz / nranks);
+  *ze = (int32_t)((int64_t)(rank + 1) * nz / nranks);
+  return DG_OK;
+}
+
+dg_status dg_halo_plan(const dg_desc* d, int64_t out[6]) {
+  if (!d || !out) return fail(DG_ERR_INVALID, "NULL argument");
+  if (d->p < 1 || d->p > 7 || d->nx < 1 || d->ny < 1) return fail(DG_ERR_INVALID, "bad desc");
+  int32_t zb, ze;
+  dg_status st = dg_slab_range(d->nz, d->rank, d->nranks, &zb, &ze);
+  if (st != DG_OK) return st;
+  const int64_t n = d->p + 1, layer = (int64_t)d->nx * d->ny * n * n * n;
+  const int64_t nzl = ze - zb;
+  out[0] = d->rank > 0 ? 0 : -1;
+  out[1] = d->rank < d->nranks - 1 ? (nzl - 1) * layer : -1;
+  out[2] = layer;
+  out[3] = d->rank > 0 ? d->rank - 1 : -1;
+  out[4] = d->rank < d->nranks - 1 ? d->rank + 1 : -1;
+  out[5] = nzl * layer;
+  return DG_OK;
+}
 
 dg_status dg_nccl_unique_id(void* out128) {
   if (!out128) return fail(DG_ERR_INVALID, "out is NULL");

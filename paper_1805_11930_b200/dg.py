@@ -24,7 +24,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_local_block_solve", "dg_set_local_solver", "dg_get_stats", "dg_apply_parts",
            "dg_block_diag_apply", "dg_ghost_layers", "dg_fill_ghosts", "dg_tables",
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
-           "dg_microbench_dfma"]
+           "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan"]
 
 
 class DGError(RuntimeError):
@@ -84,6 +84,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_version": ([], ctypes.c_char_p),
         "dg_nccl_unique_id": ([P], i32),
         "dg_microbench_dfma": ([P, i32, i32, ctypes.POINTER(i64), P], i32),
+        "dg_slab_range": ([i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
+        "dg_halo_plan": ([ctypes.POINTER(dg_desc), ctypes.POINTER(i64)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -112,6 +114,44 @@ def tables(p: int):
         out[name] = a[o:o + size].reshape((n, n) if size == n * n else (n,))
         o += size
     return out
+
+
+def slab_range(nz: int, rank: int, nranks: int):
+    """Host-only: this rank's z-layers [z_begin, z_end)."""
+    lib = load_library()
+    zb, ze = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib.dg_slab_range(nz, rank, nranks, ctypes.byref(zb), ctypes.byref(ze)))
+    return zb.value, ze.value
+
+
+def make_desc(problem, rank: int = 0, nranks: int = 1, device: int = 0, halo_mode: int = DG_HALO_NCCL):
+    """dg_desc for a synth.Problem (the arrays it points to are returned to keep them alive)."""
+    import numpy as np
+    P = problem
+    K = np.ascontiguousarray(np.asarray(P.K, dtype=np.float64))
+    c = None if P.c is None else np.ascontiguousarray(np.asarray(P.c, dtype=np.float64))
+    d = dg_desc()
+    d.nx, d.ny, d.nz = P.nx, P.ny, P.nz
+    d.Lx, d.Ly, d.Lz = P.Lx, P.Ly, P.Lz
+    d.bc[:] = list(P.bc)
+    d.p = P.p
+    d.alpha = P.alpha
+    d.k_components = 1 if K.ndim == 1 else 3
+    d.K = K.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    d.b[:] = list(P.b)
+    d.c = c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if c is not None else None
+    d.rank, d.nranks, d.halo_mode, d.device = rank, nranks, halo_mode, device
+    return d, (K, c)
+
+
+def halo_plan(problem, rank: int, nranks: int) -> dict:
+    """Host-only: the halo plan of dg_halo_plan as a dict."""
+    lib = load_library()
+    d, keep = make_desc(problem, rank, nranks)
+    out = (ctypes.c_int64 * 6)()
+    _check(lib.dg_halo_plan(ctypes.byref(d), out))
+    keys = ["send_lo_offset", "send_hi_offset", "layer_dof", "peer_lo", "peer_hi", "n_local_dof"]
+    return dict(zip(keys, list(out)))
 
 
 def nccl_unique_id() -> bytes:
@@ -155,24 +195,9 @@ class DGContext:
         P = problem
         if device is None:
             device = torch.cuda.current_device()
-        K = np.ascontiguousarray(np.asarray(P.K, dtype=np.float64))
-        kc = 1 if K.ndim == 1 else 3
-        c = None if P.c is None else np.ascontiguousarray(np.asarray(P.c, dtype=np.float64))
-        self._keep = (K, c)
-        d = dg_desc()
-        d.nx, d.ny, d.nz = P.nx, P.ny, P.nz
-        d.Lx, d.Ly, d.Lz = P.Lx, P.Ly, P.Lz
-        d.bc[:] = list(P.bc)
-        d.p = P.p
-        d.alpha = P.alpha
-        d.k_components = kc
-        d.K = K.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        d.b[:] = list(P.b)
-        d.c = c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if c is not None else None
-        d.rank, d.nranks, d.halo_mode = rank, nranks, halo_mode
+        d, self._keep = make_desc(P, rank, nranks, device, halo_mode)
         self._id = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
         d.nccl_id = ctypes.cast(self._id, ctypes.c_void_p) if self._id is not None else None
-        d.device = device
         self.device = device
         h = ctypes.c_void_p()
         _check(lib.dg_create(ctypes.byref(d), ctypes.byref(h)))
