@@ -120,6 +120,45 @@ __device__ __forceinline__ void stage_tile(double* TB, const double* __restrict_
     if (e < G::C * G::N3) TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = v[m];
   }
 }
+// base pointer of the face-f neighbour of local cell `cell` (u, or a ghost layer), nullptr at
+// the domain boundary -- the same rule as setup_cells, without waiting for it
+template <int N>
+__device__ __forceinline__ const double* nbr_ptr(const KParams& kp, const double* u, int cell, int f) {
+  constexpr int N3 = N * N * N;
+  const int nxy = kp.nx * kp.ny;
+  const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / nxy;
+  const int axis = f >> 1, hi = f & 1;
+  const int c = axis == 0 ? cx : (axis == 1 ? cy : cz);
+  const int dim = axis == 0 ? kp.nx : (axis == 1 ? kp.ny : kp.nzl);
+  const int step = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
+  const int nc = c + (hi ? 1 : -1);
+  if (nc >= 0 && nc < dim) return u + (size_t)(cell + (hi ? step : -step)) * N3;
+  if (kp.slab_face[f] == FK_GHOST) return (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)(cx + kp.nx * cy) * N3;
+  return nullptr;
+}
+// the group's own tile / a neighbour tile into registers (coalesced, all loads in flight)
+template <int N>
+__device__ __forceinline__ void load_own(double (&v)[Geo<N>::PER], const double* __restrict__ src,
+                                         int nvalid) {
+  using G = Geo<N>;
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    v[m] = (e < G::C * G::N3 && e / G::N3 < nvalid) ? __ldg(src + e) : 0.0;
+  }
+}
+template <int N>
+__device__ __forceinline__ void load_nbr_direct(double (&v)[Geo<N>::PER], const KParams& kp,
+                                                const double* u, int cell0, int f) {
+  using G = Geo<N>;
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    const int cell = cell0 + e / G::N3;
+    const double* p = (e < G::C * G::N3 && cell < kp.ncells) ? nbr_ptr<N>(kp, u, cell, f) : nullptr;
+    v[m] = p ? __ldg(p + e % G::N3) : 0.0;
+  }
+}
 // neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
 template <int N>
 __device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N>& cl, int f) {
@@ -172,7 +211,8 @@ __device__ __forceinline__ void write_plane(double* TB, const Lane& L, const dou
 // Must be called by all threads; leaves TB free. Face order f = 2*axis + hi.
 template <int N>
 __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& L, double* TB,
-                             double* FY, double* FX, double* FZ, const double* tile) {
+                             double* FY, double* FX, double* FZ, const double* tile,
+                             double (&pv0)[Geo<N>::PER], double (&pv1)[Geo<N>::PER]) {
   using G = Geo<N>;
   const int k = L.t;
   // x faces: the neighbour is usually the next / previous cell of the group, whose tile is
@@ -220,9 +260,6 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& 
   }
   // y / z neighbours: two tiles per round (the y pair, then the z pair) staged into the two
   // halves of TB; the z pair's global loads are in flight while the y traces are extracted.
-  double pv0[G::PER], pv1[G::PER];
-  load_nbr<N>(pv0, cl, 2);
-  load_nbr<N>(pv1, cl, 3);
 #pragma unroll 1
   for (int axis = 1; axis < 3; ++axis) {
     __syncthreads();
@@ -656,11 +693,19 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   const Lane L = lane_id<N>();
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  stage_tile<N>(TB, u + (size_t)cell0 * G::N3, nvalid);
+  // all global loads of the own tile and the y-neighbour pair are in flight during the setup
+  double own[G::PER], pv0[G::PER], pv1[G::PER];
+  load_own<N>(own, u + (size_t)cell0 * G::N3, nvalid);
   setup<N>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
+  if (NBR) {
+    load_nbr<N>(pv0, cl, 2);
+    load_nbr<N>(pv1, cl, 3);
+  }
+  store_tile<N>(TB, own);
+  __syncthreads();
   double in[N][N], o[N][N];
   read_plane<N>(TB, L, in);
-  if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3);
+  if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3, pv0, pv1);
   else __syncthreads();
   plane_op<N, NBR>(kp, cl, L, rw, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
@@ -695,7 +740,10 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   read_plane<N>(TB, L, P);
   if (SWEEP) {
     double Q[N][N];
-    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    double pv0[G::PER], pv1[G::PER];
+    load_nbr<N>(pv0, cl, 2);
+    load_nbr<N>(pv1, cl, 3);
+    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     plane_op<N, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
@@ -827,7 +875,10 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   read_plane<N>(TB, L, W);
   if (SWEEP) {
     double T[N][N];
-    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    double pv0[G::PER], pv1[G::PER];
+    load_nbr<N>(pv0, cl, 2);
+    load_nbr<N>(pv1, cl, 3);
+    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     plane_op<N, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
