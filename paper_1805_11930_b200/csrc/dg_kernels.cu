@@ -143,6 +143,7 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
   const int t = threadIdx.x;
   const int nxy = kp.nx * kp.ny;
   const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+  const int c0x = cell0 % kp.nx, c0y = (cell0 / kp.nx) % kp.ny, c0z = cell0 / nxy;
   for (int it = t; it < C * 6; it += NT) {
     const int cs = it / 6, f = it % 6, axis = f >> 1, hi = f & 1;
     const int cell = cell0 + cs;
@@ -154,19 +155,23 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
       double* vc = vc_[cs];
       if (valid && (kp.mask & 1u)) {
         const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
-        vc[0] = vol * Kc[0] / (kp.h[0] * kp.h[0]);
-        vc[1] = vol * Kc[1] / (kp.h[1] * kp.h[1]);
-        vc[2] = vol * Kc[2] / (kp.h[2] * kp.h[2]);
+        vc[0] = Kc[0] * vol * kp.ih[0] * kp.ih[0];
+        vc[1] = Kc[1] * vol * kp.ih[1] * kp.ih[1];
+        vc[2] = Kc[2] * vol * kp.ih[2] * kp.ih[2];
         vc[3] = kp.c ? vol * kp.c[cell] : 0.0;
       } else {
         vc[0] = vc[1] = vc[2] = vc[3] = 0.0;
       }
     }
     if (valid) {
-      const int coord[3] = {cell % kp.nx, (cell / kp.nx) % kp.ny, cell / nxy};
+      // coordinates of cell0 + cs without per-item integer division (cs < C is small)
+      int cx = c0x + cs, cy = c0y, cz = c0z;
+      while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
+      while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
+      const int coord[3] = {cx, cy, cz};
       const int dims[3] = {kp.nx, kp.ny, kp.nzl};
       const int dstep[3] = {1, kp.nx, nxy};
-      const double hk = kp.h[axis];
+      const double ihk = kp.ih[axis];
       const double KT = kp.K[(size_t)(cell + nxy) * 3 + axis];
       const int ncoord = coord[axis] + (hi ? 1 : -1);
       int kind;  // 0 interior, 1 Dirichlet, 2 Neumann
@@ -191,21 +196,22 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
       if (kind == 0 && (kp.mask & 2u)) {
         const double KN = kp.K[(size_t)kidx * 3 + axis];
         const double s = KT + KN;
-        const double wT = s > 0.0 ? KN / s : 0.5, wN = s > 0.0 ? KT / s : 0.5;
-        const double gam = kp.pen * (s > 0.0 ? 2.0 * KT * KN / s : 0.0) / hk;  // <dT,dN>|F|/|T|
+        const double rs = s > 0.0 ? 1.0 / s : 0.0;   // the only division of the face setup
+        const double wT = s > 0.0 ? KN * rs : 0.5, wN = s > 0.0 ? KT * rs : 0.5;
+        const double gam = kp.pen * (2.0 * KT * KN * rs) * ihk;  // <dT,dN>|F|/|T|
         if (hi) {
           co[0] = fmax(bn, 0.0) + gam;  co[1] = -wT * KT;
           co[2] = fmin(bn, 0.0) - gam;  co[3] = -wN * KN;
-          co[4] = -wT * KT / hk;        co[5] = wT * KT / hk;
+          co[4] = -wT * KT * ihk;       co[5] = wT * KT * ihk;
         } else {
           co[0] = fmax(-bn, 0.0) + gam; co[1] = wT * KT;
           co[2] = fmin(-bn, 0.0) - gam; co[3] = wN * KN;
-          co[4] = wT * KT / hk;         co[5] = -wT * KT / hk;
+          co[4] = wT * KT * ihk;        co[5] = -wT * KT * ihk;
         }
       } else if (kind == 1 && (kp.mask & 4u)) {
-        const double gam = kp.pen * KT / hk;  // delta |F| / |T|
-        if (hi) { co[0] = fmax(bn, 0.0) + gam;  co[1] = -KT; co[4] = -KT / hk; }
-        else    { co[0] = fmax(-bn, 0.0) + gam; co[1] = KT;  co[4] = KT / hk; }
+        const double gam = kp.pen * KT * ihk;  // delta |F| / |T|
+        if (hi) { co[0] = fmax(bn, 0.0) + gam;  co[1] = -KT; co[4] = -KT * ihk; }
+        else    { co[0] = fmax(-bn, 0.0) + gam; co[1] = KT;  co[4] = KT * ihk; }
       }
       if (kind != 0) nbp = nullptr;
     }
