@@ -47,10 +47,13 @@ template <int N_> struct Geo {
 
 template <int N> struct Cells {
   static constexpr int C = Geo<N>::C;
+  static constexpr int BS = 2 * N * N + 1;   // odd stride: the cells of a half-warp hit distinct banks
   double vc[C][4];
   double fc[C][6][6];
   const double* nb[C][6];
   int cell[C];
+  // per-cell self-face operators at the Gauss points: B[cs][0] acts on x-rows, B[cs][1] on z-columns
+  double B[C][BS];
 };
 
 // per-lane identity
@@ -327,7 +330,7 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& 
 // The quadrature-point residual R is kept UNWEIGHTED: the Gauss weights (and |T|, face
 // areas through kp) are folded into the transposed 1D tables AW = A w, GW = G w,
 // DW = D w_q / w_r and the end-point injection vectors E/w, F/w.
-template <int N, bool NBR>
+template <int N, bool NBR, bool USEB>
 __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, const Lane& L,
                                          const Rows<N>& rw, bool vol, const double (&in)[N][N],
                                          double (&out)[N][N], double* TB, double* FY,
@@ -500,8 +503,8 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
         for (int k = 0; k < N; ++k) tb[G::ARR + k * G::KS + qy * N + qx] = 0.0;
       }
     }
-    // x faces at the face Gauss points (qz, qy): traces from the x-rows of U
-    {
+    if (!USEB) {
+      // x faces at the face Gauss points (qz, qy): traces from the x-rows of U
       const double* clo = fc + 0 * 6;
       const double* chi = fc + 1 * 6;
       const double* fx = FX + L.cs * G::FS;
@@ -534,11 +537,9 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
           R[qz][q] += fma(c_tab[N].E0W[q], Slo,
                           fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
-    }
-    // z faces at the face Gauss points (qy, qx): traces from the z-columns of U
-    {
-      const double* clo = fc + 4 * 6;
-      const double* chi = fc + 5 * 6;
+      // z faces at the face Gauss points (qy, qx): traces from the z-columns of U
+      const double* zlo = fc + 4 * 6;
+      const double* zhi = fc + 5 * 6;
       const double* fz = FZ + L.cs * G::FS;
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
@@ -550,8 +551,8 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
           glo = fma(c_tab[N].F0[q], U[q][qx], glo);
           ghi = fma(c_tab[N].F1[q], U[q][qx], ghi);
         }
-        double Slo = fma(clo[0], alo, clo[1] * glo * kp.ih[2]), Tlo = clo[4] * alo;
-        double Shi = fma(chi[0], ahi, chi[1] * ghi * kp.ih[2]), Thi = chi[4] * ahi;
+        double Slo = fma(zlo[0], alo, zlo[1] * glo * kp.ih[2]), Tlo = zlo[4] * alo;
+        double Shi = fma(zhi[0], ahi, zhi[1] * ghi * kp.ih[2]), Thi = zhi[4] * ahi;
         if (NBR) {  // neighbour traces at (j, qx) -> interpolate in y (row qy of A)
 #pragma unroll
           for (int j = 0; j < N; ++j) {
@@ -562,13 +563,87 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
             Thi = fma(A, fz[3 * G::N2 + j * N + qx], Thi);
           }
         }
-        const double fa = kp.fa[2];
-        Slo *= fa; Tlo *= fa; Shi *= fa; Thi *= fa;
+        const double fb = kp.fa[2];
+        Slo *= fb; Tlo *= fb; Shi *= fb; Thi *= fb;
 #pragma unroll
         for (int q = 0; q < N; ++q)
           R[q][qx] += fma(c_tab[N].E0W[q], Slo,
                           fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
+    } else {
+      // x and z self faces: the per-cell Gauss-point operators B (rows / columns of U)
+    {
+      const double* Bc = cl.B[L.cs];
+      double Bm[N][N];
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r) Bm[q][r] = Bc[q * N + r];
+#pragma unroll
+      for (int qz = 0; qz < N; ++qz)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double s = R[qz][q];
+#pragma unroll
+          for (int r = 0; r < N; ++r) s = fma(Bm[q][r], U[qz][r], s);
+          R[qz][q] = s;
+        }
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+#pragma unroll
+        for (int r = 0; r < N; ++r) Bm[q][r] = Bc[G::N2 + q * N + r];
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx)
+#pragma unroll
+        for (int q = 0; q < N; ++q) {
+          double s = R[q][qx];
+#pragma unroll
+          for (int r = 0; r < N; ++r) s = fma(Bm[q][r], U[r][qx], s);
+          R[q][qx] = s;
+        }
+    }
+    if (NBR) {
+      // neighbour traces of the x faces at (k, qy) -> interpolate in z; inject through A^-T / w
+      const double* fx = FX + L.cs * G::FS;
+      const double fa = kp.fa[0];
+#pragma unroll
+      for (int qz = 0; qz < N; ++qz) {
+        double Slo = 0.0, Tlo = 0.0, Shi = 0.0, Thi = 0.0;
+#pragma unroll
+        for (int k = 0; k < N; ++k) {
+          const double A = T_A<N>(qz * N + k);
+          Slo = fma(A, fx[0 * G::N2 + k * N + qy], Slo);
+          Tlo = fma(A, fx[1 * G::N2 + k * N + qy], Tlo);
+          Shi = fma(A, fx[2 * G::N2 + k * N + qy], Shi);
+          Thi = fma(A, fx[3 * G::N2 + k * N + qy], Thi);
+        }
+        Slo *= fa; Tlo *= fa; Shi *= fa; Thi *= fa;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          R[qz][q] += fma(c_tab[N].E0W[q], Slo,
+                          fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
+      }
+      // neighbour traces of the z faces at (j, qx) -> interpolate in y (row qy of A)
+      const double* fz = FZ + L.cs * G::FS;
+      const double fb = kp.fa[2];
+#pragma unroll
+      for (int qx = 0; qx < N; ++qx) {
+        double Slo = 0.0, Tlo = 0.0, Shi = 0.0, Thi = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double A = rw.Arow[j];
+          Slo = fma(A, fz[0 * G::N2 + j * N + qx], Slo);
+          Tlo = fma(A, fz[1 * G::N2 + j * N + qx], Tlo);
+          Shi = fma(A, fz[2 * G::N2 + j * N + qx], Shi);
+          Thi = fma(A, fz[3 * G::N2 + j * N + qx], Thi);
+        }
+        Slo *= fb; Tlo *= fb; Shi *= fb; Thi *= fb;
+#pragma unroll
+        for (int q = 0; q < N; ++q)
+          R[q][qx] += fma(c_tab[N].E0W[q], Slo,
+                          fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
+      }
+    }
     }
     // (A w)_z^T on R, stored in place of t2 (same index set (., qy, .))
 #pragma unroll
@@ -671,10 +746,29 @@ __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>
 }
 
 // =============================== kernels ================================================
-template <int N>
+// Self-face operator of the x (z) faces at the Gauss points, unweighted quadrature level:
+//   B[q][r] = |F| sum_{s=lo,hi} ( E_s^w[q] (cs_a E_s[r] + cs_g F_s[r] / h) + F_s^w[q] ct_a E_s[r] ),
+// i.e. traces a_s = E_s.U, g_s = F_s.U of a Gauss-value line U, the flux combinations
+// S = cs_a a + cs_g g / h, T = ct_a a, and their injection through A^-T / w (see plane_op).
+template <int N, bool USEB = true>
 __device__ __forceinline__ void setup(const KParams& kp, Cells<N>& cl, int cell0, const double* u) {
   using G = Geo<N>;
   setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.fc, cl.nb, cl.cell, cell0, u);
+  if (!USEB) return;
+  for (int it = threadIdx.x; it < G::C * 2 * G::N2; it += G::NT) {
+    const int cs = it / (2 * G::N2), rem = it % (2 * G::N2), d = rem / G::N2;
+    const int q = (rem % G::N2) / N, r = rem % N;
+    const int axis = d == 0 ? 0 : 2;
+    const double* lo = cl.fc[cs][2 * axis];
+    const double* hi = cl.fc[cs][2 * axis + 1];
+    const double ih = kp.ih[axis];
+    double b = c_tab[N].E0W[q] * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) +
+               c_tab[N].F0W[q] * lo[4] * c_tab[N].E0[r];
+    b += c_tab[N].E1W[q] * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) +
+         c_tab[N].F1W[q] * hi[4] * c_tab[N].E1[r];
+    cl.B[cs][d * G::N2 + q * N + r] = b * kp.fa[axis];
+  }
+  __syncthreads();
 }
 
 // out = A u (with_nbr) or D_T u, selected parts by kp.mask
@@ -696,7 +790,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   // all global loads of the own tile and the y-neighbour pair are in flight during the setup
   double own[G::PER], pv0[G::PER], pv1[G::PER];
   load_own<N>(own, u + (size_t)cell0 * G::N3, nvalid);
-  setup<N>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
+  setup<N, false>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
   if (NBR) {
     load_nbr<N>(pv0, cl, 2);
     load_nbr<N>(pv1, cl, 3);
@@ -707,7 +801,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   read_plane<N>(TB, L, in);
   if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3, pv0, pv1);
   else __syncthreads();
-  plane_op<N, NBR>(kp, cl, L, rw, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
+  plane_op<N, NBR, false>(kp, cl, L, rw, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
@@ -744,7 +838,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     load_nbr<N>(pv0, cl, 2);
     load_nbr<N>(pv1, cl, 3);
     nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
-    plane_op<N, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
+    plane_op<N, true, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
@@ -791,7 +885,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     const int done = __syncthreads_and(conv || !L.active);
     if (done || iter >= kp.max_it) break;
     double Q[N][N];
-    plane_op<N, false>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+    plane_op<N, false, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
     double pq = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -879,7 +973,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     load_nbr<N>(pv0, cl, 2);
     load_nbr<N>(pv1, cl, 3);
     nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
-    plane_op<N, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
+    plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
@@ -963,7 +1057,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       }
     rst = false;
     double T[N][N];
-    plane_op<N, false>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
+    plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
     double rv = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -995,7 +1089,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       conv = true;
       ++its;
     }
-    plane_op<N, false>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
+    plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
     double ts = 0.0, tt = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
