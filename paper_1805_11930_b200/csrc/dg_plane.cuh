@@ -571,37 +571,25 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
                           fma(c_tab[N].F0W[q], Tlo, fma(c_tab[N].E1W[q], Shi, c_tab[N].F1W[q] * Thi)));
       }
     } else {
-      // x and z self faces: the per-cell Gauss-point operators B (rows / columns of U)
-    {
+      // x and z self faces: the per-cell Gauss-point operators B (rows / columns of U), read
+      // from shared memory at the point of use (broadcast within the cell's lanes)
       const double* Bc = cl.B[L.cs];
-      double Bm[N][N];
 #pragma unroll
       for (int q = 0; q < N; ++q)
 #pragma unroll
-        for (int r = 0; r < N; ++r) Bm[q][r] = Bc[q * N + r];
+        for (int r = 0; r < N; ++r) {
+          const double bx = Bc[q * N + r];
 #pragma unroll
-      for (int qz = 0; qz < N; ++qz)
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          double s = R[qz][q];
-#pragma unroll
-          for (int r = 0; r < N; ++r) s = fma(Bm[q][r], U[qz][r], s);
-          R[qz][q] = s;
+          for (int qz = 0; qz < N; ++qz) R[qz][q] = fma(bx, U[qz][r], R[qz][q]);
         }
 #pragma unroll
       for (int q = 0; q < N; ++q)
 #pragma unroll
-        for (int r = 0; r < N; ++r) Bm[q][r] = Bc[G::N2 + q * N + r];
+        for (int r = 0; r < N; ++r) {
+          const double bz = Bc[G::N2 + q * N + r];
 #pragma unroll
-      for (int qx = 0; qx < N; ++qx)
-#pragma unroll
-        for (int q = 0; q < N; ++q) {
-          double s = R[q][qx];
-#pragma unroll
-          for (int r = 0; r < N; ++r) s = fma(Bm[q][r], U[r][qx], s);
-          R[q][qx] = s;
+          for (int qx = 0; qx < N; ++qx) R[q][qx] = fma(bz, U[r][qx], R[q][qx]);
         }
-    }
     if (NBR) {
       // neighbour traces of the x faces at (k, qy) -> interpolate in z; inject through A^-T / w
       const double* fx = FX + L.cs * G::FS;
