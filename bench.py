@@ -308,6 +308,21 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = t.item()
 
+    # ---- the volume kernel alone (a^v terms, Stages 1-3; north_star's >= 50 % target at p >= 3)
+    vol_calls = 20
+    for _ in range(3):
+        ctx.apply_parts(u, Au, dg.MASK_VOLUME)
+    flush.fill_(1.0)
+    a, b = ev(), ev()
+    a.record(stream)
+    for _ in range(vol_calls):
+        ctx.apply_parts(u, Au, dg.MASK_VOLUME)
+    b.record(stream)
+    torch.cuda.synchronize()
+    vol_s = a.elapsed_time(b) * 1e-3 / vol_calls
+    n = P.p + 1
+    vol_flops = (ctx.cell_end - ctx.cell_begin) * (24 * n ** 4 + 8 * n ** 3)
+
     # ---- fp64 peak: derived and measured (DFMA microbenchmark)
     sink = torch.empty(148 * 8 * 256, dtype=torch.float64, device=dev)
     dg.microbench_dfma(sink, 148 * 8, 1000)
@@ -366,6 +381,9 @@ def run_ours(args):
                   "frac_fp64_peak": sweep_launch_flops / sweep_launch_s / 1e12 / peak_derived,
                   "local_iterations_mean": it_stats[0]["it_mean"], "local_iterations_max": it_stats[0]["it_max"],
                   "local_nonconverged": it_stats[0]["n_nonconverged"]},
+        "volume_kernel": {"us_per_call": vol_s * 1e6, "gflops_model": vol_flops / vol_s / 1e9,
+                          "frac_fp64_peak": vol_flops / vol_s / 1e12 / peak_derived,
+                          "model": "24 n^4 + 8 n^3 flop per cell (SURVEY 8(d)); dg_apply_parts(mask=volume)"},
         "roofline": {"bound": "alu", "kernel": "k_cg<4,true> (fused defect + local CG + update)"
                      if dominant == "sweep" else "k_apply<4>",
                      "achieved": achieved, "peak": peak_derived, "unit": "TFLOP/s",

@@ -23,6 +23,7 @@
 #include "dg_kernels.h"
 
 #include <cstdio>
+#include <cstdlib>
 
 namespace dg {
 namespace {
@@ -963,48 +964,66 @@ cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, c
   return cudaGetLastError();
 }
 
+// DG_KERNEL_FAMILY=line forces the line-per-thread kernels for every degree (A/B comparisons).
+static bool force_line() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DG_KERNEL_FAMILY");
+    v = (e && e[0] == 'l') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Kernel family of the operator application per degree, chosen by measurement on C1-C5
+// (profiles/r01_kernel_family.md): the plane kernels win for n = 2, 4; at n = 3 and 5 the
+// line kernels' higher occupancy wins for a single application. The local solvers always use
+// the plane kernels for n <= 5 (register-resident Krylov vectors).
+template <int N> constexpr bool plane_apply() { return N == 2 || N == 4; }
+
 template <int N>
 cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
-  if constexpr (N <= 5) {
-    using G = pk::Geo<N>;
-    const int grid = (kp.ncells + G::C - 1) / G::C;
-    if (grid == 0) return cudaSuccess;
-    const size_t smem = pk::smem_apply<N>();
-    auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<grid, G::NT, smem, s>>>(kp, u, out);
-    return cudaGetLastError();
-  } else {
-    using G = Geo<N>;
-    const int grid = (kp.ncells + G::C - 1) / G::C;
-    if (grid == 0) return cudaSuccess;
-    const size_t smem = smem_bytes<N>(3);
-    cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
-    return cudaGetLastError();
+  if constexpr (plane_apply<N>()) {
+    if (!force_line()) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      const size_t smem = pk::smem_apply<N>();
+      auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, G::NT, smem, s>>>(kp, u, out);
+      return cudaGetLastError();
+    }
   }
+  using G = Geo<N>;
+  const int grid = (kp.ncells + G::C - 1) / G::C;
+  if (grid == 0) return cudaSuccess;
+  const size_t smem = smem_bytes<N>(3);
+  cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
+  return cudaGetLastError();
 }
 
 template <int N, bool SWEEP>
 cudaError_t solve_n(int method, const KParams& kp, const double* in, const double* f, double* out,
                     cudaStream_t s) {
   if constexpr (N <= 5) {
-    using G = pk::Geo<N>;
-    const int grid = (kp.ncells + G::C - 1) / G::C;
-    if (grid == 0) return cudaSuccess;
-    if (method == LM_BICGSTAB)
-      return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
-    return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
-  } else {
-    using G = Geo<N>;
-    const int grid = (kp.ncells + G::C - 1) / G::C;
-    if (grid == 0) return cudaSuccess;
-    if (method == LM_BICGSTAB)
-      return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
-    return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
+    if (!force_line()) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      if (method == LM_BICGSTAB)
+        return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+      return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
+    }
   }
+  using G = Geo<N>;
+  const int grid = (kp.ncells + G::C - 1) / G::C;
+  if (grid == 0) return cudaSuccess;
+  if (method == LM_BICGSTAB)
+    return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
+  return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
 }
 
 #define DG_DISPATCH(p, CALL)             \
@@ -1063,7 +1082,9 @@ bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
 }
 
 cudaError_t launch_apply(int p, const KParams& kp, const double* u, double* out, cudaStream_t s) {
-  DG_DISPATCH(p, (apply_n<N>(kp, u, out, s, 1)));
+  // without interior-face terms no neighbour data is needed (e.g. the volume-only hook)
+  const int with_nbr = (kp.mask & 2u) ? 1 : 0;
+  DG_DISPATCH(p, (apply_n<N>(kp, u, out, s, with_nbr)));
 }
 
 cudaError_t launch_block_diag_apply(int p, const KParams& kp, const double* u, double* out,
