@@ -5,13 +5,15 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libdg_b200.so")
-SOURCES = ["dg_kernels.cu", "dg_api.cpp", "dg_tables.cpp"]
+# one translation unit per degree n = p+1 (compiled in parallel), the dispatch, the C ABI, tables
+SOURCES = [f"dg_kernels_n{n}.cu" for n in range(2, 9)] + ["dg_kernels.cu", "dg_api.cpp", "dg_tables.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -35,7 +37,7 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    jobs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", INCLUDE, "-I", CSRC,
               *ARCH, *extra]
     for src in SOURCES:
@@ -45,8 +47,13 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             cmd += ["-Xptxas", "-v"] if verbose else []
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        jobs.append((cmd, obj))
+    # the biggest units first; each nvcc is single-threaded
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for r in ex.map(lambda j: subprocess.run(j[0], capture_output=not verbose, text=True), jobs):
+            if r.returncode != 0:
+                raise RuntimeError("nvcc failed: " + " ".join(r.args) + "\n" + (r.stderr or "")[-4000:])
+    objs = [o for _, o in jobs]
     tmp = LIB + ".tmp"
     cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)

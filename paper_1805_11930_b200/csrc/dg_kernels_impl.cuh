@@ -1,0 +1,1070 @@
+// fp64 sm_100a kernels of the matrix-free DG hot path (arXiv 1805.11930).
+// Included once per degree by dg_kernels_n<N>.cu (one translation unit per n = p+1, so the
+// degrees compile in parallel); each unit instantiates Deg<N> at the end of this file.
+//
+// One CTA owns a group of C consecutive cells (contiguous in the cell-major DoF
+// vector, so tile loads/stores are fully coalesced). Each cell tensor lives in
+// shared memory with a padded (bank-conflict-reduced) layout; every pass maps one
+// thread to one 1D line of n values along x, y or z and applies an n x n 1D
+// matrix held in __constant__ memory with compile-time indices (so the matrix
+// entries are uniform constant-bank operands of DFMA, no shared-memory traffic).
+//
+//  Volume (§3.1), with collocation derivatives at the Gauss points:
+//    Stage 1  U = (A_z A_y A_x) u                          passes P1-P3
+//    Stage 2  F_k = W|T|(K_k/h_k^2 D_k U - b_k/h_k U), F_0 = W|T| c U
+//    Stage 3  v = (A_x^T A_y^T A_z^T)(F_0 + sum_k D_k^T F_k)   passes P3-P7
+//  Faces: per face node the value/normal-derivative traces
+//    of the cell (and, for A, of the neighbour) are combined into a value-test
+//    array S and a derivative-test array T, the tangential face mass
+//    (h M^ x h M^, exact Gauss quadrature with m = n) is applied, and the result is
+//    scattered with the 1D end-point profiles (e0/e1, d0/d1) in the last pass.
+//  D_T = the same with only the cell's own face traces.
+//  Local solves: Jacobi-preconditioned CG or BiCGStab per
+//    cell, all C cells of a CTA iterating together with per-cell convergence masks
+//    and deterministic per-cell reductions (no atomics).
+#include "dg_kernels.h"
+#include "dg_degree.h"
+
+#include <cstdio>
+#include <cstdlib>
+
+namespace dg {
+namespace {
+
+struct DevTab {
+  double A[64], D[64], M[64], G[64];
+  double w[8], d0[8], d1[8], Sd[8], Cd[8], Md[8];
+  double E0[8], E1[8], F0[8], F1[8];  // A^-T e0, A^-T e1, A^-T d0, A^-T d1 (trace/derivative at 0/1 from Gauss values)
+  // weight-folded variants for the unweighted quadrature residual of the plane kernels:
+  double AW[64], GW[64];              // A[q][j] w_q, G[q][j] w_q
+  double DW[64];                      // D[q][r] w_q / w_r
+  double E0W[8], E1W[8], F0W[8], F1W[8];  // E0/w, E1/w, F0/w, F1/w
+};
+__constant__ DevTab c_tab[kMaxN + 1];
+
+// Padded tensor layout per n: element (i,j,k) of cell slot cs at cs*CS + k*ZS + j*YS + i.
+// Chosen offline to minimise shared-memory bank conflicts of x/y/z line passes.
+template <int N> struct Lay;
+template <> struct Lay<2> { static constexpr int YS = 2, ZS = 5, CS = 12; };
+template <> struct Lay<3> { static constexpr int YS = 3, ZS = 9, CS = 27; };
+template <> struct Lay<4> { static constexpr int YS = 4, ZS = 19, CS = 76; };
+template <> struct Lay<5> { static constexpr int YS = 5, ZS = 25, CS = 125; };
+template <> struct Lay<6> { static constexpr int YS = 9, ZS = 54, CS = 324; };
+template <> struct Lay<7> { static constexpr int YS = 7, ZS = 52, CS = 369; };
+template <> struct Lay<8> { static constexpr int YS = 9, ZS = 72, CS = 576; };
+
+// cells per CTA
+template <int N> struct Cells;
+template <> struct Cells<2> { static constexpr int C = 32; };
+template <> struct Cells<3> { static constexpr int C = 32; };
+template <> struct Cells<4> { static constexpr int C = 16; };
+template <> struct Cells<5> { static constexpr int C = 8; };
+template <> struct Cells<6> { static constexpr int C = 4; };
+template <> struct Cells<7> { static constexpr int C = 4; };
+template <> struct Cells<8> { static constexpr int C = 2; };
+
+template <int N_> struct Geo {
+  static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
+  static constexpr int C = Cells<N>::C;
+  static constexpr int YS = Lay<N>::YS, ZS = Lay<N>::ZS, CS = Lay<N>::CS;
+  static constexpr int LINES = C * N2;
+  static constexpr int NT = ((LINES + 31) / 32) * 32;
+  static constexpr int TENSOR = C * CS;
+  static constexpr int FACE = C * 12 * N2;
+};
+
+template <int N> struct Group {
+  static constexpr int C = Cells<N>::C;
+  int cell[C];
+  double vc[C][4];              // |T|K_x/h_x^2, |T|K_y/h_y^2, |T|K_z/h_z^2, |T|c
+  double fc[C][6][6];           // per face: cs_a, cs_g, cn_a, cn_g, ct_a, ct_n
+  const double* nb[C][6];       // neighbour cell base pointer (nullptr: none / not needed)
+  double tw[N], td0[N], td1[N]; // runtime-indexed copies of w, d0, d1
+  double red[2][C * N * N];     // per-line partial sums
+  double sc[8][C];              // per-cell solver scalars
+  int conv[C], its[C], rst[C];
+};
+
+enum { S_RR0 = 0, S_RZ, S_ALPHA, S_BETA, S_RHO, S_OMEGA, S_RHON, S_TMP };
+
+// ---- table access with compile-time indices (constant-bank operands) ---------
+template <int N, int W> __device__ __forceinline__ double tab(int idx) {
+  if constexpr (W == 0) return c_tab[N].A[idx];
+  else if constexpr (W == 1) return c_tab[N].D[idx];
+  else return c_tab[N].M[idx];
+}
+
+// out[q] = sum_j M[q][j] in[j]
+template <int N, int W> __device__ __forceinline__ void mv(const double* in, double* out) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(tab<N, W>(q * N + j), in[j], s);
+    out[q] = s;
+  }
+}
+// out[j] = sum_q M[q][j] in[q]
+template <int N, int W> __device__ __forceinline__ void mtv(const double* in, double* out) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) s = fma(tab<N, W>(q * N + j), in[q], s);
+    out[j] = s;
+  }
+}
+
+template <int N, int S> __device__ __forceinline__ void ld(const double* p, double* v) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) v[e] = p[e * S];
+}
+template <int N, int S> __device__ __forceinline__ void st(double* p, const double* v) {
+#pragma unroll
+  for (int e = 0; e < N; ++e) p[e * S] = v[e];
+}
+
+// Stage 2 + the derivative half of stage 3 along one line of direction k:
+// R += D^T ( Wl * w_q * (sK * (D U)_q - sb * U_q) )
+template <int N> __device__ __forceinline__ void dir_term(const double* U, double* R, double Wl,
+                                                          double sK, double sb) {
+  double du[N], F[N], t[N];
+  mv<N, 1>(U, du);
+#pragma unroll
+  for (int q = 0; q < N; ++q) F[q] = Wl * c_tab[N].w[q] * fma(sK, du[q], -sb * U[q]);
+  mtv<N, 1>(F, t);
+#pragma unroll
+  for (int r = 0; r < N; ++r) R[r] += t[r];
+}
+
+// ---- group setup: coefficients, face parameters, neighbour pointers ------------
+// Per cell of the group: volume scalings vc, face coefficients fc, neighbour pointers nb
+// (nullptr when u == nullptr, i.e. for D_T-only operators). Ends with __syncthreads.
+template <int N, int C, int NT>
+__device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6][6],
+                            const double* (*nb_)[6], int* cellv, int cell0, const double* u) {
+  constexpr int N3 = N * N * N;
+  const int t = threadIdx.x;
+  const int nxy = kp.nx * kp.ny;
+  const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+  const int c0x = cell0 % kp.nx, c0y = (cell0 / kp.nx) % kp.ny, c0z = cell0 / nxy;
+  for (int it = t; it < C * 6; it += NT) {
+    const int cs = it / 6, f = it % 6, axis = f >> 1, hi = f & 1;
+    const int cell = cell0 + cs;
+    const bool valid = cell < kp.ncells;
+    double co[6] = {0, 0, 0, 0, 0, 0};
+    const double* nbp = nullptr;
+    if (f == 0) {
+      if (cellv) cellv[cs] = valid ? cell : -1;
+      double* vc = vc_[cs];
+      if (valid && (kp.mask & 1u)) {
+        const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
+        vc[0] = Kc[0] * vol * kp.ih[0] * kp.ih[0];
+        vc[1] = Kc[1] * vol * kp.ih[1] * kp.ih[1];
+        vc[2] = Kc[2] * vol * kp.ih[2] * kp.ih[2];
+        vc[3] = kp.c ? vol * kp.c[cell] : 0.0;
+      } else {
+        vc[0] = vc[1] = vc[2] = vc[3] = 0.0;
+      }
+    }
+    if (valid) {
+      // coordinates of cell0 + cs without per-item integer division (cs < C is small)
+      int cx = c0x + cs, cy = c0y, cz = c0z;
+      while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
+      while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
+      const int coord[3] = {cx, cy, cz};
+      const int dims[3] = {kp.nx, kp.ny, kp.nzl};
+      const int dstep[3] = {1, kp.nx, nxy};
+      const double ihk = kp.ih[axis];
+      const double KT = kp.K[(size_t)(cell + nxy) * 3 + axis];
+      const int ncoord = coord[axis] + (hi ? 1 : -1);
+      int kind;  // 0 interior, 1 Dirichlet, 2 Neumann
+      long kidx = 0;
+      if (ncoord >= 0 && ncoord < dims[axis]) {
+        kind = 0;
+        const long nb = cell + (hi ? dstep[axis] : -dstep[axis]);
+        kidx = nb + nxy;
+        if (u) nbp = u + (size_t)nb * N3;
+      } else {
+        const int sk = kp.slab_face[f];
+        if (sk == FK_GHOST) {
+          kind = 0;
+          const int col = coord[0] + kp.nx * coord[1];
+          kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
+          if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * N3;
+        } else {
+          kind = (sk == FK_DIRICHLET) ? 1 : 2;
+        }
+      }
+      const double bn = kp.b[axis];
+      if (kind == 0 && (kp.mask & 2u)) {
+        const double KN = kp.K[(size_t)kidx * 3 + axis];
+        const double s = KT + KN;
+        const double rs = s > 0.0 ? 1.0 / s : 0.0;   // the only division of the face setup
+        const double wT = s > 0.0 ? KN * rs : 0.5, wN = s > 0.0 ? KT * rs : 0.5;
+        const double gam = kp.pen * (2.0 * KT * KN * rs) * ihk;  // <dT,dN>|F|/|T|
+        if (hi) {
+          co[0] = fmax(bn, 0.0) + gam;  co[1] = -wT * KT;
+          co[2] = fmin(bn, 0.0) - gam;  co[3] = -wN * KN;
+          co[4] = -wT * KT * ihk;       co[5] = wT * KT * ihk;
+        } else {
+          co[0] = fmax(-bn, 0.0) + gam; co[1] = wT * KT;
+          co[2] = fmin(-bn, 0.0) - gam; co[3] = wN * KN;
+          co[4] = wT * KT * ihk;        co[5] = -wT * KT * ihk;
+        }
+      } else if (kind == 1 && (kp.mask & 4u)) {
+        const double gam = kp.pen * KT * ihk;  // delta |F| / |T|
+        if (hi) { co[0] = fmax(bn, 0.0) + gam;  co[1] = -KT; co[4] = -KT * ihk; }
+        else    { co[0] = fmax(-bn, 0.0) + gam; co[1] = KT;  co[4] = KT * ihk; }
+      }
+      if (kind != 0) nbp = nullptr;
+    }
+#pragma unroll
+    for (int e = 0; e < 6; ++e) fc_[cs][f][e] = co[e];
+    nb_[cs][f] = nbp;
+  }
+  __syncthreads();
+}
+
+template <int N>
+__device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const double* u) {
+  using G = Geo<N>;
+  const int t = threadIdx.x;
+  if (t < N) {
+    g.tw[t] = c_tab[N].w[t];
+    g.td0[t] = c_tab[N].d0[t];
+    g.td1[t] = c_tab[N].d1[t];
+  }
+  setup_cells<N, G::C, G::NT>(kp, g.vc, g.fc, g.nb, g.cell, cell0, u);
+}
+
+// ---- tiles ---------------------------------------------------------------------
+template <int N>
+__device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncells,
+                                          const double* __restrict__ src, double* dst) {
+  using G = Geo<N>;
+  const int nvalid = min(G::C, ncells - cell0);
+  const double* s = src + (size_t)cell0 * G::N3;
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    const int i = r % N, j = (r / N) % N, k = r / G::N2;
+    dst[cs * G::CS + k * G::ZS + j * G::YS + i] = (cs < nvalid) ? s[e] : 0.0;
+  }
+}
+
+// ---- faces, part 1: traces -> S/T arrays per face node (+ tangential mass) ------
+// face buffer: FB[((cs*3 + axis)*4 + arr)*N2 + l], arr: 0 S_lo, 1 T_lo, 2 S_hi, 3 T_hi
+template <int N, int AX>
+__device__ __forceinline__ void face_line(const Group<N>& g, const double* src, double* FB,
+                                          int cs, int a, int b, double inv_h) {
+  using G = Geo<N>;
+  int off, goff;
+  constexpr int SS = AX == 0 ? 1 : (AX == 1 ? G::YS : G::ZS);   // smem stride along the line
+  constexpr int GS = AX == 0 ? 1 : (AX == 1 ? N : G::N2);       // global stride
+  if (AX == 0) { off = b * G::ZS + a * G::YS; goff = b * G::N2 + a * N; }
+  else if (AX == 1) { off = b * G::ZS + a; goff = b * G::N2 + a; }
+  else { off = b * G::YS + a; goff = b * N + a; }
+  double v[N];
+  ld<N, SS>(src + cs * G::CS + off, v);
+  double glo = 0.0, ghi = 0.0;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    glo = fma(c_tab[N].d0[e], v[e], glo);
+    ghi = fma(c_tab[N].d1[e], v[e], ghi);
+  }
+  glo *= inv_h;
+  ghi *= inv_h;
+  const double* clo = g.fc[cs][2 * AX];
+  const double* chi = g.fc[cs][2 * AX + 1];
+  double Slo = clo[0] * v[0] + clo[1] * glo, Tlo = clo[4] * v[0];
+  double Shi = chi[0] * v[N - 1] + chi[1] * ghi, Thi = chi[4] * v[N - 1];
+  const double* nlo = g.nb[cs][2 * AX];
+  const double* nhi = g.nb[cs][2 * AX + 1];
+  if (nlo) {  // neighbour below: its hi trace (node N-1) and d1 derivative
+    double w[N];
+    ld<N, GS>(nlo + goff, w);
+    double gn = 0.0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+    Slo += clo[2] * w[N - 1] + clo[3] * gn * inv_h;
+    Tlo += clo[5] * w[N - 1];
+  }
+  if (nhi) {  // neighbour above: its lo trace (node 0) and d0 derivative
+    double w[N];
+    ld<N, GS>(nhi + goff, w);
+    double gn = 0.0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+    Shi += chi[2] * w[0] + chi[3] * gn * inv_h;
+    Thi += chi[5] * w[0];
+  }
+  double* fb = FB + (cs * 3 + AX) * 4 * G::N2 + a + N * b;
+  fb[0 * G::N2] = Slo;
+  fb[1 * G::N2] = Tlo;
+  fb[2 * G::N2] = Shi;
+  fb[3 * G::N2] = Thi;
+}
+
+// ---- the full cell operator: faces + volume, result handed to `out` line by line ----
+// src: input tensors (smem), SA/SB scratch tensors, FB face buffer.
+// out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
+template <int N, class Out>
+__device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
+                                              const double* src, double* SA, double* SB,
+                                              double* FB, bool vol, Out out) {
+  using G = Geo<N>;
+  constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = G::NT;
+  const int tid = threadIdx.x;
+  const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
+  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
+  const double sb[3] = {T3 * kp.b[0] * inv_h[0], T3 * kp.b[1] * inv_h[1], T3 * kp.b[2] * inv_h[2]};
+  const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
+
+  // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
+  for (int it = tid; it < 3 * LINES; it += NT) {
+    const int ax = it / LINES, r = it % LINES, cs = r / N2, l = r % N2;
+    const int a = l % N, b = l / N;
+    if (ax == 0) face_line<N, 0>(g, src, FB, cs, a, b, inv_h[0]);
+    else if (ax == 1) face_line<N, 1>(g, src, FB, cs, a, b, inv_h[1]);
+    else face_line<N, 2>(g, src, FB, cs, a, b, inv_h[2]);
+  }
+  if (vol) {
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
+      const int off = cs * G::CS + b * G::ZS + a * G::YS;
+      double v[N], o[N];
+      ld<N, 1>(src + off, v);
+      mv<N, 0>(v, o);
+      st<N, 1>(SA + off, o);
+    }
+  }
+  __syncthreads();
+  // pass 2: F2 (tangential mass along t1) + P2 (y-lines: SB = A_y SA)
+  for (int it = tid; it < C * 12 * N; it += NT) {
+    const int t2 = it % N, rest = it / N;
+    double* fa = FB + rest * N2 + N * t2;
+    double v[N], o[N];
+    ld<N, 1>(fa, v);
+    mv<N, 2>(v, o);
+    st<N, 1>(fa, o);
+  }
+  if (vol) {
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
+      const int off = cs * G::CS + b * G::ZS + a;
+      double v[N], o[N];
+      ld<N, G::YS>(SA + off, v);
+      mv<N, 0>(v, o);
+      st<N, G::YS>(SB + off, o);
+    }
+  }
+  __syncthreads();
+  // pass 3: F3 (tangential mass along t2, area scaling) + P3 (z-lines: U = A_z SB -> SA,
+  //         R = reaction + z-term -> SB)
+  for (int it = tid; it < C * 12 * N; it += NT) {
+    const int t1 = it % N, rest = it / N;
+    const int ax = (rest >> 2) % 3;
+    double* fa = FB + rest * N2 + t1;
+    double v[N], o[N];
+    ld<N, N>(fa, v);
+    mv<N, 2>(v, o);
+#pragma unroll
+    for (int e = 0; e < N; ++e) o[e] *= area[ax];
+    st<N, N>(fa, o);
+  }
+  if (vol) {
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qx, b = qy
+      const int off = cs * G::CS + b * G::YS + a;
+      double t[N], U[N], R[N];
+      ld<N, G::ZS>(SB + off, t);
+      mv<N, 0>(t, U);
+      const double Wl = g.tw[a] * g.tw[b];
+      const double sc = g.vc[cs][3];
+#pragma unroll
+      for (int q = 0; q < N; ++q) R[q] = Wl * c_tab[N].w[q] * sc * U[q];
+      dir_term<N>(U, R, Wl, g.vc[cs][2], sb[2]);
+      st<N, G::ZS>(SA + off, U);
+      st<N, G::ZS>(SB + off, R);
+    }
+    __syncthreads();
+    // pass 4: x-lines, R += x-term
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qy, b = qz
+      const int off = cs * G::CS + b * G::ZS + a * G::YS;
+      double U[N], R[N];
+      ld<N, 1>(SA + off, U);
+      ld<N, 1>(SB + off, R);
+      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], sb[0]);
+      st<N, 1>(SB + off, R);
+    }
+    __syncthreads();
+    // pass 5: y-lines, R += y-term, then A_y^T
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qx, b = qz
+      const int off = cs * G::CS + b * G::ZS + a;
+      double U[N], R[N], o[N];
+      ld<N, G::YS>(SA + off, U);
+      ld<N, G::YS>(SB + off, R);
+      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], sb[1]);
+      mtv<N, 0>(R, o);
+      st<N, G::YS>(SB + off, o);
+    }
+    __syncthreads();
+    // pass 6: z-lines, A_z^T
+    for (int it = tid; it < LINES; it += NT) {
+      const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
+      const int off = cs * G::CS + b * G::YS + a;
+      double v[N], o[N];
+      ld<N, G::ZS>(SB + off, v);
+      mtv<N, 0>(v, o);
+      st<N, G::ZS>(SB + off, o);
+    }
+  }
+  __syncthreads();
+  // pass 7: x-lines, A_x^T + scatter of all face terms
+  for (int it = tid; it < LINES; it += NT) {
+    const int cs = it / N2, l = it % N2, j = l % N, k = l / N;
+    double v[N];
+    if (vol) {
+      double t[N];
+      ld<N, 1>(SB + cs * G::CS + k * G::ZS + j * G::YS, t);
+      mtv<N, 0>(t, v);
+    } else {
+#pragma unroll
+      for (int e = 0; e < N; ++e) v[e] = 0.0;
+    }
+    const double* fx = FB + (cs * 3 + 0) * 4 * N2;
+    const double* fy = FB + (cs * 3 + 1) * 4 * N2;
+    const double* fz = FB + (cs * 3 + 2) * 4 * N2;
+    // x faces: index (j,k)
+    {
+      const double Slo = fx[0 * N2 + l], Tlo = fx[1 * N2 + l], Shi = fx[2 * N2 + l], Thi = fx[3 * N2 + l];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = fma(c_tab[N].d0[i], Tlo, fma(c_tab[N].d1[i], Thi, v[i]));
+      v[0] += Slo;
+      v[N - 1] += Shi;
+    }
+    // y faces: index (i,k); profile in j.   z faces: index (i,j); profile in k.
+    {
+      const double e0j = (j == 0) ? 1.0 : 0.0, e1j = (j == N - 1) ? 1.0 : 0.0;
+      const double d0j = g.td0[j], d1j = g.td1[j];
+      const double e0k = (k == 0) ? 1.0 : 0.0, e1k = (k == N - 1) ? 1.0 : 0.0;
+      const double d0k = g.td0[k], d1k = g.td1[k];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const int iy = i + N * k, iz = i + N * j;
+        double s = v[i];
+        s = fma(e0j, fy[0 * N2 + iy], s);
+        s = fma(d0j, fy[1 * N2 + iy], s);
+        s = fma(e1j, fy[2 * N2 + iy], s);
+        s = fma(d1j, fy[3 * N2 + iy], s);
+        s = fma(e0k, fz[0 * N2 + iz], s);
+        s = fma(d0k, fz[1 * N2 + iz], s);
+        s = fma(e1k, fz[2 * N2 + iz], s);
+        s = fma(d1k, fz[3 * N2 + iz], s);
+        v[i] = s;
+      }
+    }
+    out(cs, j, k, v);
+  }
+}
+
+// ---- diag(D_T) from 1D diagonals (Jacobi preconditioner) --------------
+template <int N>
+__device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
+  using G = Geo<N>;
+  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
+  const double sb[3] = {T3 * kp.b[0] / kp.h[0], T3 * kp.b[1] / kp.h[1], T3 * kp.b[2] / kp.h[2]};
+  const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    const int idx[3] = {r % N, (r / N) % N, r / G::N2};
+    double Md[3], Sd[3], Cd[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      Md[a] = c_tab[N].Md[idx[a]];
+      Sd[a] = c_tab[N].Sd[idx[a]];
+      Cd[a] = c_tab[N].Cd[idx[a]];
+    }
+    const double* vc = g.vc[cs];
+    double d = vc[3] * Md[0] * Md[1] * Md[2];
+    d += (vc[0] * Sd[0] - sb[0] * Cd[0]) * Md[1] * Md[2];
+    d += (vc[1] * Sd[1] - sb[1] * Cd[1]) * Md[0] * Md[2];
+    d += (vc[2] * Sd[2] - sb[2] * Cd[2]) * Md[0] * Md[1];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const double tm = area[a] * Md[(a + 1) % 3] * Md[(a + 2) % 3];
+      const double ih = 1.0 / kp.h[a];
+      if (idx[a] == 0) {
+        const double* c = g.fc[cs][2 * a];
+        const double dd = c_tab[N].d0[0];
+        d += tm * (c[0] + c[1] * dd * ih + c[4] * dd);
+      }
+      if (idx[a] == N - 1) {
+        const double* c = g.fc[cs][2 * a + 1];
+        const double dd = c_tab[N].d1[N - 1];
+        d += tm * (c[0] + c[1] * dd * ih + c[4] * dd);
+      }
+    }
+    Dg[cs * G::CS + idx[2] * G::ZS + idx[1] * G::YS + idx[0]] = d;
+  }
+}
+
+// per-cell sum of the per-line partials red[q][cs*N2 + l] -> result[q][cs]
+template <int N>
+__device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
+  constexpr int N2 = N * N;
+  double s = 0.0;
+  for (int l = 0; l < N2; ++l) s += g.red[q][cs * N2 + l];
+  return s;
+}
+
+// line iteration helper over x-lines of the group: f(cs, off, item)
+#define DG_FOR_XLINES(...)                                                             \
+  for (int it = threadIdx.x; it < G::LINES; it += G::NT) {                            \
+    const int cs = it / G::N2, l_ = it % G::N2;                                      \
+    const int off = cs * G::CS + (l_ / N) * G::ZS + (l_ % N) * G::YS;                 \
+    (void)off;                                                                        \
+    __VA_ARGS__                                                                       \
+  }
+
+// =============================== kernels ========================================
+
+template <int N>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  __shared__ Group<N> g;
+  double* SRC = sm;
+  double* SA = SRC + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = SB + G::TENSOR;
+  const int cell0 = blockIdx.x * G::C;
+  load_tile<N>(g, cell0, kp.ncells, u, SRC);
+  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
+  const int nvalid = min(G::C, kp.ncells - cell0);
+  double* o = out + (size_t)cell0 * G::N3;
+  cell_operator<N>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
+                   [&](int cs, int j, int k, const double* v) {
+                     if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
+                   });
+}
+
+// Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
+// SWEEP: in = u (defect d = f - A u formed first), result u + omega du; else in = d, result du.
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+     double* __restrict__ out) {
+  using G = Geo<N>;
+  constexpr int C = G::C;
+  extern __shared__ double sm[];
+  __shared__ Group<N> g;
+  double* X = sm;
+  double* R = X + G::TENSOR;
+  double* P = R + G::TENSOR;
+  double* Q = P + G::TENSOR;
+  double* Dg = Q + G::TENSOR;
+  double* SA = Dg + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = SB + G::TENSOR;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(C, kp.ncells - cell0);
+  const int tid = threadIdx.x;
+  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  KParams kq = kp;
+  kq.mask = 7u;
+  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
+    const double* fb = f + (size_t)cell0 * G::N3;
+    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      double fl[N] = {};
+      if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
+      double r[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
+      st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
+    });
+    __syncthreads();
+    // D_T uses self faces only
+    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+  }
+  diag_setup<N>(kp, g, Dg);
+  __syncthreads();
+  // r0 = d, p = M^-1 r, x = 0
+  DG_FOR_XLINES({
+    double r[N], dg[N], z[N], zero[N] = {};
+    ld<N, 1>(R + off, r);
+    ld<N, 1>(Dg + off, dg);
+    double rr = 0.0, rz = 0.0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) { z[e] = r[e] / dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
+    st<N, 1>(P + off, z);
+    st<N, 1>(X + off, zero);
+    g.red[0][it] = rr;
+    g.red[1][it] = rz;
+  })
+  __syncthreads();
+  if (tid < C) {
+    const double rr0 = cell_sum<N>(g, 0, tid);
+    g.sc[S_RR0][tid] = rr0;
+    g.sc[S_RZ][tid] = cell_sum<N>(g, 1, tid);
+    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0);
+    g.its[tid] = 0;
+  }
+  for (int iter = 0;; ++iter) {
+    const int done = __syncthreads_and(tid >= C || g.conv[tid]);
+    if (done || iter >= kp.max_it) break;
+    // q = D_T p
+    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      st<N, 1>(Q + cs * G::CS + k * G::ZS + j * G::YS, v);
+    });
+    __syncthreads();
+    DG_FOR_XLINES({
+      double p[N], q[N];
+      ld<N, 1>(P + off, p);
+      ld<N, 1>(Q + off, q);
+      double s = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) s = fma(p[e], q[e], s);
+      g.red[0][it] = s;
+    })
+    __syncthreads();
+    if (tid < C) {
+      const double pq = cell_sum<N>(g, 0, tid);
+      double alpha = 0.0;
+      if (!g.conv[tid]) {
+        if (pq > 0.0) alpha = g.sc[S_RZ][tid] / pq;
+        else g.conv[tid] = 1;  // breakdown (p = 0): keep the last iterate
+      }
+      g.sc[S_ALPHA][tid] = alpha;
+    }
+    __syncthreads();
+    DG_FOR_XLINES({
+      const double alpha = g.sc[S_ALPHA][cs];
+      double x[N], r[N], p[N], q[N], dg[N];
+      ld<N, 1>(X + off, x);
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(P + off, p);
+      ld<N, 1>(Q + off, q);
+      ld<N, 1>(Dg + off, dg);
+      double rr = 0.0, rz = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        x[e] = fma(alpha, p[e], x[e]);
+        r[e] = fma(-alpha, q[e], r[e]);
+        rr = fma(r[e], r[e], rr);
+        rz = fma(r[e], r[e] / dg[e], rz);
+      }
+      st<N, 1>(X + off, x);
+      st<N, 1>(R + off, r);
+      g.red[0][it] = rr;
+      g.red[1][it] = rz;
+    })
+    __syncthreads();
+    if (tid < C && !g.conv[tid]) {
+      const double rr = cell_sum<N>(g, 0, tid), rzn = cell_sum<N>(g, 1, tid);
+      g.its[tid] += 1;
+      if (rr <= kp.tol2 * g.sc[S_RR0][tid]) g.conv[tid] = 1;
+      g.sc[S_BETA][tid] = rzn / g.sc[S_RZ][tid];
+      g.sc[S_RZ][tid] = rzn;
+    }
+    __syncthreads();
+    DG_FOR_XLINES({
+      if (!g.conv[cs]) {
+        const double beta = g.sc[S_BETA][cs];
+        double r[N], p[N], dg[N];
+        ld<N, 1>(R + off, r);
+        ld<N, 1>(P + off, p);
+        ld<N, 1>(Dg + off, dg);
+#pragma unroll
+        for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], r[e] / dg[e]);
+        st<N, 1>(P + off, p);
+      }
+    })
+  }
+  // write result (u + omega du for a sweep, du for a solve)
+  const double* ib = in + (size_t)cell0 * G::N3;
+  double* ob = out + (size_t)cell0 * G::N3;
+  DG_FOR_XLINES({
+    if (cs < nvalid) {
+      const int j = l_ % N, k = l_ / N;
+      double x[N];
+      ld<N, 1>(X + off, x);
+      if (SWEEP) {
+        double uu[N];
+        ld<N, 1>(ib + cs * G::N3 + k * G::N2 + j * N, uu);
+#pragma unroll
+        for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+      }
+      st<N, 1>(ob + cs * G::N3 + k * G::N2 + j * N, x);
+    }
+  })
+  if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] ? g.its[tid] : (g.its[tid] | (1 << 30));
+}
+
+// Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks, b != 0).
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+           double* __restrict__ out) {
+  using G = Geo<N>;
+  constexpr int C = G::C;
+  extern __shared__ double sm[];
+  __shared__ Group<N> g;
+  double* X = sm;
+  double* R = X + G::TENSOR;
+  double* RH = R + G::TENSOR;
+  double* P = RH + G::TENSOR;
+  double* V = P + G::TENSOR;
+  double* PS = V + G::TENSOR;
+  double* T = PS + G::TENSOR;
+  double* Dg = T + G::TENSOR;
+  double* SA = Dg + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = SB + G::TENSOR;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(C, kp.ncells - cell0);
+  const int tid = threadIdx.x;
+  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  KParams kq = kp;
+  kq.mask = 7u;
+  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  if (SWEEP) {
+    const double* fb = f + (size_t)cell0 * G::N3;
+    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      double fl[N] = {};
+      if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
+      double r[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
+      st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
+    });
+    __syncthreads();
+    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+  }
+  diag_setup<N>(kp, g, Dg);
+  __syncthreads();
+  DG_FOR_XLINES({
+    double r[N], zero[N] = {};
+    ld<N, 1>(R + off, r);
+    double rr = 0.0;
+#pragma unroll
+    for (int e = 0; e < N; ++e) rr = fma(r[e], r[e], rr);
+    st<N, 1>(RH + off, r);
+    st<N, 1>(X + off, zero);
+    st<N, 1>(P + off, zero);
+    st<N, 1>(V + off, zero);
+    g.red[0][it] = rr;
+  })
+  __syncthreads();
+  if (tid < C) {
+    const double rr0 = cell_sum<N>(g, 0, tid);
+    g.sc[S_RR0][tid] = rr0;
+    g.sc[S_RHO][tid] = 1.0;
+    g.sc[S_ALPHA][tid] = 1.0;
+    g.sc[S_OMEGA][tid] = 1.0;
+    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0);
+    g.its[tid] = 0;
+    g.rst[tid] = 0;
+  }
+  for (int iter = 0;; ++iter) {
+    const int done = __syncthreads_and(tid >= C || g.conv[tid]);
+    if (done || iter >= kp.max_it) break;
+    // rho_new = <rh, r>, rr = <r, r>
+    DG_FOR_XLINES({
+      double r[N], rh[N];
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(RH + off, rh);
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) { a = fma(rh[e], r[e], a); b = fma(r[e], r[e], b); }
+      g.red[0][it] = a;
+      g.red[1][it] = b;
+    })
+    __syncthreads();
+    if (tid < C && !g.conv[tid]) {
+      double rhon = cell_sum<N>(g, 0, tid);
+      const double rr = cell_sum<N>(g, 1, tid);
+      int rst = g.rst[tid];
+      if (fabs(rhon) <= 1e-24 * rr) rst = 1;  // breakdown: restart with rh = r
+      if (rst) rhon = rr;
+      g.rst[tid] = rst;
+      g.sc[S_BETA][tid] = rst ? 0.0 : (rhon / g.sc[S_RHO][tid]) * (g.sc[S_ALPHA][tid] / g.sc[S_OMEGA][tid]);
+      g.sc[S_RHON][tid] = rhon;
+    }
+    __syncthreads();
+    // p = r + beta (p - omega v); ps = M^-1 p
+    DG_FOR_XLINES({
+      if (!g.conv[cs]) {
+        const double beta = g.sc[S_BETA][cs], om = g.sc[S_OMEGA][cs];
+        const int rst = g.rst[cs];
+        double r[N], p[N], v[N], dg[N], ps[N];
+        ld<N, 1>(R + off, r);
+        ld<N, 1>(P + off, p);
+        ld<N, 1>(V + off, v);
+        ld<N, 1>(Dg + off, dg);
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          p[e] = rst ? r[e] : fma(beta, fma(-om, v[e], p[e]), r[e]);
+          ps[e] = p[e] / dg[e];
+        }
+        if (rst) st<N, 1>(RH + off, r);
+        st<N, 1>(P + off, p);
+        st<N, 1>(PS + off, ps);
+      }
+    })
+    __syncthreads();
+    cell_operator<N>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      st<N, 1>(V + cs * G::CS + k * G::ZS + j * G::YS, v);
+    });
+    __syncthreads();
+    DG_FOR_XLINES({
+      double rh[N], v[N];
+      ld<N, 1>(RH + off, rh);
+      ld<N, 1>(V + off, v);
+      double a = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) a = fma(rh[e], v[e], a);
+      g.red[0][it] = a;
+    })
+    __syncthreads();
+    if (tid < C) {
+      g.rst[tid] = 0;
+      double alpha = 0.0;
+      if (!g.conv[tid]) {
+        const double rv = cell_sum<N>(g, 0, tid);
+        if (rv != 0.0) alpha = g.sc[S_RHON][tid] / rv;
+        else g.rst[tid] = 1;
+      }
+      g.sc[S_ALPHA][tid] = alpha;
+    }
+    __syncthreads();
+    // x += alpha ps; s = r - alpha v (stored in R); ps <- M^-1 s
+    DG_FOR_XLINES({
+      if (!g.conv[cs]) {
+        const double alpha = g.sc[S_ALPHA][cs];
+        double x[N], r[N], v[N], ps[N], dg[N];
+        ld<N, 1>(X + off, x);
+        ld<N, 1>(R + off, r);
+        ld<N, 1>(V + off, v);
+        ld<N, 1>(PS + off, ps);
+        ld<N, 1>(Dg + off, dg);
+        double ss = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          x[e] = fma(alpha, ps[e], x[e]);
+          r[e] = fma(-alpha, v[e], r[e]);
+          ss = fma(r[e], r[e], ss);
+          ps[e] = r[e] / dg[e];
+        }
+        st<N, 1>(X + off, x);
+        st<N, 1>(R + off, r);
+        st<N, 1>(PS + off, ps);
+        g.red[0][it] = ss;
+      } else {
+        g.red[0][it] = 0.0;
+      }
+    })
+    __syncthreads();
+    if (tid < C && !g.conv[tid]) {
+      const double ss = cell_sum<N>(g, 0, tid);
+      if (ss <= kp.tol2 * g.sc[S_RR0][tid]) { g.conv[tid] = 1; g.its[tid] += 1; }
+    }
+    __syncthreads();
+    cell_operator<N>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      st<N, 1>(T + cs * G::CS + k * G::ZS + j * G::YS, v);
+    });
+    __syncthreads();
+    DG_FOR_XLINES({
+      double t[N], s[N];
+      ld<N, 1>(T + off, t);
+      ld<N, 1>(R + off, s);
+      double a = 0.0, b = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) { a = fma(t[e], s[e], a); b = fma(t[e], t[e], b); }
+      g.red[0][it] = a;
+      g.red[1][it] = b;
+    })
+    __syncthreads();
+    if (tid < C && !g.conv[tid]) {
+      const double ts = cell_sum<N>(g, 0, tid), tt = cell_sum<N>(g, 1, tid);
+      const double om = tt > 0.0 ? ts / tt : 0.0;
+      g.sc[S_OMEGA][tid] = om;
+      if (om == 0.0) g.rst[tid] = 1;
+    }
+    __syncthreads();
+    // x += omega s^; r = s - omega t
+    DG_FOR_XLINES({
+      if (!g.conv[cs]) {
+        const double om = g.sc[S_OMEGA][cs];
+        double x[N], r[N], t[N], ps[N];
+        ld<N, 1>(X + off, x);
+        ld<N, 1>(R + off, r);
+        ld<N, 1>(T + off, t);
+        ld<N, 1>(PS + off, ps);
+        double rr = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          x[e] = fma(om, ps[e], x[e]);
+          r[e] = fma(-om, t[e], r[e]);
+          rr = fma(r[e], r[e], rr);
+        }
+        st<N, 1>(X + off, x);
+        st<N, 1>(R + off, r);
+        g.red[0][it] = rr;
+      } else {
+        g.red[0][it] = 0.0;
+      }
+    })
+    __syncthreads();
+    if (tid < C && !g.conv[tid]) {
+      const double rr = cell_sum<N>(g, 0, tid);
+      g.its[tid] += 1;
+      if (rr <= kp.tol2 * g.sc[S_RR0][tid]) g.conv[tid] = 1;
+      g.sc[S_RHO][tid] = g.sc[S_RHON][tid];
+      if (g.sc[S_OMEGA][tid] == 0.0) { g.sc[S_OMEGA][tid] = 1.0; }
+    }
+  }
+  const double* ib = in + (size_t)cell0 * G::N3;
+  double* ob = out + (size_t)cell0 * G::N3;
+  DG_FOR_XLINES({
+    if (cs < nvalid) {
+      const int j = l_ % N, k = l_ / N;
+      double x[N];
+      ld<N, 1>(X + off, x);
+      if (SWEEP) {
+        double uu[N];
+        ld<N, 1>(ib + cs * G::N3 + k * G::N2 + j * N, uu);
+#pragma unroll
+        for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+      }
+      st<N, 1>(ob + cs * G::N3 + k * G::N2 + j * N, x);
+    }
+  })
+  if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] ? g.its[tid] : (g.its[tid] | (1 << 30));
+}
+
+}  // namespace
+
+#include "dg_plane.cuh"
+
+namespace {
+
+// ---- host-side launch helpers ------------------------------------------------------
+template <int N> constexpr size_t smem_bytes(int tensors) {
+  return sizeof(double) * ((size_t)tensors * Geo<N>::TENSOR + Geo<N>::FACE);
+}
+
+template <class K>
+cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, const KParams& kp,
+                   const double* a, const double* b, double* c) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  kernel<<<grid, block, smem, s>>>(kp, a, b, c);
+  return cudaGetLastError();
+}
+
+// DG_KERNEL_FAMILY=line forces the line-per-thread kernels for every degree (A/B comparisons).
+static bool force_line() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DG_KERNEL_FAMILY");
+    v = (e && e[0] == 'l') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Kernel family of the operator application per degree, chosen by measurement on C1-C5
+// (profiles/r01_kernel_family.md): the plane kernels win for n = 2, 4; at n = 3 and 5 the
+// line kernels' higher occupancy wins for a single application. The local solvers always use
+// the plane kernels for n <= 5 (register-resident Krylov vectors).
+template <int N> constexpr bool plane_apply() { return N == 2 || N == 4; }
+
+template <int N>
+cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
+  if constexpr (plane_apply<N>()) {
+    if (!force_line()) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      const size_t smem = pk::smem_apply<N>();
+      auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
+      if (kp.mask == 1u) kern = pk::k_apply<N, false, false>;   // volume terms only
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<grid, G::NT, smem, s>>>(kp, u, out);
+      return cudaGetLastError();
+    }
+  }
+  using G = Geo<N>;
+  const int grid = (kp.ncells + G::C - 1) / G::C;
+  if (grid == 0) return cudaSuccess;
+  const size_t smem = smem_bytes<N>(3);
+  cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
+  return cudaGetLastError();
+}
+
+template <int N, bool SWEEP>
+cudaError_t solve_n(int method, const KParams& kp, const double* in, const double* f, double* out,
+                    cudaStream_t s) {
+  if constexpr (N <= 5) {
+    if (!force_line()) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      if (method == LM_BICGSTAB)
+        return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+      return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
+    }
+  }
+  using G = Geo<N>;
+  const int grid = (kp.ncells + G::C - 1) / G::C;
+  if (grid == 0) return cudaSuccess;
+  if (method == LM_BICGSTAB)
+    return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
+  return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
+}
+
+// ---- per-degree entry points (dg_degree.h) ---------------------------------------------
+template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
+  DevTab d{};
+  const int n = t.n;
+  for (int i = 0; i < n * n; ++i) { d.A[i] = t.A[i]; d.D[i] = t.D[i]; d.M[i] = t.M[i]; d.G[i] = t.G[i]; }
+  for (int i = 0; i < n; ++i) {
+    d.w[i] = t.wq[i]; d.d0[i] = t.d0[i]; d.d1[i] = t.d1[i];
+    d.Sd[i] = t.Sdiag[i]; d.Cd[i] = t.Cdiag[i]; d.Md[i] = t.Mdiag[i];
+    d.E0[i] = t.E0[i]; d.E1[i] = t.E1[i]; d.F0[i] = t.F0[i]; d.F1[i] = t.F1[i];
+    d.E0W[i] = t.E0[i] / t.wq[i]; d.E1W[i] = t.E1[i] / t.wq[i];
+    d.F0W[i] = t.F0[i] / t.wq[i]; d.F1W[i] = t.F1[i] / t.wq[i];
+  }
+  for (int q = 0; q < n; ++q)
+    for (int j = 0; j < n; ++j) {
+      d.AW[q * n + j] = t.A[q * n + j] * t.wq[q];
+      d.GW[q * n + j] = t.G[q * n + j] * t.wq[q];
+      d.DW[q * n + j] = t.D[q * n + j] * t.wq[q] / t.wq[j];
+    }
+  *err = cudaMemcpyToSymbol(c_tab, &d, sizeof(DevTab), sizeof(DevTab) * N);
+  return *err == cudaSuccess;
+}
+
+}  // namespace
+
+#define DG_INSTANTIATE_DEGREE(NN)                                                              \
+  template <> bool Deg<NN>::upload(const Tables1D& t, cudaError_t* err) { return upload_n<NN>(t, err); } \
+  template <> cudaError_t Deg<NN>::apply(const KParams& kp, const double* u, double* out,        \
+                                         cudaStream_t s, int with_nbr) {                         \
+    return apply_n<NN>(kp, u, out, s, with_nbr);                                                 \
+  }                                                                                              \
+  template <> cudaError_t Deg<NN>::solve(int method, bool sweep, const KParams& kp,              \
+                                         const double* in, const double* f, double* out,         \
+                                         cudaStream_t s) {                                       \
+    return sweep ? solve_n<NN, true>(method, kp, in, f, out, s)                                  \
+                 : solve_n<NN, false>(method, kp, in, f, out, s);                                \
+  }
+
+}  // namespace dg

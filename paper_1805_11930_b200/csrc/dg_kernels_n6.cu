@@ -1,0 +1,6 @@
+// Degree p = 5 (n = 6) of the fp64 sm_100a kernels (see dg_kernels_impl.cuh).
+#include "dg_kernels_impl.cuh"
+
+namespace dg {
+DG_INSTANTIATE_DEGREE(6)
+}  // namespace dg

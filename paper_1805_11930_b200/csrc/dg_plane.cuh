@@ -326,11 +326,12 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& 
 }
 
 // ---- the operator: out = A u (NBR) or D_T u (self faces only) on the lane's plane ---------
-// All threads must call it (two __syncthreads inside). TB must be free on entry.
+// All lanes of the warp must call it (two __syncwarp inside: a cell's n lanes are in one warp,
+// so both transposes are warp-local). The cell's TB / FY slots must be free on entry.
 // The quadrature-point residual R is kept UNWEIGHTED: the Gauss weights (and |T|, face
 // areas through kp) are folded into the transposed 1D tables AW = A w, GW = G w,
 // DW = D w_q / w_r and the end-point injection vectors E/w, F/w.
-template <int N, bool NBR, bool USEB>
+template <int N, bool NBR, bool USEB, bool FACES = true>
 __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, const Lane& L,
                                          const Rows<N>& rw, bool vol, const double (&in)[N][N],
                                          double (&out)[N][N], double* TB, double* FY,
@@ -339,6 +340,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
   double* tb = TB + L.cs * G::CTB;
   double* fy = FY + L.cs * G::FS;
   const double* fc = &cl.fc[L.cs][0][0];
+  __syncwarp();   // the previous call's Q3 reads of TB / FY (other lanes of the cell) are done
   // ---------------- Q1: lane = z node k ----------------
   if (L.active) {
     const int k = L.t;
@@ -368,6 +370,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
         }
     }
     // y faces (normal y; tangential z = this lane, x): nodal S/T combos, then A_x
+    if constexpr (FACES) {
     const double* clo = fc + 2 * 6;
     const double* chi = fc + 3 * 6;
     double X0[N], X1[N], X2[N], X3[N];
@@ -407,8 +410,9 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
       fy[2 * G::N2 + k * N + q] = s2;
       fy[3 * G::N2 + k * N + q] = s3;
     }
+    }
   }
-  __syncthreads();
+  __syncwarp();   // the transposes stay inside the cell's own warp
   // ---------------- Q2: lane = y Gauss point qy ----------------
   if (L.active) {
     const int qy = L.t;
@@ -503,7 +507,8 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
         for (int k = 0; k < N; ++k) tb[G::ARR + k * G::KS + qy * N + qx] = 0.0;
       }
     }
-    if (!USEB) {
+    if constexpr (!FACES) {
+    } else if (!USEB) {
       // x faces at the face Gauss points (qz, qy): traces from the x-rows of U
       const double* clo = fc + 0 * 6;
       const double* chi = fc + 1 * 6;
@@ -644,7 +649,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
         tb[k * G::KS + qy * N + qx] = s;
       }
   }
-  __syncthreads();
+  __syncwarp();
   // ---------------- Q3: lane = z node k ----------------
   if (L.active) {
     const int k = L.t;
@@ -670,7 +675,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, 
     }
     // y faces: z face mass (row k of Mhat) on the (k', qx) arrays, end profiles in j
 #pragma unroll
-    for (int qx = 0; qx < N; ++qx) {
+    for (int qx = 0; qx < N && FACES; ++qx) {
       double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
 #pragma unroll
       for (int kk = 0; kk < N; ++kk) {
@@ -760,7 +765,8 @@ __device__ __forceinline__ void setup(const KParams& kp, Cells<N>& cl, int cell0
 }
 
 // out = A u (with_nbr) or D_T u, selected parts by kp.mask
-template <int N, bool NBR>
+// FACES = false: the volume terms alone (dg_apply_parts with mask = volume), no face code.
+template <int N, bool NBR, bool FACES = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
@@ -789,7 +795,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   read_plane<N>(TB, L, in);
   if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3, pv0, pv1);
   else __syncthreads();
-  plane_op<N, NBR, false>(kp, cl, L, rw, (kp.mask & 1u) != 0, in, o, TB, FY, FX, FZ);
+  plane_op<N, NBR, false, FACES>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
@@ -870,7 +876,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   bool conv = !valid || rr0 == 0.0;
   int its = 0;
   for (int iter = 0;; ++iter) {
-    const int done = __syncthreads_and(conv || !L.active);
+    const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
     if (done || iter >= kp.max_it) break;
     double Q[N][N];
     plane_op<N, false, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
@@ -1011,7 +1017,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   bool rst = false;
   int its = 0;
   for (int iter = 0;; ++iter) {
-    const int done = __syncthreads_and(conv || !L.active);
+    const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
     if (done || iter >= kp.max_it) break;
     double a = 0.0, b = 0.0;
 #pragma unroll
