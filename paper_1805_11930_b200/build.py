@@ -32,10 +32,12 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) -> str:
+    """Builds `out` (default: the in-tree libdg_b200.so). `extra` nvcc flags with another `out`
+    give A/B variants of the same sources (e.g. -DDG_PL_WARPS4=1), loaded through DG_LIB."""
+    if out == LIB and not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build") if out == LIB else out + ".objs"
     os.makedirs(objdir, exist_ok=True)
     jobs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", INCLUDE, "-I", CSRC,
@@ -54,11 +56,11 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
             if r.returncode != 0:
                 raise RuntimeError("nvcc failed: " + " ".join(r.args) + "\n" + (r.stderr or "")[-4000:])
     objs = [o for _, o in jobs]
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     cmd = [nvcc(), "-shared", *ARCH, "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

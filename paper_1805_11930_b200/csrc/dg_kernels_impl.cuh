@@ -990,9 +990,10 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
       using G = pk::Geo<N>;
       const int grid = (kp.ncells + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
-      const size_t smem = pk::smem_apply<N>();
+      const bool faces = kp.mask != 1u;   // mask = volume: the volume terms alone
+      const size_t smem = pk::smem_apply<N>(with_nbr, faces);
       auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
-      if (kp.mask == 1u) kern = pk::k_apply<N, false, false>;   // volume terms only
+      if (!faces) kern = pk::k_apply<N, false, false>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, G::NT, smem, s>>>(kp, u, out);

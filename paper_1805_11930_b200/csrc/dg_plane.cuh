@@ -25,10 +25,22 @@ namespace pk {
 template <int N> struct PL;
 // KS/CTB: transpose-buffer plane / cell strides; QS/PS: plane / cell strides of the per-lane
 // plane storage (X, diag, ...). All chosen by an offline search for conflict-free lane patterns.
-template <> struct PL<2> { static constexpr int WARPS = 4, KS = 5, CTB = 22, QS = 8, PS = 17; };
-template <> struct PL<3> { static constexpr int WARPS = 4, KS = 19, CTB = 121, QS = 13, PS = 39; };
-template <> struct PL<4> { static constexpr int WARPS = 4, KS = 20, CTB = 161, QS = 17, PS = 68; };
-template <> struct PL<5> { static constexpr int WARPS = 2, KS = 25, CTB = 253, QS = 25, PS = 125; };
+#ifndef DG_PL_WARPS2
+#define DG_PL_WARPS2 4
+#endif
+#ifndef DG_PL_WARPS3
+#define DG_PL_WARPS3 4
+#endif
+#ifndef DG_PL_WARPS4
+#define DG_PL_WARPS4 4
+#endif
+#ifndef DG_PL_WARPS5
+#define DG_PL_WARPS5 2
+#endif
+template <> struct PL<2> { static constexpr int WARPS = DG_PL_WARPS2, KS = 5, CTB = 22, QS = 8, PS = 17; };
+template <> struct PL<3> { static constexpr int WARPS = DG_PL_WARPS3, KS = 19, CTB = 121, QS = 13, PS = 39; };
+template <> struct PL<4> { static constexpr int WARPS = DG_PL_WARPS4, KS = 20, CTB = 161, QS = 17, PS = 68; };
+template <> struct PL<5> { static constexpr int WARPS = DG_PL_WARPS5, KS = 25, CTB = 253, QS = 25, PS = 125; };
 
 template <int N_> struct Geo {
   static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
@@ -45,7 +57,8 @@ template <int N_> struct Geo {
   static constexpr int FZ = C * FS;       // z-neighbour arrays (j, qx)
 };
 
-template <int N> struct Cells {
+// WB: with the per-cell self-face operators B (local solvers); the apply kernels omit them.
+template <int N, bool WB = true> struct Cells {
   static constexpr int C = Geo<N>::C;
   static constexpr int BS = 2 * N * N + 1;   // odd stride: the cells of a half-warp hit distinct banks
   double vc[C][4];
@@ -53,7 +66,7 @@ template <int N> struct Cells {
   const double* nb[C][6];
   int cell[C];
   // per-cell self-face operators at the Gauss points: B[cs][0] acts on x-rows, B[cs][1] on z-columns
-  double B[C][BS];
+  double B[WB ? C : 1][BS];
 };
 
 // per-lane identity
@@ -163,8 +176,8 @@ __device__ __forceinline__ void load_nbr_direct(double (&v)[Geo<N>::PER], const 
   }
 }
 // neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
-template <int N>
-__device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N>& cl, int f) {
+template <int N, bool WB>
+__device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N, WB>& cl, int f) {
   using G = Geo<N>;
 #pragma unroll
   for (int m = 0; m < G::PER; ++m) {
@@ -212,8 +225,8 @@ __device__ __forceinline__ void write_plane(double* TB, const Lane& L, const dou
 
 // ---- neighbour prologue: traces of the 6 face neighbours -> FY (nodal), FX, FZ ----------
 // Must be called by all threads; leaves TB free. Face order f = 2*axis + hi.
-template <int N>
-__device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& L, double* TB,
+template <int N, bool WB>
+__device__ void nbr_prologue(const KParams& kp, const Cells<N, WB>& cl, const Lane& L, double* TB,
                              double* FY, double* FX, double* FZ, const double* tile,
                              double (&pv0)[Geo<N>::PER], double (&pv1)[Geo<N>::PER]) {
   using G = Geo<N>;
@@ -331,8 +344,8 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N>& cl, const Lane& 
 // The quadrature-point residual R is kept UNWEIGHTED: the Gauss weights (and |T|, face
 // areas through kp) are folded into the transposed 1D tables AW = A w, GW = G w,
 // DW = D w_q / w_r and the end-point injection vectors E/w, F/w.
-template <int N, bool NBR, bool USEB, bool FACES = true>
-__device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N>& cl, const Lane& L,
+template <int N, bool NBR, bool USEB, bool FACES = true, bool WB>
+__device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& cl, const Lane& L,
                                          const Rows<N>& rw, bool vol, const double (&in)[N][N],
                                          double (&out)[N][N], double* TB, double* FY,
                                          const double* FX, const double* FZ) {
@@ -738,16 +751,128 @@ __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>
     }
 }
 
+// ---- group setup in two halves ------------------------------------------------------------
+// setup_issue: one thread per (cell, axis) writes the two neighbour pointers of that axis and
+// issues the loads of K_T, K of both neighbours (and c) into registers; after a barrier the
+// caller issues its neighbour-tile loads, which are then in flight together with these;
+// setup_finish turns the registers into the volume scalings vc and face coefficients fc
+// (harmonic weights, penalty gamma_F = alpha p(p+2) <delta>|F|/|T|, upwind b_nu).
+template <int N> struct SetupRegs {
+  static constexpr int C = Geo<N>::C, NT = Geo<N>::NT;
+  static constexpr int IT = (3 * C + NT - 1) / NT;   // (cell, axis) items per thread
+  double KT[IT], Kn[IT][2], cR[IT];
+  int kind[IT][2];   // 0 interior (or ghost), 1 Dirichlet, 2 Neumann; -1: item not valid
+};
+
+template <int N, bool WB>
+__device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl, SetupRegs<N>& sr,
+                                            int cell0, const double* u) {
+  using G = Geo<N>;
+  const int nxy = kp.nx * kp.ny;
+  const int c0x = cell0 % kp.nx, c0y = (cell0 / kp.nx) % kp.ny, c0z = cell0 / nxy;
+#pragma unroll
+  for (int r = 0; r < SetupRegs<N>::IT; ++r) {
+    const int it = threadIdx.x + r * G::NT;
+    const int cs = it / 3, axis = it % 3;
+    const int cell = cell0 + cs;
+    sr.kind[r][0] = sr.kind[r][1] = -1;
+    if (it >= 3 * G::C) continue;
+    if (axis == 0) cl.cell[cs] = cell < kp.ncells ? cell : -1;
+    if (cell >= kp.ncells) {
+      cl.nb[cs][2 * axis] = cl.nb[cs][2 * axis + 1] = nullptr;
+      continue;
+    }
+    int cx = c0x + cs, cy = c0y, cz = c0z;
+    while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
+    while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
+    const int co = axis == 0 ? cx : (axis == 1 ? cy : cz);
+    const int dim = axis == 0 ? kp.nx : (axis == 1 ? kp.ny : kp.nzl);
+    const int step = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
+    sr.KT[r] = __ldg(kp.K + (size_t)(cell + nxy) * 3 + axis);
+    sr.cR[r] = (axis == 0 && kp.c) ? __ldg(kp.c + cell) : 0.0;
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const int f = 2 * axis + hi;
+      const int nc = co + (hi ? 1 : -1);
+      const double* nbp = nullptr;
+      long kidx = -1;
+      int kind;
+      if (nc >= 0 && nc < dim) {
+        kind = 0;
+        const long nb = cell + (hi ? step : -step);
+        kidx = nb + nxy;
+        if (u) nbp = u + (size_t)nb * G::N3;
+      } else if (kp.slab_face[f] == FK_GHOST) {
+        kind = 0;
+        const int col = cx + kp.nx * cy;
+        kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
+        if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * G::N3;
+      } else {
+        kind = kp.slab_face[f] == FK_DIRICHLET ? 1 : 2;
+      }
+      sr.kind[r][hi] = kind;
+      sr.Kn[r][hi] = kidx >= 0 ? __ldg(kp.K + (size_t)kidx * 3 + axis) : 0.0;
+      cl.nb[cs][f] = nbp;
+    }
+  }
+}
+
+template <int N, bool WB>
+__device__ __forceinline__ void setup_finish(const KParams& kp, Cells<N, WB>& cl,
+                                             const SetupRegs<N>& sr) {
+  using G = Geo<N>;
+  const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+#pragma unroll
+  for (int r = 0; r < SetupRegs<N>::IT; ++r) {
+    const int it = threadIdx.x + r * G::NT;
+    const int cs = it / 3, axis = it % 3;
+    if (it >= 3 * G::C) continue;
+    const bool valid = sr.kind[r][0] >= 0;
+    const double ihk = kp.ih[axis];
+    const double KT = valid ? sr.KT[r] : 0.0;
+    cl.vc[cs][axis] = (valid && (kp.mask & 1u)) ? KT * vol * ihk * ihk : 0.0;
+    if (axis == 0) cl.vc[cs][3] = (valid && (kp.mask & 1u)) ? vol * sr.cR[r] : 0.0;
+    const double bn = kp.b[axis];
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      double co[6] = {0, 0, 0, 0, 0, 0};
+      const int kind = sr.kind[r][hi];
+      if (kind == 0 && (kp.mask & 2u)) {
+        const double KN = sr.Kn[r][hi];
+        const double sum = KT + KN;
+        const double rs = sum > 0.0 ? 1.0 / sum : 0.0;
+        const double wT = sum > 0.0 ? KN * rs : 0.5, wN = sum > 0.0 ? KT * rs : 0.5;
+        const double gam = kp.pen * (2.0 * KT * KN * rs) * ihk;   // <dT,dN>|F|/|T|
+        if (hi) {
+          co[0] = fmax(bn, 0.0) + gam;  co[1] = -wT * KT;
+          co[2] = fmin(bn, 0.0) - gam;  co[3] = -wN * KN;
+          co[4] = -wT * KT * ihk;       co[5] = wT * KT * ihk;
+        } else {
+          co[0] = fmax(-bn, 0.0) + gam; co[1] = wT * KT;
+          co[2] = fmin(-bn, 0.0) - gam; co[3] = wN * KN;
+          co[4] = wT * KT * ihk;        co[5] = -wT * KT * ihk;
+        }
+      } else if (kind == 1 && (kp.mask & 4u)) {
+        const double gam = kp.pen * KT * ihk;   // delta |F| / |T|
+        if (hi) { co[0] = fmax(bn, 0.0) + gam;  co[1] = -KT; co[4] = -KT * ihk; }
+        else    { co[0] = fmax(-bn, 0.0) + gam; co[1] = KT;  co[4] = KT * ihk; }
+      }
+#pragma unroll
+      for (int e = 0; e < 6; ++e) cl.fc[cs][2 * axis + hi][e] = co[e];
+    }
+  }
+}
+
 // =============================== kernels ================================================
 // Self-face operator of the x (z) faces at the Gauss points, unweighted quadrature level:
 //   B[q][r] = |F| sum_{s=lo,hi} ( E_s^w[q] (cs_a E_s[r] + cs_g F_s[r] / h) + F_s^w[q] ct_a E_s[r] ),
 // i.e. traces a_s = E_s.U, g_s = F_s.U of a Gauss-value line U, the flux combinations
 // S = cs_a a + cs_g g / h, T = ct_a a, and their injection through A^-T / w (see plane_op).
-template <int N, bool USEB = true>
-__device__ __forceinline__ void setup(const KParams& kp, Cells<N>& cl, int cell0, const double* u) {
+template <int N, bool USEB = true, bool WB>
+__device__ __forceinline__ void setup(const KParams& kp, Cells<N, WB>& cl, int cell0, const double* u) {
   using G = Geo<N>;
   setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.fc, cl.nb, cl.cell, cell0, u);
-  if (!USEB) return;
+  if constexpr (!USEB || !WB) return;
   for (int it = threadIdx.x; it < G::C * 2 * G::N2; it += G::NT) {
     const int cs = it / (2 * G::N2), rem = it % (2 * G::N2), d = rem / G::N2;
     const int q = (rem % G::N2) / N, r = rem % N;
@@ -771,7 +896,7 @@ __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
   extern __shared__ double sm[];
-  __shared__ Cells<N> cl;
+  __shared__ Cells<N, false> cl;
   double* TB = sm;
   double* FY = TB + G::TB;
   double* FX = FY + G::FY;
@@ -784,11 +909,14 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   // all global loads of the own tile and the y-neighbour pair are in flight during the setup
   double own[G::PER], pv0[G::PER], pv1[G::PER];
   load_own<N>(own, u + (size_t)cell0 * G::N3, nvalid);
-  setup<N, false>(kp, cl, cell0, NBR ? u : nullptr);  // ends with a barrier
+  SetupRegs<N> sr;
+  setup_issue<N>(kp, cl, sr, cell0, NBR ? u : nullptr);
+  __syncthreads();   // neighbour pointers
   if (NBR) {
     load_nbr<N>(pv0, cl, 2);
     load_nbr<N>(pv1, cl, 3);
   }
+  setup_finish<N>(kp, cl, sr);
   store_tile<N>(TB, own);
   __syncthreads();
   double in[N][N], o[N][N];
@@ -1132,9 +1260,9 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
 }
 
-template <int N> constexpr size_t smem_apply() {
+template <int N> constexpr size_t smem_apply(bool nbr, bool faces) {
   using G = Geo<N>;
-  return sizeof(double) * (size_t)(G::TB + G::FY + G::FX + G::FZ);
+  return sizeof(double) * (size_t)(G::TB + (faces ? G::FY : 0) + (nbr ? G::FX + G::FZ : 0));
 }
 template <int N> constexpr size_t smem_solve(int planes) {
   using G = Geo<N>;

@@ -12,7 +12,8 @@ import os
 from typing import Optional
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdg_b200.so")
+# DG_LIB overrides the library path (A/B builds of the same sources); default: the in-tree build
+LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg_b200.so")
 
 DG_OK, DG_ERR_INVALID, DG_ERR_NOMEM, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_STATE, DG_ERR_UNSUPPORTED = range(7)
 DG_LOCAL_AUTO, DG_LOCAL_CG, DG_LOCAL_BICGSTAB = 0, 1, 2

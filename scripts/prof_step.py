@@ -20,3 +20,7 @@ for _ in range(2):
     ctx.sweep(ut, ft, 1.0, 1e-12)
 torch.cuda.synchronize()
 print("ok", ctx.stats())
+# the volume kernel alone (dg_apply_parts, mask = volume)
+for _ in range(2):
+    ctx.apply_parts(ut, Au, dg.MASK_VOLUME)
+torch.cuda.synchronize()
