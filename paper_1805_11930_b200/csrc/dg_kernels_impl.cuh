@@ -958,10 +958,19 @@ template <int N> constexpr size_t smem_bytes(int tensors) {
   return sizeof(double) * ((size_t)tensors * Geo<N>::TENSOR + Geo<N>::FACE);
 }
 
+// Dynamic shared memory limit + the maximum shared-memory carveout (the kernels are sized by
+// shared memory per resident cell; a smaller carveout would cap the resident CTAs per SM).
+template <class K> cudaError_t set_smem(K kernel, size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                              (int)cudaSharedmemCarveoutMaxShared);
+}
+
 template <class K>
 cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, const KParams& kp,
                    const double* a, const double* b, double* c) {
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, block, smem, s>>>(kp, a, b, c);
   return cudaGetLastError();
@@ -978,13 +987,42 @@ static bool force_line() {
 }
 
 // Kernel family of the operator application per degree, chosen by measurement on C1-C5
-// (profiles/r01_kernel_family.md): the plane kernels win for n = 2, 4; at n = 3 and 5 the
-// line kernels' higher occupancy wins for a single application. The local solvers always use
-// the plane kernels for n <= 5 (register-resident Krylov vectors).
-template <int N> constexpr bool plane_apply() { return N == 2 || N == 4; }
+// (profiles/r01_kernel_family.md, profiles/r01_session2_ab.md): the plane kernels for n = 2, 3, 4;
+// at n = 5 the line kernels' higher occupancy wins for A u and D_T u (the volume-only hook uses
+// the persistent plane kernel k_volume for every n <= 5). The local solvers always use the plane
+// kernels for n <= 5 (register-resident Krylov vectors).
+#ifndef DG_PLANE_APPLY3
+#define DG_PLANE_APPLY3 1   // n = 3: plane kernels (C5: D_T 832 -> 351 us, A 900 -> 847 us)
+#endif
+template <int N> constexpr bool plane_apply() { return N == 2 || N == 4 || (N == 3 && DG_PLANE_APPLY3); }
 
 template <int N>
 cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
+  if constexpr (N <= 5) {
+#ifndef DG_VOL_PERSIST
+#define DG_VOL_PERSIST 1
+#endif
+    if (kp.mask == 1u && DG_VOL_PERSIST && N <= 5) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      // persistent volume kernel: one CTA per resident slot
+      static int slots = 0;
+      const size_t vsm = pk::smem_apply<N>(false, false);
+      if (slots == 0) {
+        cudaError_t e = set_smem(pk::k_volume<N>, vsm);
+        if (e != cudaSuccess) return e;
+        int per_sm = 0, dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk::k_volume<N>, G::NT, vsm);
+        if (e != cudaSuccess) return e;
+        slots = max(1, per_sm) * nsm;
+      }
+      pk::k_volume<N><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
+      return cudaGetLastError();
+    }
+  }
   if constexpr (plane_apply<N>()) {
     if (!force_line()) {
       using G = pk::Geo<N>;
@@ -994,7 +1032,7 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
       const size_t smem = pk::smem_apply<N>(with_nbr, faces);
       auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
       if (!faces) kern = pk::k_apply<N, false, false>;
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaError_t e = set_smem(kern, smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, G::NT, smem, s>>>(kp, u, out);
       return cudaGetLastError();
@@ -1004,7 +1042,7 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
   const size_t smem = smem_bytes<N>(3);
-  cudaError_t e = cudaFuncSetAttribute(k_apply<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = set_smem(k_apply<N>, smem);
   if (e != cudaSuccess) return e;
   k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
   return cudaGetLastError();
@@ -1020,7 +1058,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       if (grid == 0) return cudaSuccess;
       if (method == LM_BICGSTAB)
         return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
-      return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
+      return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
     }
   }
   using G = Geo<N>;

@@ -22,6 +22,10 @@
 
 namespace pk {
 
+#ifndef DG_VOL_MINB
+#define DG_VOL_MINB 3   // resident CTAs per SM the persistent volume kernel is compiled for
+#endif
+
 template <int N> struct PL;
 // KS/CTB: transpose-buffer plane / cell strides; QS/PS: plane / cell strides of the per-lane
 // plane storage (X, diag, ...). All chosen by an offline search for conflict-free lane patterns.
@@ -333,6 +337,185 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N, WB>& cl, const La
           fz[G::N2 + q] = tt;
         }
       }
+    }
+  }
+  __syncthreads();
+}
+
+// ---- asynchronous neighbour staging (cp.async, no registers held while in flight) --------
+// All five tiles a cell group needs for A u (own, y-lo, y-hi, z-lo, z-hi) are copied global ->
+// shared with 8-byte cp.async as soon as their addresses are known, so their latencies overlap
+// each other and the coefficient setup; missing neighbours (domain boundary) are zero-filled.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  // no "memory" clobber: the copies may be issued in any order relative to other smem reads
+  // (the destination is read only after cp_async_wait_all + a barrier)
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// own tile (contiguous in global) -> TB layout, half h
+template <int N>
+__device__ __forceinline__ void async_own(double* TB, const double* __restrict__ src, int nvalid) {
+  using G = Geo<N>;
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    if (e < G::C * G::N3) {
+      const int cs = e / G::N3, r = e % G::N3;
+      cp_async8(TB + cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2), src + (cs < nvalid ? e : 0), cs < nvalid);
+    }
+  }
+}
+// face-f neighbour tiles: into TB layout (KSX = KS, cell stride CTB) or into a face region
+// (KSX = N2, cell stride FS >= N3)
+template <int N, int KSX, int CSX, bool WB>
+__device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, int f, const double* any) {
+  using G = Geo<N>;
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    if (e < G::C * G::N3) {
+      const int cs = e / G::N3, r = e % G::N3;
+      const double* p = cl.nb[cs][f];
+      cp_async8(dst + cs * CSX + (r / G::N2) * KSX + (r % G::N2), p ? p + r : any, p != nullptr);
+    }
+  }
+}
+
+// y-face traces of the neighbour on side `hi` (plane k of the neighbour, nodal in i), lane k:
+// out[0..N) = S row (k, i), out[N..2N) = T row (k, i)
+template <int N, int KSX>
+__device__ __forceinline__ void ytrace(const double* nb, const double* c, double ih, int hi, int k,
+                                       double (&S)[N], double (&T)[N]) {
+  const double cna = c[2], cng = c[3], ctn = c[5];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double g = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) g = fma(hi ? c_tab[N].d0[j] : c_tab[N].d1[j], nb[k * KSX + j * N + i], g);
+    const double a = nb[k * KSX + (hi ? 0 : N - 1) * N + i];
+    S[i] = cna * a + cng * g * ih;
+    T[i] = ctn * a;
+  }
+}
+// z-face traces (lane t = y node j): rows (kk, i) of the neighbour at fixed j, interpolated in x
+template <int N, int KSX>
+__device__ __forceinline__ void ztrace(const double* nb, const double* c, double ih, int hi, int j,
+                                       double (&S)[N], double (&T)[N]) {
+  const double cna = c[2], cng = c[3], ctn = c[5];
+  double s0[N], t0[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double g = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk) g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * KSX + j * N + i], g);
+    const double a = nb[(hi ? 0 : N - 1) * KSX + j * N + i];
+    s0[i] = cna * a + cng * g * ih;
+    t0[i] = ctn * a;
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double ss = 0.0, tt = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      ss = fma(T_A<N>(q * N + i), s0[i], ss);
+      tt = fma(T_A<N>(q * N + i), t0[i], tt);
+    }
+    S[q] = ss;
+    T[q] = tt;
+  }
+}
+// x-face traces (lane k): rows (k, j) of the neighbour's plane k, interpolated in y
+template <int N>
+__device__ __forceinline__ void xtrace(const double* plane, const double* c, double ih, int hi,
+                                       double (&S)[N], double (&T)[N]) {
+  const double cna = c[2], cng = c[3], ctn = c[5];
+  double s0[N], t0[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double row[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) row[i] = plane ? plane[j * N + i] : 0.0;
+    double g = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) g = fma(hi ? c_tab[N].d0[i] : c_tab[N].d1[i], row[i], g);
+    const double a = hi ? row[0] : row[N - 1];
+    s0[j] = cna * a + cng * g * ih;
+    t0[j] = ctn * a;
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double ss = 0.0, tt = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      ss = fma(T_A<N>(q * N + j), s0[j], ss);
+      tt = fma(T_A<N>(q * N + j), t0[j], tt);
+    }
+    S[q] = ss;
+    T[q] = tt;
+  }
+}
+
+// Neighbour prologue over the asynchronously staged tiles: own in TB half 0, y-lo in TB half 1,
+// y-hi / z-lo / z-hi in the FY / FX / FZ regions (cell stride FS, plane stride N2). The z and x
+// traces are taken first and written over the z staging, then the y traces over the y-hi
+// staging. Leaves TB free. All threads must call it (three barriers).
+template <int N, bool WB>
+__device__ void nbr_prologue_async(const KParams& kp, const Cells<N, WB>& cl, const Lane& L,
+                                   double* TB, double* FY, double* FX, double* FZ, const double* tile) {
+  using G = Geo<N>;
+  static_assert(G::FS >= G::N3, "a face region must hold one staged tile");
+  const int t = L.t;
+  {
+    double xs[2][2][N], zs[2][2][N];
+    if (L.active) {
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi) {
+        // x: the neighbour is the next / previous cell of the group (its tile is in TB half 0)
+        // unless the group ends there; then its plane t is read from global memory
+        const double* nbp = cl.nb[L.cs][hi];
+        const int ncs = L.cs + (hi ? 1 : -1);
+        const double* plane = nullptr;
+        if (nbp) {
+          if (ncs >= 0 && ncs < G::C && nbp == tile + (size_t)ncs * G::N3)
+            plane = TB + ncs * G::CTB + t * G::KS;
+          else
+            plane = nbp + t * G::N2;
+        }
+        xtrace<N>(plane, cl.fc[L.cs][hi], kp.ih[0], hi, xs[hi][0], xs[hi][1]);
+        ztrace<N, G::N2>((hi ? FZ : FX) + L.cs * G::FS, cl.fc[L.cs][4 + hi], kp.ih[2], hi, t,
+                         zs[hi][0], zs[hi][1]);
+      }
+    }
+    __syncthreads();   // z staging consumed
+    if (L.active) {
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            FX[L.cs * G::FS + (2 * hi + a) * G::N2 + t * N + q] = xs[hi][a][q];
+            FZ[L.cs * G::FS + (2 * hi + a) * G::N2 + t * N + q] = zs[hi][a][q];
+          }
+    }
+  }
+  {
+    double ys[2][2][N];
+    if (L.active) {
+      ytrace<N, G::KS>(TB + L.cs * G::CTB + G::ARR, cl.fc[L.cs][2], kp.ih[1], 0, t, ys[0][0], ys[0][1]);
+      ytrace<N, G::N2>(FY + L.cs * G::FS, cl.fc[L.cs][3], kp.ih[1], 1, t, ys[1][0], ys[1][1]);
+    }
+    __syncthreads();   // y-hi staging consumed
+    if (L.active) {
+#pragma unroll
+      for (int hi = 0; hi < 2; ++hi)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int i = 0; i < N; ++i) FY[L.cs * G::FS + (2 * hi + a) * G::N2 + t * N + i] = ys[hi][a][i];
     }
   }
   __syncthreads();
@@ -907,21 +1090,23 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   Rows<N> rw;
   load_rows<N>(rw, L.t);
   // all global loads of the own tile and the y-neighbour pair are in flight during the setup
-  double own[G::PER], pv0[G::PER], pv1[G::PER];
-  load_own<N>(own, u + (size_t)cell0 * G::N3, nvalid);
+  const double* tile = u + (size_t)cell0 * G::N3;
+  async_own<N>(TB, tile, nvalid);
   SetupRegs<N> sr;
   setup_issue<N>(kp, cl, sr, cell0, NBR ? u : nullptr);
   __syncthreads();   // neighbour pointers
   if (NBR) {
-    load_nbr<N>(pv0, cl, 2);
-    load_nbr<N>(pv1, cl, 3);
+    async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, u);   // y-lo -> TB half 1
+    async_nbr<N, G::N2, G::FS>(FY, cl, 3, u);             // y-hi, z-lo, z-hi -> FY, FX, FZ (flat)
+    async_nbr<N, G::N2, G::FS>(FX, cl, 4, u);
+    async_nbr<N, G::N2, G::FS>(FZ, cl, 5, u);
   }
   setup_finish<N>(kp, cl, sr);
-  store_tile<N>(TB, own);
+  cp_async_wait_all();
   __syncthreads();
   double in[N][N], o[N][N];
   read_plane<N>(TB, L, in);
-  if (NBR) nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, u + (size_t)cell0 * G::N3, pv0, pv1);
+  if (NBR) nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, tile);
   else __syncthreads();
   plane_op<N, NBR, false, FACES>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
@@ -929,9 +1114,65 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
 }
 
+// The volume terms alone, A^v u (Stages 1-3; dg_apply_parts with mask = volume):
+// a persistent kernel, one CTA per resident slot, walking the cell groups with a stride of the
+// grid; the next group's tile and coefficients are loaded into registers while the current
+// group is computed, so the HBM/L2 latency is hidden behind the fp64 work.
+template <int N>
+__global__ void __launch_bounds__(Geo<N>::NT, DG_VOL_MINB)
+k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  __shared__ Cells<N, false> cl;
+  double* TB = sm;
+  const int ngroups = (kp.ncells + G::C - 1) / G::C;
+  const Lane L = lane_id<N>();
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+  const int nxy = kp.nx * kp.ny;
+  double nxt[G::PER], kn[3] = {0.0, 0.0, 0.0}, cn = 0.0;
+  auto prefetch = [&](int g) {
+    const int cell0 = g * G::C;
+    load_own<N>(nxt, u + (size_t)cell0 * G::N3, min(G::C, kp.ncells - cell0));
+    const int cell = cell0 + (int)threadIdx.x;
+    if (threadIdx.x < G::C && cell < kp.ncells) {
+      const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
+      kn[0] = __ldg(Kc); kn[1] = __ldg(Kc + 1); kn[2] = __ldg(Kc + 2);
+      cn = kp.c ? __ldg(kp.c + cell) : 0.0;
+    }
+  };
+  int g = blockIdx.x;
+  if (g < ngroups) prefetch(g);
+  for (; g < ngroups; g += gridDim.x) {
+    const int cell0 = g * G::C;
+    const int nvalid = min(G::C, kp.ncells - cell0);
+    __syncthreads();   // the previous group's TB and vc reads are done
+    store_tile<N>(TB, nxt);
+    if (threadIdx.x < G::C) {
+      const int cs = threadIdx.x;
+      const bool ok = cs < nvalid;
+      cl.vc[cs][0] = ok ? kn[0] * vol * kp.ih[0] * kp.ih[0] : 0.0;
+      cl.vc[cs][1] = ok ? kn[1] * vol * kp.ih[1] * kp.ih[1] : 0.0;
+      cl.vc[cs][2] = ok ? kn[2] * vol * kp.ih[2] * kp.ih[2] : 0.0;
+      cl.vc[cs][3] = ok ? vol * cn : 0.0;
+    }
+    __syncthreads();
+    if (g + (int)gridDim.x < ngroups) prefetch(g + gridDim.x);
+    double in[N][N], o[N][N];
+    read_plane<N>(TB, L, in);
+    plane_op<N, false, false, false>(kp, cl, L, rw, true, in, o, TB, nullptr, nullptr, nullptr);
+    if (L.active) write_plane<N>(TB, L, o);
+    __syncthreads();
+    unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  }
+}
+
 // Jacobi-PCG per cell; SWEEP: defect d = f - A u first, result u + omega du.
 // Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
-template <int N, bool SWEEP>
+// VS (n = 5): r and p live in shared planes too, so nothing but the operator's own planes is
+// held in registers across an application (no spills at n = 5).
+template <int N, bool SWEEP, bool VS = (N >= 5)>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
      double* __restrict__ out) {
@@ -988,61 +1229,139 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
         for (int i = 0; i < N; ++i) ds[j * N + i] = valid ? dg[j][i] : 1.0;
   }
-  double rr = 0.0, rz = 0.0;
-#pragma unroll
-  for (int j = 0; j < N; ++j)
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
-      P[j][i] = z;
-      rr = fma(R[j][i], R[j][i], rr);
-      rz = fma(R[j][i], z, rz);
-      if (L.active) xs[j * N + i] = 0.0;
-    }
-  const double rr0 = cell_sum<N>(rr, L.lane);
-  rz = cell_sum<N>(rz, L.lane);
-  bool conv = !valid || rr0 == 0.0;
-  int its = 0;
-  for (int iter = 0;; ++iter) {
-    const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
-    if (done || iter >= kp.max_it) break;
-    double Q[N][N];
-    plane_op<N, false, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
-    double pq = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-#pragma unroll
-      for (int i = 0; i < N; ++i) pq = fma(P[j][i], Q[j][i], pq);
-    pq = cell_sum<N>(pq, L.lane);
-    double alpha = 0.0;
-    if (!conv) {
-      if (pq > 0.0) alpha = rz / pq;
-      else conv = true;
-    }
-    double r2 = 0.0, rzn = 0.0;
+  int its_out = 0;
+  if constexpr (VS) {
+    double* rs = DS + G::C * G::PS + po;
+    double* ps = rs + G::C * G::PS;
+    double rr = 0.0, rz = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
-        R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
-        r2 = fma(R[j][i], R[j][i], r2);
-        if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
+        const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
+        rr = fma(R[j][i], R[j][i], rr);
+        rz = fma(R[j][i], z, rz);
+        if (L.active) {
+          xs[j * N + i] = 0.0;
+          rs[j * N + i] = R[j][i];
+          ps[j * N + i] = z;
+        }
       }
-    r2 = cell_sum<N>(r2, L.lane);
-    rzn = cell_sum<N>(rzn, L.lane);
-    if (!conv) {
-      ++its;
-      if (r2 <= kp.tol2 * rr0) conv = true;
-      const double beta = rzn / rz;
-      rz = rzn;
-      if (!conv && L.active) {
+    const double rr0 = cell_sum<N>(rr, L.lane);
+    rz = cell_sum<N>(rz, L.lane);
+    bool conv = !valid || rr0 == 0.0;
+    int its = 0;
+    for (int iter = 0;; ++iter) {
+      const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
+      if (done || iter >= kp.max_it) break;
+      double Q[N][N];
+      {
+        double Pin[N][N];
 #pragma unroll
         for (int j = 0; j < N; ++j)
 #pragma unroll
-          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
+          for (int i = 0; i < N; ++i) Pin[j][i] = L.active ? ps[j * N + i] : 0.0;
+        plane_op<N, false, true>(kp, cl, L, rw, true, Pin, Q, TB, FY, FX, FZ);  // Q = D_T P
+      }
+      double pq = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          if (L.active) pq = fma(ps[j * N + i], Q[j][i], pq);
+      pq = cell_sum<N>(pq, L.lane);
+      double alpha = 0.0;
+      if (!conv) {
+        if (pq > 0.0) alpha = rz / pq;
+        else conv = true;
+      }
+      double r2 = 0.0, rzn = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i)
+          if (L.active) {
+            xs[j * N + i] = fma(alpha, ps[j * N + i], xs[j * N + i]);
+            const double r = fma(-alpha, Q[j][i], rs[j * N + i]);
+            rs[j * N + i] = r;
+            r2 = fma(r, r, r2);
+            rzn = fma(r, r * ds[j * N + i], rzn);
+          }
+      r2 = cell_sum<N>(r2, L.lane);
+      rzn = cell_sum<N>(rzn, L.lane);
+      if (!conv) {
+        ++its;
+        if (r2 <= kp.tol2 * rr0) conv = true;
+        const double beta = rzn / rz;
+        rz = rzn;
+        if (!conv && L.active) {
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int i = 0; i < N; ++i)
+              ps[j * N + i] = fma(beta, ps[j * N + i], rs[j * N + i] * ds[j * N + i]);
+        }
       }
     }
+    its_out = conv ? its : (its | (1 << 30));
+  } else {
+    double rr = 0.0, rz = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
+        P[j][i] = z;
+        rr = fma(R[j][i], R[j][i], rr);
+        rz = fma(R[j][i], z, rz);
+        if (L.active) xs[j * N + i] = 0.0;
+      }
+    const double rr0 = cell_sum<N>(rr, L.lane);
+    rz = cell_sum<N>(rz, L.lane);
+    bool conv = !valid || rr0 == 0.0;
+    int its = 0;
+    for (int iter = 0;; ++iter) {
+      const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
+      if (done || iter >= kp.max_it) break;
+      double Q[N][N];
+      plane_op<N, false, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+      double pq = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) pq = fma(P[j][i], Q[j][i], pq);
+      pq = cell_sum<N>(pq, L.lane);
+      double alpha = 0.0;
+      if (!conv) {
+        if (pq > 0.0) alpha = rz / pq;
+        else conv = true;
+      }
+      double r2 = 0.0, rzn = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j)
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
+          R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
+          r2 = fma(R[j][i], R[j][i], r2);
+          if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
+        }
+      r2 = cell_sum<N>(r2, L.lane);
+      rzn = cell_sum<N>(rzn, L.lane);
+      if (!conv) {
+        ++its;
+        if (r2 <= kp.tol2 * rr0) conv = true;
+        const double beta = rzn / rz;
+        rz = rzn;
+        if (!conv && L.active) {
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+#pragma unroll
+            for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
+        }
+      }
+    }
+    its_out = conv ? its : (its | (1 << 30));
   }
   // result: X (+ u) -> TB -> global
   __syncthreads();
@@ -1058,7 +1377,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   }
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
-  if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
+  if (valid && L.t == 0) kp.its[cell0 + L.cs] = its_out;
 }
 
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks).

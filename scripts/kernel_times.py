@@ -1,0 +1,63 @@
+"""Per-kernel timings on one GPU for A/B work: dg_apply, the volume kernel alone, D_T, one sweep.
+
+usage: python scripts/kernel_times.py [C2 C3 ...]   (DG_LIB selects the library build)
+Prints one JSON line per config: microseconds per call (CUDA events, 20 calls after warm-up,
+inputs resident) and the model fraction of the derived fp64 peak (SURVEY 8(d) flop model).
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_1805_11930_b200 as dg
+from synth import make_config, make_vectors
+
+PEAK = 148 * 64 * 2 * 1.965e9
+
+
+def timed(fn, calls=20):
+    for _ in range(3):
+        fn()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(calls):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) * 1e3 / calls
+
+
+def main(names):
+    for name in names:
+        P = make_config(name)
+        u, f = make_vectors(P)
+        ctx = dg.DGContext(P)
+        ut, ft = torch.from_numpy(u).cuda(), torch.from_numpy(f).cuda()
+        out = torch.empty_like(ut)
+        n = P.p + 1
+        nc = P.n_cells
+        vol = 24 * n ** 4 + 8 * n ** 3
+        sf, nf = 8 * n ** 3 + 12 * n ** 2, 10 * n ** 3
+        r = {"config": name, "p": P.p}
+        t = timed(lambda: ctx.apply_parts(ut, out, dg.MASK_VOLUME))
+        r["volume_us"], r["volume_frac"] = t, nc * vol / (t * 1e-6) / PEAK
+        t = timed(lambda: ctx.apply(ut, out))
+        r["apply_us"], r["apply_frac"] = t, nc * (vol + 6 * sf + 6 * nf) / (t * 1e-6) / PEAK
+        t = timed(lambda: ctx.block_diag_apply(ut, out))
+        r["dt_us"], r["dt_frac"] = t, nc * (vol + 6 * sf) / (t * 1e-6) / PEAK
+        uu = ut.clone()
+        t = timed(lambda: ctx.sweep(uu, ft, 1.0, 1e-12), calls=3)
+        st = ctx.stats()
+        it = 12 if P.local_solver == "cg" else 20
+        per_it = (vol + 6 * sf + it * n ** 3) * (1 if P.local_solver == "cg" else 2)
+        fl = nc * (vol + 6 * sf + 6 * nf + 4 * n ** 3) + st["it_sum"] * per_it
+        r["sweep_us"], r["sweep_frac"], r["it_mean"] = t, fl / (t * 1e-6) / PEAK, st["it_mean"]
+        print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
+        ctx.close()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1:] or ["C2"])
