@@ -14,6 +14,10 @@ Modules
           Kronecker products (derivation in SURVEY.md §8(c) step 3, re-derived in
           DESIGN.md); matrix-free-free reference apply, D_T, LU local solves and the
           block-Jacobi sweep of Alg. 2
+  hybrid  the hybrid multigrid of Alg. 1 with the P0 subspace: P, R = P^T
+          (P:725-735), A^ = P^T A P by brute force and by the rescaled finite-volume
+          construction of App. A.1, the V-cycle with an exact coarse solve,
+          and the V-cycle-preconditioned flexible CG
 
 Pins: every function is checked in tests/test_oracle_*.py against closed forms,
 invariants or the other tier (never against itself or the CUDA path).
