@@ -141,6 +141,47 @@ dg_status dg_halo_plan(const dg_desc* desc, int64_t out[6]);
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 broadcasts it to the other ranks). */
 dg_status dg_nccl_unique_id(void* out128);
 
+/* ---- Hybrid multigrid with the P0 subspace (Alg. 1) ----------
+ * Single rank (nranks = 1) and b = 0 only (the outer iteration is a CG; the paper solves the
+ * convection-dominated case with FGMRES and block SSOR instead); otherwise
+ * DG_ERR_UNSUPPORTED. The paper's AMG coarse solve (line 4) is replaced by Jacobi-PCG on A^ to
+ * coarse_tol (reading #25 of DESIGN.md). Scratch (7 DoF vectors + O(cells)) is allocated on the
+ * first call and owned by the context. */
+typedef struct {
+  int32_t n_pre, n_post;   /* block-Jacobi sweeps before / after the coarse correction */
+  double omega;            /* sweep damping (Alg. 2 line 4) */
+  double local_tol;        /* local Krylov tolerance of the sweeps */
+  double coarse_tol;       /* relative residual tolerance of the coarse Jacobi-PCG */
+  int32_t coarse_max_it;
+  double rel_tol;          /* outer: ||f - A u||_2 <= rel_tol ||f - A u_0||_2 */
+  int32_t max_it;          /* outer iteration cap */
+} dg_hybrid_params;
+
+typedef struct {
+  int32_t iterations;      /* outer flexible-CG iterations */
+  int32_t converged;       /* 1 if rel_tol was reached */
+  double rel_residual;     /* final ||r|| / ||r_0|| (recursively updated residual) */
+  int32_t vcycles;         /* preconditioner applications */
+  int32_t coarse_it_max;   /* largest coarse PCG iteration count over the V-cycles */
+  int32_t coarse_nonconverged;  /* V-cycles whose coarse solve hit coarse_max_it */
+} dg_hybrid_stats;
+
+/* A^ = P^T A P (eq. galerkin_product; App. A.1) for the local cells, copied to the
+ * HOST array Ah[7][n_cells]: row 0 the diagonal, row 1 + f the coupling of cell T to its face-f
+ * neighbour (f = 0..5: x-, x+, y-, y+, z-, z+), 0 where there is none. Synchronises. */
+dg_status dg_coarse_matrix(dg_ctx* ctx, double* Ah_host);
+
+/* One V-cycle of Alg. 1 from u_0 = 0 as a preconditioner: z = V(r). r, z: device
+ * [n_local_dof], must not alias. Stream ordered. */
+dg_status dg_hybrid_vcycle(dg_ctx* ctx, const double* r, double* z, const dg_hybrid_params* prm,
+                           void* cuda_stream);
+
+/* Solves A u = f by flexible CG (beta = z_new.(r_new - r_old) / z_old.r_old) preconditioned by
+ * the V-cycle, from the initial guess in u (device, in/out). Synchronises once per iteration
+ * (the scalars of the recurrence are read back); st may be NULL. */
+dg_status dg_hybrid_solve(dg_ctx* ctx, double* u, const double* f, const dg_hybrid_params* prm,
+                          dg_hybrid_stats* st, void* cuda_stream);
+
 /* fp64 FMA-throughput microbenchmark: launches `blocks` x 256 threads,
  * each running 16 independent DFMA chains for `iters` steps on `cuda_stream`; *flops receives
  * the flop count (2 per DFMA). sink: device buffer of blocks*256 doubles (defeats DCE). */

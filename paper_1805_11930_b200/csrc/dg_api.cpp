@@ -9,9 +9,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <utility>
 #include <string>
 #include <vector>
 
+#include "dg_hybrid.h"
 #include "dg_kernels.h"
 #include "dg_tables.h"
 
@@ -81,6 +83,13 @@ struct dg_ctx {
   double* d_ghost_hi = nullptr;
   double* d_unew = nullptr;
   int32_t* d_its = nullptr;
+  // hybrid multigrid scratch (allocated on first use)
+  double* d_Ah = nullptr;      // [7][ncells]
+  double* d_cvec = nullptr;    // rh, uh, 3 coarse work vectors: [5][ncells]
+  double* d_part = nullptr;    // [kPartials]
+  double* d_dots = nullptr;    // [3]
+  int* d_cits = nullptr;       // [1]
+  double* d_hv = nullptr;      // t, r0, r1, z, p, q: [6][ndof]
   int method = 0;  // resolved local method
   int32_t max_it = 1000;
   ncclComm_t comm = nullptr;
@@ -131,6 +140,12 @@ void release(dg_ctx* c) {
   cudaFree(c->d_ghost_hi);
   cudaFree(c->d_unew);
   cudaFree(c->d_its);
+  cudaFree(c->d_Ah);
+  cudaFree(c->d_cvec);
+  cudaFree(c->d_part);
+  cudaFree(c->d_dots);
+  cudaFree(c->d_cits);
+  cudaFree(c->d_hv);
   delete c;
 }
 
@@ -488,6 +503,180 @@ dg_status dg_microbench_dfma(double* sink, int32_t blocks, int32_t iters, int64_
   cudaError_t e = dg::launch_dfma_bench(sink, blocks, iters, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "dfma bench");
   *flops = (int64_t)blocks * 256 * 16 * 2 * (int64_t)iters;
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ---- hybrid multigrid (Alg. 1) -------------------------------------------------------------
+namespace {
+
+dg_status hybrid_prepare(dg_ctx* c, cudaStream_t s) {
+  if (c->desc.nranks != 1)
+    return fail(DG_ERR_UNSUPPORTED, "hybrid multigrid: single rank only (the coarse solve is not distributed)");
+  if (c->desc.b[0] != 0.0 || c->desc.b[1] != 0.0 || c->desc.b[2] != 0.0)
+    return fail(DG_ERR_UNSUPPORTED, "hybrid multigrid: b = 0 only (outer CG)");
+  if (c->d_Ah) return DG_OK;
+  const size_t N = (size_t)c->ncells, nd = (size_t)c->ndof;
+  cudaError_t e = cudaMalloc(&c->d_Ah, 7 * N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cvec, 5 * N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_part, (size_t)dg::kPartials * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_dots, 3 * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cits, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_hv, 6 * nd * 8);
+  if (e != cudaSuccess) return fail(DG_ERR_NOMEM, "hybrid multigrid scratch");
+  dg::KParams kp = c->kp;
+  kp.mask = 7u;
+  e = dg::launch_coarse_matrix(kp, c->d_Ah, s);
+  if (e != cudaSuccess) return cuda_fail(e, "coarse matrix");
+  return DG_OK;
+}
+
+dg_status check_params(const dg_hybrid_params* p) {
+  if (!p) return fail(DG_ERR_INVALID, "params is NULL");
+  if (p->n_pre < 0 || p->n_post < 0 || p->coarse_max_it < 1 || p->max_it < 0)
+    return fail(DG_ERR_INVALID, "need n_pre, n_post, max_it >= 0 and coarse_max_it >= 1");
+  if (!std::isfinite(p->omega) || !(p->local_tol >= 0) || !(p->coarse_tol >= 0) || !(p->rel_tol >= 0))
+    return fail(DG_ERR_INVALID, "omega finite, tolerances >= 0");
+  return DG_OK;
+}
+
+// z = V(r), Alg. 1 with u_0 = 0; *coarse_its = the coarse PCG's raw iteration word (or NULL)
+dg_status vcycle(dg_ctx* c, const double* r, double* z, const dg_hybrid_params* p, cudaStream_t s,
+                 int* coarse_its) {
+  const int64_t nd = c->ndof;
+  const int N = (int)c->ncells, n = c->desc.p + 1;
+  double* t = c->d_hv;
+  double* rh = c->d_cvec;
+  double* uh = c->d_cvec + N;
+  cudaError_t e = cudaMemsetAsync(z, 0, (size_t)nd * 8, s);
+  if (e != cudaSuccess) return cuda_fail(e, "vcycle memset");
+  for (int i = 0; i < p->n_pre; ++i) {   // line 1: presmooth
+    dg_status st = dg_block_jacobi_sweep(c, z, r, p->omega, p->local_tol, s);
+    if (st != DG_OK) return st;
+  }
+  dg_status st = dg_apply(c, z, t, s);   // line 2: residual
+  if (st != DG_OK) return st;
+  if ((e = dg::launch_sub(t, r, t, nd, s)) != cudaSuccess) return cuda_fail(e, "residual");
+  if ((e = dg::launch_restrict(t, rh, N, n * n * n, s)) != cudaSuccess) return cuda_fail(e, "restrict");   // line 3
+  dg::KParams kp = c->kp;
+  if ((e = dg::launch_coarse_pcg(kp, c->d_Ah, rh, uh, c->d_cvec + 2 * (size_t)N, c->d_part, c->d_cits,
+                                 p->coarse_tol, p->coarse_max_it, s)) != cudaSuccess)
+    return cuda_fail(e, "coarse solve");   // line 4
+  if ((e = dg::launch_prolongate_add(z, uh, nd, n * n * n, s)) != cudaSuccess) return cuda_fail(e, "prolongate");  // line 5
+  for (int i = 0; i < p->n_post; ++i) {   // line 6: postsmooth
+    st = dg_block_jacobi_sweep(c, z, r, p->omega, p->local_tol, s);
+    if (st != DG_OK) return st;
+  }
+  if (coarse_its) {
+    e = cudaMemcpyAsync(coarse_its, c->d_cits, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "coarse its");
+  }
+  return DG_OK;
+}
+
+dg_status dots(dg_ctx* c, const double* a0, const double* b0, const double* a1, const double* b1,
+               const double* a2, const double* b2, double out[3], cudaStream_t s) {
+  cudaError_t e = dg::launch_dots(a0, b0, a1, b1, a2, b2, c->ndof, c->d_part, c->d_dots, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, c->d_dots, 3 * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "dot products");
+  return DG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_coarse_matrix(dg_ctx* c, double* Ah_host) {
+  if (!c || !Ah_host) return fail(DG_ERR_INVALID, "NULL argument");
+  dg_status st = hybrid_prepare(c, nullptr);
+  if (st != DG_OK) return st;
+  cudaError_t e = cudaMemcpy(Ah_host, c->d_Ah, 7 * (size_t)c->ncells * 8, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return cuda_fail(e, "coarse matrix copy");
+  return DG_OK;
+}
+
+dg_status dg_hybrid_vcycle(dg_ctx* c, const double* r, double* z, const dg_hybrid_params* p, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(r, "r") || check_vec(z, "z")) return DG_ERR_INVALID;
+  if (r == z) return fail(DG_ERR_INVALID, "r and z must not alias");
+  dg_status st = check_params(p);
+  if (st != DG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = hybrid_prepare(c, s)) != DG_OK) return st;
+  return vcycle(c, r, z, p, s, nullptr);
+}
+
+dg_status dg_hybrid_solve(dg_ctx* c, double* u, const double* f, const dg_hybrid_params* p,
+                          dg_hybrid_stats* out, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
+  if ((const double*)u == f) return fail(DG_ERR_INVALID, "u and f must not alias");
+  dg_status st = check_params(p);
+  if (st != DG_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  if ((st = hybrid_prepare(c, s)) != DG_OK) return st;
+  const int64_t nd = c->ndof;
+  double* t = c->d_hv;   // used inside the V-cycle
+  double* r0 = c->d_hv + nd;
+  double* r1 = c->d_hv + 2 * nd;
+  double* z = c->d_hv + 3 * nd;
+  double* pv = c->d_hv + 4 * nd;
+  double* q = c->d_hv + 5 * nd;
+  dg_hybrid_stats hs{};
+  int cits = 0;
+  auto note_coarse = [&]() {
+    const int v = cits & ~(1 << 30);
+    if (v > hs.coarse_it_max) hs.coarse_it_max = v;
+    if (cits & (1 << 30)) ++hs.coarse_nonconverged;
+    ++hs.vcycles;
+  };
+  cudaError_t e;
+  if ((st = dg_apply(c, u, q, s)) != DG_OK) return st;
+  if ((e = dg::launch_sub(r0, f, q, nd, s)) != cudaSuccess) return cuda_fail(e, "initial residual");
+  double d[3];
+  if ((st = dots(c, r0, r0, nullptr, nullptr, nullptr, nullptr, d, s)) != DG_OK) return st;
+  const double rr0 = d[0];
+  hs.rel_residual = rr0 > 0.0 ? 1.0 : 0.0;
+  if (rr0 > 0.0 && p->max_it > 0) {
+    if ((st = vcycle(c, r0, z, p, s, &cits)) != DG_OK) return st;
+    if ((e = cudaMemcpyAsync(pv, z, (size_t)nd * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+      return cuda_fail(e, "p = z");
+    if ((st = dots(c, z, r0, nullptr, nullptr, nullptr, nullptr, d, s)) != DG_OK) return st;
+    note_coarse();
+    double zr = d[0];
+    for (int it = 1; it <= p->max_it; ++it) {
+      if ((st = dg_apply(c, pv, q, s)) != DG_OK) return st;
+      if ((st = dots(c, pv, q, nullptr, nullptr, nullptr, nullptr, d, s)) != DG_OK) return st;
+      if (!(d[0] > 0.0)) break;   // breakdown (A or the preconditioner not SPD)
+      const double alpha = zr / d[0];
+      if ((e = dg::launch_axpby(u, alpha, pv, 1.0, nd, s)) != cudaSuccess) return cuda_fail(e, "u update");
+      if ((e = cudaMemcpyAsync(r1, r0, (size_t)nd * 8, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return cuda_fail(e, "r copy");
+      if ((e = dg::launch_axpby(r1, -alpha, q, 1.0, nd, s)) != cudaSuccess) return cuda_fail(e, "r update");
+      if ((st = dots(c, r1, r1, nullptr, nullptr, nullptr, nullptr, d, s)) != DG_OK) return st;
+      hs.iterations = it;
+      hs.rel_residual = std::sqrt(d[0] / rr0);
+      if (hs.rel_residual <= p->rel_tol) {
+        hs.converged = 1;
+        std::swap(r0, r1);
+        break;
+      }
+      if ((st = vcycle(c, r1, z, p, s, &cits)) != DG_OK) return st;
+      if ((st = dots(c, z, r1, z, r0, nullptr, nullptr, d, s)) != DG_OK) return st;
+      note_coarse();
+      const double beta = (d[0] - d[1]) / zr;
+      zr = d[0];
+      if ((e = dg::launch_axpby(pv, 1.0, z, beta, nd, s)) != cudaSuccess) return cuda_fail(e, "p update");
+      std::swap(r0, r1);
+    }
+  } else if (rr0 == 0.0) {
+    hs.converged = 1;
+  }
+  (void)t;
+  if (out) *out = hs;
+  c->launches = 0;
   return DG_OK;
 }
 

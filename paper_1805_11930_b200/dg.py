@@ -25,7 +25,8 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_local_block_solve", "dg_set_local_solver", "dg_get_stats", "dg_apply_parts",
            "dg_block_diag_apply", "dg_ghost_layers", "dg_fill_ghosts", "dg_tables",
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
-           "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan"]
+           "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
+           "dg_hybrid_vcycle", "dg_hybrid_solve"]
 
 
 class DGError(RuntimeError):
@@ -52,6 +53,27 @@ class dg_stats(ctypes.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class dg_hybrid_params(ctypes.Structure):
+    _fields_ = [("n_pre", ctypes.c_int32), ("n_post", ctypes.c_int32), ("omega", ctypes.c_double),
+                ("local_tol", ctypes.c_double), ("coarse_tol", ctypes.c_double),
+                ("coarse_max_it", ctypes.c_int32), ("rel_tol", ctypes.c_double),
+                ("max_it", ctypes.c_int32)]
+
+
+class dg_hybrid_stats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("rel_residual", ctypes.c_double), ("vcycles", ctypes.c_int32),
+                ("coarse_it_max", ctypes.c_int32), ("coarse_nonconverged", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def hybrid_params(n_pre=1, n_post=1, omega=1.0, local_tol=1e-12, coarse_tol=1e-12,
+                  coarse_max_it=10000, rel_tol=1e-8, max_it=200) -> dg_hybrid_params:
+    return dg_hybrid_params(n_pre, n_post, omega, local_tol, coarse_tol, coarse_max_it, rel_tol, max_it)
 
 
 _lib = None
@@ -87,6 +109,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_microbench_dfma": ([P, i32, i32, ctypes.POINTER(i64), P], i32),
         "dg_slab_range": ([i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)], i32),
         "dg_halo_plan": ([ctypes.POINTER(dg_desc), ctypes.POINTER(i64)], i32),
+        "dg_coarse_matrix": ([P, ctypes.POINTER(dbl)], i32),
+        "dg_hybrid_vcycle": ([P, P, P, ctypes.POINTER(dg_hybrid_params), P], i32),
+        "dg_hybrid_solve": ([P, P, P, ctypes.POINTER(dg_hybrid_params),
+                             ctypes.POINTER(dg_hybrid_stats), P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -247,6 +273,27 @@ class DGContext:
         _check(self.lib.dg_block_jacobi_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
                                               _stream(stream)))
         return u
+
+    # ---- hybrid multigrid (Alg. 1, P0 subspace) ------------------------------
+    def coarse_matrix(self):
+        """A^ = P^T A P as a (7, n_cells) numpy array (diagonal, then x-, x+, y-, y+, z-, z+)."""
+        import numpy as np
+        n = self.cell_end - self.cell_begin
+        out = np.empty(7 * n, dtype=np.float64)
+        _check(self.lib.dg_coarse_matrix(self.h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out.reshape(7, n)
+
+    def hybrid_vcycle(self, r, z, params: Optional[dg_hybrid_params] = None, stream=None):
+        prm = params if params is not None else hybrid_params()
+        _check(self.lib.dg_hybrid_vcycle(self.h, _ptr(r), _ptr(z), ctypes.byref(prm), _stream(stream)))
+        return z
+
+    def hybrid_solve(self, u, f, params: Optional[dg_hybrid_params] = None, stream=None) -> dict:
+        prm = params if params is not None else hybrid_params()
+        st = dg_hybrid_stats()
+        _check(self.lib.dg_hybrid_solve(self.h, _ptr(u), _ptr(f), ctypes.byref(prm), ctypes.byref(st),
+                                        _stream(stream)))
+        return st.as_dict()
 
     def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000):
         _check(self.lib.dg_set_local_solver(self.h, method, max_it))
