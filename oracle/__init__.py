@@ -18,6 +18,8 @@ Modules
           (P:725-735), A^ = P^T A P by brute force and by the rescaled finite-volume
           construction of App. A.1, the V-cycle with an exact coarse solve,
           and the V-cycle-preconditioned flexible CG
+  sor     block SOR / SSOR of Alg. 3 written out for a traversal order, and its
+          red-black coloured form
 
 Pins: every function is checked in tests/test_oracle_*.py against closed forms,
 invariants or the other tier (never against itself or the CUDA path).
