@@ -96,6 +96,18 @@ dg_status dg_apply(dg_ctx* ctx, const double* u, double* Au, void* cuda_stream);
 dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double omega,
                                 double local_tol, void* cuda_stream);
 
+/* Block SOR / SSOR in the red-black cell order (Alg. 3): colour
+ * (cx + cy + cz) mod 2 (global indices), red = 0 first. A forward sweep updates all red cells
+ * from the current u, then all black cells from the updated u, each cell by
+ * u_T <- u_T + omega D_T^{-1} (f - A u)_T with the same local Krylov solve as the block-Jacobi
+ * sweep (equal to Alg. 3's (1 - omega) u + omega du with du the new block value, DESIGN reading
+ * #17); symmetric != 0 adds the backward sweep (black, then red): block SSOR.
+ * Every colour is ordered after all cells of the other colour, so each half-sweep is one fully
+ * parallel launch. The per-cell statistics (dg_get_stats) are those of the last half-sweep
+ * (0 iterations for the cells it skipped). */
+dg_status dg_block_sor_sweep(dg_ctx* ctx, double* u, const double* f, double omega, double local_tol,
+                             int32_t symmetric, void* cuda_stream);
+
 /* Alg. 2 line 3 alone: du_T = (iterative) D_T^{-1} d_T for every local cell. */
 dg_status dg_local_block_solve(dg_ctx* ctx, const double* d, double* du, double local_tol,
                                void* cuda_stream);

@@ -273,6 +273,8 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   kp.ghost_hi = r < G - 1 ? c->d_ghost_hi : nullptr;
   kp.mask = 7u;
   kp.its = c->d_its;
+  kp.colour = -1;
+  kp.zoff = c->z_begin;
   c->method = (desc->b[0] == 0.0 && desc->b[1] == 0.0 && desc->b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
   c->max_it = 1000;
 
@@ -425,6 +427,35 @@ dg_status dg_block_jacobi_sweep(dg_ctx* c, double* u, const double* f, double om
   c->last_stream = s;
   c->have_stats = true;
   c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega, double tol,
+                             int32_t symmetric, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
+  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
+  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int order[4] = {0, 1, 1, 0};   // forward: red, black; backward: black, red
+  const int halves = symmetric ? 4 : 2;
+  c->launches = 0;
+  for (int h = 0; h < halves; ++h) {
+    dg_status st = halo_exchange(c, u, s);
+    if (st != DG_OK) return st;
+    dg::KParams kp = c->kp;
+    kp.tol2 = tol * tol;
+    kp.max_it = c->max_it;
+    kp.omega = omega;
+    kp.colour = order[h];
+    cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, c->d_unew, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sor half-sweep");
+    e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "sor copy-back");
+    ++c->launches;
+  }
+  c->last_stream = s;
+  c->have_stats = true;
   return DG_OK;
 }
 

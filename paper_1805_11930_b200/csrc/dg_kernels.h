@@ -28,7 +28,17 @@ struct KParams {
   double tol2;                   // local_tol^2
   double omega;
   int32_t* its;                  // [ncells] iterations of the last solve
+  int32_t colour;                // -1: every cell; 0 / 1: only cells with (cx+cy+cz) % 2 == colour
+                                 // are updated (multicolour block SOR), the others pass through
+  int32_t zoff;                  // global z index of the slab's first layer (for the colour)
 };
+
+// the cell is outside the colour of a multicolour half-sweep (kp.colour >= 0)
+__host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
+  if (kp.colour < 0) return false;
+  const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / (kp.nx * kp.ny) + kp.zoff;
+  return ((cx + cy + cz) & 1) != kp.colour;
+}
 
 enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2 };
 

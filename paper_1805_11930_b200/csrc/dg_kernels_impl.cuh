@@ -611,7 +611,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     const double rr0 = cell_sum<N>(g, 0, tid);
     g.sc[S_RR0][tid] = rr0;
     g.sc[S_RZ][tid] = cell_sum<N>(g, 1, tid);
-    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0);
+    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0) || skip_cell(kp, cell0 + tid);
     g.its[tid] = 0;
   }
   for (int iter = 0;; ++iter) {
@@ -766,7 +766,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     g.sc[S_RHO][tid] = 1.0;
     g.sc[S_ALPHA][tid] = 1.0;
     g.sc[S_OMEGA][tid] = 1.0;
-    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0);
+    g.conv[tid] = (tid >= nvalid) || (rr0 == 0.0) || skip_cell(kp, cell0 + tid);
     g.its[tid] = 0;
     g.rst[tid] = 0;
   }

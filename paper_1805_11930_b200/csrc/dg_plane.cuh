@@ -1249,7 +1249,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       }
     const double rr0 = cell_sum<N>(rr, L.lane);
     rz = cell_sum<N>(rz, L.lane);
-    bool conv = !valid || rr0 == 0.0;
+    bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
     int its = 0;
     for (int iter = 0;; ++iter) {
       const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
@@ -1318,7 +1318,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       }
     const double rr0 = cell_sum<N>(rr, L.lane);
     rz = cell_sum<N>(rz, L.lane);
-    bool conv = !valid || rr0 == 0.0;
+    bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
     int its = 0;
     for (int iter = 0;; ++iter) {
       const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
@@ -1459,7 +1459,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       }
     }
   const double rr0 = cell_sum<N>(rr, L.lane);
-  bool conv = !valid || rr0 == 0.0;
+  bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
   double rho = 1.0, alpha = 1.0, omega = 1.0;
   bool rst = false;
   int its = 0;

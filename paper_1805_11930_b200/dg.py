@@ -26,7 +26,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_block_diag_apply", "dg_ghost_layers", "dg_fill_ghosts", "dg_tables",
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
            "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
-           "dg_hybrid_vcycle", "dg_hybrid_solve"]
+           "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep"]
 
 
 class DGError(RuntimeError):
@@ -97,6 +97,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_block_diag_apply": ([P, P, P, P], i32),
         "dg_block_jacobi_sweep": ([P, P, P, dbl, dbl, P], i32),
         "dg_local_block_solve": ([P, P, P, dbl, P], i32),
+        "dg_block_sor_sweep": ([P, P, P, dbl, dbl, i32, P], i32),
         "dg_set_local_solver": ([P, i32, i32], i32),
         "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
         "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
@@ -294,6 +295,12 @@ class DGContext:
         _check(self.lib.dg_hybrid_solve(self.h, _ptr(u), _ptr(f), ctypes.byref(prm), ctypes.byref(st),
                                         _stream(stream)))
         return st.as_dict()
+
+    def sor_sweep(self, u, f, omega: float = 1.0, tol: float = 1e-12, symmetric: bool = False, stream=None):
+        """Red-black block SOR (symmetric: SSOR) sweep, u in place (Alg. 3)."""
+        _check(self.lib.dg_block_sor_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
+                                           1 if symmetric else 0, _stream(stream)))
+        return u
 
     def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000):
         _check(self.lib.dg_set_local_solver(self.h, method, max_it))
