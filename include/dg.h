@@ -194,6 +194,18 @@ dg_status dg_hybrid_vcycle(dg_ctx* ctx, const double* r, double* z, const dg_hyb
 dg_status dg_hybrid_solve(dg_ctx* ctx, double* u, const double* f, const dg_hybrid_params* prm,
                           dg_hybrid_stats* st, void* cuda_stream);
 
+/* ---- Stored-inverse block-Jacobi smoother (the paper's partially
+ * matrix-free variant, Table 2) -----------------------------------------------------
+ * dg_pmf_setup assembles every D_T from the 1D matrices, inverts it (Gauss-Jordan in
+ * shared memory; SPD for b = 0) and keeps the inverses on the device: n_cells (p+1)^6 doubles.
+ * b = 0 and p <= 4 only (otherwise DG_ERR_UNSUPPORTED); DG_ERR_NOMEM if they do not fit.
+ * dg_pmf_sweep: one block-Jacobi sweep with exact local solves, u <- u + omega D^{-1}(f - A u),
+ * u in place (device). dg_pmf_block: HOST copy of D_T (inverse = 0) or D_T^{-1} (inverse = 1)
+ * of one local cell, nd x nd row-major (test index first), for parity tests (synchronises). */
+dg_status dg_pmf_setup(dg_ctx* ctx);
+dg_status dg_pmf_sweep(dg_ctx* ctx, double* u, const double* f, double omega, void* cuda_stream);
+dg_status dg_pmf_block(dg_ctx* ctx, int64_t cell, int32_t inverse, double* host_out);
+
 /* fp64 FMA-throughput microbenchmark: launches `blocks` x 256 threads,
  * each running 16 independent DFMA chains for `iters` steps on `cuda_stream`; *flops receives
  * the flop count (2 per DFMA). sink: device buffer of blocks*256 doubles (defeats DCE). */

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "dg_hybrid.h"
+#include "dg_pmf.h"
 #include "dg_kernels.h"
 #include "dg_tables.h"
 
@@ -90,6 +91,8 @@ struct dg_ctx {
   double* d_dots = nullptr;    // [3]
   int* d_cits = nullptr;       // [1]
   double* d_hv = nullptr;      // t, r0, r1, z, p, q: [6][ndof]
+  double* d_pmf = nullptr;     // stored inverses [ncells][nd][nd] (dg_pmf_setup)
+  double* d_pmf_au = nullptr;  // A u of a stored-inverse sweep [ndof]
   int method = 0;  // resolved local method
   int32_t max_it = 1000;
   ncclComm_t comm = nullptr;
@@ -146,6 +149,8 @@ void release(dg_ctx* c) {
   cudaFree(c->d_dots);
   cudaFree(c->d_cits);
   cudaFree(c->d_hv);
+  cudaFree(c->d_pmf);
+  cudaFree(c->d_pmf_au);
   delete c;
 }
 
@@ -708,6 +713,83 @@ dg_status dg_hybrid_solve(dg_ctx* c, double* u, const double* f, const dg_hybrid
   (void)t;
   if (out) *out = hs;
   c->launches = 0;
+  return DG_OK;
+}
+
+}  // extern "C"
+
+// ---- stored-inverse block-Jacobi smoother (NEXT-4) -------------------------------------------
+namespace {
+dg_status pmf_check(dg_ctx* c) {
+  if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "stored inverses: p <= 4 only ((p+1)^6 doubles per cell)");
+  if (c->desc.b[0] != 0.0 || c->desc.b[1] != 0.0 || c->desc.b[2] != 0.0)
+    return fail(DG_ERR_UNSUPPORTED, "stored inverses: b = 0 only (SPD blocks, no pivoting)");
+  return DG_OK;
+}
+}  // namespace
+
+extern "C" {
+
+dg_status dg_pmf_setup(dg_ctx* c) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  dg_status st = pmf_check(c);
+  if (st != DG_OK) return st;
+  const int n = c->desc.p + 1, nd = n * n * n;
+  if (!c->d_pmf) {
+    cudaError_t e = cudaMalloc(&c->d_pmf, (size_t)c->ncells * nd * nd * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_pmf_au, (size_t)c->ndof * 8);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      cudaFree(c->d_pmf);
+      c->d_pmf = nullptr;
+      return fail(DG_ERR_NOMEM, "stored inverses do not fit in device memory");
+    }
+  }
+  dg::Mat1D m;
+  dg::pmf_tables(c->tab, &m);
+  dg::KParams kp = c->kp;
+  kp.mask = 7u;
+  cudaError_t e = dg::launch_pmf_factor(kp, m, nd, 0, (int)c->ncells, 1, c->d_pmf, nullptr);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "pmf factor");
+  return DG_OK;
+}
+
+dg_status dg_pmf_sweep(dg_ctx* c, double* u, const double* f, double omega, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
+  if (!c->d_pmf) return fail(DG_ERR_STATE, "dg_pmf_setup has not run");
+  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  cudaStream_t s = (cudaStream_t)stream;
+  dg_status st = dg_apply(c, u, c->d_pmf_au, s);
+  if (st != DG_OK) return st;
+  const int n = c->desc.p + 1;
+  cudaError_t e = dg::launch_pmf_sweep(n * n * n, (int)c->ncells, c->d_pmf, u, f, c->d_pmf_au, omega, u, s);
+  if (e != cudaSuccess) return cuda_fail(e, "pmf sweep");
+  c->launches = 2;
+  return DG_OK;
+}
+
+dg_status dg_pmf_block(dg_ctx* c, int64_t cell, int32_t inverse, double* host_out) {
+  if (!c || !host_out) return fail(DG_ERR_INVALID, "NULL argument");
+  if (cell < 0 || cell >= c->ncells) return fail(DG_ERR_INVALID, "cell out of range");
+  const int n = c->desc.p + 1, nd = n * n * n;
+  if (nd * nd * 8 > 200 * 1024) return fail(DG_ERR_UNSUPPORTED, "block too large for shared memory (p <= 4)");
+  if (inverse) {
+    dg_status st = pmf_check(c);
+    if (st != DG_OK) return st;
+  }
+  double* tmp = nullptr;
+  cudaError_t e = cudaMalloc(&tmp, (size_t)nd * nd * 8);
+  if (e != cudaSuccess) return fail(DG_ERR_NOMEM, "block scratch");
+  dg::Mat1D m;
+  dg::pmf_tables(c->tab, &m);
+  dg::KParams kp = c->kp;
+  kp.mask = 7u;
+  e = dg::launch_pmf_factor(kp, m, nd, (int)cell, 1, inverse ? 1 : 0, tmp, nullptr);
+  if (e == cudaSuccess) e = cudaMemcpy(host_out, tmp, (size_t)nd * nd * 8, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "pmf block");
   return DG_OK;
 }
 

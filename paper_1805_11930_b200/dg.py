@@ -26,7 +26,8 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_block_diag_apply", "dg_ghost_layers", "dg_fill_ghosts", "dg_tables",
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
            "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
-           "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep"]
+           "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep", "dg_pmf_setup",
+           "dg_pmf_sweep", "dg_pmf_block"]
 
 
 class DGError(RuntimeError):
@@ -98,6 +99,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_block_jacobi_sweep": ([P, P, P, dbl, dbl, P], i32),
         "dg_local_block_solve": ([P, P, P, dbl, P], i32),
         "dg_block_sor_sweep": ([P, P, P, dbl, dbl, i32, P], i32),
+        "dg_pmf_setup": ([P], i32),
+        "dg_pmf_sweep": ([P, P, P, dbl, P], i32),
+        "dg_pmf_block": ([P, i64, i32, ctypes.POINTER(dbl)], i32),
         "dg_set_local_solver": ([P, i32, i32], i32),
         "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
         "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
@@ -301,6 +305,22 @@ class DGContext:
         _check(self.lib.dg_block_sor_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
                                            1 if symmetric else 0, _stream(stream)))
         return u
+
+    # ---- stored-inverse block-Jacobi smoother (NEXT-4) ------------------------
+    def pmf_setup(self):
+        _check(self.lib.dg_pmf_setup(self.h))
+
+    def pmf_sweep(self, u, f, omega: float = 1.0, stream=None):
+        _check(self.lib.dg_pmf_sweep(self.h, _ptr(u), _ptr(f), float(omega), _stream(stream)))
+        return u
+
+    def pmf_block(self, cell: int, inverse: bool = False):
+        import numpy as np
+        nd = (self.problem.p + 1) ** 3
+        out = np.empty(nd * nd, dtype=np.float64)
+        _check(self.lib.dg_pmf_block(self.h, int(cell), 1 if inverse else 0,
+                                     out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out.reshape(nd, nd)
 
     def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000):
         _check(self.lib.dg_set_local_solver(self.h, method, max_it))

@@ -55,9 +55,21 @@ def main(names):
         per_it = (vol + 6 * sf + it * n ** 3) * (1 if P.local_solver == "cg" else 2)
         fl = nc * (vol + 6 * sf + 6 * nf + 4 * n ** 3) + st["it_sum"] * per_it
         r["sweep_us"], r["sweep_frac"], r["it_mean"] = t, fl / (t * 1e-6) / PEAK, st["it_mean"]
+        if P.p <= 4 and not any(P.b) and "--pmf" in sys.argv:
+            import time
+            t0 = time.perf_counter()
+            ctx.pmf_setup()
+            r["pmf_setup_s"] = time.perf_counter() - t0
+            uu.copy_(ut)
+            t = timed(lambda: ctx.pmf_sweep(uu, ft, 1.0), calls=5)
+            nd = n ** 3
+            r["pmf_sweep_us"] = t
+            r["pmf_inverse_GB"] = nc * nd * nd * 8 / 1e9
+            # stored inverses + (u, f, Au, u_new) of the matvec kernel, over the whole sweep
+            r["pmf_sweep_GBps"] = (nc * nd * nd * 8 + 4 * nc * nd * 8) / (t * 1e-6) / 1e9
         print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
         ctx.close()
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["C2"])
+    main([a for a in sys.argv[1:] if not a.startswith("--")] or ["C2"])
