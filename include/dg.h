@@ -47,7 +47,10 @@ typedef enum {
 } dg_status;
 
 enum { DG_BC_DIRICHLET = 0, DG_BC_NEUMANN = 1 };                 /* P:284-288 */
-enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2 }; /* P:665-668 */
+/* local Krylov method; DG_LOCAL_BICGSTAB_THOMAS: BiCGStab right-preconditioned by the tridiagonal
+ * part of D_T in DoF order (Thomas algorithm), for strongly convection-dominated
+ * blocks where the diagonal fails; p <= 4 */
+enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2, DG_LOCAL_BICGSTAB_THOMAS = 3 };
 enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
 
 typedef struct {

@@ -37,7 +37,7 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) 
     give A/B variants of the same sources (e.g. -DDG_PL_WARPS4=1), loaded through DG_LIB."""
     if out == LIB and not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build") if out == LIB else out + ".objs"
+    objdir = os.path.join(HERE, "build") if out == LIB else os.path.join("/tmp", "dg_objs_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     jobs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-lineinfo", "-I", INCLUDE, "-I", CSRC,

@@ -351,6 +351,9 @@ dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it) {
     c->method = dg::LM_CG;
   } else if (method == DG_LOCAL_BICGSTAB) {
     c->method = dg::LM_BICGSTAB;
+  } else if (method == DG_LOCAL_BICGSTAB_THOMAS) {
+    if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "the tridiagonal preconditioner needs p <= 4 (plane kernels)");
+    c->method = dg::LM_BICGSTAB_THOMAS;
   } else {
     return fail(DG_ERR_INVALID, "unknown local method");
   }

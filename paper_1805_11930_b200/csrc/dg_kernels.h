@@ -40,7 +40,7 @@ __host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
   return ((cx + cy + cz) & 1) != kp.colour;
 }
 
-enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2 };
+enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3 };
 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
 

@@ -39,6 +39,8 @@ struct DevTab {
   double AW[64], GW[64];              // A[q][j] w_q, G[q][j] w_q
   double DW[64];                      // D[q][r] w_q / w_r
   double E0W[8], E1W[8], F0W[8], F1W[8];  // E0/w, E1/w, F0/w, F1/w
+  // exact 1D stiffness and (test-derivative) convection matrices, for the bands of D_T
+  double S[64], Cm[64];               // int th_i' th_j',  int th_i' th_j
 };
 __constant__ DevTab c_tab[kMaxN + 1];
 
@@ -1056,6 +1058,8 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       using G = pk::Geo<N>;
       const int grid = (kp.ncells + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
+      if (method == LM_BICGSTAB_THOMAS)
+        return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
       if (method == LM_BICGSTAB)
         return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
       return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
@@ -1064,6 +1068,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   using G = Geo<N>;
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
+  if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
   if (method == LM_BICGSTAB)
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
   return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
@@ -1086,6 +1091,16 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
       d.AW[q * n + j] = t.A[q * n + j] * t.wq[q];
       d.GW[q * n + j] = t.G[q * n + j] * t.wq[q];
       d.DW[q * n + j] = t.D[q * n + j] * t.wq[q] / t.wq[j];
+    }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double sv = 0.0, cv = 0.0;
+      for (int q = 0; q < n; ++q) {
+        sv += t.wq[q] * t.G[q * n + i] * t.G[q * n + j];
+        cv += t.wq[q] * t.G[q * n + i] * t.A[q * n + j];
+      }
+      d.S[i * n + j] = sv;
+      d.Cm[i * n + j] = cv;
     }
   *err = cudaMemcpyToSymbol(c_tab, &d, sizeof(DevTab), sizeof(DevTab) * N);
   return *err == cudaSuccess;

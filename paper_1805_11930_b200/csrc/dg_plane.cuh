@@ -1380,9 +1380,118 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   if (valid && L.t == 0) kp.its[cell0 + L.cs] = its_out;
 }
 
+// ---- tridiagonal (Thomas) local preconditioner -------------
+// D_T[I][J] from the 1D matrices (volume + self faces as Kronecker products on the
+// affine cell; the same coefficients as the operator), I = i + n j + n^2 k test, J trial.
+template <int N, bool WB>
+__device__ __forceinline__ double dt_entry(const KParams& kp, const Cells<N, WB>& cl, int cs, int I, int J) {
+  const int i = I % N, j = (I / N) % N, k = I / (N * N);
+  const int a = J % N, b = (J / N) % N, c = J / (N * N);
+  const double* M = c_tab[N].M;
+  const double* S = c_tab[N].S;
+  const double* C = c_tab[N].Cm;
+  const double* vc = cl.vc[cs];
+  const double Mx = M[i * N + a], My = M[j * N + b], Mz = M[k * N + c];
+  double v = vc[0] * S[i * N + a] * My * Mz + vc[1] * Mx * S[j * N + b] * Mz +
+             vc[2] * Mx * My * S[k * N + c] + vc[3] * Mx * My * Mz;
+  v -= kp.sb[0] * C[i * N + a] * My * Mz + kp.sb[1] * Mx * C[j * N + b] * Mz + kp.sb[2] * Mx * My * C[k * N + c];
+  const int r3[3] = {i, j, k}, c3[3] = {a, b, c};
+  const double m3[3] = {Mx, My, Mz};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const int r = r3[ax], q = c3[ax];
+    const double* lo = cl.fc[cs][2 * ax];
+    const double* hi = cl.fc[cs][2 * ax + 1];
+    const double ih = kp.ih[ax];
+    const double e0r = r == 0, e0q = q == 0, e1r = r == N - 1, e1q = q == N - 1;
+    double bf = lo[0] * e0r * e0q + lo[1] * ih * e0r * c_tab[N].d0[q] + lo[4] * c_tab[N].d0[r] * e0q;
+    bf += hi[0] * e1r * e1q + hi[1] * ih * e1r * c_tab[N].d1[q] + hi[4] * c_tab[N].d1[r] * e1q;
+    double t = kp.fa[ax] * bf;
+#pragma unroll
+    for (int o = 0; o < 3; ++o)
+      if (o != ax) t *= m3[o];
+    v += t;
+  }
+  return v;
+}
+
+// Bands of D_T in DoF order and their LU (Thomas) factors, per cell: lane t writes the sub-,
+// main and super-diagonal entries of its plane, then the cell's lane 0 eliminates sequentially:
+// SB = sub, IP = 1 / pivot, CP = super / pivot.
+template <int N, bool WB>
+__device__ void thomas_factor(const KParams& kp, const Cells<N, WB>& cl, const Lane& L, double* SB,
+                              double* IP, double* CP, bool valid) {
+  using G = Geo<N>;
+  constexpr int ND = G::N3;
+  double* sb = SB + L.cs * G::PS;
+  double* ip = IP + L.cs * G::PS;
+  double* cp = CP + L.cs * G::PS;
+  if (L.active) {
+    for (int q = 0; q < G::N2; ++q) {
+      const int I = L.t * G::N2 + q, o = L.t * G::QS + q;
+      sb[o] = (valid && I > 0) ? dt_entry<N>(kp, cl, L.cs, I, I - 1) : 0.0;
+      ip[o] = valid ? dt_entry<N>(kp, cl, L.cs, I, I) : 1.0;
+      cp[o] = (valid && I < ND - 1) ? dt_entry<N>(kp, cl, L.cs, I, I + 1) : 0.0;
+    }
+  }
+  __syncwarp();
+  if (L.active && L.t == 0) {
+    double c_prev = 0.0;
+    for (int I = 0; I < ND; ++I) {
+      const int o = (I / G::N2) * G::QS + I % G::N2;
+      const double inv = 1.0 / (ip[o] - sb[o] * c_prev);
+      ip[o] = inv;
+      c_prev = cp[o] * inv;
+      cp[o] = c_prev;
+    }
+  }
+  __syncwarp();
+}
+
+// v <- M^-1 v with M the tridiagonal part of D_T (forward / back substitution by the cell's
+// lane 0 through the cell's TB slot, which is free between two operator applications)
+template <int N>
+__device__ void thomas_apply(const Lane& L, double* TB, const double* SB, const double* IP, const double* CP,
+                             double (&v)[N][N]) {
+  using G = Geo<N>;
+  double* sc = TB + L.cs * G::CTB;
+  const double* sb = SB + L.cs * G::PS;
+  const double* ip = IP + L.cs * G::PS;
+  const double* cp = CP + L.cs * G::PS;
+  __syncwarp();
+  if (L.active)
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) sc[L.t * G::KS + j * N + i] = v[j][i];
+  __syncwarp();
+  if (L.active && L.t == 0) {
+    double y = 0.0;
+    for (int I = 0; I < G::N3; ++I) {
+      const int o = (I / G::N2) * G::QS + I % G::N2, s = (I / G::N2) * G::KS + I % G::N2;
+      y = (sc[s] - sb[o] * y) * ip[o];
+      sc[s] = y;
+    }
+    double x = 0.0;
+    for (int I = G::N3 - 1; I >= 0; --I) {
+      const int o = (I / G::N2) * G::QS + I % G::N2, s = (I / G::N2) * G::KS + I % G::N2;
+      x = fma(-cp[o], x, sc[s]);
+      sc[s] = x;
+    }
+  }
+  __syncwarp();
+  if (L.active)
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[j][i] = sc[L.t * G::KS + j * N + i];
+}
+
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks).
 // Registers: r and the operator input/output planes; shared: x, r^, p, v, diag planes.
-template <int N, bool SWEEP>
+// THOMAS: right preconditioner = the tridiagonal part of D_T in DoF order (NEXT-3) instead of
+// its diagonal; two more shared planes (the band factors) per cell.
+template <int N, bool SWEEP, bool THOMAS = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
            double* __restrict__ out) {
@@ -1396,6 +1505,8 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* PSM = RHS + G::C * G::PS;
   double* VSM = PSM + G::C * G::PS;
   double* DS = VSM + G::C * G::PS;
+  double* SBM = DS + G::C * G::PS;   // THOMAS: sub-diagonal; DS then holds 1 / pivot
+  double* CPM = SBM + G::C * G::PS;  // THOMAS: super-diagonal / pivot
   double* FX = XS;
   double* FZ = RHS;
   const int cell0 = blockIdx.x * G::C;
@@ -1436,7 +1547,9 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* vs = VSM + po;
   double* ds = DS + po;
   __syncthreads();   // the prologue's FX / FZ (aliasing XS / RHS) are consumed
-  {
+  if constexpr (THOMAS) {
+    thomas_factor<N>(kp, cl, L, SBM, DS, CPM, valid);
+  } else {
     double dg[N][N];
     plane_inv_diag<N>(kp, cl, L, rw, dg);
     if (L.active)
@@ -1492,10 +1605,11 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
             ps[j * N + i] = p;
             if (rst) rh[j * N + i] = R[j][i];
           }
-          p *= ds[j * N + i];
+          if (!THOMAS) p *= ds[j * N + i];
         }
         W[j][i] = p;
       }
+    if constexpr (THOMAS) thomas_apply<N>(L, TB, SBM, DS, CPM, W);
     rst = false;
     double T[N][N];
     plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
@@ -1523,8 +1637,9 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
         if (L.active) xs[j * N + i] = fma(alpha, W[j][i], xs[j * N + i]);
         R[j][i] = fma(-alpha, T[j][i], R[j][i]);
         ss = fma(R[j][i], R[j][i], ss);
-        W[j][i] = L.active ? R[j][i] * ds[j * N + i] : 0.0;
+        W[j][i] = L.active ? (THOMAS ? R[j][i] : R[j][i] * ds[j * N + i]) : 0.0;
       }
+    if constexpr (THOMAS) thomas_apply<N>(L, TB, SBM, DS, CPM, W);
     ss = cell_sum<N>(ss, L.lane);
     if (!conv && ss <= kp.tol2 * rr0) {
       conv = true;
