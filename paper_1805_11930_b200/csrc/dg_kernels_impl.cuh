@@ -998,6 +998,11 @@ static bool force_line() {
 #endif
 template <int N> constexpr bool plane_apply() { return N == 2 || N == 4 || (N == 3 && DG_PLANE_APPLY3); }
 
+// convective or reaction terms present (else the pure-diffusion instantiations, GEN = false)
+inline bool gen_terms(const KParams& kp) {
+  return kp.c != nullptr || kp.b[0] != 0.0 || kp.b[1] != 0.0 || kp.b[2] != 0.0;
+}
+
 template <int N>
 cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
   if constexpr (N <= 5) {
@@ -1012,7 +1017,8 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
       static int slots = 0;
       const size_t vsm = pk::smem_apply<N>(false, false);
       if (slots == 0) {
-        cudaError_t e = set_smem(pk::k_volume<N>, vsm);
+        cudaError_t e = set_smem(pk::k_volume<N, true>, vsm);
+        if (e == cudaSuccess) e = set_smem(pk::k_volume<N, false>, vsm);
         if (e != cudaSuccess) return e;
         int per_sm = 0, dev = 0, nsm = 0;
         cudaGetDevice(&dev);
@@ -1021,7 +1027,8 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
         if (e != cudaSuccess) return e;
         slots = max(1, per_sm) * nsm;
       }
-      pk::k_volume<N><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
+      if (gen_terms(kp)) pk::k_volume<N, true><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
+      else pk::k_volume<N, false><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
       return cudaGetLastError();
     }
   }
@@ -1032,8 +1039,10 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
       if (grid == 0) return cudaSuccess;
       const bool faces = kp.mask != 1u;   // mask = volume: the volume terms alone
       const size_t smem = pk::smem_apply<N>(with_nbr, faces);
-      auto kern = with_nbr ? pk::k_apply<N, true> : pk::k_apply<N, false>;
-      if (!faces) kern = pk::k_apply<N, false, false>;
+      const bool gen = gen_terms(kp);
+      auto kern = with_nbr ? (gen ? pk::k_apply<N, true, true, true> : pk::k_apply<N, true, true, false>)
+                           : (gen ? pk::k_apply<N, false, true, true> : pk::k_apply<N, false, true, false>);
+      if (!faces) kern = gen ? pk::k_apply<N, false, false, true> : pk::k_apply<N, false, false, false>;
       cudaError_t e = set_smem(kern, smem);
       if (e != cudaSuccess) return e;
       kern<<<grid, G::NT, smem, s>>>(kp, u, out);
@@ -1062,7 +1071,9 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
       if (method == LM_BICGSTAB)
         return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
-      return launch(pk::k_cg<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
+      if (gen_terms(kp))
+        return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
+      return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
     }
   }
   using G = Geo<N>;

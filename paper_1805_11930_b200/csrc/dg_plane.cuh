@@ -527,7 +527,9 @@ __device__ void nbr_prologue_async(const KParams& kp, const Cells<N, WB>& cl, co
 // The quadrature-point residual R is kept UNWEIGHTED: the Gauss weights (and |T|, face
 // areas through kp) are folded into the transposed 1D tables AW = A w, GW = G w,
 // DW = D w_q / w_r and the end-point injection vectors E/w, F/w.
-template <int N, bool NBR, bool USEB, bool FACES = true, bool WB>
+// GEN = false: pure diffusion (b = 0, no reaction), the convective and reaction terms are
+// compiled out (the b = 0 / c = 0 configurations C1-C3, C5).
+template <int N, bool NBR, bool USEB, bool FACES = true, bool GEN = true, bool WB>
 __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& cl, const Lane& L,
                                          const Rows<N>& rw, bool vol, const double (&in)[N][N],
                                          double (&out)[N][N], double* TB, double* FY,
@@ -635,8 +637,8 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
             s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
           }
           U[qz][qx] = s;
-          R[qz][qx] = cR * s;
-          fy_[qz] = fma(cK, s1, -kp.sb[1] * s);
+          R[qz][qx] = GEN ? cR * s : 0.0;
+          fy_[qz] = GEN ? fma(cK, s1, -kp.sb[1] * s) : cK * s1;
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -655,7 +657,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[qz][r], du);
-          F[q] = fma(vcell[0], du, -kp.sb[0] * U[qz][q]);
+          F[q] = GEN ? fma(vcell[0], du, -kp.sb[0] * U[qz][q]) : vcell[0] * du;
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -674,7 +676,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[r][qx], du);
-          F[q] = fma(vcell[2], du, -kp.sb[2] * U[q][qx]);
+          F[q] = GEN ? fma(vcell[2], du, -kp.sb[2] * U[q][qx]) : vcell[2] * du;
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -1074,7 +1076,7 @@ __device__ __forceinline__ void setup(const KParams& kp, Cells<N, WB>& cl, int c
 
 // out = A u (with_nbr) or D_T u, selected parts by kp.mask
 // FACES = false: the volume terms alone (dg_apply_parts with mask = volume), no face code.
-template <int N, bool NBR, bool FACES = true>
+template <int N, bool NBR, bool FACES = true, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
@@ -1108,7 +1110,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   read_plane<N>(TB, L, in);
   if (NBR) nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, tile);
   else __syncthreads();
-  plane_op<N, NBR, false, FACES>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
+  plane_op<N, NBR, false, FACES, GEN>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
@@ -1118,7 +1120,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
 // a persistent kernel, one CTA per resident slot, walking the cell groups with a stride of the
 // grid; the next group's tile and coefficients are loaded into registers while the current
 // group is computed, so the HBM/L2 latency is hidden behind the fp64 work.
-template <int N>
+template <int N, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT, DG_VOL_MINB)
 k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
@@ -1161,7 +1163,7 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
     if (g + (int)gridDim.x < ngroups) prefetch(g + gridDim.x);
     double in[N][N], o[N][N];
     read_plane<N>(TB, L, in);
-    plane_op<N, false, false, false>(kp, cl, L, rw, true, in, o, TB, nullptr, nullptr, nullptr);
+    plane_op<N, false, false, false, GEN>(kp, cl, L, rw, true, in, o, TB, nullptr, nullptr, nullptr);
     if (L.active) write_plane<N>(TB, L, o);
     __syncthreads();
     unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
@@ -1172,7 +1174,7 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
 // Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
 // VS (n = 5): r and p live in shared planes too, so nothing but the operator's own planes is
 // held in registers across an application (no spills at n = 5).
-template <int N, bool SWEEP, bool VS = (N >= 5)>
+template <int N, bool SWEEP, bool GEN = true, bool VS = (N >= 5)>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
      double* __restrict__ out) {
@@ -1201,7 +1203,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     load_nbr<N>(pv0, cl, 2);
     load_nbr<N>(pv1, cl, 3);
     nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
-    plane_op<N, true, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
+    plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
@@ -1261,7 +1263,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         for (int j = 0; j < N; ++j)
 #pragma unroll
           for (int i = 0; i < N; ++i) Pin[j][i] = L.active ? ps[j * N + i] : 0.0;
-        plane_op<N, false, true>(kp, cl, L, rw, true, Pin, Q, TB, FY, FX, FZ);  // Q = D_T P
+        plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, Pin, Q, TB, FY, FX, FZ);  // Q = D_T P
       }
       double pq = 0.0;
 #pragma unroll
@@ -1324,7 +1326,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
       if (done || iter >= kp.max_it) break;
       double Q[N][N];
-      plane_op<N, false, true>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+      plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
       double pq = 0.0;
 #pragma unroll
       for (int j = 0; j < N; ++j)
