@@ -69,6 +69,11 @@ template <int N, bool WB = true> struct Cells {
   double fc[C][6][6];
   const double* nb[C][6];
   int cell[C];
+  // per face: bit cs set when cell cs has an in-slab neighbour there (its tile is then at
+  // tile +- step n^3, contiguous); nbg[f] != 0 when some cell's neighbour is a ghost-layer cell
+  static_assert(C <= 64, "neighbour masks hold 64 cells");
+  unsigned int nbm[6][2];
+  int nbg[6];
   // per-cell self-face operators at the Gauss points: B[cs][0] acts on x-rows, B[cs][1] on z-columns
   double B[WB ? C : 1][BS];
 };
@@ -370,9 +375,27 @@ __device__ __forceinline__ void async_own(double* TB, const double* __restrict__
 }
 // face-f neighbour tiles: into TB layout (KSX = KS, cell stride CTB) or into a face region
 // (KSX = N2, cell stride FS >= N3)
+// fast path (no ghost-layer neighbour on face f): the neighbour tile is the group's own tile
+// shifted by +- step cells, so the sources are contiguous and no per-cell pointer is loaded
 template <int N, int KSX, int CSX, bool WB>
-__device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, int f, const double* any) {
+__device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, int f, const double* any,
+                                          const KParams& kp, const double* tile) {
   using G = Geo<N>;
+  if (cl.nbg[f] == 0) {
+    const unsigned m0 = cl.nbm[f][0], m1 = cl.nbm[f][1];
+    const long step = (f >> 1) == 0 ? 1 : ((f >> 1) == 1 ? kp.nx : (long)kp.nx * kp.ny);
+    const double* src = tile + ((f & 1) ? step : -step) * (long)G::N3;
+#pragma unroll
+    for (int m = 0; m < G::PER; ++m) {
+      const int e = threadIdx.x + m * G::NT;
+      if (e < G::C * G::N3) {
+        const int cs = e / G::N3, r = e % G::N3;
+        const bool ok = ((cs < 32 ? m0 >> cs : m1 >> (cs - 32)) & 1u) != 0;
+        cp_async8(dst + cs * CSX + (r / G::N2) * KSX + (r % G::N2), ok ? src + e : any, ok);
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
@@ -949,6 +972,12 @@ template <int N> struct SetupRegs {
   int kind[IT][2];   // 0 interior (or ghost), 1 Dirichlet, 2 Neumann; -1: item not valid
 };
 
+// zero the neighbour masks (call before setup_issue, followed by a barrier)
+template <int N, bool WB> __device__ __forceinline__ void clear_masks(Cells<N, WB>& cl) {
+  if (threadIdx.x < 12) (&cl.nbm[0][0])[threadIdx.x] = 0u;
+  if (threadIdx.x < 6) cl.nbg[threadIdx.x] = 0;
+}
+
 template <int N, bool WB>
 __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl, SetupRegs<N>& sr,
                                             int cell0, const double* u) {
@@ -998,6 +1027,8 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
       sr.kind[r][hi] = kind;
       sr.Kn[r][hi] = kidx >= 0 ? __ldg(kp.K + (size_t)kidx * 3 + axis) : 0.0;
       cl.nb[cs][f] = nbp;
+      if (nc >= 0 && nc < dim) atomicOr(&cl.nbm[f][cs >> 5], 1u << (cs & 31));
+      else if (kind == 0) cl.nbg[f] = 1;
     }
   }
 }
@@ -1094,14 +1125,16 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   // all global loads of the own tile and the y-neighbour pair are in flight during the setup
   const double* tile = u + (size_t)cell0 * G::N3;
   async_own<N>(TB, tile, nvalid);
+  clear_masks<N>(cl);
+  __syncthreads();
   SetupRegs<N> sr;
   setup_issue<N>(kp, cl, sr, cell0, NBR ? u : nullptr);
-  __syncthreads();   // neighbour pointers
+  __syncthreads();   // neighbour pointers and masks
   if (NBR) {
-    async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, u);   // y-lo -> TB half 1
-    async_nbr<N, G::N2, G::FS>(FY, cl, 3, u);             // y-hi, z-lo, z-hi -> FY, FX, FZ (flat)
-    async_nbr<N, G::N2, G::FS>(FX, cl, 4, u);
-    async_nbr<N, G::N2, G::FS>(FZ, cl, 5, u);
+    async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, u, kp, tile);   // y-lo -> TB half 1
+    async_nbr<N, G::N2, G::FS>(FY, cl, 3, u, kp, tile);             // y-hi, z-lo, z-hi -> FY, FX, FZ
+    async_nbr<N, G::N2, G::FS>(FX, cl, 4, u, kp, tile);
+    async_nbr<N, G::N2, G::FS>(FZ, cl, 5, u, kp, tile);
   }
   setup_finish<N>(kp, cl, sr);
   cp_async_wait_all();
