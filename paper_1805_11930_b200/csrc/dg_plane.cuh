@@ -145,22 +145,6 @@ __device__ __forceinline__ void stage_tile(double* TB, const double* __restrict_
     if (e < G::C * G::N3) TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)] = v[m];
   }
 }
-// base pointer of the face-f neighbour of local cell `cell` (u, or a ghost layer), nullptr at
-// the domain boundary -- the same rule as setup_cells, without waiting for it
-template <int N>
-__device__ __forceinline__ const double* nbr_ptr(const KParams& kp, const double* u, int cell, int f) {
-  constexpr int N3 = N * N * N;
-  const int nxy = kp.nx * kp.ny;
-  const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / nxy;
-  const int axis = f >> 1, hi = f & 1;
-  const int c = axis == 0 ? cx : (axis == 1 ? cy : cz);
-  const int dim = axis == 0 ? kp.nx : (axis == 1 ? kp.ny : kp.nzl);
-  const int step = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
-  const int nc = c + (hi ? 1 : -1);
-  if (nc >= 0 && nc < dim) return u + (size_t)(cell + (hi ? step : -step)) * N3;
-  if (kp.slab_face[f] == FK_GHOST) return (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)(cx + kp.nx * cy) * N3;
-  return nullptr;
-}
 // the group's own tile / a neighbour tile into registers (coalesced, all loads in flight)
 template <int N>
 __device__ __forceinline__ void load_own(double (&v)[Geo<N>::PER], const double* __restrict__ src,
@@ -170,18 +154,6 @@ __device__ __forceinline__ void load_own(double (&v)[Geo<N>::PER], const double*
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
     v[m] = (e < G::C * G::N3 && e / G::N3 < nvalid) ? __ldg(src + e) : 0.0;
-  }
-}
-template <int N>
-__device__ __forceinline__ void load_nbr_direct(double (&v)[Geo<N>::PER], const KParams& kp,
-                                                const double* u, int cell0, int f) {
-  using G = Geo<N>;
-#pragma unroll
-  for (int m = 0; m < G::PER; ++m) {
-    const int e = threadIdx.x + m * G::NT;
-    const int cell = cell0 + e / G::N3;
-    const double* p = (e < G::C * G::N3 && cell < kp.ncells) ? nbr_ptr<N>(kp, u, cell, f) : nullptr;
-    v[m] = p ? __ldg(p + e % G::N3) : 0.0;
   }
 }
 // neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
