@@ -50,7 +50,9 @@ template <int N_> struct Geo {
   static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
   static constexpr int CPW = 32 / N, WARPS = PL<N>::WARPS, C = CPW * WARPS, NT = 32 * WARPS;
   static constexpr int KS = PL<N>::KS, ARR = N * KS, CTB = PL<N>::CTB;
-  static constexpr int FS = 4 * N2 + 1;   // per-cell stride of a block of 4 face arrays
+  // per-cell stride of a block of 4 face arrays; even at n = 4 so that staged neighbour tiles
+  // can be copied with 16-byte cp.async (see async_nbr)
+  static constexpr int FS = 4 * N2 + (N == 4 ? 2 : 1);
   static constexpr int QS = PL<N>::QS, PS = PL<N>::PS;  // plane storage (X, Dg, ...)
   static_assert(PS >= N * QS && PS >= FS, "plane storage must hold a cell and a face block");
   static constexpr int PER = (C * N3 + NT - 1) / NT;      // tile elements per thread
@@ -329,6 +331,10 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
   // (the destination is read only after cp_async_wait_all + a barrier)
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
 }
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 16 : 0));
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -357,6 +363,18 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
     const unsigned m0 = cl.nbm[f][0], m1 = cl.nbm[f][1];
     const long step = (f >> 1) == 0 ? 1 : ((f >> 1) == 1 ? kp.nx : (long)kp.nx * kp.ny);
     const double* src = tile + ((f & 1) ? step : -step) * (long)G::N3;
+    if constexpr (N % 2 == 0 && CSX % 2 == 0 && KSX % 2 == 0) {
+      // element pairs (same cell and plane, 16-byte aligned on both sides)
+      static_assert((G::C * G::N3 / 2) % G::NT == 0, "pairs tile the group evenly");
+#pragma unroll
+      for (int m = 0; m < G::C * G::N3 / 2 / G::NT; ++m) {
+        const int e = 2 * (threadIdx.x + m * G::NT);
+        const int cs = e / G::N3, r = e % G::N3;
+        const bool ok = ((cs < 32 ? m0 >> cs : m1 >> (cs - 32)) & 1u) != 0;
+        cp_async16(dst + cs * CSX + (r / G::N2) * KSX + (r % G::N2), ok ? src + e : any, ok);
+      }
+      return;
+    }
 #pragma unroll
     for (int m = 0; m < G::PER; ++m) {
       const int e = threadIdx.x + m * G::NT;
