@@ -1074,11 +1074,20 @@ __device__ __forceinline__ void setup_finish(const KParams& kp, Cells<N, WB>& cl
 //   B[q][r] = |F| sum_{s=lo,hi} ( E_s^w[q] (cs_a E_s[r] + cs_g F_s[r] / h) + F_s^w[q] ct_a E_s[r] ),
 // i.e. traces a_s = E_s.U, g_s = F_s.U of a Gauss-value line U, the flux combinations
 // S = cs_a a + cs_g g / h, T = ct_a a, and their injection through A^-T / w (see plane_op).
+template <int N, bool WB> __device__ __forceinline__ void setup_B(const KParams& kp, Cells<N, WB>& cl);
+
 template <int N, bool USEB = true, bool WB>
 __device__ __forceinline__ void setup(const KParams& kp, Cells<N, WB>& cl, int cell0, const double* u) {
   using G = Geo<N>;
   setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.fc, cl.nb, cl.cell, cell0, u);
   if constexpr (!USEB || !WB) return;
+  setup_B<N>(kp, cl);
+}
+
+// the x / z self-face operators B of every cell (needs fc complete); ends with a barrier
+template <int N, bool WB>
+__device__ __forceinline__ void setup_B(const KParams& kp, Cells<N, WB>& cl) {
+  using G = Geo<N>;
   for (int it = threadIdx.x; it < G::C * 2 * G::N2; it += G::NT) {
     const int cs = it / (2 * G::N2), rem = it % (2 * G::N2), d = rem / G::N2;
     const int q = (rem % G::N2) / N, r = rem % N;
@@ -1137,6 +1146,32 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+}
+
+// Solver prologue: coefficients, self-face operators and (SWEEP) the defect's neighbour tiles
+// staged with cp.async exactly as in the apply kernel; the own tile lands in TB half 0.
+template <int N, bool SWEEP, bool WB>
+__device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl, double* TB, double* FY,
+                                             double* FX, double* FZ, const double* in, int cell0, int nvalid) {
+  using G = Geo<N>;
+  const double* tile = in + (size_t)cell0 * G::N3;
+  async_own<N>(TB, tile, nvalid);
+  clear_masks<N>(cl);
+  __syncthreads();
+  SetupRegs<N> sr;
+  setup_issue<N>(kp, cl, sr, cell0, SWEEP ? in : nullptr);
+  __syncthreads();   // neighbour pointers and masks
+  if (SWEEP) {
+    async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, in, kp, tile);
+    async_nbr<N, G::N2, G::FS>(FY, cl, 3, in, kp, tile);
+    async_nbr<N, G::N2, G::FS>(FX, cl, 4, in, kp, tile);
+    async_nbr<N, G::N2, G::FS>(FZ, cl, 5, in, kp, tile);
+  }
+  setup_finish<N>(kp, cl, sr);
+  __syncthreads();   // fc of every cell
+  setup_B<N>(kp, cl);
+  cp_async_wait_all();
+  __syncthreads();
 }
 
 // The volume terms alone, A^v u (Stages 1-3; dg_apply_parts with mask = volume):
@@ -1216,16 +1251,27 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
-  setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
+  // n <= 4: neighbour tiles staged with cp.async (a face region holds a tile); n = 5: through
+  // registers, one pair of tiles at a time
+  constexpr bool ASYNC = G::FS >= G::N3;
+  if constexpr (ASYNC) {
+    solver_setup<N, SWEEP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+  } else {
+    stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+    setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
+  }
   double R[N][N], P[N][N];
   read_plane<N>(TB, L, P);
   if (SWEEP) {
     double Q[N][N];
-    double pv0[G::PER], pv1[G::PER];
-    load_nbr<N>(pv0, cl, 2);
-    load_nbr<N>(pv1, cl, 3);
-    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
+    if constexpr (ASYNC) {
+      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    } else {
+      double pv0[G::PER], pv1[G::PER];
+      load_nbr<N>(pv0, cl, 2);
+      load_nbr<N>(pv1, cl, 3);
+      nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
+    }
     plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
@@ -1540,16 +1586,27 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
-  setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
+  // n <= 4: neighbour tiles staged with cp.async (a face region holds a tile); n = 5: through
+  // registers, one pair of tiles at a time
+  constexpr bool ASYNC = G::FS >= G::N3;
+  if constexpr (ASYNC) {
+    solver_setup<N, SWEEP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+  } else {
+    stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+    setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
+  }
   double R[N][N], W[N][N];
   read_plane<N>(TB, L, W);
   if (SWEEP) {
     double T[N][N];
-    double pv0[G::PER], pv1[G::PER];
-    load_nbr<N>(pv0, cl, 2);
-    load_nbr<N>(pv1, cl, 3);
-    nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
+    if constexpr (ASYNC) {
+      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    } else {
+      double pv0[G::PER], pv1[G::PER];
+      load_nbr<N>(pv0, cl, 2);
+      load_nbr<N>(pv1, cl, 3);
+      nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
+    }
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
