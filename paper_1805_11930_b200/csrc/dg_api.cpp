@@ -86,7 +86,7 @@ struct dg_ctx {
   int32_t* d_its = nullptr;
   // hybrid multigrid scratch (allocated on first use)
   double* d_Ah = nullptr;      // [7][ncells]
-  double* d_cvec = nullptr;    // rh, uh, 3 coarse work vectors: [5][ncells]
+  double* d_cvec = nullptr;    // rh, uh, 5 coarse work vectors: [7][ncells]
   double* d_part = nullptr;    // [kPartials]
   double* d_dots = nullptr;    // [3]
   int* d_cits = nullptr;       // [1]
@@ -558,7 +558,7 @@ dg_status hybrid_prepare(dg_ctx* c, cudaStream_t s) {
   if (c->d_Ah) return DG_OK;
   const size_t N = (size_t)c->ncells, nd = (size_t)c->ndof;
   cudaError_t e = cudaMalloc(&c->d_Ah, 7 * N * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_cvec, 5 * N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&c->d_cvec, 7 * N * 8);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_part, (size_t)dg::kPartials * 8);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_dots, 3 * 8);
   if (e == cudaSuccess) e = cudaMalloc(&c->d_cits, sizeof(int));

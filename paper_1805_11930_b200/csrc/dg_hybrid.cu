@@ -25,7 +25,7 @@ namespace cg = cooperative_groups;
 namespace dg {
 namespace {
 
-constexpr int kCoarseThreads = 256;
+constexpr int kCoarseThreads = 1024;   // one 1024-thread block per SM for the cooperative coarse solve
 
 __device__ __forceinline__ void cell_coords(const KParams& kp, int cell, int& cx, int& cy, int& cz) {
   cx = cell % kp.nx;
@@ -147,64 +147,75 @@ __device__ __forceinline__ double sum_partials(const double* part, int k) {
   return s;
 }
 
-// Jacobi-PCG on A^ x = rhs from x = 0 until ||r|| <= tol ||rhs|| or max_it.
+// Jacobi-PCG on A^ x = rhs from x = 0 until ||r|| <= tol ||rhs|| or max_it, in the
+// Chronopoulos-Gear form (one reduction phase per iteration: gamma = (r,u), delta = (w,u) and
+// ||r||^2 together, w = A^ u), so each iteration costs two grid-wide barriers: after the vector
+// updates (u complete before the stencil) and after the block partial sums.
 __global__ void __launch_bounds__(kCoarseThreads) k_coarse_pcg(CoarseArgs a) {
   cg::grid_group grid = cg::this_grid();
   const int N = a.kp.ncells;
   const int t0 = blockIdx.x * blockDim.x + threadIdx.x, ts = gridDim.x * blockDim.x;
   double* P0 = a.part;
   double* P1 = a.part + 3 * gridDim.x;
-  {
-    double v[2] = {0.0, 0.0};
-    for (int i = t0; i < N; i += ts) {
-      const double r = a.rhs[i], z = r / a.Ah[i];
-      a.x[i] = 0.0;
-      a.r[i] = r;
-      a.p[i] = z;
-      v[0] = fma(r, r, v[0]);
-      v[1] = fma(r, z, v[1]);
-    }
-    block_partials<2>(v, P1);
+  double* u = a.r + 3 * (size_t)N;     // work: r, p, q(= z = A p), u, w
+  double* w = a.r + 4 * (size_t)N;
+  // x = 0, r = rhs, u = D^-1 r
+  for (int i = t0; i < N; i += ts) {
+    const double r = a.rhs[i];
+    a.x[i] = 0.0;
+    a.r[i] = r;
+    u[i] = r / a.Ah[i];
   }
   grid.sync();
-  const double rr0 = sum_partials(P1, 0);
-  double rz = sum_partials(P1, 1);
+  double alpha = 0.0, gamma_old = 0.0, rr0 = 0.0;
   int it = 0;
-  bool conv = rr0 == 0.0;
-  while (!conv && it < a.max_it) {
+  bool conv = false;
+  double* part = P0;
+  for (;;) {
+    // w = A^ u and the three dot products
     {
-      double v[1] = {0.0};
+      double v[3] = {0.0, 0.0, 0.0};
       for (int i = t0; i < N; i += ts) {
-        const double q = stencil(a, a.p, i);
-        a.q[i] = q;
-        v[0] = fma(a.p[i], q, v[0]);
+        const double wi = stencil(a, u, i);
+        w[i] = wi;
+        const double ri = a.r[i], ui = u[i];
+        v[0] = fma(ri, ui, v[0]);
+        v[1] = fma(wi, ui, v[1]);
+        v[2] = fma(ri, ri, v[2]);
       }
-      block_partials<1>(v, P0);
+      block_partials<3>(v, part);
     }
     grid.sync();
-    const double pq = sum_partials(P0, 0);
-    const double alpha = pq > 0.0 ? rz / pq : 0.0;
-    {
-      double v[2] = {0.0, 0.0};
-      for (int i = t0; i < N; i += ts) {
-        a.x[i] = fma(alpha, a.p[i], a.x[i]);
-        const double r = fma(-alpha, a.q[i], a.r[i]);
-        a.r[i] = r;
-        v[0] = fma(r, r, v[0]);
-        v[1] = fma(r, r / a.Ah[i], v[1]);
-      }
-      block_partials<2>(v, P1);
-    }
-    grid.sync();
-    ++it;
-    const double rr = sum_partials(P1, 0), rzn = sum_partials(P1, 1);
-    if (rr <= a.tol2 * rr0 || !(pq > 0.0)) {
-      conv = rr <= a.tol2 * rr0;
+    const double gamma = sum_partials(part, 0), delta = sum_partials(part, 1), rr = sum_partials(part, 2);
+    part = part == P0 ? P1 : P0;   // the next phase writes the other buffer
+    if (it == 0) {
+      rr0 = rr;
+      if (rr0 == 0.0) { conv = true; break; }
+    } else if (rr <= a.tol2 * rr0) {
+      conv = true;
       break;
     }
-    const double beta = rzn / rz;
-    rz = rzn;
-    for (int i = t0; i < N; i += ts) a.p[i] = fma(beta, a.p[i], a.r[i] / a.Ah[i]);
+    if (it >= a.max_it) break;
+    double beta = 0.0, den = delta;
+    if (it > 0) {
+      beta = gamma / gamma_old;
+      den = delta - beta * gamma / alpha;
+    }
+    if (!(den > 0.0)) break;   // breakdown: A^ or the preconditioner not SPD
+    alpha = gamma / den;
+    gamma_old = gamma;
+    // q = w + beta q (= A p), p = u + beta p, x += alpha p, r -= alpha q, u = D^-1 r
+    for (int i = t0; i < N; i += ts) {
+      const double q = fma(beta, it > 0 ? a.q[i] : 0.0, w[i]);
+      const double pp = fma(beta, it > 0 ? a.p[i] : 0.0, u[i]);
+      a.q[i] = q;
+      a.p[i] = pp;
+      a.x[i] = fma(alpha, pp, a.x[i]);
+      const double r = fma(-alpha, q, a.r[i]);
+      a.r[i] = r;
+      u[i] = r / a.Ah[i];
+    }
+    ++it;
     grid.sync();
   }
   if (t0 == 0) a.its[0] = conv ? it : (it | (1 << 30));
@@ -232,12 +243,22 @@ __global__ void __launch_bounds__(kCoarseThreads) k_dots(const double* a0, const
   }
   block_partials<3>(v, part);
 }
-__global__ void k_dots_final(const double* part, int nblocks, double* out) {
-  if (threadIdx.x < 3) {
+// fixed-order final sum: thread t adds partials t, t + 256, ... (same order every call), then
+// a fixed tree over the 256 thread sums
+__global__ void __launch_bounds__(256) k_dots_final(const double* part, int nblocks, double* out) {
+  __shared__ double sh[3][256];
+  for (int k = 0; k < 3; ++k) {
     double s = 0.0;
-    for (int i = 0; i < nblocks; ++i) s += part[threadIdx.x * nblocks + i];
-    out[threadIdx.x] = s;
+    for (int i = threadIdx.x; i < nblocks; i += 256) s += part[k * nblocks + i];
+    sh[k][threadIdx.x] = s;
   }
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int k = 0; k < 3; ++k) sh[k][threadIdx.x] += sh[k][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[threadIdx.x] = sh[threadIdx.x][0];
 }
 
 int sm_count() {
@@ -294,7 +315,9 @@ cudaError_t launch_coarse_pcg(const KParams& kp, const double* Ah, const double*
   a.its = its;
   a.tol2 = tol * tol;
   a.max_it = max_it;
+  // one block per SM (fewer blocks make the grid-wide barriers cheaper; measured on C2 / C3 / C5)
   int grid = (N + kCoarseThreads - 1) / kCoarseThreads;
+  grid = grid < sm_count() ? grid : sm_count();
   grid = grid < blocks ? grid : blocks;
   if (grid < 1) grid = 1;
   void* args[] = {&a};
@@ -318,7 +341,7 @@ cudaError_t launch_dots(const double* a0, const double* b0, const double* a1, co
   k_dots<<<nb, kCoarseThreads, 0, s>>>(a0, b0, a1, b1, a2, b2, n, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_dots_final<<<1, 32, 0, s>>>(part, nb, out);
+  k_dots_final<<<1, 256, 0, s>>>(part, nb, out);
   return cudaGetLastError();
 }
 

@@ -16,7 +16,7 @@ int vec_blocks();
 cudaError_t launch_coarse_matrix(const KParams& kp, double* Ah, cudaStream_t s);
 cudaError_t launch_restrict(const double* r, double* rh, int ncells, int nd, cudaStream_t s);
 cudaError_t launch_prolongate_add(double* u, const double* uh, int64_t ndof, int nd, cudaStream_t s);
-// x = (Jacobi-PCG) A^-1 rhs to ||r|| <= tol ||rhs||; work: 3N doubles; part: kPartials doubles;
+// x = (Jacobi-PCG) A^-1 rhs to ||r|| <= tol ||rhs||; work: 5N doubles; part: kPartials doubles;
 // its[0] = iterations (| 1 << 30 when max_it was hit). One cooperative launch.
 cudaError_t launch_coarse_pcg(const KParams& kp, const double* Ah, const double* rhs, double* x,
                               double* work, double* part, int* its, double tol, int max_it,
