@@ -279,6 +279,7 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   kp.mask = 7u;
   kp.its = c->d_its;
   kp.colour = -1;
+  kp.cmap = 0;
   kp.zoff = c->z_begin;
   c->method = (desc->b[0] == 0.0 && desc->b[1] == 0.0 && desc->b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
   c->max_it = 1000;
@@ -447,6 +448,10 @@ dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega
   cudaStream_t s = (cudaStream_t)stream;
   const int order[4] = {0, 1, 1, 0};   // forward: red, black; backward: black, red
   const int halves = symmetric ? 4 : 2;
+  // p <= 3 (plane solvers with cp.async staging) and nx even: the launch enumerates the cells of
+  // one colour only and updates them in place (their neighbours are of the other colour and are
+  // not written); otherwise every cell is launched and the other colour passes through
+  const bool compact = c->desc.p <= 3 && c->desc.nx % 2 == 0;
   c->launches = 0;
   for (int h = 0; h < halves; ++h) {
     dg_status st = halo_exchange(c, u, s);
@@ -456,10 +461,13 @@ dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega
     kp.max_it = c->max_it;
     kp.omega = omega;
     kp.colour = order[h];
-    cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, c->d_unew, s);
+    kp.cmap = compact ? 1 : 0;
+    cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, compact ? u : c->d_unew, s);
     if (e != cudaSuccess) return cuda_fail(e, "sor half-sweep");
-    e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(e, "sor copy-back");
+    if (!compact) {
+      e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) return cuda_fail(e, "sor copy-back");
+    }
     ++c->launches;
   }
   c->last_stream = s;

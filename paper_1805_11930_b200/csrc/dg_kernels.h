@@ -31,14 +31,30 @@ struct KParams {
   int32_t colour;                // -1: every cell; 0 / 1: only cells with (cx+cy+cz) % 2 == colour
                                  // are updated (multicolour block SOR), the others pass through
   int32_t zoff;                  // global z index of the slab's first layer (for the colour)
+  int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
+                                 // group_cell), the other colour is not touched
 };
 
-// the cell is outside the colour of a multicolour half-sweep (kp.colour >= 0)
+// the cell is outside the colour of a multicolour half-sweep (kp.colour >= 0, masked mode)
 __host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
-  if (kp.colour < 0) return false;
+  if (kp.colour < 0 || kp.cmap) return false;
   const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / (kp.nx * kp.ny) + kp.zoff;
   return ((cx + cy + cz) & 1) != kp.colour;
 }
+
+// Cell of slot cs of the group starting at item g0: consecutive cells, or (kp.cmap) the
+// (g0 + cs)-th cell of colour kp.colour in lexicographic order (nx even: nx / 2 per row);
+// -1 past the end.
+__host__ __device__ inline int group_cell(const KParams& kp, int g0, int cs) {
+  const int m = g0 + cs;
+  if (!kp.cmap) return m < kp.ncells ? m : -1;
+  const int half = kp.nx >> 1;
+  if (m >= kp.ncells / 2) return -1;
+  const int row = m / half, i = m - row * half;
+  const int cy = row % kp.ny, cz = row / kp.ny;
+  return 2 * i + ((kp.colour + cy + cz + kp.zoff) & 1) + kp.nx * row;
+}
+__host__ __device__ inline int group_items(const KParams& kp) { return kp.cmap ? kp.ncells / 2 : kp.ncells; }
 
 enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3 };
 

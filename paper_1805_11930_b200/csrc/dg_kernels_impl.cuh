@@ -1065,15 +1065,28 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if constexpr (N <= 5) {
     if (!force_line()) {
       using G = pk::Geo<N>;
-      const int grid = (kp.ncells + G::C - 1) / G::C;
+      const int grid = (group_items(kp) + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
+      constexpr size_t cg_smem = pk::smem_solve<N>(N >= 5 ? 4 : 2);
+      // compact colour map (red-black SOR half-sweeps, n <= 4 sweeps only): own instantiations
+      if constexpr (SWEEP && N <= 4) {
+        if (kp.cmap) {
+          if (method == LM_BICGSTAB_THOMAS)
+            return launch(pk::k_bicgstab<N, true, true, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
+          if (method == LM_BICGSTAB)
+            return launch(pk::k_bicgstab<N, true, false, true>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+          if (gen_terms(kp))
+            return launch(pk::k_cg<N, true, true, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+          return launch(pk::k_cg<N, true, false, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+        }
+      }
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
       if (method == LM_BICGSTAB)
         return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
       if (gen_terms(kp))
-        return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
-      return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, pk::smem_solve<N>(N >= 5 ? 4 : 2), s, kp, in, f, out);
+        return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+      return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, cg_smem, s, kp, in, f, out);
     }
   }
   using G = Geo<N>;

@@ -20,6 +20,9 @@
 // Neighbour traces (A only) are staged tile by tile through shared memory with coalesced
 // loads in a prologue and enter Q1/Q2 as extra face arrays.
 
+#ifndef DG_RESTRICT
+#define DG_RESTRICT
+#endif
 namespace pk {
 
 #ifndef DG_VOL_MINB
@@ -968,7 +971,7 @@ template <int N, bool WB> __device__ __forceinline__ void clear_masks(Cells<N, W
   if (threadIdx.x < 6) cl.nbg[threadIdx.x] = 0;
 }
 
-template <int N, bool WB>
+template <int N, bool CMAP = false, bool WB>
 __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl, SetupRegs<N>& sr,
                                             int cell0, const double* u) {
   using G = Geo<N>;
@@ -978,17 +981,24 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
   for (int r = 0; r < SetupRegs<N>::IT; ++r) {
     const int it = threadIdx.x + r * G::NT;
     const int cs = it / 3, axis = it % 3;
-    const int cell = cell0 + cs;
+    const int cell = CMAP ? group_cell(kp, cell0, cs) : (cell0 + cs < kp.ncells ? cell0 + cs : -1);
     sr.kind[r][0] = sr.kind[r][1] = -1;
     if (it >= 3 * G::C) continue;
-    if (axis == 0) cl.cell[cs] = cell < kp.ncells ? cell : -1;
-    if (cell >= kp.ncells) {
+    if (axis == 0) cl.cell[cs] = cell;
+    if (cell < 0) {
       cl.nb[cs][2 * axis] = cl.nb[cs][2 * axis + 1] = nullptr;
       continue;
     }
-    int cx = c0x + cs, cy = c0y, cz = c0z;
-    while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
-    while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
+    int cx, cy, cz;
+    if (CMAP) {
+      cx = cell % kp.nx;
+      cy = (cell / kp.nx) % kp.ny;
+      cz = cell / nxy;
+    } else {
+      cx = c0x + cs; cy = c0y; cz = c0z;
+      while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
+      while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
+    }
     const int co = axis == 0 ? cx : (axis == 1 ? cy : cz);
     const int dim = axis == 0 ? kp.nx : (axis == 1 ? kp.ny : kp.nzl);
     const int step = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
@@ -1018,7 +1028,7 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
       sr.Kn[r][hi] = kidx >= 0 ? __ldg(kp.K + (size_t)kidx * 3 + axis) : 0.0;
       cl.nb[cs][f] = nbp;
       if (nc >= 0 && nc < dim) atomicOr(&cl.nbm[f][cs >> 5], 1u << (cs & 31));
-      else if (kind == 0) cl.nbg[f] = 1;
+      if ((kind == 0 && !(nc >= 0 && nc < dim)) || CMAP) cl.nbg[f] = 1;   // per-cell pointers
     }
   }
 }
@@ -1148,19 +1158,58 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
 }
 
+// Tile transfers through the group's cell list (cl.cell; compact colour map): each cell's n^3
+// values are contiguous in global memory, the cells are not.
+template <int N, bool WB>
+__device__ __forceinline__ void async_own_map(double* TB, const double* __restrict__ src, const Cells<N, WB>& cl) {
+  using G = Geo<N>;
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    if (e < G::C * G::N3) {
+      const int cs = e / G::N3, r = e % G::N3;
+      const int cell = cl.cell[cs];
+      cp_async8(TB + cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2), src + (cell >= 0 ? (size_t)cell * G::N3 + r : 0),
+                cell >= 0);
+    }
+  }
+}
+template <int N, bool WB>
+__device__ __forceinline__ void stage_tile_map(double* TB, const double* __restrict__ src, const Cells<N, WB>& cl) {
+  using G = Geo<N>;
+  double v[G::PER];
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    const int cell = e < G::C * G::N3 ? cl.cell[e / G::N3] : -1;
+    v[m] = cell >= 0 ? src[(size_t)cell * G::N3 + e % G::N3] : 0.0;
+  }
+  store_tile<N>(TB, v);
+}
+template <int N, bool WB>
+__device__ __forceinline__ void unstage_tile_map(const double* TB, double* __restrict__ dst, const Cells<N, WB>& cl) {
+  using G = Geo<N>;
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    const int cell = cl.cell[cs];
+    if (cell >= 0) dst[(size_t)cell * G::N3 + r] = TB[cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2)];
+  }
+}
+
 // Solver prologue: coefficients, self-face operators and (SWEEP) the defect's neighbour tiles
 // staged with cp.async exactly as in the apply kernel; the own tile lands in TB half 0.
-template <int N, bool SWEEP, bool WB>
+template <int N, bool SWEEP, bool CMAP, bool WB>
 __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl, double* TB, double* FY,
                                              double* FX, double* FZ, const double* in, int cell0, int nvalid) {
   using G = Geo<N>;
   const double* tile = in + (size_t)cell0 * G::N3;
-  async_own<N>(TB, tile, nvalid);
+  if (!CMAP) async_own<N>(TB, tile, nvalid);
   clear_masks<N>(cl);
   __syncthreads();
   SetupRegs<N> sr;
-  setup_issue<N>(kp, cl, sr, cell0, SWEEP ? in : nullptr);
+  setup_issue<N, CMAP>(kp, cl, sr, cell0, SWEEP ? in : nullptr);
   __syncthreads();   // neighbour pointers and masks
+  if (CMAP) async_own_map<N>(TB, in, cl);
   if (SWEEP) {
     async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, in, kp, tile);
     async_nbr<N, G::N2, G::FS>(FY, cl, 3, in, kp, tile);
@@ -1232,10 +1281,10 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
 // Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
 // VS (n = 5): r and p live in shared planes too, so nothing but the operator's own planes is
 // held in registers across an application (no spills at n = 5).
-template <int N, bool SWEEP, bool GEN = true, bool VS = (N >= 5)>
+template <int N, bool SWEEP, bool GEN = true, bool VS = (N >= 5), bool CMAP = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
-k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
-     double* __restrict__ out) {
+k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
+     double* DG_RESTRICT out) {
   using G = Geo<N>;
   extern __shared__ double sm[];
   __shared__ Cells<N> cl;
@@ -1246,7 +1295,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   double* FX = XS;
   double* FZ = DS;
   const int cell0 = blockIdx.x * G::C;
-  const int nvalid = min(G::C, kp.ncells - cell0);
+  const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
@@ -1255,7 +1304,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   // registers, one pair of tiles at a time
   constexpr bool ASYNC = G::FS >= G::N3;
   if constexpr (ASYNC) {
-    solver_setup<N, SWEEP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+    solver_setup<N, SWEEP, CMAP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
   } else {
     stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
     setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
@@ -1265,7 +1314,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   if (SWEEP) {
     double Q[N][N];
     if constexpr (ASYNC) {
-      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
       load_nbr<N>(pv0, cl, 2);
@@ -1274,7 +1323,8 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     }
     plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
-    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    if (CMAP) stage_tile_map<N>(TB, f, cl);
+    else stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
     read_plane<N>(TB, L, R);
 #pragma unroll
@@ -1436,7 +1486,10 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   }
   // result: X (+ u) -> TB -> global
   __syncthreads();
-  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  if (SWEEP) {
+    if (CMAP) stage_tile_map<N>(TB, in, cl);
+    else stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  }
   __syncthreads();
   if (L.active) {
     double* b = TB + L.cs * G::CTB + L.t * G::KS;
@@ -1447,8 +1500,9 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         b[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], b[j * N + i]) : xs[j * N + i];
   }
   __syncthreads();
-  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
-  if (valid && L.t == 0) kp.its[cell0 + L.cs] = its_out;
+  if (CMAP) unstage_tile_map<N>(TB, out, cl);
+  else unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  if (valid && L.t == 0) kp.its[CMAP ? cl.cell[L.cs] : cell0 + L.cs] = its_out;
 }
 
 // ---- tridiagonal (Thomas) local preconditioner -------------
@@ -1562,10 +1616,10 @@ __device__ void thomas_apply(const Lane& L, double* TB, const double* SB, const 
 // Registers: r and the operator input/output planes; shared: x, r^, p, v, diag planes.
 // THOMAS: right preconditioner = the tridiagonal part of D_T in DoF order (NEXT-3) instead of
 // its diagonal; two more shared planes (the band factors) per cell.
-template <int N, bool SWEEP, bool THOMAS = false>
+template <int N, bool SWEEP, bool THOMAS = false, bool CMAP = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
-k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
-           double* __restrict__ out) {
+k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
+           double* DG_RESTRICT out) {
   using G = Geo<N>;
   extern __shared__ double sm[];
   __shared__ Cells<N> cl;
@@ -1581,7 +1635,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* FX = XS;
   double* FZ = RHS;
   const int cell0 = blockIdx.x * G::C;
-  const int nvalid = min(G::C, kp.ncells - cell0);
+  const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
@@ -1590,7 +1644,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   // registers, one pair of tiles at a time
   constexpr bool ASYNC = G::FS >= G::N3;
   if constexpr (ASYNC) {
-    solver_setup<N, SWEEP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+    solver_setup<N, SWEEP, CMAP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
   } else {
     stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
     setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
@@ -1600,7 +1654,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   if (SWEEP) {
     double T[N][N];
     if constexpr (ASYNC) {
-      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
       load_nbr<N>(pv0, cl, 2);
@@ -1609,7 +1663,8 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     }
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
-    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    if (CMAP) stage_tile_map<N>(TB, f, cl);
+    else stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
     read_plane<N>(TB, L, R);
 #pragma unroll
@@ -1761,7 +1816,10 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     }
   }
   __syncthreads();
-  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  if (SWEEP) {
+    if (CMAP) stage_tile_map<N>(TB, in, cl);
+    else stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  }
   __syncthreads();
   if (L.active) {
     double* bb = TB + L.cs * G::CTB + L.t * G::KS;
@@ -1772,8 +1830,9 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
         bb[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], bb[j * N + i]) : xs[j * N + i];
   }
   __syncthreads();
-  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
-  if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
+  if (CMAP) unstage_tile_map<N>(TB, out, cl);
+  else unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  if (valid && L.t == 0) kp.its[CMAP ? cl.cell[L.cs] : cell0 + L.cs] = conv ? its : (its | (1 << 30));
 }
 
 template <int N> constexpr size_t smem_apply(bool nbr, bool faces) {

@@ -34,8 +34,14 @@ for p in range(1, 8):
                                      bc=MIXED, L=(1.0, 0.6, 1.4)), p % 2 == 1, 1.2))
 
 
+# even nx: p <= 3 runs the compact colour map (in-place half-sweeps over one colour's cells)
+for p, shape in ((1, (8, 5, 3)), (2, (6, 4, 3)), (3, (4, 3, 5))):
+    CASES.append((random_problem(*shape, p, seed=650 + p, spread=1.0), True, 1.1))
+    CASES.append((random_problem(*shape, p, seed=660 + p, b=(0.7, 0.4, -0.3), c=True, bc=MIXED), False, 0.9))
+
+
 @pytest.mark.parametrize("P,symmetric,omega", CASES,
-                         ids=[f"p{c[0].p}-{'conv' if any(c[0].b) else 'diff'}-{'ssor' if c[1] else 'sor'}"
+                         ids=[f"p{c[0].p}-nx{c[0].nx}-{'conv' if any(c[0].b) else 'diff'}-{'ssor' if c[1] else 'sor'}"
                               for c in CASES])
 def test_sor_matches_oracle(P, symmetric, omega):
     u = uniform_pm1(620 + P.p, 0, P.n_dof)
