@@ -106,8 +106,10 @@ dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double 
  * sweep (equal to Alg. 3's (1 - omega) u + omega du with du the new block value, DESIGN reading
  * #17); symmetric != 0 adds the backward sweep (black, then red): block SSOR.
  * Every colour is ordered after all cells of the other colour, so each half-sweep is one fully
- * parallel launch. The per-cell statistics (dg_get_stats) are those of the last half-sweep
- * (0 iterations for the cells it skipped). */
+ * parallel launch (p <= 3 with nx even: only that colour's cells are launched, updated in place).
+ * With nranks > 1 the z-halo is exchanged before every half-sweep (NCCL halo mode only;
+ * DG_ERR_UNSUPPORTED in external-halo mode). The per-cell statistics (dg_get_stats) are those of
+ * the last half-sweep (0 iterations for the cells it skipped). */
 dg_status dg_block_sor_sweep(dg_ctx* ctx, double* u, const double* f, double omega, double local_tol,
                              int32_t symmetric, void* cuda_stream);
 

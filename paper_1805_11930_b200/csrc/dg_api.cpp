@@ -445,6 +445,9 @@ dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega
   if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
   if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
   if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  if (c->desc.nranks > 1 && c->desc.halo_mode == DG_HALO_EXTERNAL)
+    return fail(DG_ERR_UNSUPPORTED, "block SOR with external halos: the ghost layers would have to be "
+                                    "refreshed between the colour half-sweeps (use the NCCL halo mode)");
   cudaStream_t s = (cudaStream_t)stream;
   const int order[4] = {0, 1, 1, 0};   // forward: red, black; backward: black, red
   const int halves = symmetric ? 4 : 2;
