@@ -509,7 +509,8 @@ __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
         d += tm * (c[0] + c[1] * dd * ih + c[4] * dd);
       }
     }
-    Dg[cs * G::CS + idx[2] * G::ZS + idx[1] * G::YS + idx[0]] = d;
+    // stored inverted: the solvers multiply (no division per element and iteration)
+    Dg[cs * G::CS + idx[2] * G::ZS + idx[1] * G::YS + idx[0]] = d != 0.0 ? 1.0 / d : 1.0;
   }
 }
 
@@ -602,7 +603,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     ld<N, 1>(Dg + off, dg);
     double rr = 0.0, rz = 0.0;
 #pragma unroll
-    for (int e = 0; e < N; ++e) { z[e] = r[e] / dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
+    for (int e = 0; e < N; ++e) { z[e] = r[e] * dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
     st<N, 1>(P + off, z);
     st<N, 1>(X + off, zero);
     g.red[0][it] = rr;
@@ -658,7 +659,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         x[e] = fma(alpha, p[e], x[e]);
         r[e] = fma(-alpha, q[e], r[e]);
         rr = fma(r[e], r[e], rr);
-        rz = fma(r[e], r[e] / dg[e], rz);
+        rz = fma(r[e], r[e] * dg[e], rz);
       }
       st<N, 1>(X + off, x);
       st<N, 1>(R + off, r);
@@ -682,7 +683,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         ld<N, 1>(P + off, p);
         ld<N, 1>(Dg + off, dg);
 #pragma unroll
-        for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], r[e] / dg[e]);
+        for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], r[e] * dg[e]);
         st<N, 1>(P + off, p);
       }
     })
@@ -811,7 +812,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
 #pragma unroll
         for (int e = 0; e < N; ++e) {
           p[e] = rst ? r[e] : fma(beta, fma(-om, v[e], p[e]), r[e]);
-          ps[e] = p[e] / dg[e];
+          ps[e] = p[e] * dg[e];
         }
         if (rst) st<N, 1>(RH + off, r);
         st<N, 1>(P + off, p);
@@ -860,7 +861,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
           x[e] = fma(alpha, ps[e], x[e]);
           r[e] = fma(-alpha, v[e], r[e]);
           ss = fma(r[e], r[e], ss);
-          ps[e] = r[e] / dg[e];
+          ps[e] = r[e] * dg[e];
         }
         st<N, 1>(X + off, x);
         st<N, 1>(R + off, r);

@@ -15,7 +15,7 @@ from synth import Problem, uniform_pm1
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from kernel_times import PEAK, timed   # noqa: E402
 
-for p in range(1, 8):
+for p in ([int(a) for a in sys.argv[1:]] or range(1, 8)):
     n = p + 1
     m = int(round((8e6 / n ** 3) ** (1 / 3)))
     P = Problem(m, m, m, p, K=np.ones(m ** 3))

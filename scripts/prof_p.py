@@ -1,0 +1,26 @@
+"""Short run for ncu at degree p (Poisson cube of ~8M DoF): 3 applies, 3 volume-only, 1 sweep."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1805_11930_b200 as dg
+from synth import Problem, uniform_pm1
+
+p = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+n = p + 1
+m = int(round((8e6 / n ** 3) ** (1 / 3)))
+P = Problem(m, m, m, p, K=np.ones(m ** 3))
+ctx = dg.DGContext(P)
+ut = torch.from_numpy(uniform_pm1(900 + p, 0, P.n_dof)).cuda()
+ft = torch.from_numpy(uniform_pm1(910 + p, 0, P.n_dof)).cuda()
+out = torch.empty_like(ut)
+for _ in range(3):
+    ctx.apply(ut, out)
+for _ in range(3):
+    ctx.apply_parts(ut, out, dg.MASK_VOLUME)
+ctx.sweep(ut, ft, 1.0, 1e-12)
+torch.cuda.synchronize()
+print("ok")
