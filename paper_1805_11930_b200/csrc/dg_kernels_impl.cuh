@@ -310,7 +310,8 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // ---- the full cell operator: faces + volume, result handed to `out` line by line ----
 // src: input tensors (smem), SA/SB scratch tensors, FB face buffer.
 // out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
-template <int N, class Out>
+// FACES = false: the volume terms alone (the face passes are skipped)
+template <int N, bool FACES = true, class Out>
 __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
                                               const double* src, double* SA, double* SB,
                                               double* FB, bool vol, Out out) {
@@ -323,7 +324,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
 
   // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
-  for (int it = tid; it < 3 * LINES; it += NT) {
+  for (int it = tid; FACES && it < 3 * LINES; it += NT) {
     const int ax = it / LINES, r = it % LINES, cs = r / N2, l = r % N2;
     const int a = l % N, b = l / N;
     if (ax == 0) face_line<N, 0>(g, src, FB, cs, a, b, inv_h[0]);
@@ -342,7 +343,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   }
   __syncthreads();
   // pass 2: F2 (tangential mass along t1) + P2 (y-lines: SB = A_y SA)
-  for (int it = tid; it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
     const int t2 = it % N, rest = it / N;
     double* fa = FB + rest * N2 + N * t2;
     double v[N], o[N];
@@ -363,7 +364,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   __syncthreads();
   // pass 3: F3 (tangential mass along t2, area scaling) + P3 (z-lines: U = A_z SB -> SA,
   //         R = reaction + z-term -> SB)
-  for (int it = tid; it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
     const int t1 = it % N, rest = it / N;
     const int ax = (rest >> 2) % 3;
     double* fa = FB + rest * N2 + t1;
@@ -436,6 +437,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
 #pragma unroll
       for (int e = 0; e < N; ++e) v[e] = 0.0;
     }
+    if constexpr (FACES) {
     const double* fx = FB + (cs * 3 + 0) * 4 * N2;
     const double* fy = FB + (cs * 3 + 1) * 4 * N2;
     const double* fz = FB + (cs * 3 + 2) * 4 * N2;
@@ -467,6 +469,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
         s = fma(d1k, fz[3 * N2 + iz], s);
         v[i] = s;
       }
+    }
     }
     out(cs, j, k, v);
   }
@@ -534,7 +537,7 @@ __device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
 
 // =============================== kernels ========================================
 
-template <int N>
+template <int N, bool FACES = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
   using G = Geo<N>;
@@ -549,10 +552,10 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
   const int nvalid = min(G::C, kp.ncells - cell0);
   double* o = out + (size_t)cell0 * G::N3;
-  cell_operator<N>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
-                   [&](int cs, int j, int k, const double* v) {
-                     if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
-                   });
+  cell_operator<N, FACES>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
+                          [&](int cs, int j, int k, const double* v) {
+                            if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
+                          });
 }
 
 // Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
@@ -1054,9 +1057,10 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
   const size_t smem = smem_bytes<N>(3);
-  cudaError_t e = set_smem(k_apply<N>, smem);
+  auto kl = kp.mask == 1u ? k_apply<N, false> : k_apply<N, true>;   // mask = volume: no face passes
+  cudaError_t e = set_smem(kl, smem);
   if (e != cudaSuccess) return e;
-  k_apply<N><<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
+  kl<<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
   return cudaGetLastError();
 }
 
