@@ -75,6 +75,9 @@ template <int N_> struct Geo {
   static constexpr int FACE = C * 12 * N2;
 };
 
+// the solvers' face buffer fits in two tensors (it then aliases two the defect does not use)
+template <int N> __host__ __device__ constexpr bool fb_alias() { return 2 * Geo<N>::TENSOR >= Geo<N>::FACE; }
+
 template <int N> struct Group {
   static constexpr int C = Cells<N>::C;
   int cell[C];
@@ -83,6 +86,9 @@ template <int N> struct Group {
   const double* nb[C][6];       // neighbour cell base pointer (nullptr: none / not needed)
   double tw[N], td0[N], td1[N]; // runtime-indexed copies of w, d0, d1
   double red[2][C * N * N];     // per-line partial sums
+  // self-face operators of D_T at the Gauss points, weighted residual form, per axis (x, y, z):
+  // R_line += w_t1 w_t2 Bf U_line (the local solvers' D_T applications, no face passes)
+  double Bf[C][3][N * N];
   double sc[8][C];              // per-cell solver scalars
   int conv[C], its[C], rst[C];
 };
@@ -137,6 +143,36 @@ template <int N> __device__ __forceinline__ void dir_term(const double* U, doubl
   mtv<N, 1>(F, t);
 #pragma unroll
   for (int r = 0; r < N; ++r) R[r] += t[r];
+}
+
+// R += Wl B U (B: a cell's self-face operator along the line direction, from shared memory)
+template <int N> __device__ __forceinline__ void bterm(const double* B, const double* U, double* R, double Wl) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) s = fma(B[q * N + r], U[r], s);
+    R[q] = fma(Wl, s, R[q]);
+  }
+}
+
+// Bf[cs][a][q][r] = |F_a| sum_{s = lo, hi} (E_s[q] (sa_s E_s[r] + sg_s F_s[r] / h_a) + F_s[q] ta_s E_s[r])
+// (traces of a Gauss-value line: u(s) = E_s.U, u'(s) = F_s.U; injection of the value- and
+// derivative-test fluxes into the weighted Gauss residual). Needs g.fc; ends with a barrier.
+template <int N> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
+  using G = Geo<N>;
+  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += G::NT) {
+    const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
+    const int q = (rem % (N * N)) / N, r = rem % N;
+    const double* lo = g.fc[cs][2 * a];
+    const double* hi = g.fc[cs][2 * a + 1];
+    const double ih = 1.0 / kp.h[a];
+    const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
+    double b = c_tab[N].E0[q] * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) + c_tab[N].F0[q] * lo[4] * c_tab[N].E0[r];
+    b += c_tab[N].E1[q] * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) + c_tab[N].F1[q] * hi[4] * c_tab[N].E1[r];
+    g.Bf[cs][a][q * N + r] = area * b;
+  }
+  __syncthreads();
 }
 
 // ---- group setup: coefficients, face parameters, neighbour pointers ------------
@@ -310,8 +346,9 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // ---- the full cell operator: faces + volume, result handed to `out` line by line ----
 // src: input tensors (smem), SA/SB scratch tensors, FB face buffer.
 // out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
-// FACES = false: the volume terms alone (the face passes are skipped)
-template <int N, bool FACES = true, class Out>
+// FACES = false: the volume terms alone (the face passes are skipped); USEB (with FACES = false):
+// plus the self-face terms through g.Bf inside the Gauss-point passes (D_T without face passes)
+template <int N, bool FACES = true, bool USEB = false, class Out>
 __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
                                               const double* src, double* SA, double* SB,
                                               double* FB, bool vol, Out out) {
@@ -387,6 +424,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
 #pragma unroll
       for (int q = 0; q < N; ++q) R[q] = Wl * c_tab[N].w[q] * sc * U[q];
       dir_term<N>(U, R, Wl, g.vc[cs][2], sb[2]);
+      if constexpr (USEB) bterm<N>(g.Bf[cs][2], U, R, Wl);
       st<N, G::ZS>(SA + off, U);
       st<N, G::ZS>(SB + off, R);
     }
@@ -399,6 +437,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       ld<N, 1>(SA + off, U);
       ld<N, 1>(SB + off, R);
       dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], sb[0]);
+      if constexpr (USEB) bterm<N>(g.Bf[cs][0], U, R, g.tw[a] * g.tw[b]);
       st<N, 1>(SB + off, R);
     }
     __syncthreads();
@@ -410,6 +449,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       ld<N, G::YS>(SA + off, U);
       ld<N, G::YS>(SB + off, R);
       dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], sb[1]);
+      if constexpr (USEB) bterm<N>(g.Bf[cs][1], U, R, g.tw[a] * g.tw[b]);
       mtv<N, 0>(R, o);
       st<N, G::YS>(SB + off, o);
     }
@@ -561,7 +601,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
 // Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
 // SWEEP: in = u (defect d = f - A u formed first), result u + omega du; else in = d, result du.
 template <int N, bool SWEEP>
-__global__ void __launch_bounds__(Geo<N>::NT)
+__global__ void __launch_bounds__(Geo<N>::NT, 2)   // two CTAs per SM (n = 7: <= 146 registers)
 k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
      double* __restrict__ out) {
   using G = Geo<N>;
@@ -575,7 +615,9 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   double* Dg = Q + G::TENSOR;
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
-  double* FB = SB + G::TENSOR;
+  // the face buffer is only used by the defect (the loop's D_T takes the self faces through
+  // g.Bf), before Q and Dg are: it aliases them when it fits
+  double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
   const int cell0 = blockIdx.x * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
@@ -583,6 +625,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   KParams kq = kp;
   kq.mask = 7u;
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
     const double* fb = f + (size_t)cell0 * G::N3;
     cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
@@ -624,7 +667,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     const int done = __syncthreads_and(tid >= C || g.conv[tid]);
     if (done || iter >= kp.max_it) break;
     // q = D_T p
-    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       st<N, 1>(Q + cs * G::CS + k * G::ZS + j * G::YS, v);
     });
     __syncthreads();
@@ -713,7 +756,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks, b != 0).
 template <int N, bool SWEEP>
-__global__ void __launch_bounds__(Geo<N>::NT)
+__global__ void __launch_bounds__(Geo<N>::NT, 2)   // two CTAs per SM (n = 7: <= 146 registers)
 k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
            double* __restrict__ out) {
   using G = Geo<N>;
@@ -730,7 +773,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* Dg = T + G::TENSOR;
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
-  double* FB = SB + G::TENSOR;
+  double* FB = fb_alias<N>() ? T : SB + G::TENSOR;   // defect only: aliases T and Dg when it fits
   const int cell0 = blockIdx.x * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
@@ -738,6 +781,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   KParams kq = kp;
   kq.mask = 7u;
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
     cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
@@ -823,7 +867,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       }
     })
     __syncthreads();
-    cell_operator<N>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       st<N, 1>(V + cs * G::CS + k * G::ZS + j * G::YS, v);
     });
     __syncthreads();
@@ -880,7 +924,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       if (ss <= kp.tol2 * g.sc[S_RR0][tid]) { g.conv[tid] = 1; g.its[tid] += 1; }
     }
     __syncthreads();
-    cell_operator<N>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       st<N, 1>(T + cs * G::CS + k * G::ZS + j * G::YS, v);
     });
     __syncthreads();
@@ -1099,8 +1143,10 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
   if (method == LM_BICGSTAB)
-    return launch(k_bicgstab<N, SWEEP>, grid, G::NT, smem_bytes<N>(10), s, kp, in, f, out);
-  return launch(k_cg<N, SWEEP>, grid, G::NT, smem_bytes<N>(7), s, kp, in, f, out);
+    return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
+                  fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
+  return launch(k_cg<N, SWEEP>, grid, G::NT,
+                fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);
 }
 
 // ---- per-degree entry points (dg_degree.h) ---------------------------------------------
