@@ -1111,12 +1111,15 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
 template <int N, bool SWEEP>
 cudaError_t solve_n(int method, const KParams& kp, const double* in, const double* f, double* out,
                     cudaStream_t s) {
+  // plane solvers for n <= 4; at n = 5 the line solvers (self faces as Gauss-point operators,
+  // two CTAs per SM) beat the register-starved plane ones (C3 sweep 32.7 -> 20.1 ms), except
+  // for the tridiagonal preconditioner, which exists in the plane family only
   if constexpr (N <= 5) {
-    if (!force_line()) {
+    if (!force_line() && (N <= 4 || method == LM_BICGSTAB_THOMAS)) {
       using G = pk::Geo<N>;
       const int grid = (group_items(kp) + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
-      constexpr size_t cg_smem = pk::smem_solve<N>(N >= 5 ? 4 : 2);
+      constexpr size_t cg_smem = pk::smem_solve<N>(2);
       // compact colour map (red-black SOR half-sweeps, n <= 4 sweeps only): own instantiations
       if constexpr (SWEEP && N <= 4) {
         if (kp.cmap) {
@@ -1125,17 +1128,19 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
           if (method == LM_BICGSTAB)
             return launch(pk::k_bicgstab<N, true, false, true>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
           if (gen_terms(kp))
-            return launch(pk::k_cg<N, true, true, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
-          return launch(pk::k_cg<N, true, false, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+            return launch(pk::k_cg<N, true, true, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+          return launch(pk::k_cg<N, true, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
         }
       }
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
-      if (method == LM_BICGSTAB)
-        return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
-      if (gen_terms(kp))
-        return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
-      return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, cg_smem, s, kp, in, f, out);
+      if constexpr (N <= 4) {
+        if (method == LM_BICGSTAB)
+          return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+        if (gen_terms(kp))
+          return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
+        return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, cg_smem, s, kp, in, f, out);
+      }
     }
   }
   using G = Geo<N>;

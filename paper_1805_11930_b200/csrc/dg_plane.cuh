@@ -1279,9 +1279,7 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
 
 // Jacobi-PCG per cell; SWEEP: defect d = f - A u first, result u + omega du.
 // Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
-// VS (n = 5): r and p live in shared planes too, so nothing but the operator's own planes is
-// held in registers across an application (no spills at n = 5).
-template <int N, bool SWEEP, bool GEN = true, bool VS = (N >= 5), bool CMAP = false>
+template <int N, bool SWEEP, bool GEN = true, bool CMAP = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
      double* DG_RESTRICT out) {
@@ -1351,139 +1349,63 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
         for (int i = 0; i < N; ++i) ds[j * N + i] = valid ? dg[j][i] : 1.0;
   }
   int its_out = 0;
-  if constexpr (VS) {
-    double* rs = DS + G::C * G::PS + po;
-    double* ps = rs + G::C * G::PS;
-    double rr = 0.0, rz = 0.0;
+  double rr = 0.0, rz = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
+      P[j][i] = z;
+      rr = fma(R[j][i], R[j][i], rr);
+      rz = fma(R[j][i], z, rz);
+      if (L.active) xs[j * N + i] = 0.0;
+    }
+  const double rr0 = cell_sum<N>(rr, L.lane);
+  rz = cell_sum<N>(rz, L.lane);
+  bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
+  int its = 0;
+  for (int iter = 0;; ++iter) {
+    const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
+    if (done || iter >= kp.max_it) break;
+    double Q[N][N];
+    plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+    double pq = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) pq = fma(P[j][i], Q[j][i], pq);
+    pq = cell_sum<N>(pq, L.lane);
+    double alpha = 0.0;
+    if (!conv) {
+      if (pq > 0.0) alpha = rz / pq;
+      else conv = true;
+    }
+    double r2 = 0.0, rzn = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
-        rr = fma(R[j][i], R[j][i], rr);
-        rz = fma(R[j][i], z, rz);
-        if (L.active) {
-          xs[j * N + i] = 0.0;
-          rs[j * N + i] = R[j][i];
-          ps[j * N + i] = z;
-        }
+        if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
+        R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
+        r2 = fma(R[j][i], R[j][i], r2);
+        if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
       }
-    const double rr0 = cell_sum<N>(rr, L.lane);
-    rz = cell_sum<N>(rz, L.lane);
-    bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
-    int its = 0;
-    for (int iter = 0;; ++iter) {
-      const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
-      if (done || iter >= kp.max_it) break;
-      double Q[N][N];
-      {
-        double Pin[N][N];
+    r2 = cell_sum<N>(r2, L.lane);
+    rzn = cell_sum<N>(rzn, L.lane);
+    if (!conv) {
+      ++its;
+      if (r2 <= kp.tol2 * rr0) conv = true;
+      const double beta = rzn / rz;
+      rz = rzn;
+      if (!conv && L.active) {
 #pragma unroll
         for (int j = 0; j < N; ++j)
 #pragma unroll
-          for (int i = 0; i < N; ++i) Pin[j][i] = L.active ? ps[j * N + i] : 0.0;
-        plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, Pin, Q, TB, FY, FX, FZ);  // Q = D_T P
-      }
-      double pq = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j)
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-          if (L.active) pq = fma(ps[j * N + i], Q[j][i], pq);
-      pq = cell_sum<N>(pq, L.lane);
-      double alpha = 0.0;
-      if (!conv) {
-        if (pq > 0.0) alpha = rz / pq;
-        else conv = true;
-      }
-      double r2 = 0.0, rzn = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j)
-#pragma unroll
-        for (int i = 0; i < N; ++i)
-          if (L.active) {
-            xs[j * N + i] = fma(alpha, ps[j * N + i], xs[j * N + i]);
-            const double r = fma(-alpha, Q[j][i], rs[j * N + i]);
-            rs[j * N + i] = r;
-            r2 = fma(r, r, r2);
-            rzn = fma(r, r * ds[j * N + i], rzn);
-          }
-      r2 = cell_sum<N>(r2, L.lane);
-      rzn = cell_sum<N>(rzn, L.lane);
-      if (!conv) {
-        ++its;
-        if (r2 <= kp.tol2 * rr0) conv = true;
-        const double beta = rzn / rz;
-        rz = rzn;
-        if (!conv && L.active) {
-#pragma unroll
-          for (int j = 0; j < N; ++j)
-#pragma unroll
-            for (int i = 0; i < N; ++i)
-              ps[j * N + i] = fma(beta, ps[j * N + i], rs[j * N + i] * ds[j * N + i]);
-        }
+          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
       }
     }
-    its_out = conv ? its : (its | (1 << 30));
-  } else {
-    double rr = 0.0, rz = 0.0;
-#pragma unroll
-    for (int j = 0; j < N; ++j)
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double z = L.active ? R[j][i] * ds[j * N + i] : 0.0;
-        P[j][i] = z;
-        rr = fma(R[j][i], R[j][i], rr);
-        rz = fma(R[j][i], z, rz);
-        if (L.active) xs[j * N + i] = 0.0;
-      }
-    const double rr0 = cell_sum<N>(rr, L.lane);
-    rz = cell_sum<N>(rz, L.lane);
-    bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
-    int its = 0;
-    for (int iter = 0;; ++iter) {
-      const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
-      if (done || iter >= kp.max_it) break;
-      double Q[N][N];
-      plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
-      double pq = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j)
-#pragma unroll
-        for (int i = 0; i < N; ++i) pq = fma(P[j][i], Q[j][i], pq);
-      pq = cell_sum<N>(pq, L.lane);
-      double alpha = 0.0;
-      if (!conv) {
-        if (pq > 0.0) alpha = rz / pq;
-        else conv = true;
-      }
-      double r2 = 0.0, rzn = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j)
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
-          R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
-          r2 = fma(R[j][i], R[j][i], r2);
-          if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
-        }
-      r2 = cell_sum<N>(r2, L.lane);
-      rzn = cell_sum<N>(rzn, L.lane);
-      if (!conv) {
-        ++its;
-        if (r2 <= kp.tol2 * rr0) conv = true;
-        const double beta = rzn / rz;
-        rz = rzn;
-        if (!conv && L.active) {
-#pragma unroll
-          for (int j = 0; j < N; ++j)
-#pragma unroll
-            for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
-        }
-      }
-    }
-    its_out = conv ? its : (its | (1 << 30));
   }
+  its_out = conv ? its : (its | (1 << 30));
   // result: X (+ u) -> TB -> global
   __syncthreads();
   if (SWEEP) {
