@@ -577,7 +577,8 @@ __device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
 
 // =============================== kernels ========================================
 
-template <int N, bool FACES = true>
+// FACES = false, USEB = true: D_T (self faces as Gauss-point operators, no face passes)
+template <int N, bool FACES = true, bool USEB = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
   using G = Geo<N>;
@@ -590,9 +591,10 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   const int cell0 = blockIdx.x * G::C;
   load_tile<N>(g, cell0, kp.ncells, u, SRC);
   group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
+  if constexpr (USEB) self_face_ops<N>(kp, g);
   const int nvalid = min(G::C, kp.ncells - cell0);
   double* o = out + (size_t)cell0 * G::N3;
-  cell_operator<N, FACES>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
+  cell_operator<N, FACES, USEB>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
                           [&](int cs, int j, int k, const double* v) {
                             if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
                           });
@@ -1101,7 +1103,8 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
   const size_t smem = smem_bytes<N>(3);
-  auto kl = kp.mask == 1u ? k_apply<N, false> : k_apply<N, true>;   // mask = volume: no face passes
+  // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point operators
+  auto kl = kp.mask == 1u ? k_apply<N, false> : (!with_nbr && kp.mask == 7u ? k_apply<N, false, true> : k_apply<N, true>);
   cudaError_t e = set_smem(kl, smem);
   if (e != cudaSuccess) return e;
   kl<<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
