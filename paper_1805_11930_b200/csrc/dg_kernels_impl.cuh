@@ -22,6 +22,9 @@
 //  Local solves: Jacobi-preconditioned CG or BiCGStab per
 //    cell, all C cells of a CTA iterating together with per-cell convergence masks
 //    and deterministic per-cell reductions (no atomics).
+#ifndef DG_PDL
+#define DG_PDL 1
+#endif
 #include "dg_kernels.h"
 #include "dg_degree.h"
 
@@ -1095,8 +1098,18 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
       if (!faces) kern = gen ? pk::k_apply<N, false, false, true> : pk::k_apply<N, false, false, false>;
       cudaError_t e = set_smem(kern, smem);
       if (e != cudaSuccess) return e;
-      kern<<<grid, G::NT, smem, s>>>(kp, u, out);
-      return cudaGetLastError();
+      // programmatic dependent launch (the kernel waits on griddepcontrol before touching u)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(G::NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kern, kp, u, out);
     }
   }
   using G = Geo<N>;

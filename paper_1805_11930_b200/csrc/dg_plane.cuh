@@ -1131,13 +1131,17 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   const Lane L = lane_id<N>();
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  // all global loads of the own tile and the y-neighbour pair are in flight during the setup
+  // programmatic dependent launch: the next kernel in the stream may start launching now; this
+  // one's coefficient setup (K, c: constant) runs before it waits for the previous kernel's
+  // results (u, the ghost layers), so the setup overlaps the previous kernel's tail
+  asm volatile("griddepcontrol.launch_dependents;");
   const double* tile = u + (size_t)cell0 * G::N3;
-  async_own<N>(TB, tile, nvalid);
   clear_masks<N>(cl);
   __syncthreads();
   SetupRegs<N> sr;
   setup_issue<N>(kp, cl, sr, cell0, NBR ? u : nullptr);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  async_own<N>(TB, tile, nvalid);
   __syncthreads();   // neighbour pointers and masks
   if (NBR) {
     async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, u, kp, tile);   // y-lo -> TB half 1
