@@ -6,7 +6,9 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <utility>
@@ -19,6 +21,12 @@
 #include "dg_tables.h"
 
 namespace {
+
+bool getenv_flag(const char* name) {
+  const char* v = std::getenv(name);
+  return v && *v && *v != '0';
+}
+
 
 thread_local std::string g_err;
 
@@ -84,6 +92,7 @@ struct dg_ctx {
   double* d_ghost_hi = nullptr;
   double* d_unew = nullptr;
   int32_t* d_its = nullptr;
+  int32_t* d_gperm = nullptr;  // solver CTA -> cell group, boundary-heavy groups first
   // hybrid multigrid scratch (allocated on first use)
   double* d_Ah = nullptr;      // [7][ncells]
   double* d_cvec = nullptr;    // rh, uh, 5 coarse work vectors: [7][ncells]
@@ -143,6 +152,7 @@ void release(dg_ctx* c) {
   cudaFree(c->d_ghost_hi);
   cudaFree(c->d_unew);
   cudaFree(c->d_its);
+  cudaFree(c->d_gperm);
   cudaFree(c->d_Ah);
   cudaFree(c->d_cvec);
   cudaFree(c->d_part);
@@ -281,6 +291,30 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   kp.colour = -1;
   kp.cmap = 0;
   kp.zoff = c->z_begin;
+  kp.gperm = nullptr;
+  if (const int C = dg::solver_group_cells(desc->p); C > 0 && !getenv_flag("DG_NO_GPERM")) {
+    // Longest-processing-time-first order for the local-solver CTAs: cells with Dirichlet faces
+    // take more local iterations (the penalty stiffens their block), so the groups holding them
+    // start first and the ragged tail of the launch is made of cheap groups.
+    const int ng = (int)((c->ncells + C - 1) / C);
+    std::vector<int> weight(ng, 0), perm(ng);
+    const int64_t nx = desc->nx, ny = desc->ny, nzl = c->ncells / (nx * ny);
+    for (int64_t cell = 0; cell < c->ncells; ++cell) {
+      const int64_t co[3] = {cell % nx, (cell / nx) % ny, cell / (nx * ny)};
+      const int64_t dims[3] = {nx, ny, nzl};
+      int w = 0;
+      for (int f = 0; f < 6; ++f) {
+        const int64_t cc = co[f >> 1] + ((f & 1) ? 1 : -1);
+        if ((cc < 0 || cc >= dims[f >> 1]) && kp.slab_face[f] == dg::FK_DIRICHLET) ++w;
+      }
+      weight[cell / C] += w;
+    }
+    for (int g = 0; g < ng; ++g) perm[g] = g;
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return weight[a] > weight[b]; });
+    if (alloc((void**)&c->d_gperm, (size_t)ng * 4) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc gperm"); }
+    cudaMemcpy(c->d_gperm, perm.data(), (size_t)ng * 4, cudaMemcpyHostToDevice);
+    kp.gperm = c->d_gperm;
+  }
   c->method = (desc->b[0] == 0.0 && desc->b[1] == 0.0 && desc->b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
   c->max_it = 1000;
 

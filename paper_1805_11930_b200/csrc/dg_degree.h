@@ -10,6 +10,7 @@ template <int N> struct Deg {
   static cudaError_t apply(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr);
   static cudaError_t solve(int method, bool sweep, const KParams& kp, const double* in,
                            const double* f, double* out, cudaStream_t s);
+  static int solver_group_cells();   // cells per CTA of the plane solvers (0: line family)
 };
 
 }  // namespace dg

@@ -39,6 +39,15 @@ cudaError_t launch_dfma_bench(double* sink, int blocks, int iters, cudaStream_t 
   return cudaGetLastError();
 }
 
+int solver_group_cells(int p) {
+  switch (p) {
+    case 1: return Deg<2>::solver_group_cells();
+    case 2: return Deg<3>::solver_group_cells();
+    case 3: return Deg<4>::solver_group_cells();
+    default: return 0;
+  }
+}
+
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
   switch (p) {
     case 1: return Deg<2>::upload(t, err);

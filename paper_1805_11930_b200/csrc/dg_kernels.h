@@ -31,6 +31,8 @@ struct KParams {
   int32_t colour;                // -1: every cell; 0 / 1: only cells with (cx+cy+cz) % 2 == colour
                                  // are updated (multicolour block SOR), the others pass through
   int32_t zoff;                  // global z index of the slab's first layer (for the colour)
+  const int32_t* gperm;          // order in which the solver CTAs take the cell groups (longest
+                                 // first: groups with Dirichlet faces), nullptr = in order
   int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
                                  // group_cell), the other colour is not touched
 };
@@ -59,6 +61,9 @@ __host__ __device__ inline int group_items(const KParams& kp) { return kp.cmap ?
 enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3 };
 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
+
+// cells per CTA of the plane local solvers for degree p (0 when the line family runs them)
+int solver_group_cells(int p);
 
 // Au (or selected parts) for all local cells.
 cudaError_t launch_apply(int p, const KParams& kp, const double* u, double* out, cudaStream_t s);

@@ -1210,6 +1210,7 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
                                          cudaStream_t s, int with_nbr) {                         \
     return apply_n<NN>(kp, u, out, s, with_nbr);                                                 \
   }                                                                                              \
+  template <> int Deg<NN>::solver_group_cells() { return NN <= 4 ? pk::Geo<(NN <= 5 ? NN : 5)>::C : 0; } \
   template <> cudaError_t Deg<NN>::solve(int method, bool sweep, const KParams& kp,              \
                                          const double* in, const double* f, double* out,         \
                                          cudaStream_t s) {                                       \

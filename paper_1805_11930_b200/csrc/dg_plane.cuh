@@ -1296,7 +1296,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   double* DS = XS + G::C * G::PS;
   double* FX = XS;
   double* FZ = DS;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = (kp.gperm && !CMAP ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
   const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
@@ -1560,7 +1560,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   double* CPM = SBM + G::C * G::PS;  // THOMAS: super-diagonal / pivot
   double* FX = XS;
   double* FZ = RHS;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = (kp.gperm && !CMAP ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
   const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
