@@ -1031,6 +1031,17 @@ cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, c
   return cudaGetLastError();
 }
 
+// BiCGStab at n = 4 keeps x, p, v in tensor memory (2 CTAs per SM); DG_NO_TMEM=1 selects the
+// shared-memory variant (A/B comparisons)
+static bool use_tmem() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DG_NO_TMEM");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // DG_KERNEL_FAMILY=line forces the line-per-thread kernels for every degree (A/B comparisons).
 static bool force_line() {
   static int v = -1;
@@ -1141,8 +1152,12 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
         if (kp.cmap) {
           if (method == LM_BICGSTAB_THOMAS)
             return launch(pk::k_bicgstab<N, true, true, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
-          if (method == LM_BICGSTAB)
+          if (method == LM_BICGSTAB) {
+            if constexpr (N == 4)
+              if (use_tmem())
+                return launch(pk::k_bicgstab<N, true, false, true, true>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
             return launch(pk::k_bicgstab<N, true, false, true>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+          }
           if (gen_terms(kp))
             return launch(pk::k_cg<N, true, true, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
           return launch(pk::k_cg<N, true, false, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
@@ -1151,8 +1166,12 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
       if constexpr (N <= 4) {
-        if (method == LM_BICGSTAB)
+        if (method == LM_BICGSTAB) {
+          if constexpr (N == 4)
+            if (use_tmem())
+              return launch(pk::k_bicgstab<N, SWEEP, false, false, true>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
           return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
+        }
         if (gen_terms(kp))
           return launch(pk::k_cg<N, SWEEP, true>, grid, G::NT, cg_smem, s, kp, in, f, out);
         return launch(pk::k_cg<N, SWEEP, false>, grid, G::NT, cg_smem, s, kp, in, f, out);

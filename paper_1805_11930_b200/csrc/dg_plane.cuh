@@ -1538,28 +1538,90 @@ __device__ void thomas_apply(const Lane& L, double* TB, const double* SB, const 
       for (int i = 0; i < N; ++i) v[j][i] = sc[L.t * G::KS + j * N + i];
 }
 
+
+// ---- tensor memory (TMEM) as per-lane storage of Krylov vectors ------------------------------
+// The fp64 local solvers never issue tcgen05.mma, so the SM's 256 KB of TMEM is otherwise idle.
+// The BiCGStab kernel keeps three of its per-lane vectors there (x, p, v: each lane owns one TMEM
+// lane, a row of N doubles = 2N 32-bit columns), which takes them out of shared memory and lets
+// two CTAs (8 warps) share an SM instead of one. Warp w of the CTA owns TMEM lanes 32w..32w+31
+// (the tcgen05.ld/st lane-quadrant rule), so the CTA must have at most 4 warps.
+template <int NCOL> __device__ __forceinline__ uint32_t tm_alloc(uint32_t* slot) {
+  static_assert(NCOL == 32 || NCOL == 64 || NCOL == 128 || NCOL == 256, "TMEM allocation: power of 2");
+  if ((threadIdx.x >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
+                 ::"r"((unsigned)__cvta_generic_to_shared(slot)), "n"(NCOL));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  return *slot;
+}
+// all warps' TMEM accesses are complete (tcgen05.wait inside the row helpers) before the call
+template <int NCOL> __device__ __forceinline__ void tm_free(uint32_t base) {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "n"(NCOL));
+}
+// one row of N doubles of the lane's plane at TMEM address a (warp-collective: every lane of the
+// warp executes it; the load waits for its data inside the same asm block)
+template <int N> struct TmRow;
+template <> struct TmRow<4> {
+  static __device__ __forceinline__ void ld(uint32_t a, double (&v)[4]) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7])
+                 : "r"(a));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const double (&v)[4]) {
+    uint32_t r[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      r[2 * i] = (uint32_t)__double2loint(v[i]);
+      r[2 * i + 1] = (uint32_t)__double2hiint(v[i]);
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
+                 ::"r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+                   "r"(r[7]));
+  }
+};
+// stores of this thread are complete (before TMEM data is read back or freed)
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n"); }
+
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks).
 // Registers: r and the operator input/output planes; shared: x, r^, p, v, diag planes.
 // THOMAS: right preconditioner = the tridiagonal part of D_T in DoF order (NEXT-3) instead of
 // its diagonal; two more shared planes (the band factors) per cell.
-template <int N, bool SWEEP, bool THOMAS = false, bool CMAP = false>
+// TM: x, p and v in tensor memory (see tm_alloc), r^ and the inverse diagonal in shared memory;
+// the dynamic shared memory drops from 5 planes to 2, two CTAs per SM.
+template <int N, bool SWEEP, bool THOMAS = false, bool CMAP = false, bool TM = false>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
            double* DG_RESTRICT out) {
   using G = Geo<N>;
+  static_assert(!TM || (N == 4 && !THOMAS && G::WARPS <= 4), "TMEM vectors: n = 4, one lane quadrant per warp");
+  constexpr int PLN = G::C * G::PS;
   extern __shared__ double sm[];
   __shared__ Cells<N> cl;
+  __shared__ uint32_t tm_slot;
   double* TB = sm;
   double* FY = TB + G::TB;
-  double* XS = FY + G::FY;          // FX / FZ (defect prologue only) alias XS / RHS
-  double* RHS = XS + G::C * G::PS;
-  double* PSM = RHS + G::C * G::PS;
-  double* VSM = PSM + G::C * G::PS;
-  double* DS = VSM + G::C * G::PS;
-  double* SBM = DS + G::C * G::PS;   // THOMAS: sub-diagonal; DS then holds 1 / pivot
-  double* CPM = SBM + G::C * G::PS;  // THOMAS: super-diagonal / pivot
+  double* XS = FY + G::FY;          // FX / FZ (defect prologue only) alias the first two planes
+  double* RHS = TM ? XS : XS + PLN;
+  double* PSM = RHS + PLN;
+  double* VSM = PSM + PLN;
+  double* DS = TM ? RHS + PLN : VSM + PLN;
+  double* SBM = DS + PLN;            // THOMAS: sub-diagonal; DS then holds 1 / pivot
+  double* CPM = SBM + PLN;           // THOMAS: super-diagonal / pivot
   double* FX = XS;
-  double* FZ = RHS;
+  double* FZ = XS + PLN;
+  // TMEM: columns [0, 2N^2) x, [32, ...) p, [64, ...) v; this warp's lane quadrant
   const int cell0 = (kp.gperm && !CMAP ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
   const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
@@ -1609,7 +1671,29 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   double* ps = PSM + po;
   double* vs = VSM + po;
   double* ds = DS + po;
-  __syncthreads();   // the prologue's FX / FZ (aliasing XS / RHS) are consumed
+  // the prologue's FX / FZ (aliasing the first two planes) are consumed; the TMEM allocation
+  // (TM) comes with its own barrier, late so that its address is not live through the prologue
+  if constexpr (TM) tm_alloc<128>(&tm_slot);
+  else __syncthreads();
+  // TMEM addresses re-derived at each use (no register held through the operator)
+#define tx (*(volatile uint32_t*)&tm_slot + ((uint32_t)((threadIdx.x >> 5) * 32) << 16))
+#define tp (tx + 32)
+#define tv (tx + 64)
+#define tr (tx + 96)
+  // TM: the residual waits in TMEM while the operator runs (frees 2 N^2 registers there)
+  auto park = [&](double (&R_)[N][N]) {
+    if constexpr (TM) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) TmRow<N>::st(tr + 2 * N * j, R_[j]);
+      tm_wait_st();
+    }
+  };
+  auto unpark = [&](double (&R_)[N][N]) {
+    if constexpr (TM) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) TmRow<N>::ld(tr + 2 * N * j, R_[j]);
+    }
+  };
   if constexpr (THOMAS) {
     thomas_factor<N>(kp, cl, L, SBM, DS, CPM, valid);
   } else {
@@ -1628,12 +1712,24 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     for (int i = 0; i < N; ++i) {
       rr = fma(R[j][i], R[j][i], rr);
       if (L.active) {
-        xs[j * N + i] = 0.0;
         rh[j * N + i] = R[j][i];
-        ps[j * N + i] = 0.0;
-        vs[j * N + i] = 0.0;
+        if constexpr (!TM) {
+          xs[j * N + i] = 0.0;
+          ps[j * N + i] = 0.0;
+          vs[j * N + i] = 0.0;
+        }
       }
     }
+  if constexpr (TM) {
+    const double z[N] = {};
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      TmRow<N>::st(tx + 2 * N * j, z);
+      TmRow<N>::st(tp + 2 * N * j, z);
+      TmRow<N>::st(tv + 2 * N * j, z);
+    }
+    tm_wait_st();
+  }
   const double rr0 = cell_sum<N>(rr, L.lane);
   bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
   double rho = 1.0, alpha = 1.0, omega = 1.0;
@@ -1656,6 +1752,24 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     if (rst) rhon = r2;
     const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
     // p = r + beta (p - omega v);  W = M^-1 p
+    if constexpr (TM) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double pr[N], vr[N];
+        TmRow<N>::ld(tp + 2 * N * j, pr);
+        TmRow<N>::ld(tv + 2 * N * j, vr);
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          if (!conv) {
+            pr[i] = rst ? R[j][i] : fma(beta, fma(-omega, vr[i], pr[i]), R[j][i]);
+            if (rst && L.active) rh[j * N + i] = R[j][i];
+          }
+          W[j][i] = L.active ? pr[i] * ds[j * N + i] : 0.0;
+        }
+        TmRow<N>::st(tp + 2 * N * j, pr);
+      }
+      tm_wait_st();
+    } else {
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
@@ -1672,19 +1786,24 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
         }
         W[j][i] = p;
       }
+    }
     if constexpr (THOMAS) thomas_apply<N>(L, TB, SBM, DS, CPM, W);
     rst = false;
     double T[N][N];
+    park(R);
     plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^
+    unpark(R);
     double rv = 0.0;
 #pragma unroll
-    for (int j = 0; j < N; ++j)
+    for (int j = 0; j < N; ++j) {
+      if constexpr (TM) TmRow<N>::st(tv + 2 * N * j, T[j]);
 #pragma unroll
       for (int i = 0; i < N; ++i)
         if (L.active) {
-          vs[j * N + i] = T[j][i];
+          if constexpr (!TM) vs[j * N + i] = T[j][i];
           rv = fma(rh[j * N + i], T[j][i], rv);
         }
+    }
     rv = cell_sum<N>(rv, L.lane);
     alpha = 0.0;
     if (!conv) {
@@ -1693,11 +1812,22 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     }
     // x += alpha p^;  s = r - alpha v (in R);  W = M^-1 s
     double ss = 0.0;
+    if constexpr (TM) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double xr[N];
+        TmRow<N>::ld(tx + 2 * N * j, xr);
+#pragma unroll
+        for (int i = 0; i < N; ++i) xr[i] = fma(alpha, W[j][i], xr[i]);
+        TmRow<N>::st(tx + 2 * N * j, xr);
+      }
+      tm_wait_st();
+    }
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        if (L.active) xs[j * N + i] = fma(alpha, W[j][i], xs[j * N + i]);
+        if (!TM && L.active) xs[j * N + i] = fma(alpha, W[j][i], xs[j * N + i]);
         R[j][i] = fma(-alpha, T[j][i], R[j][i]);
         ss = fma(R[j][i], R[j][i], ss);
         W[j][i] = L.active ? (THOMAS ? R[j][i] : R[j][i] * ds[j * N + i]) : 0.0;
@@ -1708,7 +1838,9 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       conv = true;
       ++its;
     }
+    park(R);
     plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // t = D_T s^
+    unpark(R);
     double ts = 0.0, tt = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
@@ -1721,11 +1853,22 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     tt = cell_sum<N>(tt, L.lane);
     const double om = (!conv && tt > 0.0) ? ts / tt : 0.0;
     double r2n = 0.0;
+    if constexpr (TM) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double xr[N];
+        TmRow<N>::ld(tx + 2 * N * j, xr);
+#pragma unroll
+        for (int i = 0; i < N; ++i) xr[i] = fma(om, W[j][i], xr[i]);
+        TmRow<N>::st(tx + 2 * N * j, xr);
+      }
+      tm_wait_st();
+    }
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
       for (int i = 0; i < N; ++i) {
-        if (L.active) xs[j * N + i] = fma(om, W[j][i], xs[j * N + i]);
+        if (!TM && L.active) xs[j * N + i] = fma(om, W[j][i], xs[j * N + i]);
         R[j][i] = fma(-om, T[j][i], R[j][i]);
         r2n = fma(R[j][i], R[j][i], r2n);
       }
@@ -1747,6 +1890,18 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     else stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
   }
   __syncthreads();
+  if constexpr (TM) {
+    double* bb = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double xr[N];
+      TmRow<N>::ld(tx + 2 * N * j, xr);
+      if (L.active)
+#pragma unroll
+        for (int i = 0; i < N; ++i) bb[j * N + i] = SWEEP ? fma(kp.omega, xr[i], bb[j * N + i]) : xr[i];
+    }
+    tm_free<128>(tm_slot);   // includes the barrier below
+  } else {
   if (L.active) {
     double* bb = TB + L.cs * G::CTB + L.t * G::KS;
 #pragma unroll
@@ -1756,9 +1911,14 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
         bb[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], bb[j * N + i]) : xs[j * N + i];
   }
   __syncthreads();
+  }
   if (CMAP) unstage_tile_map<N>(TB, out, cl);
   else unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
   if (valid && L.t == 0) kp.its[CMAP ? cl.cell[L.cs] : cell0 + L.cs] = conv ? its : (its | (1 << 30));
+#undef tx
+#undef tp
+#undef tv
+#undef tr
 }
 
 template <int N> constexpr size_t smem_apply(bool nbr, bool faces) {
