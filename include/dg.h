@@ -49,8 +49,12 @@ typedef enum {
 enum { DG_BC_DIRICHLET = 0, DG_BC_NEUMANN = 1 };
 /* local Krylov method; DG_LOCAL_BICGSTAB_THOMAS: BiCGStab right-preconditioned by the tridiagonal
  * part of D_T in DoF order (Thomas algorithm), for strongly convection-dominated
- * blocks where the diagonal fails; p <= 4 */
-enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2, DG_LOCAL_BICGSTAB_THOMAS = 3 };
+ * blocks where the diagonal fails; p <= 4. DG_LOCAL_GMRES / DG_LOCAL_GMRES_THOMAS:
+ * restarted GMRES(k) (the paper's local method for the convection test; k = 15 at
+ * p = 1 and 3, 13 at p = 2) with the diagonal or the tridiagonal right preconditioner; p <= 3
+ * (Krylov basis in tensor memory). dg_get_stats counts Arnoldi steps for GMRES. */
+enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2, DG_LOCAL_BICGSTAB_THOMAS = 3,
+       DG_LOCAL_GMRES = 4, DG_LOCAL_GMRES_THOMAS = 5 };
 enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
 
 typedef struct {

@@ -389,6 +389,9 @@ dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it) {
   } else if (method == DG_LOCAL_BICGSTAB_THOMAS) {
     if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "the tridiagonal preconditioner needs p <= 4 (plane kernels)");
     c->method = dg::LM_BICGSTAB_THOMAS;
+  } else if (method == DG_LOCAL_GMRES || method == DG_LOCAL_GMRES_THOMAS) {
+    if (c->desc.p > 3) return fail(DG_ERR_UNSUPPORTED, "local GMRES needs p <= 3 (Krylov basis in tensor memory)");
+    c->method = method == DG_LOCAL_GMRES ? dg::LM_GMRES : dg::LM_GMRES_THOMAS;
   } else {
     return fail(DG_ERR_INVALID, "unknown local method");
   }
@@ -488,7 +491,8 @@ dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega
   // p <= 3 (plane solvers with cp.async staging) and nx even: the launch enumerates the cells of
   // one colour only and updates them in place (their neighbours are of the other colour and are
   // not written); otherwise every cell is launched and the other colour passes through
-  const bool compact = c->desc.p <= 3 && c->desc.nx % 2 == 0;
+  const bool compact = c->desc.p <= 3 && c->desc.nx % 2 == 0 && c->method != dg::LM_GMRES &&
+                       c->method != dg::LM_GMRES_THOMAS;
   c->launches = 0;
   for (int h = 0; h < halves; ++h) {
     dg_status st = halo_exchange(c, u, s);

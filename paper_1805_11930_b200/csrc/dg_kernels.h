@@ -58,7 +58,7 @@ __host__ __device__ inline int group_cell(const KParams& kp, int g0, int cs) {
 }
 __host__ __device__ inline int group_items(const KParams& kp) { return kp.cmap ? kp.ncells / 2 : kp.ncells; }
 
-enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3 };
+enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3, LM_GMRES = 4, LM_GMRES_THOMAS = 5 };
 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
 

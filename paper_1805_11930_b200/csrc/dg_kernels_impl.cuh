@@ -1166,6 +1166,17 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
       if constexpr (N <= 4) {
+        // restarted GMRES(KR), Krylov basis + diagonal in TMEM (compact colour maps not
+        // supported: the SOR half-sweeps run masked). KR fills 256 TMEM columns at n = 2, 3
+        // (two CTAs per SM) and all 512 at n = 4 (one CTA per SM: GMRES(7) with two CTAs was
+        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_session2_ab.md)
+        constexpr int KR = N == 4 ? 15 : N == 3 ? 13 : 15;
+        if (method == LM_GMRES)
+          return launch(pk::k_gmres<N, SWEEP, false, KR>, grid, G::NT, pk::smem_gmres<N, KR>(false), s, kp, in, f, out);
+        if (method == LM_GMRES_THOMAS)
+          return launch(pk::k_gmres<N, SWEEP, true, KR>, grid, G::NT, pk::smem_gmres<N, KR>(true), s, kp, in, f, out);
+      }
+      if constexpr (N <= 4) {
         if (method == LM_BICGSTAB) {
           if constexpr (N == 4)
             if (use_tmem())

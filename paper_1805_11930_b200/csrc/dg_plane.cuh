@@ -1546,7 +1546,7 @@ __device__ void thomas_apply(const Lane& L, double* TB, const double* SB, const 
 // two CTAs (8 warps) share an SM instead of one. Warp w of the CTA owns TMEM lanes 32w..32w+31
 // (the tcgen05.ld/st lane-quadrant rule), so the CTA must have at most 4 warps.
 template <int NCOL> __device__ __forceinline__ uint32_t tm_alloc(uint32_t* slot) {
-  static_assert(NCOL == 32 || NCOL == 64 || NCOL == 128 || NCOL == 256, "TMEM allocation: power of 2");
+  static_assert(NCOL == 32 || NCOL == 64 || NCOL == 128 || NCOL == 256 || NCOL == 512, "TMEM allocation: power of 2");
   if ((threadIdx.x >> 5) == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n"
                  ::"r"((unsigned)__cvta_generic_to_shared(slot)), "n"(NCOL));
@@ -1589,6 +1589,40 @@ template <> struct TmRow<4> {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n"
                  ::"r"(a), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
                    "r"(r[7]));
+  }
+};
+template <> struct TmRow<2> {
+  static __device__ __forceinline__ void ld(uint32_t a, double (&v)[2]) {
+    uint32_t r[4];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(a));
+#pragma unroll
+    for (int i = 0; i < 2; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const double (&v)[2]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};\n"
+                 ::"r"(a), "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])), "r"(__double2loint(v[1])),
+                   "r"(__double2hiint(v[1])));
+  }
+};
+template <> struct TmRow<3> {
+  static __device__ __forceinline__ void ld(uint32_t a, double (&v)[3]) {
+    uint32_t r[6];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%6];\n"
+                 "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%4,%5}, [%7];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5])
+                 : "r"(a), "r"(a + 4));
+#pragma unroll
+    for (int i = 0; i < 3; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const double (&v)[3]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%2,%3,%4,%5};\n"
+                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%1], {%6,%7};\n"
+                 ::"r"(a), "r"(a + 4), "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])),
+                   "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])),
+                   "r"(__double2hiint(v[2])));
   }
 };
 // stores of this thread are complete (before TMEM data is read back or freed)
@@ -1919,6 +1953,271 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
 #undef tp
 #undef tv
 #undef tr
+}
+
+
+// ---- restarted GMRES(KR) per cell (the paper's local GMRES with the
+// tridiagonal preconditioner for convection-dominated blocks) -------
+// Right preconditioning (M = diag(D_T), or its tridiagonal part in DoF order with THOMAS),
+// Arnoldi with modified Gram-Schmidt, Givens rotations on the Hessenberg columns, restart
+// after KR steps: x += M^-1 V y, r -= D_T M^-1 V y (one operator application per cycle).
+// The Krylov basis V (KR vectors) and, for Jacobi, M^-1 live in tensor memory: each lane owns
+// a TMEM lane and keeps its plane of every basis vector there (2N^2 columns per vector).
+// Per-cell scalars (the rotated Hessenberg columns R, g, the rotations) in shared memory,
+// written by the cell's lane 0. All lanes of a warp run the same number of steps (lock-step);
+// a cell that has converged inside a cycle freezes its column count jl.
+template <int N, int KR> struct Gm {
+  static constexpr int PSZ = 2 * N * N;                           // TMEM columns per vector
+  static constexpr int COLS = (KR + 1) * PSZ;                     // basis + M^-1
+  static constexpr int ALLOC = COLS <= 32 ? 32 : COLS <= 64 ? 64 : COLS <= 128 ? 128 : COLS <= 256 ? 256 : 512;
+  static_assert(COLS <= 512, "GMRES basis must fit the SM's 512 TMEM columns");
+  static constexpr int RT = KR * (KR + 1) / 2;                     // packed upper triangle
+  static constexpr int SCS = RT + (KR + 1) + 2 * KR + 1;           // per-cell scalar stride (odd)
+};
+template <int N, int KR> constexpr size_t smem_gmres(bool thomas) {
+  using G = Geo<N>;
+  constexpr int PLN = G::C * G::PS;
+  const int tail = (thomas ? 4 * PLN : PLN) + G::C * Gm<N, KR>::SCS;
+  return sizeof(double) * (size_t)(G::TB + G::FY + (tail > 2 * PLN ? tail : 2 * PLN));
+}
+
+template <int N, bool SWEEP, bool THOMAS, int KR>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
+        double* DG_RESTRICT out) {
+  using G = Geo<N>;
+  using M = Gm<N, KR>;
+  static_assert(G::WARPS <= 4, "one TMEM lane quadrant per warp");
+  constexpr int PLN = G::C * G::PS;
+  extern __shared__ double sm[];
+  __shared__ Cells<N> cl;
+  __shared__ uint32_t tm_slot;
+  double* TB = sm;
+  double* FY = TB + G::TB;
+  double* XS = FY + G::FY;           // FX / FZ (defect prologue only) alias XS and what follows
+  double* SBM = XS + PLN;            // THOMAS: sub-diagonal, 1 / pivot, super-diagonal / pivot
+  double* IPM = SBM + PLN;
+  double* CPM = IPM + PLN;
+  double* SC = THOMAS ? CPM + PLN : XS + PLN;
+  double* FX = XS;
+  double* FZ = XS + PLN;
+  const int cell0 = (kp.gperm ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
+  const int nvalid = min(G::C, kp.ncells - cell0);
+  const Lane L = lane_id<N>();
+  const bool valid = L.active && L.cs < nvalid;
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  solver_setup<N, SWEEP, false>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+  double R[N][N], W[N][N], T[N][N];
+  read_plane<N>(TB, L, W);
+  if (SWEEP) {
+    nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
+    __syncthreads();
+    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    __syncthreads();
+    read_plane<N>(TB, L, R);
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? R[j][i] - T[j][i] : 0.0;
+  } else {
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) R[j][i] = valid ? W[j][i] : 0.0;
+  }
+  const int po = L.cs * G::PS + L.t * G::QS;
+  double* xs = XS + po;
+  double* sc = SC + L.cs * M::SCS;    // [0, RT) R packed by columns, then g[KR+1], c[KR], s[KR]
+  double* gv = sc + M::RT;
+  double* cv = gv + KR + 1;
+  double* sv = cv + KR;
+  // the prologue's FX / FZ are consumed (barrier inside the TMEM allocation)
+  tm_alloc<M::ALLOC>(&tm_slot);
+#define tq (*(volatile uint32_t*)&tm_slot + ((uint32_t)((threadIdx.x >> 5) * 32) << 16))
+  // M^-1: Jacobi in TMEM (vector slot KR), or the Thomas factors in shared memory
+  if constexpr (THOMAS) {
+    thomas_factor<N>(kp, cl, L, SBM, IPM, CPM, valid);
+  } else {
+    double dg[N][N];
+    plane_inv_diag<N>(kp, cl, L, rw, dg);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) dg[j][i] = valid ? dg[j][i] : 1.0;
+      TmRow<N>::st(tq + KR * M::PSZ + 2 * N * j, dg[j]);
+    }
+  }
+  double rr = 0.0;
+#pragma unroll
+  for (int j = 0; j < N; ++j)
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      rr = fma(R[j][i], R[j][i], rr);
+      if (L.active) xs[j * N + i] = 0.0;
+    }
+  const double rr0 = cell_sum<N>(rr, L.lane);
+  bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
+  const double lim = kp.tol2 * rr0;
+  int its = 0;     // Arnoldi steps of this cell
+  int steps = 0;   // Arnoldi steps of the warp (warp-uniform: the cap must not split the warp)
+  // M^-1 applied to W in place
+  auto precond = [&]() {
+    if constexpr (THOMAS) {
+      thomas_apply<N>(L, TB, SBM, IPM, CPM, W);
+    } else {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double d[N];
+        TmRow<N>::ld(tq + KR * M::PSZ + 2 * N * j, d);
+#pragma unroll
+        for (int i = 0; i < N; ++i) W[j][i] = L.active ? W[j][i] * d[i] : 0.0;
+      }
+    }
+  };
+  for (int cycle = 0;; ++cycle) {
+    double b2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i) b2 = fma(R[j][i], R[j][i], b2);
+    b2 = cell_sum<N>(b2, L.lane);
+    if (!conv && b2 <= lim) conv = true;
+    if (__all_sync(0xffffffffu, conv || !L.active) || steps >= kp.max_it) break;
+    // v_0 = r / |r|
+    const double beta = sqrt(b2);
+    const double ib = conv ? 0.0 : 1.0 / beta;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double v[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) v[i] = R[j][i] * ib;
+      TmRow<N>::st(tq + 2 * N * j, v);
+    }
+    tm_wait_st();
+    if (L.active && L.t == 0) gv[0] = beta;
+    bool live = !conv;
+    int jl = -1;
+    for (int j = 0; j < KR; ++j) {
+      if (__all_sync(0xffffffffu, !live || !L.active) || steps >= kp.max_it) break;
+      ++steps;
+      // W = M^-1 v_j;  T = D_T W
+#pragma unroll
+      for (int r = 0; r < N; ++r) TmRow<N>::ld(tq + j * M::PSZ + 2 * N * r, W[r]);
+      precond();
+      plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
+      // modified Gram-Schmidt against v_0 .. v_j; h_i -> column j of R (lane 0)
+      for (int i = 0; i <= j; ++i) {
+        double V[N][N], h = 0.0;
+#pragma unroll
+        for (int r = 0; r < N; ++r) TmRow<N>::ld(tq + i * M::PSZ + 2 * N * r, V[r]);
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q < N; ++q) h = fma(T[r][q], V[r][q], h);
+        h = cell_sum<N>(h, L.lane);
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q < N; ++q) T[r][q] = fma(-h, V[r][q], T[r][q]);
+        if (live && L.active && L.t == 0) sc[j * (j + 1) / 2 + i] = h;
+      }
+      double hn = 0.0;
+#pragma unroll
+      for (int r = 0; r < N; ++r)
+#pragma unroll
+        for (int q = 0; q < N; ++q) hn = fma(T[r][q], T[r][q], hn);
+      hn = sqrt(cell_sum<N>(hn, L.lane));
+      if (j + 1 < KR) {
+        const double ih = (live && hn > 0.0) ? 1.0 / hn : 0.0;
+#pragma unroll
+        for (int r = 0; r < N; ++r) {
+          double v[N];
+#pragma unroll
+          for (int q = 0; q < N; ++q) v[q] = T[r][q] * ih;
+          TmRow<N>::st(tq + (j + 1) * M::PSZ + 2 * N * r, v);
+        }
+        tm_wait_st();
+      }
+      // Givens: previous rotations on column j, then the new one zeroing hn (lane 0 of the cell)
+      if (live && L.active && L.t == 0) {
+        double* col = sc + j * (j + 1) / 2;
+        for (int i = 0; i < j; ++i) {
+          const double a = col[i], b = col[i + 1];
+          col[i] = cv[i] * a + sv[i] * b;
+          col[i + 1] = -sv[i] * a + cv[i] * b;
+        }
+        const double a = col[j];
+        const double rn = sqrt(a * a + hn * hn);
+        const double c = rn > 0.0 ? a / rn : 1.0, s_ = rn > 0.0 ? hn / rn : 0.0;
+        col[j] = rn;
+        cv[j] = c;
+        sv[j] = s_;
+        const double g = gv[j];
+        gv[j] = c * g;
+        gv[j + 1] = -s_ * g;
+      }
+      __syncwarp();
+      if (live) {
+        jl = j;
+        ++its;
+        const double gn = gv[j + 1];
+        if (gn * gn <= lim || hn == 0.0) live = false;
+      }
+    }
+    // y = R^-1 g (lane 0, into g), then W = V y, W = M^-1 W, x += W, R -= D_T W
+    if (L.active && L.t == 0)
+      for (int i = jl; i >= 0; --i) {
+        double y = gv[i];
+        for (int k = i + 1; k <= jl; ++k) y = fma(-sc[k * (k + 1) / 2 + i], gv[k], y);
+        gv[i] = y / sc[i * (i + 1) / 2 + i];
+      }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int q = 0; q < N; ++q) W[r][q] = 0.0;
+    const int jw = __reduce_max_sync(0xffffffffu, L.active ? jl : -1);
+    for (int i = 0; i <= jw; ++i) {
+      double V[N][N];
+#pragma unroll
+      for (int r = 0; r < N; ++r) TmRow<N>::ld(tq + i * M::PSZ + 2 * N * r, V[r]);
+      if (i <= jl) {
+        const double y = gv[i];
+#pragma unroll
+        for (int r = 0; r < N; ++r)
+#pragma unroll
+          for (int q = 0; q < N; ++q) W[r][q] = fma(y, V[r][q], W[r][q]);
+      }
+    }
+    precond();
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+        if (L.active) xs[r * N + q] += W[r][q];
+    plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
+#pragma unroll
+    for (int r = 0; r < N; ++r)
+#pragma unroll
+      for (int q = 0; q < N; ++q) R[r][q] -= T[r][q];
+  }
+  tm_free<M::ALLOC>(tm_slot);
+#undef tq
+  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  __syncthreads();
+  if (L.active) {
+    double* bb = TB + L.cs * G::CTB + L.t * G::KS;
+#pragma unroll
+    for (int j = 0; j < N; ++j)
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        bb[j * N + i] = SWEEP ? fma(kp.omega, xs[j * N + i], bb[j * N + i]) : xs[j * N + i];
+  }
+  __syncthreads();
+  unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+  if (valid && L.t == 0) kp.its[cell0 + L.cs] = conv ? its : (its | (1 << 30));
 }
 
 template <int N> constexpr size_t smem_apply(bool nbr, bool faces) {

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("DG_LIB") or os.path.join(HERE, "libdg_b200.so")
 
 DG_OK, DG_ERR_INVALID, DG_ERR_NOMEM, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_STATE, DG_ERR_UNSUPPORTED = range(7)
 DG_LOCAL_AUTO, DG_LOCAL_CG, DG_LOCAL_BICGSTAB, DG_LOCAL_BICGSTAB_THOMAS = 0, 1, 2, 3
+DG_LOCAL_GMRES, DG_LOCAL_GMRES_THOMAS = 4, 5
 DG_HALO_NCCL, DG_HALO_EXTERNAL = 0, 1
 MASK_VOLUME, MASK_INTERIOR_FACES, MASK_BOUNDARY_FACES = 1, 2, 4
 
