@@ -1385,6 +1385,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       else conv = true;
     }
     double r2 = 0.0, rzn = 0.0;
+    double Z[N][N];   // M^-1 r, formed once (reused by the direction update)
 #pragma unroll
     for (int j = 0; j < N; ++j)
 #pragma unroll
@@ -1392,7 +1393,8 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
         if (L.active) xs[j * N + i] = fma(alpha, P[j][i], xs[j * N + i]);
         R[j][i] = fma(-alpha, Q[j][i], R[j][i]);
         r2 = fma(R[j][i], R[j][i], r2);
-        if (L.active) rzn = fma(R[j][i], R[j][i] * ds[j * N + i], rzn);
+        Z[j][i] = L.active ? R[j][i] * ds[j * N + i] : 0.0;
+        rzn = fma(R[j][i], Z[j][i], rzn);
       }
     r2 = cell_sum<N>(r2, L.lane);
     rzn = cell_sum<N>(rzn, L.lane);
@@ -1405,7 +1407,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
 #pragma unroll
         for (int j = 0; j < N; ++j)
 #pragma unroll
-          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], R[j][i] * ds[j * N + i]);
+          for (int i = 0; i < N; ++i) P[j][i] = fma(beta, P[j][i], Z[j][i]);
       }
     }
   }
