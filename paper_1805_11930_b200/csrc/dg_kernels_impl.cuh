@@ -74,6 +74,9 @@ template <int N_> struct Geo {
   static constexpr int YS = Lay<N>::YS, ZS = Lay<N>::ZS, CS = Lay<N>::CS;
   static constexpr int LINES = C * N2;
   static constexpr int NT = ((LINES + 31) / 32) * 32;
+  // one warp per cell (n = 5: 25 of 32 lanes hold a line): the thread count of k_cg_w, whose
+  // iterations then need no CTA barrier. The CTA-wide helpers use the first NT threads only.
+  static constexpr int NTW = C * 32;
   static constexpr int TENSOR = C * CS;
   static constexpr int FACE = C * 12 * N2;
 };
@@ -164,7 +167,7 @@ template <int N> __device__ __forceinline__ void bterm(const double* B, const do
 // derivative-test fluxes into the weighted Gauss residual). Needs g.fc; ends with a barrier.
 template <int N> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
   using G = Geo<N>;
-  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += G::NT) {
+  for (int it = threadIdx.x; threadIdx.x < G::NT && it < G::C * 3 * N * N; it += G::NT) {
     const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
     const int q = (rem % (N * N)) / N, r = rem % N;
     const double* lo = g.fc[cs][2 * a];
@@ -286,7 +289,7 @@ __device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncel
   using G = Geo<N>;
   const int nvalid = min(G::C, ncells - cell0);
   const double* s = src + (size_t)cell0 * G::N3;
-  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+  for (int e = threadIdx.x; threadIdx.x < G::NT && e < G::C * G::N3; e += G::NT) {
     const int cs = e / G::N3, r = e % G::N3;
     const int i = r % N, j = (r / N) % N, k = r / G::N2;
     dst[cs * G::CS + k * G::ZS + j * G::YS + i] = (cs < nvalid) ? s[e] : 0.0;
@@ -351,20 +354,27 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
 // FACES = false: the volume terms alone (the face passes are skipped); USEB (with FACES = false):
 // plus the self-face terms through g.Bf inside the Gauss-point passes (D_T without face passes)
-template <int N, bool FACES = true, bool USEB = false, class Out>
+template <int N, bool FACES = true, bool USEB = false, bool WARP = false, bool WIDE = false, class Out>
 __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
                                               const double* src, double* SA, double* SB,
                                               double* FB, bool vol, Out out) {
   using G = Geo<N>;
   constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = G::NT;
   const int tid = threadIdx.x;
+  static_assert(!WARP || (!FACES && N2 <= 32), "warp mode: one cell per warp, no face passes");
+  // WARP: the calling warp applies the operator to its own cell (cs = warp) alone, one line per
+  // lane, __syncwarp between the passes; otherwise the whole CTA over all lines of the group
+  const int lb = WARP ? (tid >> 5) * N2 + (tid & 31) : tid;
+  // WIDE: launched with more than NT threads (k_cg_w's defect); the ones past NT idle
+  const int le = WARP ? ((tid >> 5) + 1) * N2 : ((!WIDE || tid < NT) ? LINES : 0);
+  constexpr int ls = WARP ? 32 : NT;
   const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
   const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
   const double sb[3] = {T3 * kp.b[0] * inv_h[0], T3 * kp.b[1] * inv_h[1], T3 * kp.b[2] * inv_h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
 
   // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
-  for (int it = tid; FACES && it < 3 * LINES; it += NT) {
+  for (int it = tid; FACES && (!WIDE || tid < NT) && it < 3 * LINES; it += NT) {
     const int ax = it / LINES, r = it % LINES, cs = r / N2, l = r % N2;
     const int a = l % N, b = l / N;
     if (ax == 0) face_line<N, 0>(g, src, FB, cs, a, b, inv_h[0]);
@@ -372,7 +382,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
     else face_line<N, 2>(g, src, FB, cs, a, b, inv_h[2]);
   }
   if (vol) {
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
       const int off = cs * G::CS + b * G::ZS + a * G::YS;
       double v[N], o[N];
@@ -381,9 +391,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       st<N, 1>(SA + off, o);
     }
   }
-  __syncthreads();
+  if constexpr (WARP) __syncwarp(); else __syncthreads();
   // pass 2: F2 (tangential mass along t1) + P2 (y-lines: SB = A_y SA)
-  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && (!WIDE || tid < NT) && it < C * 12 * N; it += NT) {
     const int t2 = it % N, rest = it / N;
     double* fa = FB + rest * N2 + N * t2;
     double v[N], o[N];
@@ -392,7 +402,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
     st<N, 1>(fa, o);
   }
   if (vol) {
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
       const int off = cs * G::CS + b * G::ZS + a;
       double v[N], o[N];
@@ -401,10 +411,10 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       st<N, G::YS>(SB + off, o);
     }
   }
-  __syncthreads();
+  if constexpr (WARP) __syncwarp(); else __syncthreads();
   // pass 3: F3 (tangential mass along t2, area scaling) + P3 (z-lines: U = A_z SB -> SA,
   //         R = reaction + z-term -> SB)
-  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && (!WIDE || tid < NT) && it < C * 12 * N; it += NT) {
     const int t1 = it % N, rest = it / N;
     const int ax = (rest >> 2) % 3;
     double* fa = FB + rest * N2 + t1;
@@ -416,7 +426,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
     st<N, N>(fa, o);
   }
   if (vol) {
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qx, b = qy
       const int off = cs * G::CS + b * G::YS + a;
       double t[N], U[N], R[N];
@@ -431,9 +441,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       st<N, G::ZS>(SA + off, U);
       st<N, G::ZS>(SB + off, R);
     }
-    __syncthreads();
+    if constexpr (WARP) __syncwarp(); else __syncthreads();
     // pass 4: x-lines, R += x-term
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qy, b = qz
       const int off = cs * G::CS + b * G::ZS + a * G::YS;
       double U[N], R[N];
@@ -443,9 +453,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       if constexpr (USEB) bterm<N>(g.Bf[cs][0], U, R, g.tw[a] * g.tw[b]);
       st<N, 1>(SB + off, R);
     }
-    __syncthreads();
+    if constexpr (WARP) __syncwarp(); else __syncthreads();
     // pass 5: y-lines, R += y-term, then A_y^T
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;  // a = qx, b = qz
       const int off = cs * G::CS + b * G::ZS + a;
       double U[N], R[N], o[N];
@@ -456,9 +466,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       mtv<N, 0>(R, o);
       st<N, G::YS>(SB + off, o);
     }
-    __syncthreads();
+    if constexpr (WARP) __syncwarp(); else __syncthreads();
     // pass 6: z-lines, A_z^T
-    for (int it = tid; it < LINES; it += NT) {
+    for (int it = lb; it < le; it += ls) {
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
       const int off = cs * G::CS + b * G::YS + a;
       double v[N], o[N];
@@ -467,9 +477,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       st<N, G::ZS>(SB + off, o);
     }
   }
-  __syncthreads();
+  if constexpr (WARP) __syncwarp(); else __syncthreads();
   // pass 7: x-lines, A_x^T + scatter of all face terms
-  for (int it = tid; it < LINES; it += NT) {
+  for (int it = lb; it < le; it += ls) {
     const int cs = it / N2, l = it % N2, j = l % N, k = l / N;
     double v[N];
     if (vol) {
@@ -525,7 +535,7 @@ __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
   const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
   const double sb[3] = {T3 * kp.b[0] / kp.h[0], T3 * kp.b[1] / kp.h[1], T3 * kp.b[2] / kp.h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
-  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+  for (int e = threadIdx.x; threadIdx.x < G::NT && e < G::C * G::N3; e += G::NT) {
     const int cs = e / G::N3, r = e % G::N3;
     const int idx[3] = {r % N, (r / N) % N, r / G::N2};
     double Md[3], Sd[3], Cd[3];
@@ -757,6 +767,141 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     }
   })
   if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] ? g.its[tid] : (g.its[tid] | (1 << 30));
+}
+
+// Jacobi-preconditioned CG with one warp per cell (n = 5: 25 lanes hold the cell's lines).
+// The group setup and the defect are CTA-wide; the iterations are warp-local (the operator in
+// WARP mode, shuffle reductions, per-lane copies of the cell's scalars), so no CTA barrier is
+// left in the loop and each warp leaves it when its own cell has converged.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NTW, 2)
+k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+       double* __restrict__ out) {
+  using G = Geo<N>;
+  constexpr int C = G::C;
+  static_assert(G::N2 <= 32, "one warp per cell");
+  extern __shared__ double sm[];
+  __shared__ Group<N> g;
+  double* X = sm;
+  double* R = X + G::TENSOR;
+  double* P = R + G::TENSOR;
+  double* Q = P + G::TENSOR;
+  double* Dg = Q + G::TENSOR;
+  double* SA = Dg + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(C, kp.ncells - cell0);
+  const int tid = threadIdx.x;
+  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  KParams kq = kp;
+  kq.mask = 7u;
+  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N>(kq, g);
+  if (SWEEP) {  // d = f - A u  (Alg. 2 line 2), CTA-wide
+    const double* fb = f + (size_t)cell0 * G::N3;
+    cell_operator<N, true, false, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      double fl[N] = {};
+      if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
+      double r[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
+      st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
+    });
+    __syncthreads();
+    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+  }
+  diag_setup<N>(kp, g, Dg);
+  __syncthreads();
+  // from here on: warp w owns cell slot cs = w, lane l < n^2 its x-line l
+  const int cs = tid >> 5, lane = tid & 31;
+  const bool act = lane < G::N2;
+  const int off = cs * G::CS + (lane / N) * G::ZS + (lane % N) * G::YS;
+  double rr = 0.0, rz = 0.0;
+  if (act) {
+    double r[N], dg[N], z[N], zero[N] = {};
+    ld<N, 1>(R + off, r);
+    ld<N, 1>(Dg + off, dg);
+#pragma unroll
+    for (int e = 0; e < N; ++e) { z[e] = r[e] * dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
+    st<N, 1>(P + off, z);
+    st<N, 1>(X + off, zero);
+  }
+  const double rr0 = warp_sum(rr);
+  rz = warp_sum(rz);
+  bool conv = cs >= nvalid || rr0 == 0.0 || skip_cell(kp, cell0 + cs);
+  int its = 0;
+  for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
+    __syncwarp();
+    cell_operator<N, false, true, true>(kq, g, P, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+      st<N, 1>(Q + c * G::CS + k * G::ZS + j * G::YS, v);
+    });
+    __syncwarp();
+    double pq = 0.0;
+    double x[N], r[N], p[N], q[N], dg[N];
+    if (act) {
+      ld<N, 1>(P + off, p);
+      ld<N, 1>(Q + off, q);
+#pragma unroll
+      for (int e = 0; e < N; ++e) pq = fma(p[e], q[e], pq);
+    }
+    pq = warp_sum(pq);
+    if (!(pq > 0.0)) {   // breakdown (p = 0): keep the last iterate
+      conv = true;
+      break;
+    }
+    const double alpha = rz / pq;
+    double r2 = 0.0, rzn = 0.0;
+    if (act) {
+      ld<N, 1>(X + off, x);
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(Dg + off, dg);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        x[e] = fma(alpha, p[e], x[e]);
+        r[e] = fma(-alpha, q[e], r[e]);
+        r2 = fma(r[e], r[e], r2);
+        dg[e] *= r[e];   // z = M^-1 r
+        rzn = fma(r[e], dg[e], rzn);
+      }
+      st<N, 1>(X + off, x);
+      st<N, 1>(R + off, r);
+    }
+    r2 = warp_sum(r2);
+    rzn = warp_sum(rzn);
+    ++its;
+    if (r2 <= kp.tol2 * rr0) {
+      conv = true;
+      break;
+    }
+    const double beta = rzn / rz;
+    rz = rzn;
+    if (act) {
+#pragma unroll
+      for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], dg[e]);
+      st<N, 1>(P + off, p);
+    }
+  }
+  __syncwarp();
+  // write result (u + omega du for a sweep, du for a solve), warp by warp
+  if (act && cs < nvalid) {
+    const int j = lane % N, k = lane / N;
+    double x[N];
+    ld<N, 1>(X + off, x);
+    if (SWEEP) {
+      double uu[N];
+      ld<N, 1>(in + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, uu);
+#pragma unroll
+      for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+    }
+    st<N, 1>(out + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, x);
+  }
+  if (lane == 0 && cs < nvalid) kp.its[cell0 + cs] = conv ? its : (its | (1 << 30));
 }
 
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks, b != 0).
@@ -1196,6 +1341,12 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if (method == LM_BICGSTAB)
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
+  if constexpr (N == 5) {
+    static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
+    if (!cta)
+      return launch(k_cg_w<N, SWEEP>, grid, G::NTW,
+                    fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);
+  }
   return launch(k_cg<N, SWEEP>, grid, G::NT,
                 fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);
 }
