@@ -152,7 +152,8 @@ def cpu_oracle_sample(P, u, f, seconds: float, kind: str):
 def extras_single_gpu(dev, peak_derived):
     """Context for the judge, outside the timed step (N = 1 only): the volume kernel alone on
     the larger p >= 3 configs (north_star's >= 50 % target is stated for the volume kernel at
-    p >= 3; C2 is small and tail-bound), and the SURVEY 8(f) NEXT rows on the bench workload:
+    p >= 3; C2 is small and tail-bound), dg_apply and a block-Jacobi sweep on C3, C4 and C5
+    (BASELINE configs[2:]), and the SURVEY 8(f) NEXT rows on the bench workload:
     the stored-inverse block-Jacobi sweep (NEXT-4), a red-black block SSOR sweep (NEXT-2) and the
     hybrid-multigrid-preconditioned solve (NEXT-1)."""
     import torch
@@ -171,20 +172,38 @@ def extras_single_gpu(dev, peak_derived):
         torch.cuda.synchronize()
         return a.elapsed_time(b) * 1e-3 / calls
 
-    out = {"volume_kernel_p_ge_3": {}}
-    for name in ("C4", "C3"):
+    out = {"volume_kernel_p_ge_3": {}, "other_configs": {}}
+    for name in ("C4", "C3", "C5"):
         P = make_config(name)
-        u, _ = make_vectors(P)
+        u, f = make_vectors(P)
         ctx = dg.DGContext(P, device=dev.index or 0)
-        ut = torch.from_numpy(u).to(dev)
+        ut, ft = torch.from_numpy(u).to(dev), torch.from_numpy(f).to(dev)
         o = torch.empty_like(ut)
-        t = timed(lambda: ctx.apply_parts(ut, o, dg.MASK_VOLUME), 20)
         n = P.p + 1
-        fl = P.n_cells * (24 * n ** 4 + 8 * n ** 3)
-        out["volume_kernel_p_ge_3"][name] = {"p": P.p, "n_dof": P.n_dof, "us_per_call": t * 1e6,
-                                             "frac_fp64_peak": fl / t / 1e12 / peak_derived}
+        vol = 24 * n ** 4 + 8 * n ** 3
+        if name != "C5":
+            t = timed(lambda: ctx.apply_parts(ut, o, dg.MASK_VOLUME), 20)
+            out["volume_kernel_p_ge_3"][name] = {"p": P.p, "n_dof": P.n_dof, "us_per_call": t * 1e6,
+                                                 "frac_fp64_peak": P.n_cells * vol / t / 1e12 / peak_derived}
+        # dg_apply and one block-Jacobi sweep of the config (SURVEY 8(d) flop model; a
+        # BiCGStab iteration counts two D_T applications)
+        sf, nf = 8 * n ** 3 + 12 * n ** 2, 10 * n ** 3
+        t_a = timed(lambda: ctx.apply(ut, o), 10)
+        w = ut.clone()
+        t_s = timed(lambda: ctx.sweep(w, ft, 1.0, 1e-12), 3)
+        st = ctx.stats()
+        cg = P.local_solver == "cg"
+        per_it = (vol + 6 * sf + (12 if cg else 20) * n ** 3) * (1 if cg else 2)
+        fl_s = P.n_cells * (vol + 6 * sf + 6 * nf + 4 * n ** 3) + st["it_sum"] * per_it
+        out["other_configs"][name] = {
+            "p": P.p, "n_dof": P.n_dof, "local_solver": P.local_solver,
+            "apply_us": t_a * 1e6, "apply_gdof_s": P.n_dof / t_a / 1e9,
+            "apply_frac_fp64_peak": P.n_cells * (vol + 6 * sf + 6 * nf) / t_a / 1e12 / peak_derived,
+            "sweep_us": t_s * 1e6, "sweep_gdof_s": P.n_dof / t_s / 1e9,
+            "sweep_frac_fp64_peak": fl_s / t_s / 1e12 / peak_derived,
+            "local_iterations_mean": st["it_mean"], "local_nonconverged": st["n_nonconverged"]}
         ctx.close()
-        del ut, o
+        del ut, ft, o, w
     P = make_config("C2")
     u, f = make_vectors(P)
     ctx = dg.DGContext(P, device=dev.index or 0)
