@@ -268,3 +268,41 @@ def test_partition_invariance_external_halo(G):
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("p,method,b", [(3, dg.DG_LOCAL_BICGSTAB, (0.7, -0.4, 0.3)),
+                                        (3, dg.DG_LOCAL_GMRES_THOMAS, (0.7, -0.4, 0.3)),
+                                        (2, dg.DG_LOCAL_GMRES, (0.5, 0.2, -0.6)),
+                                        (4, dg.DG_LOCAL_CG, (0.0, 0.0, 0.0))],
+                         ids=["p3-bicgstab-tmem", "p3-gmres-thomas", "p2-gmres", "p4-cg-warp-per-cell"])
+def test_partition_invariance_local_methods(p, method, b):
+    """The same bit-for-bit z-slab invariance for the sweeps whose local solvers keep state in
+    tensor memory (BiCGStab at n = 4, GMRES) or run one warp per cell (CG at n = 5)."""
+    P = random_problem(5, 3, 6, p, seed=23 + p, spread=1.0, b=b)
+    u, f = vec(P, 29)
+    with dg.DGContext(P) as one:
+        one.set_local_solver(method, 1000)
+        ut = cuda(u)
+        one.sweep(ut, cuda(f), 0.9, 1e-12)
+        assert one.stats()["n_nonconverged"] == 0
+        ref_S = host(ut)
+    nd, nxy = P.nd, P.nx * P.ny
+    G = 2
+    ctxs = [dg.DGContext(P, rank=r, nranks=G, halo_mode=dg.DG_HALO_EXTERNAL) for r in range(G)]
+    try:
+        for c in ctxs:
+            c.set_local_solver(method, 1000)
+        parts_u = [cuda(u[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+        parts_f = [cuda(f[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+        for r, c in enumerate(ctxs):
+            lo = parts_u[r - 1][-nxy * nd:] if r > 0 else None
+            hi = parts_u[r + 1][:nxy * nd] if r < G - 1 else None
+            c.fill_ghosts(lo, hi)
+        torch.cuda.synchronize()
+        for r, c in enumerate(ctxs):
+            c.sweep(parts_u[r], parts_f[r], 0.9, 1e-12)
+        got = np.concatenate([host(x) for x in parts_u])
+        assert np.array_equal(got, ref_S)
+    finally:
+        for c in ctxs:
+            c.close()
