@@ -904,6 +904,198 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   if (lane == 0 && cs < nvalid) kp.its[cell0 + cs] = conv ? its : (its | (1 << 30));
 }
 
+// Jacobi right-preconditioned BiCGStab with one warp per cell (n = 5), the same scheme as k_cg_w:
+// CTA-wide setup and defect, warp-local iterations without CTA barriers.
+template <int N, bool SWEEP>
+__global__ void __launch_bounds__(Geo<N>::NTW, 2)
+k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
+             double* __restrict__ out) {
+  using G = Geo<N>;
+  constexpr int C = G::C;
+  static_assert(G::N2 <= 32, "one warp per cell");
+  extern __shared__ double sm[];
+  __shared__ Group<N> g;
+  double* X = sm;
+  double* R = X + G::TENSOR;
+  double* RH = R + G::TENSOR;
+  double* P = RH + G::TENSOR;
+  double* V = P + G::TENSOR;
+  double* PS = V + G::TENSOR;
+  double* T = PS + G::TENSOR;
+  double* Dg = T + G::TENSOR;
+  double* SA = Dg + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = fb_alias<N>() ? T : SB + G::TENSOR;
+  const int cell0 = blockIdx.x * G::C;
+  const int nvalid = min(C, kp.ncells - cell0);
+  const int tid = threadIdx.x;
+  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  KParams kq = kp;
+  kq.mask = 7u;
+  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N>(kq, g);
+  if (SWEEP) {
+    const double* fb = f + (size_t)cell0 * G::N3;
+    cell_operator<N, true, false, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      double fl[N] = {};
+      if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
+      double r[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
+      st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
+    });
+    __syncthreads();
+    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+  }
+  diag_setup<N>(kp, g, Dg);
+  __syncthreads();
+  const int cs = tid >> 5, lane = tid & 31;
+  const bool act = lane < G::N2;
+  const int off = cs * G::CS + (lane / N) * G::ZS + (lane % N) * G::YS;
+  auto op = [&](double* dst) {   // dst = D_T PS on this warp's cell
+    __syncwarp();
+    cell_operator<N, false, true, true>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+      st<N, 1>(dst + c * G::CS + k * G::ZS + j * G::YS, v);
+    });
+    __syncwarp();
+  };
+  double rr = 0.0;
+  if (act) {
+    double r[N], zero[N] = {};
+    ld<N, 1>(R + off, r);
+#pragma unroll
+    for (int e = 0; e < N; ++e) rr = fma(r[e], r[e], rr);
+    st<N, 1>(RH + off, r);
+    st<N, 1>(X + off, zero);
+    st<N, 1>(P + off, zero);
+    st<N, 1>(V + off, zero);
+  }
+  const double rr0 = warp_sum(rr);
+  bool conv = cs >= nvalid || rr0 == 0.0 || skip_cell(kp, cell0 + cs);
+  double rho = 1.0, alpha = 1.0, omega = 1.0;
+  bool rst = false;
+  int its = 0;
+  for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
+    double a = 0.0, b = 0.0;
+    if (act) {
+      double r[N], rh[N];
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(RH + off, rh);
+#pragma unroll
+      for (int e = 0; e < N; ++e) { a = fma(rh[e], r[e], a); b = fma(r[e], r[e], b); }
+    }
+    double rhon = warp_sum(a);
+    const double r2 = warp_sum(b);
+    if (fabs(rhon) <= 1e-24 * r2) rst = true;   // breakdown: restart with rh = r
+    if (rst) rhon = r2;
+    const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
+    // p = r + beta (p - omega v); ps = M^-1 p
+    if (act) {
+      double r[N], p[N], v[N], dg[N], ps[N];
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(P + off, p);
+      ld<N, 1>(V + off, v);
+      ld<N, 1>(Dg + off, dg);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        p[e] = rst ? r[e] : fma(beta, fma(-omega, v[e], p[e]), r[e]);
+        ps[e] = p[e] * dg[e];
+      }
+      if (rst) st<N, 1>(RH + off, r);
+      st<N, 1>(P + off, p);
+      st<N, 1>(PS + off, ps);
+    }
+    rst = false;
+    op(V);
+    double rvl = 0.0;
+    if (act) {
+      double rh[N], v[N];
+      ld<N, 1>(RH + off, rh);
+      ld<N, 1>(V + off, v);
+#pragma unroll
+      for (int e = 0; e < N; ++e) rvl = fma(rh[e], v[e], rvl);
+    }
+    const double rv = warp_sum(rvl);
+    alpha = 0.0;
+    if (rv != 0.0) alpha = rhon / rv;
+    else rst = true;
+    // x += alpha ps; s = r - alpha v (in R); ps <- M^-1 s
+    double ss = 0.0;
+    if (act) {
+      double x[N], r[N], v[N], ps[N], dg[N];
+      ld<N, 1>(X + off, x);
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(V + off, v);
+      ld<N, 1>(PS + off, ps);
+      ld<N, 1>(Dg + off, dg);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        x[e] = fma(alpha, ps[e], x[e]);
+        r[e] = fma(-alpha, v[e], r[e]);
+        ss = fma(r[e], r[e], ss);
+        ps[e] = r[e] * dg[e];
+      }
+      st<N, 1>(X + off, x);
+      st<N, 1>(R + off, r);
+      st<N, 1>(PS + off, ps);
+    }
+    ss = warp_sum(ss);
+    if (ss <= kp.tol2 * rr0) {
+      ++its;
+      conv = true;
+      break;
+    }
+    op(T);
+    double tsl = 0.0, ttl = 0.0;
+    if (act) {
+      double t[N], sv[N];
+      ld<N, 1>(T + off, t);
+      ld<N, 1>(R + off, sv);
+#pragma unroll
+      for (int e = 0; e < N; ++e) { tsl = fma(t[e], sv[e], tsl); ttl = fma(t[e], t[e], ttl); }
+    }
+    const double ts = warp_sum(tsl), tt = warp_sum(ttl);
+    const double om = tt > 0.0 ? ts / tt : 0.0;
+    if (om == 0.0) rst = true;
+    // x += omega s^; r = s - omega t
+    double r2n = 0.0;
+    if (act) {
+      double x[N], r[N], t[N], ps[N];
+      ld<N, 1>(X + off, x);
+      ld<N, 1>(R + off, r);
+      ld<N, 1>(T + off, t);
+      ld<N, 1>(PS + off, ps);
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        x[e] = fma(om, ps[e], x[e]);
+        r[e] = fma(-om, t[e], r[e]);
+        r2n = fma(r[e], r[e], r2n);
+      }
+      st<N, 1>(X + off, x);
+      st<N, 1>(R + off, r);
+    }
+    r2n = warp_sum(r2n);
+    ++its;
+    if (r2n <= kp.tol2 * rr0) conv = true;
+    rho = rhon;
+    omega = om == 0.0 ? 1.0 : om;
+  }
+  __syncwarp();
+  if (act && cs < nvalid) {
+    const int j = lane % N, k = lane / N;
+    double x[N];
+    ld<N, 1>(X + off, x);
+    if (SWEEP) {
+      double uu[N];
+      ld<N, 1>(in + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, uu);
+#pragma unroll
+      for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+    }
+    st<N, 1>(out + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, x);
+  }
+  if (lane == 0 && cs < nvalid) kp.its[cell0 + cs] = conv ? its : (its | (1 << 30));
+}
+
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks, b != 0).
 template <int N, bool SWEEP>
 __global__ void __launch_bounds__(Geo<N>::NT, 2)   // two CTAs per SM (n = 7: <= 146 registers)
@@ -1338,6 +1530,12 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
+  if constexpr (N == 5) {
+    static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
+    if (method == LM_BICGSTAB && !cta)
+      return launch(k_bicgstab_w<N, SWEEP>, grid, G::NTW,
+                    fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
+  }
   if (method == LM_BICGSTAB)
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
