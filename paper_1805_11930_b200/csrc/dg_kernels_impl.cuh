@@ -74,8 +74,8 @@ template <int N_> struct Geo {
   static constexpr int YS = Lay<N>::YS, ZS = Lay<N>::ZS, CS = Lay<N>::CS;
   static constexpr int LINES = C * N2;
   static constexpr int NT = ((LINES + 31) / 32) * 32;
-  // one warp per cell (n = 5: 25 of 32 lanes hold a line): the thread count of k_cg_w, whose
-  // iterations then need no CTA barrier. The CTA-wide helpers use the first NT threads only.
+  // one warp per cell: the thread count of k_cg_w / k_bicgstab_w, whose iterations then need no
+  // CTA barrier (n = 5: 25 of 32 lanes hold a line; n >= 6: a lane holds up to two lines)
   static constexpr int NTW = C * 32;
   static constexpr int TENSOR = C * CS;
   static constexpr int FACE = C * 12 * N2;
@@ -165,9 +165,9 @@ template <int N> __device__ __forceinline__ void bterm(const double* B, const do
 // Bf[cs][a][q][r] = |F_a| sum_{s = lo, hi} (E_s[q] (sa_s E_s[r] + sg_s F_s[r] / h_a) + F_s[q] ta_s E_s[r])
 // (traces of a Gauss-value line: u(s) = E_s.U, u'(s) = F_s.U; injection of the value- and
 // derivative-test fluxes into the weighted Gauss residual). Needs g.fc; ends with a barrier.
-template <int N> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
+template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
   using G = Geo<N>;
-  for (int it = threadIdx.x; threadIdx.x < G::NT && it < G::C * 3 * N * N; it += G::NT) {
+  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
     const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
     const int q = (rem % (N * N)) / N, r = rem % N;
     const double* lo = g.fc[cs][2 * a];
@@ -270,7 +270,7 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
   __syncthreads();
 }
 
-template <int N>
+template <int N, int NTH = Geo<N>::NT>
 __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const double* u) {
   using G = Geo<N>;
   const int t = threadIdx.x;
@@ -279,17 +279,17 @@ __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const dou
     g.td0[t] = c_tab[N].d0[t];
     g.td1[t] = c_tab[N].d1[t];
   }
-  setup_cells<N, G::C, G::NT>(kp, g.vc, g.fc, g.nb, g.cell, cell0, u);
+  setup_cells<N, G::C, NTH>(kp, g.vc, g.fc, g.nb, g.cell, cell0, u);
 }
 
 // ---- tiles ---------------------------------------------------------------------
-template <int N>
+template <int N, int NTH = Geo<N>::NT>
 __device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncells,
                                           const double* __restrict__ src, double* dst) {
   using G = Geo<N>;
   const int nvalid = min(G::C, ncells - cell0);
   const double* s = src + (size_t)cell0 * G::N3;
-  for (int e = threadIdx.x; threadIdx.x < G::NT && e < G::C * G::N3; e += G::NT) {
+  for (int e = threadIdx.x; e < G::C * G::N3; e += NTH) {
     const int cs = e / G::N3, r = e % G::N3;
     const int i = r % N, j = (r / N) % N, k = r / G::N2;
     dst[cs * G::CS + k * G::ZS + j * G::YS + i] = (cs < nvalid) ? s[e] : 0.0;
@@ -354,19 +354,18 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
 // FACES = false: the volume terms alone (the face passes are skipped); USEB (with FACES = false):
 // plus the self-face terms through g.Bf inside the Gauss-point passes (D_T without face passes)
-template <int N, bool FACES = true, bool USEB = false, bool WARP = false, bool WIDE = false, class Out>
+template <int N, bool FACES = true, bool USEB = false, bool WARP = false, int NTH = Geo<N>::NT, class Out>
 __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
                                               const double* src, double* SA, double* SB,
                                               double* FB, bool vol, Out out) {
   using G = Geo<N>;
-  constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = G::NT;
+  constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = NTH;   // NTH: the launch's thread count
   const int tid = threadIdx.x;
-  static_assert(!WARP || (!FACES && N2 <= 32), "warp mode: one cell per warp, no face passes");
+  static_assert(!WARP || !FACES, "warp mode: one cell per warp, no face passes");
   // WARP: the calling warp applies the operator to its own cell (cs = warp) alone, one line per
   // lane, __syncwarp between the passes; otherwise the whole CTA over all lines of the group
   const int lb = WARP ? (tid >> 5) * N2 + (tid & 31) : tid;
-  // WIDE: launched with more than NT threads (k_cg_w's defect); the ones past NT idle
-  const int le = WARP ? ((tid >> 5) + 1) * N2 : ((!WIDE || tid < NT) ? LINES : 0);
+  const int le = WARP ? ((tid >> 5) + 1) * N2 : LINES;
   constexpr int ls = WARP ? 32 : NT;
   const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
   const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
@@ -374,7 +373,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
 
   // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
-  for (int it = tid; FACES && (!WIDE || tid < NT) && it < 3 * LINES; it += NT) {
+  for (int it = tid; FACES && it < 3 * LINES; it += NT) {
     const int ax = it / LINES, r = it % LINES, cs = r / N2, l = r % N2;
     const int a = l % N, b = l / N;
     if (ax == 0) face_line<N, 0>(g, src, FB, cs, a, b, inv_h[0]);
@@ -393,7 +392,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   }
   if constexpr (WARP) __syncwarp(); else __syncthreads();
   // pass 2: F2 (tangential mass along t1) + P2 (y-lines: SB = A_y SA)
-  for (int it = tid; FACES && (!WIDE || tid < NT) && it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
     const int t2 = it % N, rest = it / N;
     double* fa = FB + rest * N2 + N * t2;
     double v[N], o[N];
@@ -414,7 +413,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   if constexpr (WARP) __syncwarp(); else __syncthreads();
   // pass 3: F3 (tangential mass along t2, area scaling) + P3 (z-lines: U = A_z SB -> SA,
   //         R = reaction + z-term -> SB)
-  for (int it = tid; FACES && (!WIDE || tid < NT) && it < C * 12 * N; it += NT) {
+  for (int it = tid; FACES && it < C * 12 * N; it += NT) {
     const int t1 = it % N, rest = it / N;
     const int ax = (rest >> 2) % 3;
     double* fa = FB + rest * N2 + t1;
@@ -529,13 +528,13 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
 }
 
 // ---- diag(D_T) from 1D diagonals (Jacobi preconditioner) --------------
-template <int N>
+template <int N, int NTH = Geo<N>::NT>
 __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
   using G = Geo<N>;
   const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
   const double sb[3] = {T3 * kp.b[0] / kp.h[0], T3 * kp.b[1] / kp.h[1], T3 * kp.b[2] / kp.h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
-  for (int e = threadIdx.x; threadIdx.x < G::NT && e < G::C * G::N3; e += G::NT) {
+  for (int e = threadIdx.x; e < G::C * G::N3; e += NTH) {
     const int cs = e / G::N3, r = e % G::N3;
     const int idx[3] = {r % N, (r / N) % N, r / G::N2};
     double Md[3], Sd[3], Cd[3];
@@ -784,7 +783,6 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
        double* __restrict__ out) {
   using G = Geo<N>;
   constexpr int C = G::C;
-  static_assert(G::N2 <= 32, "one warp per cell");
   extern __shared__ double sm[];
   __shared__ Group<N> g;
   double* X = sm;
@@ -798,14 +796,14 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   const int cell0 = blockIdx.x * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
-  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   KParams kq = kp;
   kq.mask = 7u;
-  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N>(kq, g);
+  group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2), CTA-wide
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N, true, false, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
@@ -814,24 +812,33 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
     });
     __syncthreads();
-    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+    for (int it = tid; it < C * 6; it += G::NTW) g.nb[it / 6][it % 6] = nullptr;
   }
-  diag_setup<N>(kp, g, Dg);
+  diag_setup<N, G::NTW>(kp, g, Dg);
   __syncthreads();
-  // from here on: warp w owns cell slot cs = w, lane l < n^2 its x-line l
+  // from here on: warp w owns cell slot cs = w; lane l holds the x-lines l, l + 32, ... < n^2
+  constexpr int LPL = (G::N2 + 31) / 32;   // lines per lane
   const int cs = tid >> 5, lane = tid & 31;
-  const bool act = lane < G::N2;
-  const int off = cs * G::CS + (lane / N) * G::ZS + (lane % N) * G::YS;
-  double rr = 0.0, rz = 0.0;
-  if (act) {
-    double r[N], dg[N], z[N], zero[N] = {};
-    ld<N, 1>(R + off, r);
-    ld<N, 1>(Dg + off, dg);
+  int off[LPL];
+  bool act[LPL];
 #pragma unroll
-    for (int e = 0; e < N; ++e) { z[e] = r[e] * dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
-    st<N, 1>(P + off, z);
-    st<N, 1>(X + off, zero);
+  for (int m = 0; m < LPL; ++m) {
+    const int l = lane + 32 * m;
+    act[m] = l < G::N2;
+    off[m] = cs * G::CS + (l / N) * G::ZS + (l % N) * G::YS;
   }
+  double rr = 0.0, rz = 0.0;
+#pragma unroll
+  for (int m = 0; m < LPL; ++m)
+    if (act[m]) {
+      double r[N], dg[N], z[N], zero[N] = {};
+      ld<N, 1>(R + off[m], r);
+      ld<N, 1>(Dg + off[m], dg);
+#pragma unroll
+      for (int e = 0; e < N; ++e) { z[e] = r[e] * dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
+      st<N, 1>(P + off[m], z);
+      st<N, 1>(X + off[m], zero);
+    }
   const double rr0 = warp_sum(rr);
   rz = warp_sum(rz);
   bool conv = cs >= nvalid || rr0 == 0.0 || skip_cell(kp, cell0 + cs);
@@ -843,13 +850,15 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     });
     __syncwarp();
     double pq = 0.0;
-    double x[N], r[N], p[N], q[N], dg[N];
-    if (act) {
-      ld<N, 1>(P + off, p);
-      ld<N, 1>(Q + off, q);
+    double p[LPL][N], q[LPL][N], dg[LPL][N];
 #pragma unroll
-      for (int e = 0; e < N; ++e) pq = fma(p[e], q[e], pq);
-    }
+    for (int m = 0; m < LPL; ++m)
+      if (act[m]) {
+        ld<N, 1>(P + off[m], p[m]);
+        ld<N, 1>(Q + off[m], q[m]);
+#pragma unroll
+        for (int e = 0; e < N; ++e) pq = fma(p[m][e], q[m][e], pq);
+      }
     pq = warp_sum(pq);
     if (!(pq > 0.0)) {   // breakdown (p = 0): keep the last iterate
       conv = true;
@@ -857,21 +866,24 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     }
     const double alpha = rz / pq;
     double r2 = 0.0, rzn = 0.0;
-    if (act) {
-      ld<N, 1>(X + off, x);
-      ld<N, 1>(R + off, r);
-      ld<N, 1>(Dg + off, dg);
 #pragma unroll
-      for (int e = 0; e < N; ++e) {
-        x[e] = fma(alpha, p[e], x[e]);
-        r[e] = fma(-alpha, q[e], r[e]);
-        r2 = fma(r[e], r[e], r2);
-        dg[e] *= r[e];   // z = M^-1 r
-        rzn = fma(r[e], dg[e], rzn);
+    for (int m = 0; m < LPL; ++m)
+      if (act[m]) {
+        double x[N], r[N];
+        ld<N, 1>(X + off[m], x);
+        ld<N, 1>(R + off[m], r);
+        ld<N, 1>(Dg + off[m], dg[m]);
+#pragma unroll
+        for (int e = 0; e < N; ++e) {
+          x[e] = fma(alpha, p[m][e], x[e]);
+          r[e] = fma(-alpha, q[m][e], r[e]);
+          r2 = fma(r[e], r[e], r2);
+          dg[m][e] *= r[e];   // z = M^-1 r
+          rzn = fma(r[e], dg[m][e], rzn);
+        }
+        st<N, 1>(X + off[m], x);
+        st<N, 1>(R + off[m], r);
       }
-      st<N, 1>(X + off, x);
-      st<N, 1>(R + off, r);
-    }
     r2 = warp_sum(r2);
     rzn = warp_sum(rzn);
     ++its;
@@ -881,26 +893,30 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     }
     const double beta = rzn / rz;
     rz = rzn;
-    if (act) {
 #pragma unroll
-      for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], dg[e]);
-      st<N, 1>(P + off, p);
-    }
+    for (int m = 0; m < LPL; ++m)
+      if (act[m]) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) p[m][e] = fma(beta, p[m][e], dg[m][e]);
+        st<N, 1>(P + off[m], p[m]);
+      }
   }
   __syncwarp();
   // write result (u + omega du for a sweep, du for a solve), warp by warp
-  if (act && cs < nvalid) {
-    const int j = lane % N, k = lane / N;
-    double x[N];
-    ld<N, 1>(X + off, x);
-    if (SWEEP) {
-      double uu[N];
-      ld<N, 1>(in + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, uu);
 #pragma unroll
-      for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+  for (int m = 0; m < LPL; ++m)
+    if (act[m] && cs < nvalid) {
+      const int l = lane + 32 * m, j = l % N, k = l / N;
+      double x[N];
+      ld<N, 1>(X + off[m], x);
+      if (SWEEP) {
+        double uu[N];
+        ld<N, 1>(in + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, uu);
+#pragma unroll
+        for (int e = 0; e < N; ++e) x[e] = fma(kp.omega, x[e], uu[e]);
+      }
+      st<N, 1>(out + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, x);
     }
-    st<N, 1>(out + (size_t)(cell0 + cs) * G::N3 + k * G::N2 + j * N, x);
-  }
   if (lane == 0 && cs < nvalid) kp.its[cell0 + cs] = conv ? its : (its | (1 << 30));
 }
 
@@ -929,14 +945,14 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   const int cell0 = blockIdx.x * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
-  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   KParams kq = kp;
   kq.mask = 7u;
-  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N>(kq, g);
+  group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
+  self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N, true, false, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
@@ -945,9 +961,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
     });
     __syncthreads();
-    for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
+    for (int it = tid; it < C * 6; it += G::NTW) g.nb[it / 6][it % 6] = nullptr;
   }
-  diag_setup<N>(kp, g, Dg);
+  diag_setup<N, G::NTW>(kp, g, Dg);
   __syncthreads();
   const int cs = tid >> 5, lane = tid & 31;
   const bool act = lane < G::N2;
@@ -1539,7 +1555,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if (method == LM_BICGSTAB)
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
-  if constexpr (N == 5) {
+  if constexpr (N >= 5 && N <= 7) {   // n = 8: 255 registers with spills, the CTA version is faster
     static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
     if (!cta)
       return launch(k_cg_w<N, SWEEP>, grid, G::NTW,
