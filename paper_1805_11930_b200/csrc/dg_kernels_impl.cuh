@@ -928,7 +928,6 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
              double* __restrict__ out) {
   using G = Geo<N>;
   constexpr int C = G::C;
-  static_assert(G::N2 <= 32, "one warp per cell");
   extern __shared__ double sm[];
   __shared__ Group<N> g;
   double* X = sm;
@@ -965,9 +964,16 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   }
   diag_setup<N, G::NTW>(kp, g, Dg);
   __syncthreads();
+  constexpr int LPL = (G::N2 + 31) / 32;   // x-lines per lane
   const int cs = tid >> 5, lane = tid & 31;
-  const bool act = lane < G::N2;
-  const int off = cs * G::CS + (lane / N) * G::ZS + (lane % N) * G::YS;
+  int offs[LPL];
+  bool acts[LPL];
+#pragma unroll
+  for (int m = 0; m < LPL; ++m) {
+    const int l = lane + 32 * m;
+    acts[m] = l < G::N2;
+    offs[m] = cs * G::CS + (l / N) * G::ZS + (l % N) * G::YS;
+  }
   auto op = [&](double* dst) {   // dst = D_T PS on this warp's cell
     __syncwarp();
     cell_operator<N, false, true, true>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
@@ -976,7 +982,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     __syncwarp();
   };
   double rr = 0.0;
-  if (act) {
+#pragma unroll
+  for (int m = 0; m < LPL; ++m) if (acts[m]) {
+    const int off = offs[m];
     double r[N], zero[N] = {};
     ld<N, 1>(R + off, r);
 #pragma unroll
@@ -993,7 +1001,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   int its = 0;
   for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
     double a = 0.0, b = 0.0;
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double r[N], rh[N];
       ld<N, 1>(R + off, r);
       ld<N, 1>(RH + off, rh);
@@ -1006,7 +1016,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     if (rst) rhon = r2;
     const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
     // p = r + beta (p - omega v); ps = M^-1 p
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double r[N], p[N], v[N], dg[N], ps[N];
       ld<N, 1>(R + off, r);
       ld<N, 1>(P + off, p);
@@ -1024,7 +1036,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     rst = false;
     op(V);
     double rvl = 0.0;
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double rh[N], v[N];
       ld<N, 1>(RH + off, rh);
       ld<N, 1>(V + off, v);
@@ -1037,7 +1051,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     else rst = true;
     // x += alpha ps; s = r - alpha v (in R); ps <- M^-1 s
     double ss = 0.0;
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double x[N], r[N], v[N], ps[N], dg[N];
       ld<N, 1>(X + off, x);
       ld<N, 1>(R + off, r);
@@ -1063,7 +1079,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     }
     op(T);
     double tsl = 0.0, ttl = 0.0;
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double t[N], sv[N];
       ld<N, 1>(T + off, t);
       ld<N, 1>(R + off, sv);
@@ -1075,7 +1093,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     if (om == 0.0) rst = true;
     // x += omega s^; r = s - omega t
     double r2n = 0.0;
-    if (act) {
+#pragma unroll
+    for (int m = 0; m < LPL; ++m) if (acts[m]) {
+      const int off = offs[m];
       double x[N], r[N], t[N], ps[N];
       ld<N, 1>(X + off, x);
       ld<N, 1>(R + off, r);
@@ -1097,8 +1117,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     omega = om == 0.0 ? 1.0 : om;
   }
   __syncwarp();
-  if (act && cs < nvalid) {
-    const int j = lane % N, k = lane / N;
+#pragma unroll
+  for (int m = 0; m < LPL; ++m) if (acts[m] && cs < nvalid) {
+    const int off = offs[m], l = lane + 32 * m, j = l % N, k = l / N;
     double x[N];
     ld<N, 1>(X + off, x);
     if (SWEEP) {
@@ -1546,7 +1567,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   const int grid = (kp.ncells + G::C - 1) / G::C;
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
-  if constexpr (N == 5) {
+  if constexpr (N >= 5 && N <= 7) {
     static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
     if (method == LM_BICGSTAB && !cta)
       return launch(k_bicgstab_w<N, SWEEP>, grid, G::NTW,
