@@ -180,7 +180,8 @@ def extras_single_gpu(dev, peak_derived):
         ut, ft = torch.from_numpy(u).to(dev), torch.from_numpy(f).to(dev)
         o = torch.empty_like(ut)
         n = P.p + 1
-        vol = 24 * n ** 4 + 8 * n ** 3
+        # + 4 n^3 with convection, + 2 n^3 with a reaction term
+        vol = 24 * n ** 4 + 8 * n ** 3 + (4 * n ** 3 if any(P.b) else 0) + (2 * n ** 3 if P.c is not None else 0)
         if name != "C5":
             t = timed(lambda: ctx.apply_parts(ut, o, dg.MASK_VOLUME), 20)
             out["volume_kernel_p_ge_3"][name] = {"p": P.p, "n_dof": P.n_dof, "us_per_call": t * 1e6,

@@ -39,7 +39,8 @@ def main(names):
         out = torch.empty_like(ut)
         n = P.p + 1
         nc = P.n_cells
-        vol = 24 * n ** 4 + 8 * n ** 3
+        # + 4 n^3 with convection, + 2 n^3 with a reaction term
+        vol = 24 * n ** 4 + 8 * n ** 3 + (4 * n ** 3 if any(P.b) else 0) + (2 * n ** 3 if P.c is not None else 0)
         sf, nf = 8 * n ** 3 + 12 * n ** 2, 10 * n ** 3
         r = {"config": name, "p": P.p}
         t = timed(lambda: ctx.apply_parts(ut, out, dg.MASK_VOLUME))
