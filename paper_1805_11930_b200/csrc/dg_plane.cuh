@@ -342,10 +342,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 // own tile (contiguous in global) -> TB layout, half h
-template <int N>
+template <int N, bool ROLL = false>
 __device__ __forceinline__ void async_own(double* TB, const double* __restrict__ src, int nvalid) {
   using G = Geo<N>;
-#pragma unroll
+#pragma unroll (ROLL ? 1 : 64)
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
     if (e < G::C * G::N3) {
@@ -358,7 +358,7 @@ __device__ __forceinline__ void async_own(double* TB, const double* __restrict__
 // (KSX = N2, cell stride FS >= N3)
 // fast path (no ghost-layer neighbour on face f): the neighbour tile is the group's own tile
 // shifted by +- step cells, so the sources are contiguous and no per-cell pointer is loaded
-template <int N, int KSX, int CSX, bool WB>
+template <int N, int KSX, int CSX, bool ROLL = false, bool WB>
 __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, int f, const double* any,
                                           const KParams& kp, const double* tile) {
   using G = Geo<N>;
@@ -369,7 +369,7 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
     if constexpr (N % 2 == 0 && CSX % 2 == 0 && KSX % 2 == 0) {
       // element pairs (same cell and plane, 16-byte aligned on both sides)
       static_assert((G::C * G::N3 / 2) % G::NT == 0, "pairs tile the group evenly");
-#pragma unroll
+#pragma unroll (ROLL ? 1 : 64)
       for (int m = 0; m < G::C * G::N3 / 2 / G::NT; ++m) {
         const int e = 2 * (threadIdx.x + m * G::NT);
         const int cs = e / G::N3, r = e % G::N3;
@@ -378,7 +378,7 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
       }
       return;
     }
-#pragma unroll
+#pragma unroll (ROLL ? 1 : 64)
     for (int m = 0; m < G::PER; ++m) {
       const int e = threadIdx.x + m * G::NT;
       if (e < G::C * G::N3) {
@@ -389,7 +389,7 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
     }
     return;
   }
-#pragma unroll
+#pragma unroll (ROLL ? 1 : 64)
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
     if (e < G::C * G::N3) {
@@ -1207,7 +1207,10 @@ __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl
                                              double* FX, double* FZ, const double* in, int cell0, int nvalid) {
   using G = Geo<N>;
   const double* tile = in + (size_t)cell0 * G::N3;
-  if (!CMAP) async_own<N>(TB, tile, nvalid);
+  // n = 4 solvers: the copy loops rolled (the fused sweep kernel's prologue code shrinks by
+  // ~20 KB; C2 sweep 433 -> 416 us, C4 7.40 -> 7.33 ms; n = 3 and the applies lose with it)
+  constexpr bool RL = N == 4;
+  if (!CMAP) async_own<N, RL>(TB, tile, nvalid);
   clear_masks<N>(cl);
   __syncthreads();
   SetupRegs<N> sr;
@@ -1215,10 +1218,10 @@ __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl
   __syncthreads();   // neighbour pointers and masks
   if (CMAP) async_own_map<N>(TB, in, cl);
   if (SWEEP) {
-    async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, in, kp, tile);
-    async_nbr<N, G::N2, G::FS>(FY, cl, 3, in, kp, tile);
-    async_nbr<N, G::N2, G::FS>(FX, cl, 4, in, kp, tile);
-    async_nbr<N, G::N2, G::FS>(FZ, cl, 5, in, kp, tile);
+    async_nbr<N, G::KS, G::CTB, RL>(TB + G::ARR, cl, 2, in, kp, tile);
+    async_nbr<N, G::N2, G::FS, RL>(FY, cl, 3, in, kp, tile);
+    async_nbr<N, G::N2, G::FS, RL>(FX, cl, 4, in, kp, tile);
+    async_nbr<N, G::N2, G::FS, RL>(FZ, cl, 5, in, kp, tile);
   }
   setup_finish<N>(kp, cl, sr);
   __syncthreads();   // fc of every cell
