@@ -354,6 +354,17 @@ __device__ __forceinline__ void async_own(double* TB, const double* __restrict__
     }
   }
 }
+// solvers: a tile into the TB layout; at n = 4 through rolled cp.async copies (code size: the
+// solver prologue / epilogue share the instruction cache with the iteration loop)
+template <int N>
+__device__ __forceinline__ void stage_tile_s(double* TB, const double* __restrict__ src, int nvalid) {
+  if constexpr (N == 4) {
+    async_own<N, true>(TB, src, nvalid);
+    cp_async_wait_all();
+  } else {
+    stage_tile<N>(TB, src, nvalid);
+  }
+}
 // face-f neighbour tiles: into TB layout (KSX = KS, cell stride CTB) or into a face region
 // (KSX = N2, cell stride FS >= N3)
 // fast path (no ghost-layer neighbour on face f): the neighbour tile is the group's own tile
@@ -919,6 +930,17 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
 }
 
 // 1 / diag(D_T) on the lane's plane (Jacobi preconditioner), from 1D diagonals
+// 1 / d from the hardware approximation and two Newton steps (a handful of instructions where
+// an IEEE division expands to ~35): used for the Jacobi preconditioners only, where any fixed
+// diagonal scaling is valid and the last bit does not matter (the solvers' code size does).
+__device__ __forceinline__ double rcp_nr(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
 template <int N>
 __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>& cl, const Lane& L,
                                                const Rows<N>& rw, double (&dg)[N][N]) {
@@ -948,7 +970,7 @@ __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>
       if (j == 0) d += kp.fa[1] * Mi * Mk * ylo;
       if (j == N - 1) d += kp.fa[1] * Mi * Mk * yhi;
       d += kp.fa[2] * Mi * Mj * (zlo + zhi);
-      dg[j][i] = 1.0 / d;
+      dg[j][i] = rcp_nr(d);
     }
 }
 
@@ -1329,7 +1351,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
     __syncthreads();
     if (CMAP) stage_tile_map<N>(TB, f, cl);
-    else stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    else stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
     read_plane<N>(TB, L, R);
 #pragma unroll
@@ -1419,7 +1441,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   __syncthreads();
   if (SWEEP) {
     if (CMAP) stage_tile_map<N>(TB, in, cl);
-    else stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+    else stage_tile_s<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
   }
   __syncthreads();
   if (L.active) {
@@ -1691,7 +1713,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     if (CMAP) stage_tile_map<N>(TB, f, cl);
-    else stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    else stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
     read_plane<N>(TB, L, R);
 #pragma unroll
@@ -1935,7 +1957,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   __syncthreads();
   if (SWEEP) {
     if (CMAP) stage_tile_map<N>(TB, in, cl);
-    else stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+    else stage_tile_s<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
   }
   __syncthreads();
   if constexpr (TM) {
@@ -2028,7 +2050,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
-    stage_tile<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
+    stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
     __syncthreads();
     read_plane<N>(TB, L, R);
 #pragma unroll
@@ -2219,7 +2241,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   }
   tm_free<M::ALLOC>(tm_slot);
 #undef tq
-  if (SWEEP) stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+  if (SWEEP) stage_tile_s<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
   __syncthreads();
   if (L.active) {
     double* bb = TB + L.cs * G::CTB + L.t * G::KS;
