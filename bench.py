@@ -218,7 +218,9 @@ def extras_single_gpu(dev, peak_derived):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.hybrid_solve(x, ft, dg.hybrid_params(max_it=1))
     x.zero_()
-    prm = dg.hybrid_params(local_tol=1e-2, coarse_tol=1e-6, rel_tol=1e-8, max_it=500)
+    # coarse solve to 1e-2 only: the flexible outer CG absorbs it (C2: 82 outer iterations at
+    # 1e-2 vs 81 at 1e-6, 83 vs 130 ms; profiles/r01_hybrid_coarse_tol.jsonl)
+    prm = dg.hybrid_params(local_tol=1e-2, coarse_tol=1e-2, rel_tol=1e-8, max_it=500)
     torch.cuda.synchronize()
     a.record()
     st = ctx.hybrid_solve(x, ft, prm)
@@ -229,7 +231,7 @@ def extras_single_gpu(dev, peak_derived):
         "block_ssor_red_black_cg_1e-12": t_ssor * 1e6,
         "block_jacobi_stored_inverse": t_pmf * 1e6}
     out["C2_hybrid_multigrid_solve"] = {"ms": a.elapsed_time(b), "rel_tol": 1e-8, "local_tol": 1e-2,
-                                        "coarse": "P0, Jacobi-PCG to 1e-6", **st}
+                                        "coarse": "P0, Jacobi-PCG to 1e-2", **st}
     ctx.close()
     return out
 

@@ -1,6 +1,6 @@
 """Times the hybrid-multigrid-preconditioned flexible CG (Alg. 1, P0 subspace) on b = 0 configs.
 
-usage: python scripts/hybrid_solve.py [C2 C3 C5 ...]
+usage: python scripts/hybrid_solve.py [C2 C3 C5 ...] [--coarse-tol X] [--local-tol Y]
 Prints one JSON line per config: outer iterations, coarse PCG iterations, wall time of the solve
 (CUDA events around dg_hybrid_solve, which synchronises per iteration), true relative residual.
 """
@@ -14,12 +14,22 @@ import torch
 import paper_1805_11930_b200 as dg
 from synth import make_config, make_vectors
 
-for name in sys.argv[1:] or ["C2"]:
+args = sys.argv[1:]
+def opt(name, default):
+    if name in args:
+        i = args.index(name)
+        v = float(args[i + 1])
+        del args[i:i + 2]
+        return v
+    return default
+ctol = opt("--coarse-tol", 1e-2)
+ltol = opt("--local-tol", 1e-2)
+for name in args or ["C2"]:
     P = make_config(name)
     _, f = make_vectors(P)
     ctx = dg.DGContext(P)
     ft = torch.from_numpy(f).cuda()
-    prm = dg.hybrid_params(n_pre=1, n_post=1, omega=1.0, local_tol=1e-2, coarse_tol=1e-6,
+    prm = dg.hybrid_params(n_pre=1, n_post=1, omega=1.0, local_tol=ltol, coarse_tol=ctol,
                            coarse_max_it=20000, rel_tol=1e-8, max_it=500)
     u = torch.zeros_like(ft)
     ctx.hybrid_solve(u, ft, dg.hybrid_params(max_it=1))   # warm-up (scratch, coarse matrix)
