@@ -1465,6 +1465,27 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
         if (e != cudaSuccess) return e;
         slots = max(1, per_sm) * nsm;
       }
+      if constexpr (N == 4) {
+        // slim variant (no register prefetch, 4 CTAs per SM); DG_VOLUME_SLIM=0: k_volume (A/B)
+        static const bool alt = !(getenv("DG_VOLUME_SLIM") && getenv("DG_VOLUME_SLIM")[0] == '0');
+        if (alt) {
+          static int sslots = 0;
+          const size_t ssm = sizeof(double) * (size_t)G::TB;
+          if (sslots == 0) {
+            cudaError_t e = set_smem(pk::k_volume_s<N, true>, ssm);
+            if (e == cudaSuccess) e = set_smem(pk::k_volume_s<N, false>, ssm);
+            int per_sm = 0, dev = 0, nsm = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk::k_volume_s<N>, G::NT, ssm);
+            if (e != cudaSuccess) return e;
+            sslots = max(1, per_sm) * nsm;
+          }
+          if (gen_terms(kp)) pk::k_volume_s<N, true><<<min(grid, sslots), G::NT, ssm, s>>>(kp, u, out);
+          else pk::k_volume_s<N, false><<<min(grid, sslots), G::NT, ssm, s>>>(kp, u, out);
+          return cudaGetLastError();
+        }
+      }
       if (gen_terms(kp)) pk::k_volume<N, true><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
       else pk::k_volume<N, false><<<min(grid, slots), G::NT, vsm, s>>>(kp, u, out);
       return cudaGetLastError();

@@ -1306,6 +1306,55 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   }
 }
 
+// Variant without register prefetch (n = 4): the group's tile is copied with cp.async straight
+// into TB and the coefficients into a slim shared array, so the kernel needs ~130 instead of 166
+// registers and 42 KB instead of 54 KB of shared memory: four CTAs (16 warps) per SM hide the
+// load latency instead of the prefetch.
+#ifndef DG_VOL4_MINB
+#define DG_VOL4_MINB 4
+#endif
+template <int N, bool GEN = true>
+__global__ void __launch_bounds__(Geo<N>::NT, DG_VOL4_MINB)
+k_volume_s(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
+  using G = Geo<N>;
+  extern __shared__ double sm[];
+  double* TB = sm;
+  // only vc (the first member) of the cell block is read by the volume-only operator
+  using CellsV = Cells<N, false>;
+  static_assert(offsetof(CellsV, vc) == 0, "vc leads the cell block");
+  __shared__ double vcs[G::C][4];
+  const Cells<N, false>& cl = *reinterpret_cast<const Cells<N, false>*>(&vcs[0][0]);
+  const int ngroups = (kp.ncells + G::C - 1) / G::C;
+  const Lane L = lane_id<N>();
+  Rows<N> rw;
+  load_rows<N>(rw, L.t);
+  const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+  const int nxy = kp.nx * kp.ny;
+  for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const int cell0 = g * G::C;
+    const int nvalid = min(G::C, kp.ncells - cell0);
+    async_own<N>(TB, u + (size_t)cell0 * G::N3, nvalid);
+    if (threadIdx.x < G::C) {
+      const int cs = threadIdx.x;
+      const bool ok = cs < nvalid;
+      const double* Kc = kp.K + (size_t)(cell0 + (ok ? cs : 0) + nxy) * 3;
+      vcs[cs][0] = ok ? __ldg(Kc) * vol * kp.ih[0] * kp.ih[0] : 0.0;
+      vcs[cs][1] = ok ? __ldg(Kc + 1) * vol * kp.ih[1] * kp.ih[1] : 0.0;
+      vcs[cs][2] = ok ? __ldg(Kc + 2) * vol * kp.ih[2] * kp.ih[2] : 0.0;
+      vcs[cs][3] = ok && kp.c ? vol * __ldg(kp.c + cell0 + cs) : 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double in[N][N], o[N][N];
+    read_plane<N>(TB, L, in);
+    plane_op<N, false, false, false, GEN>(kp, cl, L, rw, true, in, o, TB, nullptr, nullptr, nullptr);
+    if (L.active) write_plane<N>(TB, L, o);
+    __syncthreads();
+    unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
+    __syncthreads();   // TB and vcs are reused by the next group
+  }
+}
+
 // Jacobi-PCG per cell; SWEEP: defect d = f - A u first, result u + omega du.
 // Registers: r, p (and the operator's planes); shared: x and diag(D_T) planes.
 template <int N, bool SWEEP, bool GEN = true, bool CMAP = false>
