@@ -1427,7 +1427,7 @@ static bool force_line() {
 }
 
 // Kernel family of the operator application per degree, chosen by measurement on C1-C5
-// (profiles/r01_kernel_family.md, profiles/r01_session2_ab.md): the plane kernels for n = 2, 3, 4;
+// (profiles/r01_kernel_family.md, profiles/r01_ab.md): the plane kernels for n = 2, 3, 4;
 // at n = 5 the line kernels' higher occupancy wins for A u and D_T u (the volume-only hook uses
 // the persistent plane kernel k_volume for every n <= 5). The local solvers always use the plane
 // kernels for n <= 5 (register-resident Krylov vectors).
@@ -1564,7 +1564,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
         // restarted GMRES(KR), Krylov basis + diagonal in TMEM (compact colour maps not
         // supported: the SOR half-sweeps run masked). KR fills 256 TMEM columns at n = 2, 3
         // (two CTAs per SM) and all 512 at n = 4 (one CTA per SM: GMRES(7) with two CTAs was
-        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_session2_ab.md)
+        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_ab.md)
         constexpr int KR = N == 4 ? 15 : N == 3 ? 13 : 15;
         if (method == LM_GMRES)
           return launch(pk::k_gmres<N, SWEEP, false, KR>, grid, G::NT, pk::smem_gmres<N, KR>(false), s, kp, in, f, out);

@@ -1,5 +1,5 @@
 """L2-resident vs HBM read bandwidth on one B200 (torch sum reductions and copies), for the
-roofline of the neighbour-tile loads of dg_apply (profiles/r01_session2_ab.md)."""
+roofline of the neighbour-tile loads of dg_apply (profiles/r01_ab.md)."""
 import torch
 
 torch.cuda.init()
