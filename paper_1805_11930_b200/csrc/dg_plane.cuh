@@ -941,6 +941,17 @@ __device__ __forceinline__ double rcp_nr(double d) {
   e = fma(-d, y, 1.0);
   return fma(y, e, y);
 }
+// Krylov scalars of the plane solvers: a * (1 / b) with rcp_nr (~1 ulp; the IEEE division is
+// ~35 instructions inside loops that must stay within the instruction cache). DG_EXACT_QUOT=1:
+// IEEE division (A/B).
+#ifndef DG_EXACT_QUOT
+#define DG_EXACT_QUOT 0
+#endif
+#if DG_EXACT_QUOT
+#define DG_QUOT(a, b) ((a) / (b))
+#else
+#define DG_QUOT(a, b) ((a) * rcp_nr(b))
+#endif
 template <int N>
 __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>& cl, const Lane& L,
                                                const Rows<N>& rw, double (&dg)[N][N]) {
@@ -1455,7 +1466,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     pq = cell_sum<N>(pq, L.lane);
     double alpha = 0.0;
     if (!conv) {
-      if (pq > 0.0) alpha = rz / pq;
+      if (pq > 0.0) alpha = DG_QUOT(rz, pq);
       else conv = true;
     }
     double r2 = 0.0, rzn = 0.0;
@@ -1475,7 +1486,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     if (!conv) {
       ++its;
       if (r2 <= kp.tol2 * rr0) conv = true;
-      const double beta = rzn / rz;
+      const double beta = DG_QUOT(rzn, rz);
       rz = rzn;
       if (!conv && L.active) {
 #pragma unroll
@@ -1868,7 +1879,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       const double r2 = cell_sum<N>(b, L.lane);
       if (fabs(rhon) <= 1e-24 * r2) rst = true;   // breakdown: restart with r^ = r
       if (rst) rhon = r2;
-      const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
+      const double beta = rst ? 0.0 : DG_QUOT(rhon * alpha, rho * omega);
       // p = r + beta (p - omega v);  W = M^-1 p
       if constexpr (TM) {
 #pragma unroll
@@ -1926,7 +1937,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       rv = cell_sum<N>(rv, L.lane);
       alpha = 0.0;
       if (!conv) {
-        if (rv != 0.0) alpha = rhon / rv;
+        if (rv != 0.0) alpha = DG_QUOT(rhon, rv);
         else rst = true;
       }
       // x += alpha p^;  s = r - alpha v (in R);  W = M^-1 s
@@ -1968,7 +1979,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
         }
       ts = cell_sum<N>(ts, L.lane);
       tt = cell_sum<N>(tt, L.lane);
-      const double om = (!conv && tt > 0.0) ? ts / tt : 0.0;
+      const double om = (!conv && tt > 0.0) ? DG_QUOT(ts, tt) : 0.0;
       double r2n = 0.0;
       if constexpr (TM) {
 #pragma unroll
