@@ -772,6 +772,15 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 // The group setup and the defect are CTA-wide; the iterations are warp-local (the operator in
 // WARP mode, shuffle reductions, per-lane copies of the cell's scalars), so no CTA barrier is
 // left in the loop and each warp leaves it when its own cell has converged.
+// a / b as a * (1 / b) from rcp.approx + two Newton steps (~1 ulp), for Krylov scalars
+__device__ __forceinline__ double quot_nr(double a, double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = fma(-b, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-b, y, 1.0);
+  return a * fma(y, e, y);
+}
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -864,7 +873,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       conv = true;
       break;
     }
-    const double alpha = rz / pq;
+    const double alpha = quot_nr(rz, pq);
     double r2 = 0.0, rzn = 0.0;
 #pragma unroll
     for (int m = 0; m < LPL; ++m)
@@ -891,7 +900,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       conv = true;
       break;
     }
-    const double beta = rzn / rz;
+    const double beta = quot_nr(rzn, rz);
     rz = rzn;
 #pragma unroll
     for (int m = 0; m < LPL; ++m)
@@ -1014,7 +1023,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     const double r2 = warp_sum(b);
     if (fabs(rhon) <= 1e-24 * r2) rst = true;   // breakdown: restart with rh = r
     if (rst) rhon = r2;
-    const double beta = rst ? 0.0 : (rhon / rho) * (alpha / omega);
+    const double beta = rst ? 0.0 : quot_nr(rhon * alpha, rho * omega);
     // p = r + beta (p - omega v); ps = M^-1 p
 #pragma unroll
     for (int m = 0; m < LPL; ++m) if (acts[m]) {
@@ -1047,7 +1056,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     }
     const double rv = warp_sum(rvl);
     alpha = 0.0;
-    if (rv != 0.0) alpha = rhon / rv;
+    if (rv != 0.0) alpha = quot_nr(rhon, rv);
     else rst = true;
     // x += alpha ps; s = r - alpha v (in R); ps <- M^-1 s
     double ss = 0.0;
@@ -1089,7 +1098,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
       for (int e = 0; e < N; ++e) { tsl = fma(t[e], sv[e], tsl); ttl = fma(t[e], t[e], ttl); }
     }
     const double ts = warp_sum(tsl), tt = warp_sum(ttl);
-    const double om = tt > 0.0 ? ts / tt : 0.0;
+    const double om = tt > 0.0 ? quot_nr(ts, tt) : 0.0;
     if (om == 0.0) rst = true;
     // x += omega s^; r = s - omega t
     double r2n = 0.0;
