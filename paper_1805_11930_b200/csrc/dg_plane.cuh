@@ -1089,7 +1089,7 @@ __device__ __forceinline__ void setup_finish(const KParams& kp, Cells<N, WB>& cl
       if (kind == 0 && (kp.mask & 2u)) {
         const double KN = sr.Kn[r][hi];
         const double sum = KT + KN;
-        const double rs = sum > 0.0 ? 1.0 / sum : 0.0;
+        const double rs = sum > 0.0 ? rcp_nr(sum) : 0.0;   // ~1 ulp (code size: see rcp_nr)
         const double wT = sum > 0.0 ? KN * rs : 0.5, wN = sum > 0.0 ? KT * rs : 0.5;
         const double gam = kp.pen * (2.0 * KT * KN * rs) * ihk;   // <dT,dN>|F|/|T|
         if (hi) {
