@@ -2183,7 +2183,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     if (__all_sync(0xffffffffu, conv || !L.active) || steps >= kp.max_it) break;
     // v_0 = r / |r|
     const double beta = sqrt(b2);
-    const double ib = conv ? 0.0 : 1.0 / beta;
+    const double ib = conv ? 0.0 : rcp_nr(beta);
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       double v[N];
@@ -2226,7 +2226,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
         for (int q = 0; q < N; ++q) hn = fma(T[r][q], T[r][q], hn);
       hn = sqrt(cell_sum<N>(hn, L.lane));
       if (j + 1 < KR) {
-        const double ih = (live && hn > 0.0) ? 1.0 / hn : 0.0;
+        const double ih = (live && hn > 0.0) ? rcp_nr(hn) : 0.0;
 #pragma unroll
         for (int r = 0; r < N; ++r) {
           double v[N];
@@ -2246,7 +2246,8 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
         }
         const double a = col[j];
         const double rn = sqrt(a * a + hn * hn);
-        const double c = rn > 0.0 ? a / rn : 1.0, s_ = rn > 0.0 ? hn / rn : 0.0;
+        const double irn = rn > 0.0 ? rcp_nr(rn) : 0.0;
+        const double c = rn > 0.0 ? a * irn : 1.0, s_ = hn * irn;
         col[j] = rn;
         cv[j] = c;
         sv[j] = s_;
@@ -2267,7 +2268,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       for (int i = jl; i >= 0; --i) {
         double y = gv[i];
         for (int k = i + 1; k <= jl; ++k) y = fma(-sc[k * (k + 1) / 2 + i], gv[k], y);
-        gv[i] = y / sc[i * (i + 1) / 2 + i];
+        gv[i] = DG_QUOT(y, sc[i * (i + 1) / 2 + i]);
       }
     __syncwarp();
 #pragma unroll
