@@ -172,7 +172,7 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
     const int q = (rem % (N * N)) / N, r = rem % N;
     const double* lo = g.fc[cs][2 * a];
     const double* hi = g.fc[cs][2 * a + 1];
-    const double ih = 1.0 / kp.h[a];
+    const double ih = kp.ih[a];   // 1 / h_a (host-computed, identical IEEE quotient)
     const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
     double b = c_tab[N].E0[q] * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) + c_tab[N].F0[q] * lo[4] * c_tab[N].E0[r];
     b += c_tab[N].E1[q] * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) + c_tab[N].F1[q] * hi[4] * c_tab[N].E1[r];
@@ -552,7 +552,7 @@ __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const double tm = area[a] * Md[(a + 1) % 3] * Md[(a + 2) % 3];
-      const double ih = 1.0 / kp.h[a];
+      const double ih = kp.ih[a];   // 1 / h_a (host-computed, identical IEEE quotient)
       if (idx[a] == 0) {
         const double* c = g.fc[cs][2 * a];
         const double dd = c_tab[N].d0[0];
