@@ -33,7 +33,7 @@ def _K_full(P: Problem, K_full):
 def _b_cells(P: Problem, b_cells):
     if b_cells is not None:
         return np.asarray(b_cells, dtype=np.float64)
-    return np.tile(np.asarray(P.b, dtype=np.float64), (P.n_cells, 1))
+    return P.b3()
 
 
 class TierA:

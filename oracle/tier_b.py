@@ -53,8 +53,7 @@ class TierB:
         self.d1 = lagrange_derivs(z, [1.0])[0]
         self.h = np.array(P.h)
         self.K = P.K3()
-        self.b = (np.tile(np.asarray(P.b, dtype=np.float64), (P.n_cells, 1))
-                  if b_cells is None else np.asarray(b_cells, dtype=np.float64))
+        self.b = P.b3() if b_cells is None else np.asarray(b_cells, dtype=np.float64)
         self.c = P.c_cells()
         self.dims = (P.nx, P.ny, P.nz)
 
@@ -228,6 +227,3 @@ class TierB:
 
     def sweep(self, u, f, omega=1.0):
         return self.sweep_cells(u, f, omega, range(self.P.n_cells)).reshape(-1)
-
-    def diag_of_D(self, c):
-        return np.diag(self.diag_block(c)).copy()

@@ -45,6 +45,7 @@ class Problem:
     # per-cell diffusion: shape (N,) scalar or (N, 3) diagonal; cell c = cx + nx*(cy + ny*cz)
     K: np.ndarray = None
     b: tuple = (0.0, 0.0, 0.0)          # constant advection
+    b_cells: Optional[np.ndarray] = None  # per-cell advection (N, 3); overrides b when set
     c: Optional[np.ndarray] = None      # per-cell reaction (N,) or None
     bc: tuple = (DIRICHLET,) * 6        # x-, x+, y-, y+, z-, z+
     name: str = "custom"
@@ -76,6 +77,15 @@ class Problem:
         if K.ndim == 1:
             return np.repeat(K[:, None], 3, axis=1)
         return K
+
+    def b3(self) -> np.ndarray:
+        """Per-cell advection as (N, 3): b_cells, else the constant b on every cell."""
+        if self.b_cells is not None:
+            return np.asarray(self.b_cells, dtype=np.float64).reshape(self.n_cells, 3)
+        return np.tile(np.asarray(self.b, dtype=np.float64), (self.n_cells, 1))
+
+    def has_convection(self) -> bool:
+        return bool(np.any(self.b3() != 0.0))
 
     def c_cells(self) -> np.ndarray:
         if self.c is None:

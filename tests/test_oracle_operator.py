@@ -230,3 +230,68 @@ def test_kronecker_sum_reduction(p):
     assert rel(TierB(P).apply(u), separable_apply(P, ux, uy, uz)) < 1e-13
     A1, M1 = sipg_1d(4, 2.0, p, 2.0)
     assert np.abs(A1 - A1.T).max() < 1e-12 * np.abs(A1).max()
+
+
+def _tier_a_parts(P, b_cells=None):
+    """The three parts a^v, a^if, a^bf of A assembled separately by tier A's brute-force
+    quadrature of P:343-344, P:345-350 and P:352-357 (independent of tier B)."""
+    ta = TierA(P, b_cells=b_cells)
+    nd, N = P.nd, P.n_cells
+    parts = {m: np.zeros((N * nd, N * nd)) for m in (1, 2, 4)}
+
+    def add(m, ct, cr, M):
+        parts[m][ct * nd:(ct + 1) * nd, cr * nd:(cr + 1) * nd] += M
+
+    dims = (P.nx, P.ny, P.nz)
+    for c in range(N):
+        add(1, c, c, ta.volume_block(c))
+        co = list(ta.cell_coords(c))
+        for axis in range(3):
+            if co[axis] + 1 < dims[axis]:
+                cu = list(co)
+                cu[axis] += 1
+                for (ct, cr), M in ta.interior_face_blocks(c, ta.cell_index(*cu), axis).items():
+                    add(2, ct, cr, M)
+            if co[axis] == 0:
+                add(4, c, c, ta.boundary_face_block(c, axis, hi=False))
+            if co[axis] == dims[axis] - 1:
+                add(4, c, c, ta.boundary_face_block(c, axis, hi=True))
+    return parts
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("per_cell_b", [False, True])
+def test_apply_parts_match_tier_a_terms(p, per_cell_b):
+    """Pins TierB.apply_parts_cells (the reference of the dg_apply_parts GPU tests): each mask
+    equals tier A's assembly of that term alone (volume a^v, interior faces a^if, boundary faces
+    a^bf), with mixed Dirichlet / Neumann faces, anisotropic K, reaction and b != 0 (constant or
+    per cell), and the parts sum to the full apply. A boundary self-term filed under the
+    interior mask (or vice versa) fails here."""
+    P = random_problem(2, 3, 2, p, seed=60 + p, b=(0.8, -0.4, 0.3), c=True, L=(1.0, 0.7, 1.3),
+                       bc=MIXED)
+    bc = np.random.default_rng(p).normal(size=(P.n_cells, 3)) if per_cell_b else None
+    parts = _tier_a_parts(P, bc)
+    tb = TierB(P, b_cells=bc)
+    u = np.random.default_rng(10 + p).uniform(-1, 1, P.n_dof)
+    cells = range(P.n_cells)
+    got = {}
+    for mask in (1, 2, 4):
+        got[mask] = tb.apply_parts_cells(u, cells, mask).reshape(-1)
+        ref = parts[mask] @ u
+        assert rel(got[mask], ref) < 1e-13, mask
+    for mask in (3, 5, 6, 7):
+        combo = tb.apply_parts_cells(u, cells, mask).reshape(-1)
+        assert rel(combo, sum(got[m] for m in (1, 2, 4) if mask & m)) < 1e-14
+    assert rel(got[1] + got[2] + got[4], tb.apply(u)) < 1e-14
+    # the boundary part lives only on cells touching a Dirichlet face
+    assert np.abs(got[4].reshape(P.n_cells, P.nd)).max() > 0
+
+
+def test_problem_per_cell_b_overrides_constant():
+    """Problem.b_cells (the data the GPU ABI receives) is what both oracle tiers use."""
+    P = random_problem(2, 2, 2, 2, seed=3, b=(0.2, 0.1, -0.3))
+    bc = np.random.default_rng(0).normal(size=(P.n_cells, 3))
+    A_explicit = TierB(P, b_cells=bc).assemble()
+    P.b_cells = bc
+    assert np.array_equal(TierB(P).assemble(), A_explicit)
+    assert np.abs(TierA(P).assemble() - A_explicit).max() <= 1e-13 * np.abs(A_explicit).max()
