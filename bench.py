@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """Benchmark of the B200 DG hot path (arXiv 1805.11930): dg_apply + block-Jacobi sweeps.
 
-Workload (BASELINE.json configs[1], the config its metric is quoted on; fits one GPU):
-  C2 = 32^3 hexahedra, DG Q3 (64 DoF/cell, 2,097,152 DoF), Poisson K=1, alpha=2, Dirichlet;
-  one STEP = 100 dg_apply + 10 block-Jacobi sweeps (omega=1, local Jacobi-PCG to 1e-12),
-  the config's own unit of work, on seeded U[-1,1) u and f (synth/). With --gpus N the same
-  mesh is split into N z-slabs (strong scaling, NCCL face-layer halo per apply/sweep).
+Workload at N = 1 (BASELINE.json configs[2], the largest single-GPU config; the metric names no
+config): C3 = 64^3 hexahedra, DG Q4 (125 DoF/cell, 32,768,000 DoF), variable-coefficient
+diffusion K_T = exp(g_T), g ~ N(0, 2^2), alpha = 2, Dirichlet; one STEP = 10 dg_apply + 1
+block-Jacobi sweep (omega = 1, local Jacobi-PCG to 1e-12): the 10:1 apply:sweep mix of
+configs[1]. Inputs are seeded U[-1,1) u and f (synth/). With --gpus N the same mesh is split
+into N z-slabs (strong scaling, NCCL halo per apply/sweep); without torchrun, --gpus N > 1
+re-launches itself under torch.distributed.run. --config C1..C5 selects another BASELINE config
+(C2: 100 applies + 10 sweeps per step, as configs[1] states).
 
 Prints ONE JSON line (rank 0). `value` = DoF processed per second over the whole job
-(global DoF x 110 calls x steps / max-over-ranks device time). Timing: CUDA events on the
-launching stream, W warm-up steps, L2 flushed (512 MiB write) before every timed step, u reset
-to the seeded input before every step (outside the timed region).
+(global DoF x calls per step x steps / max-over-ranks device time). Timing: CUDA events on the
+launching stream, W warm-up steps, L2 flushed (512 MiB write) before every timed step (C3's
+vectors are 262 MB each, twice the L2, anyway), u reset to the seeded input before every step
+(outside the timed region); sweeps ping-pong two buffers (dg_block_jacobi_sweep_to).
 `--impl reference` times the CPU oracle (oracle/, numpy fp64) on a bounded cell sample of the
-same workload instead.
+same workload instead, on all host cores (one process per core).
 """
 from __future__ import annotations
 
@@ -26,7 +30,12 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_APPLY, N_SWEEP = 100, 10
+# applies and sweeps per step: configs[1] states 100 + 10; the larger configs keep its 10:1 mix
+STEP_MIX = {"C1": (1, 1), "C2": (100, 10), "C3": (10, 1), "C4": (10, 1), "C5": (10, 1)}
+DEFAULT_CONFIG = "C3"
+# the fused sweep kernel each config's sweep launches
+SWEEP_KERNEL = {1: "k_cg<2,true>", 2: "k_cg<3,true>", 3: "k_cg<4,true>", 4: "k_cg_w<5,true>",
+                5: "k_cg_w<6,true>", 6: "k_cg_w<7,true>", 7: "k_cg<8,true> (line)"}
 METRIC = "fp64 DoF/s and GFLOP/s (fraction of fp64 peak) for DG apply + block-Jacobi sweep"
 SM_COUNT, DFMA_PER_CLK_PER_SM = 148, 64   # B200: 148 SMs, 64 fp64 FMA lanes per SM per clock
 
@@ -43,8 +52,9 @@ def flops_model(p: int):
 
 
 def describe(P, local_solver):
+    na, ns = STEP_MIX[P.name]
     return (f"{P.name}: {P.nx}x{P.ny}x{P.nz} hex, DG Q{P.p} ({P.nd} DoF/cell, {P.n_dof} DoF), "
-            f"step = {N_APPLY} dg_apply + {N_SWEEP} block-Jacobi sweeps (omega=1, local "
+            f"step = {na} dg_apply + {ns} block-Jacobi sweep(s) (omega=1, local "
             f"{local_solver} to 1e-12)")
 
 
@@ -100,6 +110,18 @@ class Clocks:
                 "samples": len(self.samples), "reasons": sorted(self.reasons), "source": "nvml"}
 
 
+def relaunch_under_torchrun(gpus):
+    """--gpus N > 1 without a torchrun environment: re-exec this script as N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    os.execv(sys.executable, cmd)
+
+
 def init_dist(gpus):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -115,47 +137,84 @@ def init_dist(gpus):
     return rank, world, local
 
 
-def cpu_oracle_sample(P, u, f, seconds: float, kind: str):
-    """Times the oracle (tier B, as it stands) on a bounded sample of cells of the workload and
-    projects the time of one full step; one thread (threadpoolctl)."""
-    import numpy as np
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_worker(args):
+    """One host core: the tier-B oracle (as it stands, one BLAS thread) on its share of the
+    sampled cells; returns (apply seconds, sweep seconds, cells)."""
+    name, cells, seconds = args
     from threadpoolctl import threadpool_limits
     from oracle.tier_b import TierB
+    from synth import make_config, make_vectors
+    P = make_config(name)
+    u, f = make_vectors(P)
     tb = TierB(P)
-    rng = np.random.default_rng(0)
-    t_apply, t_sweep, n_a, n_s = 0.0, 0.0, 0, 0
+    t_apply = t_sweep = 0.0
+    n = 0
     with threadpool_limits(limits=1):
         t_end = time.perf_counter() + seconds
-        while time.perf_counter() < t_end or n_s == 0:
-            c = [int(rng.integers(0, P.n_cells))]
+        for c in cells:
+            if n > 0 and time.perf_counter() > t_end:
+                break
             t0 = time.perf_counter()
-            tb.apply_cells(u, c)
+            tb.apply_cells(u, [c])
             t1 = time.perf_counter()
-            tb.sweep_cells(u, f, 1.0, c)
+            tb.sweep_cells(u, f, 1.0, [c])
             t2 = time.perf_counter()
             t_apply += t1 - t0
             t_sweep += t2 - t1
-            n_a += 1
-            n_s += 1
-    per_cell_apply, per_cell_sweep = t_apply / n_a, t_sweep / n_s
-    step_s = P.n_cells * (N_APPLY * per_cell_apply + N_SWEEP * per_cell_sweep)
-    value = P.n_dof * (N_APPLY + N_SWEEP) / step_s
-    return {"value": value, "unit": "DoF/s", "cores": 1, "kind": kind,
-            "sample": (f"{n_a} random cells of {P.name}: oracle dg_apply (dense per-cell blocks) and "
-                       f"sweep (defect + LU of D_T) timed per cell ({t_apply + t_sweep:.1f} s, 1 thread), "
-                       f"projected to one step of {P.n_cells} cells x ({N_APPLY} applies + "
-                       f"{N_SWEEP} sweeps)"),
+            n += 1
+    return t_apply, t_sweep, n
+
+
+def cpu_oracle_sample(P, seconds: float, kind: str):
+    """Times the oracle (tier B, as it stands: dense per-cell blocks, LU solves) on all host cores
+    (one process per core, one BLAS thread each) on a bounded random sample of the workload's
+    cells, and projects the time of one full step from the measured per-cell times."""
+    import numpy as np
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    rng = np.random.default_rng(0)
+    cells = rng.integers(0, P.n_cells, 4096 * cores).tolist()
+    jobs = [(P.name, cells[w::cores], seconds) for w in range(cores)]
+    t0 = time.perf_counter()
+    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
+        res = list(ex.map(_oracle_worker, jobs))
+    wall = time.perf_counter() - t0
+    t_apply = sum(r[0] for r in res)
+    t_sweep = sum(r[1] for r in res)
+    n = sum(r[2] for r in res)
+    na, ns = STEP_MIX[P.name]
+    per_cell_apply, per_cell_sweep = t_apply / n, t_sweep / n
+    # all cores work at once: the step's cell-seconds divided by the number of cores
+    step_s = P.n_cells * (na * per_cell_apply + ns * per_cell_sweep) / cores
+    value = P.n_dof * (na + ns) / step_s
+    return {"value": value, "unit": "DoF/s", "cores": cores, "kind": kind,
+            "cpu_model": _cpu_model(), "nproc": os.cpu_count(),
+            "sample": (f"{n} random cells of {P.name} on {cores} processes (one per core, one BLAS "
+                       f"thread each, {wall:.1f} s wall): oracle dg_apply (dense per-cell blocks) and "
+                       f"sweep (defect + LU of D_T) timed per cell, projected to one step of "
+                       f"{P.n_cells} cells x ({na} applies + {ns} sweeps) spread over the cores"),
             "apply_s_per_cell": per_cell_apply, "sweep_s_per_cell": per_cell_sweep,
             "projected_step_s": step_s}
 
 
-def extras_single_gpu(dev, peak_derived):
+def extras_single_gpu(dev, peak_derived, skip=None):
     """Context for the judge, outside the timed step (N = 1 only): the volume kernel alone on
-    the larger p >= 3 configs (north_star's >= 50 % target is stated for the volume kernel at
-    p >= 3; C2 is small and tail-bound), dg_apply and a block-Jacobi sweep on C3, C4 and C5
-    (BASELINE configs[2:]), and the SURVEY 8(f) NEXT rows on the bench workload:
-    the stored-inverse block-Jacobi sweep (NEXT-4), a red-black block SSOR sweep (NEXT-2) and the
-    hybrid-multigrid-preconditioned solve (NEXT-1)."""
+    the p >= 3 configs (north_star's >= 50 % target is stated for the volume kernel at p >= 3),
+    dg_apply and a block-Jacobi sweep on the BASELINE configs other than the headline one, and
+    the SURVEY 8(f) NEXT rows on C2: the stored-inverse block-Jacobi sweep (NEXT-4), a red-black
+    block SSOR sweep (NEXT-2) and the hybrid-multigrid-preconditioned solve (NEXT-1)."""
     import torch
     import paper_1805_11930_b200 as dg
     from synth import make_config, make_vectors
@@ -173,7 +232,7 @@ def extras_single_gpu(dev, peak_derived):
         return a.elapsed_time(b) * 1e-3 / calls
 
     out = {"volume_kernel_p_ge_3": {}, "other_configs": {}}
-    for name in ("C4", "C3", "C5"):
+    for name in ("C2", "C4", "C3", "C5"):
         P = make_config(name)
         u, f = make_vectors(P)
         ctx = dg.DGContext(P, device=dev.index or 0)
@@ -182,16 +241,20 @@ def extras_single_gpu(dev, peak_derived):
         n = P.p + 1
         # + 4 n^3 with convection, + 2 n^3 with a reaction term
         vol = 24 * n ** 4 + 8 * n ** 3 + (4 * n ** 3 if any(P.b) else 0) + (2 * n ** 3 if P.c is not None else 0)
-        if name != "C5":
+        if P.p >= 3:
             t = timed(lambda: ctx.apply_parts(ut, o, dg.MASK_VOLUME), 20)
             out["volume_kernel_p_ge_3"][name] = {"p": P.p, "n_dof": P.n_dof, "us_per_call": t * 1e6,
                                                  "frac_fp64_peak": P.n_cells * vol / t / 1e12 / peak_derived}
+        if name == skip:
+            ctx.close()
+            del ut, ft, o
+            continue
         # dg_apply and one block-Jacobi sweep of the config (SURVEY 8(d) flop model; a
         # BiCGStab iteration counts two D_T applications)
         sf, nf = 8 * n ** 3 + 12 * n ** 2, 10 * n ** 3
         t_a = timed(lambda: ctx.apply(ut, o), 10)
-        w = ut.clone()
-        t_s = timed(lambda: ctx.sweep(w, ft, 1.0, 1e-12), 3)
+        w = torch.empty_like(ut)
+        t_s = timed(lambda: ctx.sweep_to(ut, ft, w, 1.0, 1e-12), 3)
         st = ctx.stats()
         cg = P.local_solver == "cg"
         per_it = (vol + 6 * sf + (12 if cg else 20) * n ** 3) * (1 if cg else 2)
@@ -210,7 +273,8 @@ def extras_single_gpu(dev, peak_derived):
     ctx = dg.DGContext(P, device=dev.index or 0)
     ut, ft = torch.from_numpy(u).to(dev), torch.from_numpy(f).to(dev)
     w = ut.clone()
-    t_jac = timed(lambda: ctx.sweep(w, ft, 1.0, 1e-12), 5)
+    w2 = torch.empty_like(ut)
+    t_jac = timed(lambda: ctx.sweep_to(ut, ft, w2, 1.0, 1e-12), 5)
     t_ssor = timed(lambda: ctx.sor_sweep(w, ft, 1.0, 1e-12, symmetric=True), 3)
     ctx.pmf_setup()
     t_pmf = timed(lambda: ctx.pmf_sweep(w, ft, 1.0), 10)
@@ -237,22 +301,23 @@ def extras_single_gpu(dev, peak_derived):
 
 
 def run_reference(args):
+    """The oracle arm: tier B as it stands on all host cores, rank 0 only (the other ranks exit)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from synth import make_config, make_vectors
+    from synth import make_config
     P = make_config(args.config)
-    u, f = make_vectors(P)
     solver = "CG" if P.local_solver == "cg" else "BiCGStab"
     per_step = []
     base = None
     for s in range(args.warmup + args.steps):
-        r = cpu_oracle_sample(P, u, f, args.ref_seconds if s >= args.warmup else 1.0, "oracle")
+        r = cpu_oracle_sample(P, args.ref_seconds if s >= args.warmup else 1.0, "oracle")
         if s >= args.warmup:
             per_step.append(r["projected_step_s"])
             base = r
+    na, ns = STEP_MIX[P.name]
     step_s = statistics.mean(per_step)
-    value = P.n_dof * (N_APPLY + N_SWEEP) / step_s
+    value = P.n_dof * (na + ns) / step_s
     base["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -274,6 +339,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     P = make_config(args.config)
+    n_apply, n_sweep = STEP_MIX[P.name]
     nid = None
     if world > 1:
         import torch.distributed as dist
@@ -285,7 +351,7 @@ def run_ours(args):
     u_h, f_h = make_vectors(P, cell_begin=ctx.cell_begin, cell_end=ctx.cell_end)
     u0 = torch.from_numpy(u_h).to(dev)
     f0 = torch.from_numpy(f_h).to(dev)
-    u = u0.clone()
+    ua, ub = u0.clone(), torch.empty_like(u0)   # sweeps ping-pong (dg_block_jacobi_sweep_to)
     Au = torch.empty_like(u0)
     stream = torch.cuda.current_stream()
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -297,30 +363,33 @@ def run_ours(args):
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    def step(record=None):
+    def step(f, record=None):
+        """n_apply dg_apply, then n_sweep sweeps from ua; returns (launches, buffer holding u)."""
         launches = 0
         e0, e1 = ev(), ev()
         e0.record(stream)
-        for _ in range(N_APPLY):
-            ctx.apply(u, Au)
+        for _ in range(n_apply):
+            ctx.apply(ua, Au)
             launches += ctx.launch_count()
         e1.record(stream)
         sweeps = []
-        for _ in range(N_SWEEP):
+        src, dst = ua, ub
+        for _ in range(n_sweep):
             a, b = ev(), ev()
             a.record(stream)
-            ctx.sweep(u, f0, 1.0, 1e-12)
+            ctx.sweep_to(src, f, dst, 1.0, 1e-12)
             b.record(stream)
             launches += ctx.launch_count()
             sweeps.append((a, b))
+            src, dst = dst, src
         if record is not None:
             record.append(((e0, e1), sweeps))
-        return launches
+        return launches, src
 
     # warm-up
     for _ in range(args.warmup):
-        u.copy_(u0)
-        step()
+        ua.copy_(u0)
+        step(f0)
     torch.cuda.synchronize()
     # timed
     clocks = Clocks(local) if rank == 0 else None
@@ -328,7 +397,7 @@ def run_ours(args):
         clocks.start()
     total_ms, t_apply_ms, sweep_ms, launches = 0.0, 0.0, [], 0
     for _ in range(args.steps):
-        u.copy_(u0)
+        ua.copy_(u0)
         flush.fill_(1.0)
         torch.cuda.synchronize()
         barrier()
@@ -336,7 +405,8 @@ def run_ours(args):
         s0, s1 = ev(), ev()
         rec = []
         s0.record(stream)
-        launches += step(rec)
+        nl, _ = step(f0, rec)
+        launches += nl
         s1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -346,13 +416,15 @@ def run_ours(args):
         sweep_ms += [a.elapsed_time(b) for a, b in sw]
     clk = clocks.stop() if clocks else None
     # iteration counts of the (deterministic) sweeps, replayed untimed
-    u.copy_(u0)
+    ua.copy_(u0)
     it_sums, it_stats = [], []
-    for _ in range(N_SWEEP):
-        ctx.sweep(u, f0, 1.0, 1e-12)
+    src, dst = ua, ub
+    for _ in range(n_sweep):
+        ctx.sweep_to(src, f0, dst, 1.0, 1e-12)
         st = ctx.stats()
         it_sums.append(st["it_sum"])
         it_stats.append(st)
+        src, dst = dst, src
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms, t_apply_ms, sum(sweep_ms)], dtype=torch.float64, device=dev)
@@ -380,18 +452,20 @@ def run_ours(args):
         barrier()
         a, b = ev(), ev()
         a.record(stream)
-        u.copy_(u_pin, non_blocking=True)
+        ua.copy_(u_pin, non_blocking=True)
         # f is first needed by the sweeps: its upload runs on a copy stream under the applies
         copy_stream.wait_stream(stream)
         with torch.cuda.stream(copy_stream):
             f_dev.copy_(f_pin, non_blocking=True)
             f_ready.record(copy_stream)
-        for _ in range(N_APPLY):
-            ctx.apply(u, Au)
+        for _ in range(n_apply):
+            ctx.apply(ua, Au)
         stream.wait_event(f_ready)
-        for _ in range(N_SWEEP):
-            ctx.sweep(u, f_dev, 1.0, 1e-12)
-        out_pin.copy_(u, non_blocking=True)
+        src, dst = ua, ub
+        for _ in range(n_sweep):
+            ctx.sweep_to(src, f_dev, dst, 1.0, 1e-12)
+            src, dst = dst, src
+        out_pin.copy_(src, non_blocking=True)
         b.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -405,12 +479,12 @@ def run_ours(args):
     # ---- the volume kernel alone (a^v terms, Stages 1-3; north_star's >= 50 % target at p >= 3)
     vol_calls = 20
     for _ in range(3):
-        ctx.apply_parts(u, Au, dg.MASK_VOLUME)
+        ctx.apply_parts(ua, Au, dg.MASK_VOLUME)
     flush.fill_(1.0)
     a, b = ev(), ev()
     a.record(stream)
     for _ in range(vol_calls):
-        ctx.apply_parts(u, Au, dg.MASK_VOLUME)
+        ctx.apply_parts(ua, Au, dg.MASK_VOLUME)
     b.record(stream)
     torch.cuda.synchronize()
     vol_s = a.elapsed_time(b) * 1e-3 / vol_calls
@@ -432,16 +506,15 @@ def run_ours(args):
         return
     steps = args.steps
     dof = P.n_dof
-    value = dof * (N_APPLY + N_SWEEP) * steps / (total_ms * 1e-3)
+    value = dof * (n_apply + n_sweep) * steps / (total_ms * 1e-3)
     fm = flops_model(P.p)
     iter_key = "cg_iter" if P.local_solver == "cg" else "bicgstab_iter"
     apply_flops = dof * fm["apply"]
-    sweep_flops_all = N_SWEEP * dof * (fm["apply"] + 4) + it_sum_total * P.nd * fm[iter_key]
-    step_flops = N_APPLY * apply_flops + sweep_flops_all
-    sweep_launch_flops = sweep_flops_all / N_SWEEP
-    sweep_launch_s = tsw * 1e-3 / (steps * N_SWEEP)
-    apply_launch_s = t_apply_ms * 1e-3 / (steps * N_APPLY)
-    sm_clock = (clk or {}).get("sm_max_mhz") or 1965.0
+    sweep_flops_all = n_sweep * dof * (fm["apply"] + 4) + it_sum_total * P.nd * fm[iter_key]
+    step_flops = n_apply * apply_flops + sweep_flops_all
+    sweep_launch_flops = sweep_flops_all / n_sweep
+    sweep_launch_s = tsw * 1e-3 / (steps * n_sweep)
+    apply_launch_s = t_apply_ms * 1e-3 / (steps * n_apply)
     peak_derived = SM_COUNT * DFMA_PER_CLK_PER_SM * 2 * 1965e6 / 1e12
     dominant = "sweep" if tsw >= t_apply_ms else "apply"
     if dominant == "sweep":
@@ -456,7 +529,8 @@ def run_ours(args):
             traffic = tj.get(P.name, {}).get(dominant)
         except Exception:
             traffic = None
-    e2e_value = dof * (N_APPLY + N_SWEEP) * e2e_steps / (e2e_ms * 1e-3)
+    e2e_value = dof * (n_apply + n_sweep) * e2e_steps / (e2e_ms * 1e-3)
+    st0 = it_stats[0]
     line = {
         "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": world, "steps": steps,
         "warmup": args.warmup, "ms_per_step": total_ms / steps, "higher_is_better": True,
@@ -473,17 +547,21 @@ def run_ours(args):
         "sweep": {"dof_per_s": dof / sweep_launch_s, "us_per_call": sweep_launch_s * 1e6,
                   "gflops_model": sweep_launch_flops / sweep_launch_s / 1e9,
                   "frac_fp64_peak": sweep_launch_flops / sweep_launch_s / 1e12 / peak_derived,
-                  "local_iterations_mean": it_stats[0]["it_mean"], "local_iterations_max": it_stats[0]["it_max"],
-                  "local_nonconverged": it_stats[0]["n_nonconverged"]},
+                  "local_iterations_mean": st0["it_mean"], "local_iterations_std": st0["it_std"],
+                  "local_iterations_max": st0["it_max"], "local_iterations_min": st0["it_min"],
+                  "local_nonconverged": st0["n_nonconverged"]},
         "volume_kernel": {"us_per_call": vol_s * 1e6, "gflops_model": vol_flops / vol_s / 1e9,
                           "frac_fp64_peak": vol_flops / vol_s / 1e12 / peak_derived,
                           "model": "24 n^4 + 8 n^3 flop per cell (SURVEY 8(d)); dg_apply_parts(mask=volume)"},
-        "roofline": {"bound": "alu", "kernel": "k_cg<4,true> (fused defect + local CG + update)"
-                     if dominant == "sweep" else "k_apply<4>",
+        "roofline": {"bound": "alu",
+                     "kernel": (SWEEP_KERNEL[P.p] + " (fused defect + local Krylov + update)")
+                     if dominant == "sweep" else f"k_apply (p = {P.p})",
                      "achieved": achieved, "peak": peak_derived, "unit": "TFLOP/s",
                      "frac": achieved / peak_derived, "traffic": traffic,
-                     "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1965 MHz (DESIGN.md)",
-                     "dfma_microbench_tflops": dfma_tflops},
+                     "peak_source": "derived: 148 SMs x 64 DFMA/clk x 2 x 1965 MHz (DESIGN.md); "
+                                    "MEASURED_PEAKS.json has no fp64 entry",
+                     "dfma_microbench_tflops": dfma_tflops,
+                     "share_of_step": (tsw if dominant == "sweep" else t_apply_ms) / total_ms},
         "e2e": {"value": e2e_value, "unit": "DoF/s",
                 "h2d_bytes_per_step": int(world * 2 * u_h.nbytes), "d2h_bytes_per_step": int(world * u_h.nbytes)},
         "gpu_launches": launches,
@@ -491,11 +569,11 @@ def run_ours(args):
     }
     if world == 1 and not args.no_extras:
         try:
-            line["extras"] = extras_single_gpu(dev, peak_derived)
+            line["extras"] = extras_single_gpu(dev, peak_derived, skip=P.name)
         except Exception as exc:   # context only: never lose the bench line over it
             line["extras"] = {"error": repr(exc)}
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_oracle_sample(P, u_h, f_h, args.cpu_seconds, "oracle")
+        line["cpu_baseline"] = cpu_oracle_sample(P, args.cpu_seconds, "oracle")
     print(json.dumps(line), flush=True)
     ctx.close()
 
@@ -506,12 +584,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(STEP_MIX))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     else:

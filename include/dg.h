@@ -50,12 +50,20 @@ enum { DG_BC_DIRICHLET = 0, DG_BC_NEUMANN = 1 };                 /* P:284-288 */
 /* local Krylov method; DG_LOCAL_BICGSTAB_THOMAS: BiCGStab right-preconditioned by the tridiagonal
  * part of D_T in DoF order (Thomas algorithm), for strongly convection-dominated
  * blocks where the diagonal fails; p <= 4. DG_LOCAL_GMRES / DG_LOCAL_GMRES_THOMAS:
- * restarted GMRES(k) (the paper's local method for the convection test; k = 15 at
- * p = 1 and 3, 13 at p = 2) with the diagonal or the tridiagonal right preconditioner; p <= 3
- * (Krylov basis in tensor memory). dg_get_stats counts Arnoldi steps for GMRES. */
+ * restarted GMRES(k) (the paper's local method for the convection test; k <= 15 at
+ * p = 1 and 3, 13 at p = 2, 9 at p = 4) with the diagonal or the tridiagonal right
+ * preconditioner; p <= 4 (Krylov basis in tensor memory). dg_get_stats counts Arnoldi steps. */
 enum { DG_LOCAL_AUTO = 0, DG_LOCAL_CG = 1, DG_LOCAL_BICGSTAB = 2, DG_LOCAL_BICGSTAB_THOMAS = 3,
        DG_LOCAL_GMRES = 4, DG_LOCAL_GMRES_THOMAS = 5 };
 enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
+/* Kernel variants (dg_set_kernel_variant): the same operator / solver through another kernel of
+ * the build, for A/B measurements and for parity tests of every kernel whose speed is reported.
+ * 0 = the measured defaults. DG_VARIANT_VOLUME_PREFETCH: the register-prefetch persistent volume
+ * kernel at p = 3 (default: the slim one); DG_VARIANT_LINE: line-per-thread kernels at every
+ * degree; DG_VARIANT_NO_TMEM: shared-memory p = 3 BiCGStab (default: Krylov vectors in tensor
+ * memory); DG_VARIANT_LINE_CG_CTA: CTA-barrier line solvers at p = 4..6 (default: warp per cell). */
+enum { DG_VARIANT_VOLUME_PREFETCH = 1, DG_VARIANT_LINE = 2, DG_VARIANT_NO_TMEM = 4,
+       DG_VARIANT_LINE_CG_CTA = 8 };
 
 typedef struct {
   int32_t nx, ny, nz;        /* GLOBAL cells per axis (uniform cells, D2 of SURVEY §2.1) */
@@ -65,7 +73,10 @@ typedef struct {
   double alpha;              /* penalty parameter of gamma_F; configs use 2.0 */
   int32_t k_components;      /* 1: scalar K per cell; 3: diagonal (Kx,Ky,Kz) per cell */
   const double* K;           /* HOST, GLOBAL [nx*ny*nz][k_components], >= 0; copied at create */
-  double b[3];               /* constant advection field b */
+  double b[3];               /* constant advection field b, used when b_cell is NULL */
+  const double* b_cell;      /* HOST, GLOBAL [nx*ny*nz][3] per-cell advection b_T (b = b(x)),
+                                finite, or NULL (constant b); copied at create. The volume term uses
+                                the cell's b_T, a face b_nu = nu . (b^- + b^+)/2 (DESIGN reading #8) */
   const double* c;           /* HOST, GLOBAL [nx*ny*nz] reaction >= 0, or NULL (c = 0) */
   int32_t rank, nranks;      /* z-slab decomposition; nranks = 1 for a single GPU */
   int32_t halo_mode;         /* DG_HALO_NCCL or DG_HALO_EXTERNAL (caller fills ghost layers) */
@@ -103,6 +114,12 @@ dg_status dg_apply(dg_ctx* ctx, const double* u, double* Au, void* cuda_stream);
 dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double omega,
                                 double local_tol, void* cuda_stream);
 
+/* The same sweep out of place: u_new = u + omega D^{-1}(f - A u). u, f, u_new: device
+ * [n_local_dof]; u_new must not alias u or f (callers ping-pong two buffers; the in-place form
+ * above writes a library scratch vector and copies it back, +16 B/DoF of traffic). */
+dg_status dg_block_jacobi_sweep_to(dg_ctx* ctx, const double* u, const double* f, double* u_new,
+                                   double omega, double local_tol, void* cuda_stream);
+
 /* Block SOR / SSOR in the red-black cell order (Alg. 3): colour
  * (cx + cy + cz) mod 2 (global indices), red = 0 first. A forward sweep updates all red cells
  * from the current u, then all black cells from the updated u, each cell by
@@ -113,7 +130,7 @@ dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double 
  * parallel launch (p <= 3 with nx even: only that colour's cells are launched, updated in place).
  * With nranks > 1 the z-halo is exchanged before every half-sweep (NCCL halo mode only;
  * DG_ERR_UNSUPPORTED in external-halo mode). The per-cell statistics (dg_get_stats) are those of
- * the last half-sweep (0 iterations for the cells it skipped). */
+ * the last half-sweep (0 iterations for the cells it skipped, in either launch mode). */
 dg_status dg_block_sor_sweep(dg_ctx* ctx, double* u, const double* f, double omega, double local_tol,
                              int32_t symmetric, void* cuda_stream);
 
@@ -121,9 +138,16 @@ dg_status dg_block_sor_sweep(dg_ctx* ctx, double* u, const double* f, double ome
 dg_status dg_local_block_solve(dg_ctx* ctx, const double* d, double* du, double local_tol,
                                void* cuda_stream);
 
-/* Local Krylov method (DG_LOCAL_AUTO: CG if b == 0 else BiCGStab) and iteration cap
- * (default 1000; reading #13 of SURVEY §8(c)). */
-dg_status dg_set_local_solver(dg_ctx* ctx, int32_t method, int32_t max_it);
+/* Local Krylov method (DG_LOCAL_AUTO: CG if b == 0 everywhere, else BiCGStab), iteration cap
+ * (default 1000; reading #13 of SURVEY §8(c)) and GMRES restart length (0: the largest basis
+ * the tensor memory holds: 15 at p = 1, 3, 13 at p = 2, 9 at p = 4; larger values are clamped to
+ * it). A CG that breaks down (p^T D_T p <= 0: D_T not SPD) stops and counts as not converged. */
+dg_status dg_set_local_solver(dg_ctx* ctx, int32_t method, int32_t max_it, int32_t gmres_restart);
+
+/* Selects the kernel variant bits (DG_VARIANT_*) used by the later calls on ctx. At create they
+ * default to the environment switches DG_VOLUME_SLIM=0, DG_KERNEL_FAMILY=line, DG_NO_TMEM=1,
+ * DG_LINE_CG_CTA=1 (else 0). Unknown bits -> DG_ERR_INVALID. */
+dg_status dg_set_kernel_variant(dg_ctx* ctx, uint32_t variant);
 
 /* Synchronises the last sweep/solve stream and reduces its per-cell iteration counts. */
 dg_status dg_get_stats(dg_ctx* ctx, dg_stats* st);
@@ -205,9 +229,10 @@ dg_status dg_hybrid_solve(dg_ctx* ctx, double* u, const double* f, const dg_hybr
 
 /* ---- Stored-inverse block-Jacobi smoother (the paper's partially
  * matrix-free variant, Table 2) -----------------------------------------------------
- * dg_pmf_setup assembles every D_T from the 1D matrices, inverts it (Gauss-Jordan in
- * shared memory; SPD for b = 0) and keeps the inverses on the device: n_cells (p+1)^6 doubles.
- * b = 0 and p <= 4 only (otherwise DG_ERR_UNSUPPORTED); DG_ERR_NOMEM if they do not fit.
+ * dg_pmf_setup assembles every D_T from the 1D matrices, inverts it (Gauss-Jordan
+ * with partial pivoting in shared memory: the blocks are nonsymmetric for b != 0) and keeps the
+ * inverses on the device: n_cells (p+1)^6 doubles. p <= 4 only (otherwise DG_ERR_UNSUPPORTED);
+ * DG_ERR_NOMEM if they do not fit. Slab-boundary faces use the ghost-layer coefficients.
  * dg_pmf_sweep: one block-Jacobi sweep with exact local solves, u <- u + omega D^{-1}(f - A u),
  * u in place (device). dg_pmf_block: HOST copy of D_T (inverse = 0) or D_T^{-1} (inverse = 1)
  * of one local cell, nd x nd row-major (test index first), for parity tests (synchronises). */

@@ -190,6 +190,17 @@ class TierB:
                         out[r] += self.embed(axis, B) @ U[nb]
         return out
 
+    def volume_apply(self, u):
+        """A^v u for every cell at once: volume_block's sum of coefficient-weighted Kronecker
+        operators, applied to all cells (rows of U) by linearity (large meshes)."""
+        U = np.asarray(u).reshape(-1, self.nd)
+        out = np.zeros_like(U)
+        for a in range(3):
+            out += self.K[:, a:a + 1] * (U @ self.embed(a, self.Sh / self.h[a]).T)
+            out -= self.b[:, a:a + 1] * (U @ self.embed(a, self.Ch).T)
+        out += self.c[:, None] * (U @ kron3(self.M1(2), self.M1(1), self.M1(0)).T)
+        return out.reshape(-1)
+
     def block_diag_apply(self, u, cells=None):
         cells = range(self.P.n_cells) if cells is None else cells
         U = np.asarray(u).reshape(-1, self.nd)

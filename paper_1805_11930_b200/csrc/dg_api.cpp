@@ -87,6 +87,8 @@ struct dg_ctx {
   dg::Tables1D tab{};
   dg::KParams kp{};
   double* d_K = nullptr;
+  double* d_bc = nullptr;      // per-cell b with ghost layers (or nullptr)
+  bool has_b = false;          // any non-zero advection (selects BiCGStab for DG_LOCAL_AUTO)
   double* d_c = nullptr;
   double* d_ghost_lo = nullptr;
   double* d_ghost_hi = nullptr;
@@ -104,6 +106,7 @@ struct dg_ctx {
   double* d_pmf_au = nullptr;  // A u of a stored-inverse sweep [ndof]
   int method = 0;  // resolved local method
   int32_t max_it = 1000;
+  int32_t krestart = 0;   // GMRES restart (0: the kernel's basis size)
   ncclComm_t comm = nullptr;
   cudaStream_t last_stream = nullptr;
   bool have_stats = false;
@@ -127,6 +130,9 @@ dg_status validate(const dg_desc* d) {
   if (!d->K) return fail(DG_ERR_INVALID, "K is NULL");
   for (int i = 0; i < 3; ++i)
     if (!std::isfinite(d->b[i])) return fail(DG_ERR_INVALID, "b must be finite");
+  if (d->b_cell)
+    for (int64_t i = 0; i < (int64_t)d->nx * d->ny * d->nz * 3; ++i)
+      if (!std::isfinite(d->b_cell[i])) return fail(DG_ERR_INVALID, "b_cell must be finite");
   if (d->nranks < 1 || d->rank < 0 || d->rank >= d->nranks)
     return fail(DG_ERR_INVALID, "need 0 <= rank < nranks");
   if (d->nranks > d->nz) return fail(DG_ERR_INVALID, "nranks must not exceed nz (empty slab)");
@@ -147,6 +153,7 @@ void release(dg_ctx* c) {
   if (!c) return;
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
   cudaFree(c->d_K);
+  cudaFree(c->d_bc);
   cudaFree(c->d_c);
   cudaFree(c->d_ghost_lo);
   cudaFree(c->d_ghost_hi);
@@ -222,6 +229,7 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   dg_ctx* c = new dg_ctx();
   c->desc = *desc;
   c->desc.K = nullptr;
+  c->desc.b_cell = nullptr;
   c->desc.c = nullptr;
   c->desc.nccl_id = nullptr;
   c->n = desc->p + 1;
@@ -252,6 +260,21 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 8); };
   if ((e = alloc((void**)&c->d_K, K3.size() * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc K"); }
   if ((e = cudaMemcpy(c->d_K, K3.data(), K3.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy K"); }
+  c->has_b = desc->b[0] != 0.0 || desc->b[1] != 0.0 || desc->b[2] != 0.0;
+  if (desc->b_cell) {
+    // per-cell b, one ghost z-layer on each side like K (the faces average both cells' b)
+    c->has_b = false;
+    for (int64_t i = 0; i < (int64_t)desc->nx * desc->ny * desc->nz * 3; ++i)
+      if (desc->b_cell[i] != 0.0) { c->has_b = true; break; }
+    std::vector<double> B3((size_t)(c->nzl + 2) * nxy * 3, 0.0);
+    for (int zl = -1; zl <= c->nzl; ++zl) {
+      const int zg = c->z_begin + zl;
+      if (zg < 0 || zg >= desc->nz) continue;
+      std::memcpy(&B3[(size_t)(zl + 1) * nxy * 3], desc->b_cell + (size_t)zg * nxy * 3, (size_t)nxy * 3 * 8);
+    }
+    if ((e = alloc((void**)&c->d_bc, B3.size() * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc b_cell"); }
+    if ((e = cudaMemcpy(c->d_bc, B3.data(), B3.size() * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy b_cell"); }
+  }
   if (desc->c) {
     if ((e = alloc((void**)&c->d_c, (size_t)c->ncells * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc c"); }
     if ((e = cudaMemcpy(c->d_c, desc->c + (size_t)c->z_begin * nxy, (size_t)c->ncells * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy c"); }
@@ -283,6 +306,7 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   kp.slab_face[4] = r > 0 ? dg::FK_GHOST : (desc->bc[4] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN);
   kp.slab_face[5] = r < G - 1 ? dg::FK_GHOST : (desc->bc[5] == DG_BC_DIRICHLET ? dg::FK_DIRICHLET : dg::FK_NEUMANN);
   kp.K = c->d_K;
+  kp.bc = c->d_bc;
   kp.c = c->d_c;
   kp.ghost_lo = r > 0 ? c->d_ghost_lo : nullptr;
   kp.ghost_hi = r < G - 1 ? c->d_ghost_hi : nullptr;
@@ -292,6 +316,15 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   kp.cmap = 0;
   kp.zoff = c->z_begin;
   kp.gperm = nullptr;
+  kp.variant = 0;
+  {
+    const char* v = std::getenv("DG_VOLUME_SLIM");
+    if (v && v[0] == '0') kp.variant |= dg::VAR_VOLUME_PREFETCH;
+    v = std::getenv("DG_KERNEL_FAMILY");
+    if (v && v[0] == 'l') kp.variant |= dg::VAR_LINE;
+  }
+  if (getenv_flag("DG_NO_TMEM")) kp.variant |= dg::VAR_NO_TMEM;
+  if (getenv_flag("DG_LINE_CG_CTA")) kp.variant |= dg::VAR_LINE_CG_CTA;
   if (const int C = dg::solver_group_cells(desc->p); C > 0 && !getenv_flag("DG_NO_GPERM")) {
     // Longest-processing-time-first order for the local-solver CTAs: cells with Dirichlet faces
     // take more local iterations (the penalty stiffens their block), so the groups holding them
@@ -315,7 +348,7 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
     cudaMemcpy(c->d_gperm, perm.data(), (size_t)ng * 4, cudaMemcpyHostToDevice);
     kp.gperm = c->d_gperm;
   }
-  c->method = (desc->b[0] == 0.0 && desc->b[1] == 0.0 && desc->b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
+  c->method = c->has_b ? dg::LM_BICGSTAB : dg::LM_CG;
   c->max_it = 1000;
 
   if (G > 1 && desc->halo_mode == DG_HALO_NCCL) {
@@ -376,26 +409,37 @@ dg_status dg_fill_ghosts(dg_ctx* c, const double* lo, const double* hi, void* st
   return DG_OK;
 }
 
-dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it) {
+dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it, int32_t gmres_restart) {
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (max_it < 1) return fail(DG_ERR_INVALID, "max_it must be >= 1");
+  if (gmres_restart < 0) return fail(DG_ERR_INVALID, "gmres_restart must be >= 0");
+  int m;
   if (method == DG_LOCAL_AUTO) {
-    const double* b = c->desc.b;
-    c->method = (b[0] == 0.0 && b[1] == 0.0 && b[2] == 0.0) ? dg::LM_CG : dg::LM_BICGSTAB;
+    m = c->has_b ? dg::LM_BICGSTAB : dg::LM_CG;
   } else if (method == DG_LOCAL_CG) {
-    c->method = dg::LM_CG;
+    m = dg::LM_CG;
   } else if (method == DG_LOCAL_BICGSTAB) {
-    c->method = dg::LM_BICGSTAB;
+    m = dg::LM_BICGSTAB;
   } else if (method == DG_LOCAL_BICGSTAB_THOMAS) {
     if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "the tridiagonal preconditioner needs p <= 4 (plane kernels)");
-    c->method = dg::LM_BICGSTAB_THOMAS;
+    m = dg::LM_BICGSTAB_THOMAS;
   } else if (method == DG_LOCAL_GMRES || method == DG_LOCAL_GMRES_THOMAS) {
-    if (c->desc.p > 3) return fail(DG_ERR_UNSUPPORTED, "local GMRES needs p <= 3 (Krylov basis in tensor memory)");
-    c->method = method == DG_LOCAL_GMRES ? dg::LM_GMRES : dg::LM_GMRES_THOMAS;
+    if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "local GMRES needs p <= 4 (Krylov basis in tensor memory)");
+    if (c->kp.variant & dg::VAR_LINE) return fail(DG_ERR_UNSUPPORTED, "local GMRES exists in the plane kernels only");
+    m = method == DG_LOCAL_GMRES ? dg::LM_GMRES : dg::LM_GMRES_THOMAS;
   } else {
     return fail(DG_ERR_INVALID, "unknown local method");
   }
+  c->method = m;
   c->max_it = max_it;
+  c->krestart = gmres_restart;
+  return DG_OK;
+}
+
+dg_status dg_set_kernel_variant(dg_ctx* c, uint32_t variant) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (variant & ~15u) return fail(DG_ERR_INVALID, "unknown kernel variant bits");
+  c->kp.variant = variant;
   return DG_OK;
 }
 
@@ -443,9 +487,30 @@ dg_status dg_local_block_solve(dg_ctx* c, const double* d, double* du, double to
   dg::KParams kp = c->kp;
   kp.tol2 = tol * tol;
   kp.max_it = c->max_it;
+  kp.krestart = c->krestart;
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = dg::launch_local_solve(c->desc.p, c->method, kp, d, du, s);
   if (e != cudaSuccess) return cuda_fail(e, "local_block_solve");
+  c->last_stream = s;
+  c->have_stats = true;
+  c->launches = 1;
+  return DG_OK;
+}
+
+static dg_status sweep_impl(dg_ctx* c, const double* u, const double* f, double* u_new, double omega,
+                            double tol, cudaStream_t s) {
+  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
+  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  c->launches = 0;
+  dg_status st = halo_exchange(c, u, s);
+  if (st != DG_OK) return st;
+  dg::KParams kp = c->kp;
+  kp.tol2 = tol * tol;
+  kp.max_it = c->max_it;
+  kp.krestart = c->krestart;
+  kp.omega = omega;
+  cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, u_new, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sweep");
   c->last_stream = s;
   c->have_stats = true;
   c->launches = 1;
@@ -456,24 +521,21 @@ dg_status dg_block_jacobi_sweep(dg_ctx* c, double* u, const double* f, double om
                                 void* stream) {
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
-  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
-  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
   cudaStream_t s = (cudaStream_t)stream;
-  c->launches = 0;
-  dg_status st = halo_exchange(c, u, s);
+  dg_status st = sweep_impl(c, u, f, c->d_unew, omega, tol, s);
   if (st != DG_OK) return st;
-  dg::KParams kp = c->kp;
-  kp.tol2 = tol * tol;
-  kp.max_it = c->max_it;
-  kp.omega = omega;
-  cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, c->d_unew, s);
-  if (e != cudaSuccess) return cuda_fail(e, "sweep");
-  e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
+  // in place: the kernel reads the neighbours' u, so it writes a scratch vector copied back
+  cudaError_t e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "sweep copy-back");
-  c->last_stream = s;
-  c->have_stats = true;
-  c->launches = 1;
   return DG_OK;
+}
+
+dg_status dg_block_jacobi_sweep_to(dg_ctx* c, const double* u, const double* f, double* u_new,
+                                   double omega, double tol, void* stream) {
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f") || check_vec(u_new, "u_new")) return DG_ERR_INVALID;
+  if (u_new == u || u_new == f) return fail(DG_ERR_INVALID, "u_new must not alias u or f");
+  return sweep_impl(c, u, f, u_new, omega, tol, (cudaStream_t)stream);
 }
 
 dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega, double tol,
@@ -500,10 +562,15 @@ dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega
     dg::KParams kp = c->kp;
     kp.tol2 = tol * tol;
     kp.max_it = c->max_it;
+    kp.krestart = c->krestart;
     kp.omega = omega;
     kp.colour = order[h];
     kp.cmap = compact ? 1 : 0;
-    cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, compact ? u : c->d_unew, s);
+    cudaError_t e = cudaSuccess;
+    // compact mode launches one colour only: clear the counts so that the skipped colour reads
+    // 0 iterations, as in masked mode (dg_get_stats = the last half-sweep)
+    if (compact) e = cudaMemsetAsync(c->d_its, 0, (size_t)c->ncells * 4, s);
+    if (e == cudaSuccess) e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, compact ? u : c->d_unew, s);
     if (e != cudaSuccess) return cuda_fail(e, "sor half-sweep");
     if (!compact) {
       e = cudaMemcpyAsync(u, c->d_unew, (size_t)c->ndof * 8, cudaMemcpyDeviceToDevice, s);
@@ -602,21 +669,34 @@ namespace {
 dg_status hybrid_prepare(dg_ctx* c, cudaStream_t s) {
   if (c->desc.nranks != 1)
     return fail(DG_ERR_UNSUPPORTED, "hybrid multigrid: single rank only (the coarse solve is not distributed)");
-  if (c->desc.b[0] != 0.0 || c->desc.b[1] != 0.0 || c->desc.b[2] != 0.0)
-    return fail(DG_ERR_UNSUPPORTED, "hybrid multigrid: b = 0 only (outer CG)");
-  if (c->d_Ah) return DG_OK;
+  if (c->has_b) return fail(DG_ERR_UNSUPPORTED, "hybrid multigrid: b = 0 only (outer CG)");
+  if (c->d_Ah) return DG_OK;   // set only once everything below has succeeded
   const size_t N = (size_t)c->ncells, nd = (size_t)c->ndof;
-  cudaError_t e = cudaMalloc(&c->d_Ah, 7 * N * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_cvec, 7 * N * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_part, (size_t)dg::kPartials * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_dots, 3 * 8);
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_cits, sizeof(int));
-  if (e == cudaSuccess) e = cudaMalloc(&c->d_hv, 6 * nd * 8);
-  if (e != cudaSuccess) return fail(DG_ERR_NOMEM, "hybrid multigrid scratch");
+  double *Ah = nullptr, *cvec = nullptr, *part = nullptr, *dts = nullptr, *hv = nullptr;
+  int* cits = nullptr;
+  auto drop = [&]() {
+    cudaFree(Ah); cudaFree(cvec); cudaFree(part); cudaFree(dts); cudaFree(cits); cudaFree(hv);
+  };
+  cudaError_t e = cudaMalloc(&Ah, 7 * N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&cvec, 7 * N * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&part, (size_t)dg::kPartials * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&dts, 3 * 8);
+  if (e == cudaSuccess) e = cudaMalloc(&cits, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&hv, 6 * nd * 8);
+  if (e != cudaSuccess) {
+    cudaGetLastError();   // clear the allocation error so later launches do not report it
+    drop();
+    return fail(DG_ERR_NOMEM, "hybrid multigrid scratch");
+  }
   dg::KParams kp = c->kp;
   kp.mask = 7u;
-  e = dg::launch_coarse_matrix(kp, c->d_Ah, s);
-  if (e != cudaSuccess) return cuda_fail(e, "coarse matrix");
+  e = dg::launch_coarse_matrix(kp, Ah, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    drop();
+    return cuda_fail(e, "coarse matrix");
+  }
+  c->d_Ah = Ah; c->d_cvec = cvec; c->d_part = part; c->d_dots = dts; c->d_cits = cits; c->d_hv = hv;
   return DG_OK;
 }
 
@@ -774,8 +854,6 @@ dg_status dg_hybrid_solve(dg_ctx* c, double* u, const double* f, const dg_hybrid
 namespace {
 dg_status pmf_check(dg_ctx* c) {
   if (c->desc.p > 4) return fail(DG_ERR_UNSUPPORTED, "stored inverses: p <= 4 only ((p+1)^6 doubles per cell)");
-  if (c->desc.b[0] != 0.0 || c->desc.b[1] != 0.0 || c->desc.b[2] != 0.0)
-    return fail(DG_ERR_UNSUPPORTED, "stored inverses: b = 0 only (SPD blocks, no pivoting)");
   return DG_OK;
 }
 }  // namespace
@@ -842,6 +920,9 @@ dg_status dg_pmf_block(dg_ctx* c, int64_t cell, int32_t inverse, double* host_ou
   if (e == cudaSuccess) e = cudaMemcpy(host_out, tmp, (size_t)nd * nd * 8, cudaMemcpyDeviceToHost);
   cudaFree(tmp);
   if (e != cudaSuccess) return cuda_fail(e, "pmf block");
+  if (inverse)   // the device keeps the inverse transposed (coalesced sweep reads)
+    for (int i = 0; i < nd; ++i)
+      for (int j = i + 1; j < nd; ++j) std::swap(host_out[(size_t)i * nd + j], host_out[(size_t)j * nd + i]);
   return DG_OK;
 }
 

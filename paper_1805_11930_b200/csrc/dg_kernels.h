@@ -8,6 +8,8 @@
 namespace dg {
 
 enum FaceKind : int32_t { FK_DIRICHLET = 0, FK_NEUMANN = 1, FK_GHOST = 2 };
+// kernel variant bits (= DG_VARIANT_* of dg.h)
+enum : uint32_t { VAR_VOLUME_PREFETCH = 1u, VAR_LINE = 2u, VAR_NO_TMEM = 4u, VAR_LINE_CG_CTA = 8u };
 
 // Everything a kernel needs about the local slab (passed by value).
 struct KParams {
@@ -21,10 +23,13 @@ struct KParams {
   int32_t slab_face[6];          // x-,x+,y-,y+,z-,z+ of the slab: FaceKind
   const double* K;               // [(nzl+2)*nx*ny][3] diagonal K, z-shifted by one ghost layer
   const double* c;               // [ncells] reaction or nullptr
+  const double* bc;              // [(nzl+2)*nx*ny][3] per-cell b (ghost layers as K) or nullptr:
+                                 // constant kp.b; volume: the cell's b, faces: (b^- + b^+)/2 . nu
   const double* ghost_lo;        // [nx*ny*n^3] neighbour rank's last layer (or nullptr)
   const double* ghost_hi;        // [nx*ny*n^3] neighbour rank's first layer
   uint32_t mask;                 // 1 volume, 2 interior faces, 4 boundary faces
   int32_t max_it;
+  int32_t krestart;              // GMRES restart length (0: the compiled basis size)
   double tol2;                   // local_tol^2
   double omega;
   int32_t* its;                  // [ncells] iterations of the last solve
@@ -33,6 +38,7 @@ struct KParams {
   int32_t zoff;                  // global z index of the slab's first layer (for the colour)
   const int32_t* gperm;          // order in which the solver CTAs take the cell groups (longest
                                  // first: groups with Dirichlet faces), nullptr = in order
+  uint32_t variant;              // VAR_* kernel variant bits (0 = the measured defaults)
   int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
                                  // group_cell), the other colour is not touched
 };

@@ -88,6 +88,7 @@ template <int N> struct Group {
   static constexpr int C = Cells<N>::C;
   int cell[C];
   double vc[C][4];              // |T|K_x/h_x^2, |T|K_y/h_y^2, |T|K_z/h_z^2, |T|c
+  double vb[C][3];              // |T| b_k / h_k (the cell's advection)
   double fc[C][6][6];           // per face: cs_a, cs_g, cn_a, cn_g, ct_a, ct_n
   const double* nb[C][6];       // neighbour cell base pointer (nullptr: none / not needed)
   double tw[N], td0[N], td1[N]; // runtime-indexed copies of w, d0, d1
@@ -185,7 +186,7 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
 // Per cell of the group: volume scalings vc, face coefficients fc, neighbour pointers nb
 // (nullptr when u == nullptr, i.e. for D_T-only operators). Ends with __syncthreads.
 template <int N, int C, int NT>
-__device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6][6],
+__device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*vb_)[3], double (*fc_)[6][6],
                             const double* (*nb_)[6], int* cellv, int cell0, const double* u) {
   constexpr int N3 = N * N * N;
   const int t = threadIdx.x;
@@ -207,8 +208,11 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
         vc[1] = Kc[1] * vol * kp.ih[1] * kp.ih[1];
         vc[2] = Kc[2] * vol * kp.ih[2] * kp.ih[2];
         vc[3] = kp.c ? vol * kp.c[cell] : 0.0;
+        const double* bcl = kp.bc ? kp.bc + (size_t)(cell + nxy) * 3 : kp.b;
+        for (int a = 0; a < 3; ++a) vb_[cs][a] = vol * bcl[a] * kp.ih[a];
       } else {
         vc[0] = vc[1] = vc[2] = vc[3] = 0.0;
+        vb_[cs][0] = vb_[cs][1] = vb_[cs][2] = 0.0;
       }
     }
     if (valid) {
@@ -240,7 +244,9 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*fc_)[6
           kind = (sk == FK_DIRICHLET) ? 1 : 2;
         }
       }
-      const double bn = kp.b[axis];
+      // b . nu_F on the face (reading #8: the mean of the two cells' b; exact for constant b)
+      const double bT = kp.bc ? kp.bc[(size_t)(cell + nxy) * 3 + axis] : kp.b[axis];
+      const double bn = kind == 0 ? 0.5 * (bT + (kp.bc ? kp.bc[(size_t)kidx * 3 + axis] : bT)) : bT;
       if (kind == 0 && (kp.mask & 2u)) {
         const double KN = kp.K[(size_t)kidx * 3 + axis];
         const double s = KT + KN;
@@ -279,7 +285,7 @@ __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const dou
     g.td0[t] = c_tab[N].d0[t];
     g.td1[t] = c_tab[N].d1[t];
   }
-  setup_cells<N, G::C, NTH>(kp, g.vc, g.fc, g.nb, g.cell, cell0, u);
+  setup_cells<N, G::C, NTH>(kp, g.vc, g.vb, g.fc, g.nb, g.cell, cell0, u);
 }
 
 // ---- tiles ---------------------------------------------------------------------
@@ -368,8 +374,6 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   const int le = WARP ? ((tid >> 5) + 1) * N2 : LINES;
   constexpr int ls = WARP ? 32 : NT;
   const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
-  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
-  const double sb[3] = {T3 * kp.b[0] * inv_h[0], T3 * kp.b[1] * inv_h[1], T3 * kp.b[2] * inv_h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
 
   // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
@@ -435,7 +439,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       const double sc = g.vc[cs][3];
 #pragma unroll
       for (int q = 0; q < N; ++q) R[q] = Wl * c_tab[N].w[q] * sc * U[q];
-      dir_term<N>(U, R, Wl, g.vc[cs][2], sb[2]);
+      dir_term<N>(U, R, Wl, g.vc[cs][2], g.vb[cs][2]);
       if constexpr (USEB) bterm<N>(g.Bf[cs][2], U, R, Wl);
       st<N, G::ZS>(SA + off, U);
       st<N, G::ZS>(SB + off, R);
@@ -448,7 +452,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N];
       ld<N, 1>(SA + off, U);
       ld<N, 1>(SB + off, R);
-      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], sb[0]);
+      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], g.vb[cs][0]);
       if constexpr (USEB) bterm<N>(g.Bf[cs][0], U, R, g.tw[a] * g.tw[b]);
       st<N, 1>(SB + off, R);
     }
@@ -460,7 +464,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N], o[N];
       ld<N, G::YS>(SA + off, U);
       ld<N, G::YS>(SB + off, R);
-      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], sb[1]);
+      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], g.vb[cs][1]);
       if constexpr (USEB) bterm<N>(g.Bf[cs][1], U, R, g.tw[a] * g.tw[b]);
       mtv<N, 0>(R, o);
       st<N, G::YS>(SB + off, o);
@@ -531,8 +535,6 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
 template <int N, int NTH = Geo<N>::NT>
 __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
   using G = Geo<N>;
-  const double T3 = kp.h[0] * kp.h[1] * kp.h[2];
-  const double sb[3] = {T3 * kp.b[0] / kp.h[0], T3 * kp.b[1] / kp.h[1], T3 * kp.b[2] / kp.h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
   for (int e = threadIdx.x; e < G::C * G::N3; e += NTH) {
     const int cs = e / G::N3, r = e % G::N3;
@@ -545,6 +547,7 @@ __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
       Cd[a] = c_tab[N].Cd[idx[a]];
     }
     const double* vc = g.vc[cs];
+    const double* sb = g.vb[cs];
     double d = vc[3] * Md[0] * Md[1] * Md[2];
     d += (vc[0] * Sd[0] - sb[0] * Cd[0]) * Md[1] * Md[2];
     d += (vc[1] * Sd[1] - sb[1] * Cd[1]) * Md[0] * Md[2];
@@ -700,7 +703,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       double alpha = 0.0;
       if (!g.conv[tid]) {
         if (pq > 0.0) alpha = g.sc[S_RZ][tid] / pq;
-        else g.conv[tid] = 1;  // breakdown (p = 0): keep the last iterate
+        else g.conv[tid] = 2;  // breakdown (D_T not SPD): keep the last iterate, not converged
       }
       g.sc[S_ALPHA][tid] = alpha;
     }
@@ -765,7 +768,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       st<N, 1>(ob + cs * G::N3 + k * G::N2 + j * N, x);
     }
   })
-  if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] ? g.its[tid] : (g.its[tid] | (1 << 30));
+  if (tid < nvalid) kp.its[cell0 + tid] = g.conv[tid] == 1 ? g.its[tid] : (g.its[tid] | (1 << 30));
 }
 
 // Jacobi-preconditioned CG with one warp per cell (n = 5: 25 lanes hold the cell's lines).
@@ -869,8 +872,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         for (int e = 0; e < N; ++e) pq = fma(p[m][e], q[m][e], pq);
       }
     pq = warp_sum(pq);
-    if (!(pq > 0.0)) {   // breakdown (p = 0): keep the last iterate
-      conv = true;
+    if (!(pq > 0.0)) {   // breakdown (D_T not SPD): keep the last iterate, not converged
       break;
     }
     const double alpha = quot_nr(rz, pq);
@@ -1414,26 +1416,11 @@ cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, c
   return cudaGetLastError();
 }
 
-// BiCGStab at n = 4 keeps x, p, v in tensor memory (2 CTAs per SM); DG_NO_TMEM=1 selects the
-// shared-memory variant (A/B comparisons)
-static bool use_tmem() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DG_NO_TMEM");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// DG_KERNEL_FAMILY=line forces the line-per-thread kernels for every degree (A/B comparisons).
-static bool force_line() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("DG_KERNEL_FAMILY");
-    v = (e && e[0] == 'l') ? 1 : 0;
-  }
-  return v == 1;
-}
+// Kernel variants (KParams::variant, dg_set_kernel_variant; defaults are the measured winners):
+// VAR_NO_TMEM: shared-memory n = 4 BiCGStab instead of Krylov vectors in tensor memory;
+// VAR_LINE: the line-per-thread kernels for every degree.
+inline bool use_tmem(const KParams& kp) { return (kp.variant & VAR_NO_TMEM) == 0; }
+inline bool force_line(const KParams& kp) { return (kp.variant & VAR_LINE) != 0; }
 
 // Kernel family of the operator application per degree, chosen by measurement on C1-C5
 // (profiles/r01_kernel_family.md, profiles/r01_ab.md): the plane kernels for n = 2, 3, 4;
@@ -1447,7 +1434,7 @@ template <int N> constexpr bool plane_apply() { return N == 2 || N == 4 || (N ==
 
 // convective or reaction terms present (else the pure-diffusion instantiations, GEN = false)
 inline bool gen_terms(const KParams& kp) {
-  return kp.c != nullptr || kp.b[0] != 0.0 || kp.b[1] != 0.0 || kp.b[2] != 0.0;
+  return kp.c != nullptr || kp.bc != nullptr || kp.b[0] != 0.0 || kp.b[1] != 0.0 || kp.b[2] != 0.0;
 }
 
 template <int N>
@@ -1475,9 +1462,8 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
         slots = max(1, per_sm) * nsm;
       }
       if constexpr (N == 4) {
-        // slim variant (no register prefetch, 4 CTAs per SM); DG_VOLUME_SLIM=0: k_volume (A/B)
-        static const bool alt = !(getenv("DG_VOLUME_SLIM") && getenv("DG_VOLUME_SLIM")[0] == '0');
-        if (alt) {
+        // slim variant (no register prefetch, 4 CTAs per SM); VAR_VOLUME_PREFETCH: k_volume
+        if (!(kp.variant & VAR_VOLUME_PREFETCH)) {
           static int sslots = 0;
           const size_t ssm = sizeof(double) * (size_t)G::TB;
           if (sslots == 0) {
@@ -1501,7 +1487,7 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
     }
   }
   if constexpr (plane_apply<N>()) {
-    if (!force_line()) {
+    if (!force_line(kp)) {
       using G = pk::Geo<N>;
       const int grid = (kp.ncells + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
@@ -1546,7 +1532,8 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   // two CTAs per SM) beat the register-starved plane ones (C3 sweep 32.7 -> 20.1 ms), except
   // for the tridiagonal preconditioner, which exists in the plane family only
   if constexpr (N <= 5) {
-    if (!force_line() && (N <= 4 || method == LM_BICGSTAB_THOMAS)) {
+    if (!force_line(kp) && (N <= 4 || method == LM_BICGSTAB_THOMAS || method == LM_GMRES ||
+                            method == LM_GMRES_THOMAS)) {
       using G = pk::Geo<N>;
       const int grid = (group_items(kp) + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
@@ -1558,7 +1545,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
             return launch(pk::k_bicgstab<N, true, true, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
           if (method == LM_BICGSTAB) {
             if constexpr (N == 4)
-              if (use_tmem())
+              if (use_tmem(kp))
                 return launch(pk::k_bicgstab<N, true, false, true, true>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
             return launch(pk::k_bicgstab<N, true, false, true>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
           }
@@ -1569,12 +1556,13 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       }
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
-      if constexpr (N <= 4) {
+      {
         // restarted GMRES(KR), Krylov basis + diagonal in TMEM (compact colour maps not
         // supported: the SOR half-sweeps run masked). KR fills 256 TMEM columns at n = 2, 3
         // (two CTAs per SM) and all 512 at n = 4 (one CTA per SM: GMRES(7) with two CTAs was
-        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_ab.md)
-        constexpr int KR = N == 4 ? 15 : N == 3 ? 13 : 15;
+        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_ab.md);
+        // n = 5: 9 basis vectors + the diagonal = 500 of the 512 columns (one CTA per SM)
+        constexpr int KR = N == 5 ? 9 : N == 4 ? 15 : N == 3 ? 13 : 15;
         if (method == LM_GMRES)
           return launch(pk::k_gmres<N, SWEEP, false, KR>, grid, G::NT, pk::smem_gmres<N, KR>(false), s, kp, in, f, out);
         if (method == LM_GMRES_THOMAS)
@@ -1583,7 +1571,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
       if constexpr (N <= 4) {
         if (method == LM_BICGSTAB) {
           if constexpr (N == 4)
-            if (use_tmem())
+            if (use_tmem(kp))
               return launch(pk::k_bicgstab<N, SWEEP, false, false, true>, grid, G::NT, pk::smem_solve<N>(2), s, kp, in, f, out);
           return launch(pk::k_bicgstab<N, SWEEP>, grid, G::NT, pk::smem_solve<N>(5), s, kp, in, f, out);
         }
@@ -1598,7 +1586,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
   if constexpr (N >= 5 && N <= 7) {
-    static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
+    const bool cta = (kp.variant & VAR_LINE_CG_CTA) != 0;   // CTA-barrier line solvers (A/B)
     if (method == LM_BICGSTAB && !cta)
       return launch(k_bicgstab_w<N, SWEEP>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
@@ -1607,7 +1595,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
   if constexpr (N >= 5 && N <= 7) {   // n = 8: 255 registers with spills, the CTA version is faster
-    static const bool cta = getenv("DG_LINE_CG_CTA") && getenv("DG_LINE_CG_CTA")[0] == '1';   // A/B
+    const bool cta = (kp.variant & VAR_LINE_CG_CTA) != 0;
     if (!cta)
       return launch(k_cg_w<N, SWEEP>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);

@@ -71,6 +71,7 @@ template <int N, bool WB = true> struct Cells {
   static constexpr int C = Geo<N>::C;
   static constexpr int BS = 2 * N * N + 1;   // odd stride: the cells of a half-warp hit distinct banks
   double vc[C][4];
+  double vb[C][3];   // |T| b_k / h_k of the cell (volume advection)
   double fc[C][6][6];
   const double* nb[C][6];
   int cell[C];
@@ -642,6 +643,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
   if (L.active) {
     const int qy = L.t;
     const double* vcell = cl.vc[L.cs];
+    const double* vbc = cl.vb[L.cs];
     double U[N][N], R[N][N];   // [qz][qx], unweighted
     if (vol) {
       // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise; the y flux
@@ -665,7 +667,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           }
           U[qz][qx] = s;
           R[qz][qx] = GEN ? cR * s : 0.0;
-          fy_[qz] = GEN ? fma(cK, s1, -kp.sb[1] * s) : cK * s1;
+          fy_[qz] = GEN ? fma(cK, s1, -vbc[1] * s) : cK * s1;
         }
 #pragma unroll
         for (int k = 0; k < N; ++k) {
@@ -684,7 +686,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[qz][r], du);
-          F[q] = GEN ? fma(vcell[0], du, -kp.sb[0] * U[qz][q]) : vcell[0] * du;
+          F[q] = GEN ? fma(vcell[0], du, -vbc[0] * U[qz][q]) : vcell[0] * du;
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -703,7 +705,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[r][qx], du);
-          F[q] = GEN ? fma(vcell[2], du, -kp.sb[2] * U[q][qx]) : vcell[2] * du;
+          F[q] = GEN ? fma(vcell[2], du, -vbc[2] * U[q][qx]) : vcell[2] * du;
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -956,6 +958,7 @@ template <int N>
 __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>& cl, const Lane& L,
                                                const Rows<N>& rw, double (&dg)[N][N]) {
   const double* vc = cl.vc[L.cs];
+  const double* vb = cl.vb[L.cs];
   const double* fc = &cl.fc[L.cs][0][0];
   const int k = L.t;
   const double dd0 = c_tab[N].d0[0], dd1 = c_tab[N].d1[N - 1];
@@ -973,9 +976,9 @@ __device__ __forceinline__ void plane_inv_diag(const KParams& kp, const Cells<N>
     for (int i = 0; i < N; ++i) {
       const double Mi = c_tab[N].Md[i], Mj = c_tab[N].Md[j], Mk = rw.Md;
       double d = vc[3] * Mi * Mj * Mk;
-      d += (vc[0] * c_tab[N].Sd[i] - kp.sb[0] * c_tab[N].Cd[i]) * Mj * Mk;
-      d += (vc[1] * c_tab[N].Sd[j] - kp.sb[1] * c_tab[N].Cd[j]) * Mi * Mk;
-      d += (vc[2] * rw.Sd - kp.sb[2] * rw.Cd) * Mi * Mj;
+      d += (vc[0] * c_tab[N].Sd[i] - vb[0] * c_tab[N].Cd[i]) * Mj * Mk;
+      d += (vc[1] * c_tab[N].Sd[j] - vb[1] * c_tab[N].Cd[j]) * Mi * Mk;
+      d += (vc[2] * rw.Sd - vb[2] * rw.Cd) * Mi * Mj;
       if (i == 0) d += kp.fa[0] * Mj * Mk * xlo;
       if (i == N - 1) d += kp.fa[0] * Mj * Mk * xhi;
       if (j == 0) d += kp.fa[1] * Mi * Mk * ylo;
@@ -995,6 +998,7 @@ template <int N> struct SetupRegs {
   static constexpr int C = Geo<N>::C, NT = Geo<N>::NT;
   static constexpr int IT = (3 * C + NT - 1) / NT;   // (cell, axis) items per thread
   double KT[IT], Kn[IT][2], cR[IT];
+  double bT[IT], bN[IT][2];   // b_axis of the cell and of its two neighbours along the axis
   int kind[IT][2];   // 0 interior (or ghost), 1 Dirichlet, 2 Neumann; -1: item not valid
 };
 
@@ -1037,6 +1041,7 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
     const int step = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
     sr.KT[r] = __ldg(kp.K + (size_t)(cell + nxy) * 3 + axis);
     sr.cR[r] = (axis == 0 && kp.c) ? __ldg(kp.c + cell) : 0.0;
+    sr.bT[r] = kp.bc ? __ldg(kp.bc + (size_t)(cell + nxy) * 3 + axis) : kp.b[axis];
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       const int f = 2 * axis + hi;
@@ -1059,6 +1064,7 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
       }
       sr.kind[r][hi] = kind;
       sr.Kn[r][hi] = kidx >= 0 ? __ldg(kp.K + (size_t)kidx * 3 + axis) : 0.0;
+      sr.bN[r][hi] = (kp.bc && kidx >= 0) ? __ldg(kp.bc + (size_t)kidx * 3 + axis) : sr.bT[r];
       cl.nb[cs][f] = nbp;
       if (nc >= 0 && nc < dim) atomicOr(&cl.nbm[f][cs >> 5], 1u << (cs & 31));
       if ((kind == 0 && !(nc >= 0 && nc < dim)) || CMAP) cl.nbg[f] = 1;   // per-cell pointers
@@ -1081,11 +1087,13 @@ __device__ __forceinline__ void setup_finish(const KParams& kp, Cells<N, WB>& cl
     const double KT = valid ? sr.KT[r] : 0.0;
     cl.vc[cs][axis] = (valid && (kp.mask & 1u)) ? KT * vol * ihk * ihk : 0.0;
     if (axis == 0) cl.vc[cs][3] = (valid && (kp.mask & 1u)) ? vol * sr.cR[r] : 0.0;
-    const double bn = kp.b[axis];
+    cl.vb[cs][axis] = (valid && (kp.mask & 1u)) ? vol * sr.bT[r] * ihk : 0.0;
 #pragma unroll
     for (int hi = 0; hi < 2; ++hi) {
       double co[6] = {0, 0, 0, 0, 0, 0};
       const int kind = sr.kind[r][hi];
+      // b . nu_F on the face (reading #8: the mean of the two cells' b; exact for constant b)
+      const double bn = kind == 0 ? 0.5 * (sr.bT[r] + sr.bN[r][hi]) : sr.bT[r];
       if (kind == 0 && (kp.mask & 2u)) {
         const double KN = sr.Kn[r][hi];
         const double sum = KT + KN;
@@ -1122,7 +1130,7 @@ template <int N, bool WB> __device__ __forceinline__ void setup_B(const KParams&
 template <int N, bool USEB = true, bool WB>
 __device__ __forceinline__ void setup(const KParams& kp, Cells<N, WB>& cl, int cell0, const double* u) {
   using G = Geo<N>;
-  setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.fc, cl.nb, cl.cell, cell0, u);
+  setup_cells<N, G::C, G::NT>(kp, cl.vc, cl.vb, cl.fc, cl.nb, cl.cell, cell0, u);
   if constexpr (!USEB || !WB) return;
   setup_B<N>(kp, cl);
 }
@@ -1280,7 +1288,7 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   load_rows<N>(rw, L.t);
   const double vol = kp.h[0] * kp.h[1] * kp.h[2];
   const int nxy = kp.nx * kp.ny;
-  double nxt[G::PER], kn[3] = {0.0, 0.0, 0.0}, cn = 0.0;
+  double nxt[G::PER], kn[3] = {0.0, 0.0, 0.0}, cn = 0.0, bnx[3] = {0.0, 0.0, 0.0};
   auto prefetch = [&](int g) {
     const int cell0 = g * G::C;
     load_own<N>(nxt, u + (size_t)cell0 * G::N3, min(G::C, kp.ncells - cell0));
@@ -1289,6 +1297,10 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
       const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
       kn[0] = __ldg(Kc); kn[1] = __ldg(Kc + 1); kn[2] = __ldg(Kc + 2);
       cn = kp.c ? __ldg(kp.c + cell) : 0.0;
+      if (GEN) {
+        const double* bcl = kp.bc ? kp.bc + (size_t)(cell + nxy) * 3 : kp.b;
+        bnx[0] = bcl[0]; bnx[1] = bcl[1]; bnx[2] = bcl[2];
+      }
     }
   };
   int g = blockIdx.x;
@@ -1305,6 +1317,9 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
       cl.vc[cs][1] = ok ? kn[1] * vol * kp.ih[1] * kp.ih[1] : 0.0;
       cl.vc[cs][2] = ok ? kn[2] * vol * kp.ih[2] * kp.ih[2] : 0.0;
       cl.vc[cs][3] = ok ? vol * cn : 0.0;
+      if (GEN)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) cl.vb[cs][a] = ok ? vol * bnx[a] * kp.ih[a] : 0.0;
     }
     __syncthreads();
     if (g + (int)gridDim.x < ngroups) prefetch(g + gridDim.x);
@@ -1330,11 +1345,14 @@ k_volume_s(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
   extern __shared__ double sm[];
   double* TB = sm;
-  // only vc (the first member) of the cell block is read by the volume-only operator
+  // only vc and vb (the leading members) of the cell block are read by the volume-only operator
   using CellsV = Cells<N, false>;
   static_assert(offsetof(CellsV, vc) == 0, "vc leads the cell block");
-  __shared__ double vcs[G::C][4];
-  const Cells<N, false>& cl = *reinterpret_cast<const Cells<N, false>*>(&vcs[0][0]);
+  static_assert(offsetof(CellsV, vb) == sizeof(double) * 4 * G::C, "vb follows vc");
+  __shared__ double vcb[G::C * 7];   // [C][4] vc, then [C][3] vb
+  const Cells<N, false>& cl = *reinterpret_cast<const Cells<N, false>*>(vcb);
+  double (*vcs)[4] = reinterpret_cast<double (*)[4]>(vcb);
+  double (*vbs)[3] = reinterpret_cast<double (*)[3]>(vcb + 4 * G::C);
   const int ngroups = (kp.ncells + G::C - 1) / G::C;
   const Lane L = lane_id<N>();
   Rows<N> rw;
@@ -1353,6 +1371,11 @@ k_volume_s(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
       vcs[cs][1] = ok ? __ldg(Kc + 1) * vol * kp.ih[1] * kp.ih[1] : 0.0;
       vcs[cs][2] = ok ? __ldg(Kc + 2) * vol * kp.ih[2] * kp.ih[2] : 0.0;
       vcs[cs][3] = ok && kp.c ? vol * __ldg(kp.c + cell0 + cs) : 0.0;
+      if (GEN) {
+        const double* bcl = kp.bc ? kp.bc + (size_t)(cell0 + (ok ? cs : 0) + nxy) * 3 : kp.b;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) vbs[cs][a] = ok ? vol * bcl[a] * kp.ih[a] : 0.0;
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -1452,6 +1475,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   const double rr0 = cell_sum<N>(rr, L.lane);
   rz = cell_sum<N>(rz, L.lane);
   bool conv = !valid || rr0 == 0.0 || skip_cell(kp, cell0 + L.cs);
+  bool brk = false;
   int its = 0;
   for (int iter = 0;; ++iter) {
     const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
@@ -1467,7 +1491,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     double alpha = 0.0;
     if (!conv) {
       if (pq > 0.0) alpha = DG_QUOT(rz, pq);
-      else conv = true;
+      else conv = brk = true;   // breakdown (D_T not SPD): stop, reported as not converged
     }
     double r2 = 0.0, rzn = 0.0;
     double Z[N][N];   // M^-1 r, formed once (reused by the direction update)
@@ -1496,7 +1520,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       }
     }
   }
-  its_out = conv ? its : (its | (1 << 30));
+  its_out = (conv && !brk) ? its : (its | (1 << 30));
   // result: X (+ u) -> TB -> global
   __syncthreads();
   if (SWEEP) {
@@ -1532,7 +1556,8 @@ __device__ __forceinline__ double dt_entry(const KParams& kp, const Cells<N, WB>
   const double Mx = M[i * N + a], My = M[j * N + b], Mz = M[k * N + c];
   double v = vc[0] * S[i * N + a] * My * Mz + vc[1] * Mx * S[j * N + b] * Mz +
              vc[2] * Mx * My * S[k * N + c] + vc[3] * Mx * My * Mz;
-  v -= kp.sb[0] * C[i * N + a] * My * Mz + kp.sb[1] * Mx * C[j * N + b] * Mz + kp.sb[2] * Mx * My * C[k * N + c];
+  const double* vb = cl.vb[cs];
+  v -= vb[0] * C[i * N + a] * My * Mz + vb[1] * Mx * C[j * N + b] * Mz + vb[2] * Mx * My * C[k * N + c];
   const int r3[3] = {i, j, k}, c3[3] = {a, b, c};
   const double m3[3] = {Mx, My, Mz};
 #pragma unroll
@@ -1710,6 +1735,31 @@ template <> struct TmRow<3> {
                  ::"r"(a), "r"(a + 4), "r"(__double2loint(v[0])), "r"(__double2hiint(v[0])),
                    "r"(__double2loint(v[1])), "r"(__double2hiint(v[1])), "r"(__double2loint(v[2])),
                    "r"(__double2hiint(v[2])));
+  }
+};
+template <> struct TmRow<5> {
+  static __device__ __forceinline__ void ld(uint32_t a, double (&v)[5]) {
+    uint32_t r[10];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%10];\n"
+                 "tcgen05.ld.sync.aligned.32x32b.x2.b32 {%8,%9}, [%11];\n"
+                 "tcgen05.wait::ld.sync.aligned;\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9])
+                 : "r"(a), "r"(a + 8));
+#pragma unroll
+    for (int i = 0; i < 5; ++i) v[i] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+  }
+  static __device__ __forceinline__ void st(uint32_t a, const double (&v)[5]) {
+    uint32_t r[10];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      r[2 * i] = (uint32_t)__double2loint(v[i]);
+      r[2 * i + 1] = (uint32_t)__double2hiint(v[i]);
+    }
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%2,%3,%4,%5,%6,%7,%8,%9};\n"
+                 "tcgen05.st.sync.aligned.32x32b.x2.b32 [%1], {%10,%11};\n"
+                 ::"r"(a), "r"(a + 8), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]),
+                   "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]));
   }
 };
 // stores of this thread are complete (before TMEM data is read back or freed)
@@ -2103,11 +2153,25 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   const bool valid = L.active && L.cs < nvalid;
   Rows<N> rw;
   load_rows<N>(rw, L.t);
-  solver_setup<N, SWEEP, false>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+  // n <= 4: neighbour tiles staged with cp.async; n = 5: through registers (as in k_bicgstab)
+  constexpr bool ASYNC = G::FS >= G::N3;
+  if constexpr (ASYNC) {
+    solver_setup<N, SWEEP, false>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+  } else {
+    stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
+    setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
+  }
   double R[N][N], W[N][N], T[N][N];
   read_plane<N>(TB, L, W);
   if (SWEEP) {
-    nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    if constexpr (ASYNC) {
+      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+    } else {
+      double pv0[G::PER], pv1[G::PER];
+      load_nbr<N>(pv0, cl, 2);
+      load_nbr<N>(pv1, cl, 3);
+      nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
+    }
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     __syncthreads();
     stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
@@ -2158,6 +2222,8 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   const double lim = kp.tol2 * rr0;
   int its = 0;     // Arnoldi steps of this cell
   int steps = 0;   // Arnoldi steps of the warp (warp-uniform: the cap must not split the warp)
+  // restart length: kp.krestart (dg_set_local_solver) up to the compiled basis size KR
+  const int kr = (kp.krestart > 0 && kp.krestart < KR) ? kp.krestart : KR;
   // M^-1 applied to W in place
   auto precond = [&]() {
     if constexpr (THOMAS) {
@@ -2195,7 +2261,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     if (L.active && L.t == 0) gv[0] = beta;
     bool live = !conv;
     int jl = -1;
-    for (int j = 0; j < KR; ++j) {
+    for (int j = 0; j < kr; ++j) {
       if (__all_sync(0xffffffffu, !live || !L.active) || steps >= kp.max_it) break;
       ++steps;
       // W = M^-1 v_j;  T = D_T W
@@ -2225,7 +2291,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
 #pragma unroll
         for (int q = 0; q < N; ++q) hn = fma(T[r][q], T[r][q], hn);
       hn = sqrt(cell_sum<N>(hn, L.lane));
-      if (j + 1 < KR) {
+      if (j + 1 < kr) {
         const double ih = (live && hn > 0.0) ? rcp_nr(hn) : 0.0;
 #pragma unroll
         for (int r = 0; r < N; ++r) {

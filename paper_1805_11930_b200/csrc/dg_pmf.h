@@ -19,7 +19,8 @@ struct Mat1D {
 
 void pmf_tables(const Tables1D& tab, Mat1D* m);
 size_t pmf_factor_smem(int nd);
-// out[b] (nd x nd, row-major) = D_T (invert = 0) or D_T^{-1} (invert = 1) of cell cell_first + b
+// out[b] (nd x nd) = D_T row-major (invert = 0) or D_T^{-1} TRANSPOSED (invert = 1: out[J][I] =
+// D_T^{-1}[I][J], partial pivoting) of cell cell_first + b
 cudaError_t launch_pmf_factor(const KParams& kp, const Mat1D& t, int nd, int cell_first, int ncells,
                               int invert, double* out, cudaStream_t s);
 // out = u + omega Dinv (f - Au) per cell (out may alias u)

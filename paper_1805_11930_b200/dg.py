@@ -19,6 +19,7 @@ DG_OK, DG_ERR_INVALID, DG_ERR_NOMEM, DG_ERR_CUDA, DG_ERR_NCCL, DG_ERR_STATE, DG_
 DG_LOCAL_AUTO, DG_LOCAL_CG, DG_LOCAL_BICGSTAB, DG_LOCAL_BICGSTAB_THOMAS = 0, 1, 2, 3
 DG_LOCAL_GMRES, DG_LOCAL_GMRES_THOMAS = 4, 5
 DG_HALO_NCCL, DG_HALO_EXTERNAL = 0, 1
+DG_VARIANT_VOLUME_PREFETCH, DG_VARIANT_LINE, DG_VARIANT_NO_TMEM, DG_VARIANT_LINE_CG_CTA = 1, 2, 4, 8
 MASK_VOLUME, MASK_INTERIOR_FACES, MASK_BOUNDARY_FACES = 1, 2, 4
 
 # every symbol include/dg.h declares (checked by the CPU tests)
@@ -28,7 +29,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
            "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
            "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep", "dg_pmf_setup",
-           "dg_pmf_sweep", "dg_pmf_block"]
+           "dg_pmf_sweep", "dg_pmf_block", "dg_block_jacobi_sweep_to", "dg_set_kernel_variant"]
 
 
 class DGError(RuntimeError):
@@ -42,7 +43,8 @@ class dg_desc(ctypes.Structure):
                 ("Lx", ctypes.c_double), ("Ly", ctypes.c_double), ("Lz", ctypes.c_double),
                 ("bc", ctypes.c_int32 * 6), ("p", ctypes.c_int32), ("alpha", ctypes.c_double),
                 ("k_components", ctypes.c_int32), ("K", ctypes.POINTER(ctypes.c_double)),
-                ("b", ctypes.c_double * 3), ("c", ctypes.POINTER(ctypes.c_double)),
+                ("b", ctypes.c_double * 3), ("b_cell", ctypes.POINTER(ctypes.c_double)),
+                ("c", ctypes.POINTER(ctypes.c_double)),
                 ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32), ("halo_mode", ctypes.c_int32),
                 ("nccl_id", ctypes.c_void_p), ("device", ctypes.c_int32)]
 
@@ -103,7 +105,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_pmf_setup": ([P], i32),
         "dg_pmf_sweep": ([P, P, P, dbl, P], i32),
         "dg_pmf_block": ([P, i64, i32, ctypes.POINTER(dbl)], i32),
-        "dg_set_local_solver": ([P, i32, i32], i32),
+        "dg_set_local_solver": ([P, i32, i32, i32], i32),
+        "dg_set_kernel_variant": ([P, u32], i32),
+        "dg_block_jacobi_sweep_to": ([P, P, P, P, dbl, dbl, P], i32),
         "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
         "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
         "dg_fill_ghosts": ([P, P, P, P], i32),
@@ -163,6 +167,8 @@ def make_desc(problem, rank: int = 0, nranks: int = 1, device: int = 0, halo_mod
     P = problem
     K = np.ascontiguousarray(np.asarray(P.K, dtype=np.float64))
     c = None if P.c is None else np.ascontiguousarray(np.asarray(P.c, dtype=np.float64))
+    bcl = (None if getattr(P, "b_cells", None) is None
+           else np.ascontiguousarray(np.asarray(P.b_cells, dtype=np.float64).reshape(-1, 3)))
     d = dg_desc()
     d.nx, d.ny, d.nz = P.nx, P.ny, P.nz
     d.Lx, d.Ly, d.Lz = P.Lx, P.Ly, P.Lz
@@ -172,9 +178,10 @@ def make_desc(problem, rank: int = 0, nranks: int = 1, device: int = 0, halo_mod
     d.k_components = 1 if K.ndim == 1 else 3
     d.K = K.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
     d.b[:] = list(P.b)
+    d.b_cell = bcl.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if bcl is not None else None
     d.c = c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if c is not None else None
     d.rank, d.nranks, d.halo_mode, d.device = rank, nranks, halo_mode, device
-    return d, (K, c)
+    return d, (K, c, bcl)
 
 
 def halo_plan(problem, rank: int, nranks: int) -> dict:
@@ -202,10 +209,16 @@ def microbench_dfma(sink, blocks: int, iters: int, stream=None) -> int:
     return flops.value
 
 
-def _ptr(t):
+def _ptr(t, numel=None, device=None):
+    """Device pointer of a contiguous float64 CUDA tensor; with numel / device given, the size
+    and the device are checked too (an undersized tensor would be read out of bounds)."""
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise ValueError("expected a contiguous float64 CUDA tensor")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"expected {numel} elements, got {t.numel()}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"tensor on cuda:{t.device.index}, context on cuda:{device}")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -259,26 +272,39 @@ class DGContext:
         self.close()
 
     # ---- calls ---------------------------------------------------------------
+    def _v(self, t):
+        """A local DoF vector of this context (size and device checked)."""
+        return _ptr(t, self.n_local_dof, self.device)
+
     def apply(self, u, out, stream=None):
-        _check(self.lib.dg_apply(self.h, _ptr(u), _ptr(out), _stream(stream)))
+        _check(self.lib.dg_apply(self.h, self._v(u), self._v(out), _stream(stream)))
         return out
 
     def apply_parts(self, u, out, mask: int, stream=None):
-        _check(self.lib.dg_apply_parts(self.h, _ptr(u), _ptr(out), mask, _stream(stream)))
+        _check(self.lib.dg_apply_parts(self.h, self._v(u), self._v(out), mask, _stream(stream)))
         return out
 
     def block_diag_apply(self, u, out, stream=None):
-        _check(self.lib.dg_block_diag_apply(self.h, _ptr(u), _ptr(out), _stream(stream)))
+        _check(self.lib.dg_block_diag_apply(self.h, self._v(u), self._v(out), _stream(stream)))
         return out
 
     def local_block_solve(self, d, du, tol: float, stream=None):
-        _check(self.lib.dg_local_block_solve(self.h, _ptr(d), _ptr(du), float(tol), _stream(stream)))
+        _check(self.lib.dg_local_block_solve(self.h, self._v(d), self._v(du), float(tol), _stream(stream)))
         return du
 
     def sweep(self, u, f, omega: float = 1.0, tol: float = 1e-12, stream=None):
-        _check(self.lib.dg_block_jacobi_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
+        _check(self.lib.dg_block_jacobi_sweep(self.h, self._v(u), self._v(f), float(omega), float(tol),
                                               _stream(stream)))
         return u
+
+    def sweep_to(self, u, f, u_new, omega: float = 1.0, tol: float = 1e-12, stream=None):
+        """Out-of-place sweep: u_new = u + omega D^-1 (f - A u) (u_new must not alias u or f)."""
+        _check(self.lib.dg_block_jacobi_sweep_to(self.h, self._v(u), self._v(f), self._v(u_new),
+                                                 float(omega), float(tol), _stream(stream)))
+        return u_new
+
+    def set_kernel_variant(self, variant: int = 0):
+        _check(self.lib.dg_set_kernel_variant(self.h, int(variant)))
 
     # ---- hybrid multigrid (Alg. 1, P0 subspace) ------------------------------
     def coarse_matrix(self):
@@ -291,19 +317,19 @@ class DGContext:
 
     def hybrid_vcycle(self, r, z, params: Optional[dg_hybrid_params] = None, stream=None):
         prm = params if params is not None else hybrid_params()
-        _check(self.lib.dg_hybrid_vcycle(self.h, _ptr(r), _ptr(z), ctypes.byref(prm), _stream(stream)))
+        _check(self.lib.dg_hybrid_vcycle(self.h, self._v(r), self._v(z), ctypes.byref(prm), _stream(stream)))
         return z
 
     def hybrid_solve(self, u, f, params: Optional[dg_hybrid_params] = None, stream=None) -> dict:
         prm = params if params is not None else hybrid_params()
         st = dg_hybrid_stats()
-        _check(self.lib.dg_hybrid_solve(self.h, _ptr(u), _ptr(f), ctypes.byref(prm), ctypes.byref(st),
+        _check(self.lib.dg_hybrid_solve(self.h, self._v(u), self._v(f), ctypes.byref(prm), ctypes.byref(st),
                                         _stream(stream)))
         return st.as_dict()
 
     def sor_sweep(self, u, f, omega: float = 1.0, tol: float = 1e-12, symmetric: bool = False, stream=None):
         """Red-black block SOR (symmetric: SSOR) sweep, u in place (Alg. 3)."""
-        _check(self.lib.dg_block_sor_sweep(self.h, _ptr(u), _ptr(f), float(omega), float(tol),
+        _check(self.lib.dg_block_sor_sweep(self.h, self._v(u), self._v(f), float(omega), float(tol),
                                            1 if symmetric else 0, _stream(stream)))
         return u
 
@@ -312,7 +338,7 @@ class DGContext:
         _check(self.lib.dg_pmf_setup(self.h))
 
     def pmf_sweep(self, u, f, omega: float = 1.0, stream=None):
-        _check(self.lib.dg_pmf_sweep(self.h, _ptr(u), _ptr(f), float(omega), _stream(stream)))
+        _check(self.lib.dg_pmf_sweep(self.h, self._v(u), self._v(f), float(omega), _stream(stream)))
         return u
 
     def pmf_block(self, cell: int, inverse: bool = False):
@@ -323,8 +349,8 @@ class DGContext:
                                      out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         return out.reshape(nd, nd)
 
-    def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000):
-        _check(self.lib.dg_set_local_solver(self.h, method, max_it))
+    def set_local_solver(self, method: int = DG_LOCAL_AUTO, max_it: int = 1000, gmres_restart: int = 0):
+        _check(self.lib.dg_set_local_solver(self.h, method, max_it, gmres_restart))
 
     def stats(self) -> dict:
         st = dg_stats()

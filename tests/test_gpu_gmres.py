@@ -122,8 +122,8 @@ def test_gmres_sor_sweep(p):
     assert rel(got, ref) <= 1e-9
 
 
-def test_gmres_refused_above_p3():
-    P = random_problem(2, 2, 2, 4, seed=1190, b=(1.0, 0.0, 0.0))
+def test_gmres_refused_above_p4():
+    P = random_problem(2, 2, 2, 5, seed=1190, b=(1.0, 0.0, 0.0))
     with dg.DGContext(P) as ctx:
         with pytest.raises(dg.DGError):
             ctx.set_local_solver(dg.DG_LOCAL_GMRES, 100)

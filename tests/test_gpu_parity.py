@@ -65,16 +65,22 @@ def test_apply_matches_oracle(kind, P):
     assert rel(got, ref) <= APPLY_TOL
 
 
-@pytest.mark.parametrize("kind,P", PROBS[::3], ids=IDS[::3])
+@pytest.mark.parametrize("kind,P", PROBS, ids=IDS)
 @pytest.mark.parametrize("mask", [1, 2, 4, 3, 6])
 def test_apply_parts_match_oracle(kind, P, mask):
+    """Every part of A (volume, interior faces, boundary faces and their sums) at every p, against
+    the pinned TierB.apply_parts_cells, at the dg_apply tolerance (mask = 1 runs the persistent
+    volume kernels k_volume / k_volume_s whose fp64 fraction bench.py reports)."""
     u, _ = vec(P, 12)
     ref = TierB(P).apply_parts_cells(u, range(P.n_cells), mask).reshape(-1)
     with dg.DGContext(P) as ctx:
         out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
         ctx.apply_parts(cuda(u), out, mask)
         got = host(out)
-    assert rel(got, ref) <= APPLY_TOL * 10 if np.linalg.norm(ref) > 0 else np.abs(got).max() == 0
+    if np.linalg.norm(ref) > 0:
+        assert rel(got, ref) <= APPLY_TOL
+    else:
+        assert np.abs(got).max() == 0
 
 
 @pytest.mark.parametrize("kind,P", PROBS, ids=IDS)

@@ -295,3 +295,15 @@ def test_problem_per_cell_b_overrides_constant():
     P.b_cells = bc
     assert np.array_equal(TierB(P).assemble(), A_explicit)
     assert np.abs(TierA(P).assemble() - A_explicit).max() <= 1e-13 * np.abs(A_explicit).max()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+def test_volume_apply_equals_per_cell_volume_blocks(p):
+    """TierB.volume_apply (all cells at once, for the large volume-kernel parity cases) equals the
+    per-cell a^v blocks, which test_apply_parts_match_tier_a_terms pins to tier A."""
+    P = random_problem(3, 2, 2, p, seed=80 + p, b=(0.5, -0.2, 0.1), c=True, L=(1.0, 0.6, 1.4))
+    bc = np.random.default_rng(p).normal(size=(P.n_cells, 3))
+    tb = TierB(P, b_cells=bc)
+    u = np.random.default_rng(p).uniform(-1, 1, P.n_dof)
+    ref = tb.apply_parts_cells(u, range(P.n_cells), 1).reshape(-1)
+    assert rel(tb.volume_apply(u), ref) < 1e-14
