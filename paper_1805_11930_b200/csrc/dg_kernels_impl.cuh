@@ -141,12 +141,12 @@ template <int N, int S> __device__ __forceinline__ void st(double* p, const doub
 
 // Stage 2 + the derivative half of stage 3 along one line of direction k:
 // R += D^T ( Wl * w_q * (sK * (D U)_q - sb * U_q) )
-template <int N> __device__ __forceinline__ void dir_term(const double* U, double* R, double Wl,
-                                                          double sK, double sb) {
+template <int N, bool GEN = true> __device__ __forceinline__ void dir_term(const double* U, double* R, double Wl,
+                                                                           double sK, double sb) {
   double du[N], F[N], t[N];
   mv<N, 1>(U, du);
 #pragma unroll
-  for (int q = 0; q < N; ++q) F[q] = Wl * c_tab[N].w[q] * fma(sK, du[q], -sb * U[q]);
+  for (int q = 0; q < N; ++q) F[q] = Wl * c_tab[N].w[q] * (GEN ? fma(sK, du[q], -sb * U[q]) : sK * du[q]);
   mtv<N, 1>(F, t);
 #pragma unroll
   for (int r = 0; r < N; ++r) R[r] += t[r];
@@ -208,8 +208,10 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*vb_)[3
         vc[1] = Kc[1] * vol * kp.ih[1] * kp.ih[1];
         vc[2] = Kc[2] * vol * kp.ih[2] * kp.ih[2];
         vc[3] = kp.c ? vol * kp.c[cell] : 0.0;
-        const double* bcl = kp.bc ? kp.bc + (size_t)(cell + nxy) * 3 : kp.b;
-        for (int a = 0; a < 3; ++a) vb_[cs][a] = vol * bcl[a] * kp.ih[a];
+        // (no pointer to the kernel parameter kp.b: that would copy KParams to local memory)
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+          vb_[cs][a] = vol * (kp.bc ? kp.bc[(size_t)(cell + nxy) * 3 + a] : kp.b[a]) * kp.ih[a];
       } else {
         vc[0] = vc[1] = vc[2] = vc[3] = 0.0;
         vb_[cs][0] = vb_[cs][1] = vb_[cs][2] = 0.0;
@@ -360,10 +362,15 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // out(cs, j, k, v[N]) receives x-line (j,k) of cell slot cs.
 // FACES = false: the volume terms alone (the face passes are skipped); USEB (with FACES = false):
 // plus the self-face terms through g.Bf inside the Gauss-point passes (D_T without face passes)
-template <int N, bool FACES = true, bool USEB = false, bool WARP = false, int NTH = Geo<N>::NT, class Out>
+// GEN = false: pure diffusion (b = 0, no reaction) with the convective and reaction terms compiled out
+template <int N, bool FACES = true, bool USEB = false, bool WARP = false, int NTH = Geo<N>::NT,
+          bool GEN = true, class Out>
 __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
                                               const double* src, double* SA, double* SB,
-                                              double* FB, bool vol, Out out) {
+                                              double* FB, bool vol, Out out,
+                                              const double* pin = nullptr) {
+  // pin (warp mode, one line per lane): the lane's own x-line of the input, from registers
+  // instead of src
   using G = Geo<N>;
   constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = NTH;   // NTH: the launch's thread count
   const int tid = threadIdx.x;
@@ -375,6 +382,13 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   constexpr int ls = WARP ? 32 : NT;
   const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
+  // advection scalings |T| b_k / h_k: in warp mode the warp's own cell's, read once (registers,
+  // like the constant-b values they replace); otherwise per line item from shared memory
+  double sbw[3] = {0.0, 0.0, 0.0};
+  if constexpr (WARP && GEN)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) sbw[a] = g.vb[tid >> 5][a];
+  auto sbk = [&](int cs, int a) { return WARP ? sbw[a] : g.vb[cs][a]; };
 
   // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
   for (int it = tid; FACES && it < 3 * LINES; it += NT) {
@@ -389,7 +403,12 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
       const int off = cs * G::CS + b * G::ZS + a * G::YS;
       double v[N], o[N];
-      ld<N, 1>(src + off, v);
+      if (WARP && pin) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) v[e] = pin[e];
+      } else {
+        ld<N, 1>(src + off, v);
+      }
       mv<N, 0>(v, o);
       st<N, 1>(SA + off, o);
     }
@@ -438,8 +457,8 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       const double Wl = g.tw[a] * g.tw[b];
       const double sc = g.vc[cs][3];
 #pragma unroll
-      for (int q = 0; q < N; ++q) R[q] = Wl * c_tab[N].w[q] * sc * U[q];
-      dir_term<N>(U, R, Wl, g.vc[cs][2], g.vb[cs][2]);
+      for (int q = 0; q < N; ++q) R[q] = GEN ? Wl * c_tab[N].w[q] * sc * U[q] : 0.0;
+      dir_term<N, GEN>(U, R, Wl, g.vc[cs][2], GEN ? sbk(cs, 2) : 0.0);
       if constexpr (USEB) bterm<N>(g.Bf[cs][2], U, R, Wl);
       st<N, G::ZS>(SA + off, U);
       st<N, G::ZS>(SB + off, R);
@@ -452,7 +471,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N];
       ld<N, 1>(SA + off, U);
       ld<N, 1>(SB + off, R);
-      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], g.vb[cs][0]);
+      dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], GEN ? sbk(cs, 0) : 0.0);
       if constexpr (USEB) bterm<N>(g.Bf[cs][0], U, R, g.tw[a] * g.tw[b]);
       st<N, 1>(SB + off, R);
     }
@@ -464,7 +483,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N], o[N];
       ld<N, G::YS>(SA + off, U);
       ld<N, G::YS>(SB + off, R);
-      dir_term<N>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], g.vb[cs][1]);
+      dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], GEN ? sbk(cs, 1) : 0.0);
       if constexpr (USEB) bterm<N>(g.Bf[cs][1], U, R, g.tw[a] * g.tw[b]);
       mtv<N, 0>(R, o);
       st<N, G::YS>(SB + off, o);
@@ -639,8 +658,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
-  KParams kq = kp;
-  kq.mask = 7u;
+  const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
   self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
@@ -789,7 +807,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-template <int N, bool SWEEP>
+template <int N, bool SWEEP, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NTW, 2)
 k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
        double* __restrict__ out) {
@@ -809,13 +827,12 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
-  KParams kq = kp;
-  kq.mask = 7u;
+  const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
   self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2), CTA-wide
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    cell_operator<N, true, false, false, G::NTW, GEN>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
@@ -855,9 +872,61 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   rz = warp_sum(rz);
   bool conv = cs >= nvalid || rr0 == 0.0 || skip_cell(kp, cell0 + cs);
   int its = 0;
+  if constexpr (LPL == 1) {
+    // one line per lane (n = 5): every Krylov vector of the cell is lane-private line by line
+    // (the operator's pass 1 reads the lane's own x-line of p, pass 7 produces the lane's own
+    // line of q = D_T p), so r, p, x and diag(D_T)^-1 stay in registers and the iterations touch
+    // shared memory only through the operator's transposes
+    double r[N], p[N], x[N], dgi[N];
+#pragma unroll
+    for (int e = 0; e < N; ++e) r[e] = p[e] = x[e] = dgi[e] = 0.0;
+    if (act[0]) {
+      ld<N, 1>(R + off[0], r);
+      ld<N, 1>(P + off[0], p);
+      ld<N, 1>(Dg + off[0], dgi);
+    }
+    for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
+      __syncwarp();
+      double q[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) q[e] = 0.0;
+      cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
+                                                           [&](int, int, int, const double* v) {
+#pragma unroll
+        for (int e = 0; e < N; ++e) q[e] = v[e];
+      }, p);
+      double pq = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) pq = fma(p[e], q[e], pq);
+      pq = warp_sum(pq);
+      if (!(pq > 0.0)) break;   // breakdown (D_T not SPD): keep the last iterate, not converged
+      const double alpha = quot_nr(rz, pq);
+      double r2 = 0.0, rzn = 0.0, z[N];
+#pragma unroll
+      for (int e = 0; e < N; ++e) {
+        x[e] = fma(alpha, p[e], x[e]);
+        r[e] = fma(-alpha, q[e], r[e]);
+        r2 = fma(r[e], r[e], r2);
+        z[e] = dgi[e] * r[e];   // z = M^-1 r
+        rzn = fma(r[e], z[e], rzn);
+      }
+      r2 = warp_sum(r2);
+      rzn = warp_sum(rzn);
+      ++its;
+      if (r2 <= kp.tol2 * rr0) {
+        conv = true;
+        break;
+      }
+      const double beta = quot_nr(rzn, rz);
+      rz = rzn;
+#pragma unroll
+      for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], z[e]);
+    }
+    if (act[0]) st<N, 1>(X + off[0], x);
+  } else {
   for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
     __syncwarp();
-    cell_operator<N, false, true, true>(kq, g, P, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+    cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
       st<N, 1>(Q + c * G::CS + k * G::ZS + j * G::YS, v);
     });
     __syncwarp();
@@ -912,6 +981,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
         st<N, 1>(P + off[m], p[m]);
       }
   }
+  }
   __syncwarp();
   // write result (u + omega du for a sweep, du for a solve), warp by warp
 #pragma unroll
@@ -956,8 +1026,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
-  KParams kq = kp;
-  kq.mask = 7u;
+  const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
   self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {
@@ -1168,8 +1237,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
-  KParams kq = kp;
-  kq.mask = 7u;
+  const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
   self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {
@@ -1597,7 +1665,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
   if constexpr (N >= 5 && N <= 7) {   // n = 8: 255 registers with spills, the CTA version is faster
     const bool cta = (kp.variant & VAR_LINE_CG_CTA) != 0;
     if (!cta)
-      return launch(k_cg_w<N, SWEEP>, grid, G::NTW,
+      return launch(gen_terms(kp) ? k_cg_w<N, SWEEP, true> : k_cg_w<N, SWEEP, false>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);
   }
   return launch(k_cg<N, SWEEP>, grid, G::NT,

@@ -1297,10 +1297,9 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
       const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
       kn[0] = __ldg(Kc); kn[1] = __ldg(Kc + 1); kn[2] = __ldg(Kc + 2);
       cn = kp.c ? __ldg(kp.c + cell) : 0.0;
-      if (GEN) {
-        const double* bcl = kp.bc ? kp.bc + (size_t)(cell + nxy) * 3 : kp.b;
-        bnx[0] = bcl[0]; bnx[1] = bcl[1]; bnx[2] = bcl[2];
-      }
+      if (GEN)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) bnx[a] = kp.bc ? __ldg(kp.bc + (size_t)(cell + nxy) * 3 + a) : kp.b[a];
     }
   };
   int g = blockIdx.x;
@@ -1371,11 +1370,10 @@ k_volume_s(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
       vcs[cs][1] = ok ? __ldg(Kc + 1) * vol * kp.ih[1] * kp.ih[1] : 0.0;
       vcs[cs][2] = ok ? __ldg(Kc + 2) * vol * kp.ih[2] * kp.ih[2] : 0.0;
       vcs[cs][3] = ok && kp.c ? vol * __ldg(kp.c + cell0 + cs) : 0.0;
-      if (GEN) {
-        const double* bcl = kp.bc ? kp.bc + (size_t)(cell0 + (ok ? cs : 0) + nxy) * 3 : kp.b;
+      if (GEN)
 #pragma unroll
-        for (int a = 0; a < 3; ++a) vbs[cs][a] = ok ? vol * bcl[a] * kp.ih[a] : 0.0;
-      }
+        for (int a = 0; a < 3; ++a)
+          vbs[cs][a] = ok ? vol * (kp.bc ? __ldg(kp.bc + (size_t)(cell0 + cs + nxy) * 3 + a) : kp.b[a]) * kp.ih[a] : 0.0;
     }
     cp_async_wait_all();
     __syncthreads();
