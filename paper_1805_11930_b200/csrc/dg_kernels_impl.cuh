@@ -44,6 +44,9 @@ struct DevTab {
   double E0W[8], E1W[8], F0W[8], F1W[8];  // E0/w, E1/w, F0/w, F1/w
   // exact 1D stiffness and (test-derivative) convection matrices, for the bands of D_T
   double S[64], Cm[64];               // int th_i' th_j',  int th_i' th_j
+  // Gauss-point line forms of the volume terms along one direction (collocation derivative D,
+  // weights w): SG = D^T W D (stiffness), CG = D^T W (convection, test derivative)
+  double SG[64], CG[64];
 };
 __constant__ DevTab c_tab[kMaxN + 1];
 
@@ -163,9 +166,22 @@ template <int N> __device__ __forceinline__ void bterm(const double* B, const do
   }
 }
 
-// Bf[cs][a][q][r] = |F_a| sum_{s = lo, hi} (E_s[q] (sa_s E_s[r] + sg_s F_s[r] / h_a) + F_s[q] ta_s E_s[r])
-// (traces of a Gauss-value line: u(s) = E_s.U, u'(s) = F_s.U; injection of the value- and
-// derivative-test fluxes into the weighted Gauss residual). Needs g.fc; ends with a barrier.
+// Degrees whose D_T applications fold the volume line terms into Bf (one matvec per direction
+// from shared memory instead of the constant-table derivative pair; measured per degree,
+// DESIGN.md §6): bit N of DG_FOLD_N.
+#ifndef DG_FOLD_N
+#define DG_FOLD_N 0x1fc   // every degree n = 2..8 (profiles/r02_fold_ab.txt)
+#endif
+template <int N> __host__ __device__ constexpr bool fold_volume() { return (DG_FOLD_N >> N) & 1; }
+
+// Per cell and direction a, the D_T line operator at the Gauss points (weighted residual
+// form, R_line += w_t1 w_t2 Bf U_line), so the local solvers' D_T applications need one matvec
+// per direction instead of the derivative pair D^T W (.) D plus the face operator:
+//   Bf[cs][a] = vc_a SG - vb_a CG + [a = z] diag(vc_3 w)                       (volume)
+//             + |F_a| sum_{s = lo, hi} (E_s[q] (sa_s E_s[r] + sg_s F_s[r] / h_a) + F_s[q] ta_s E_s[r])
+// (self faces: traces of a Gauss-value line u(s) = E_s.U, u'(s) = F_s.U, and the injection of
+// the value- and derivative-test fluxes into the weighted Gauss residual).
+// Needs g.fc, g.vc, g.vb; ends with a barrier.
 template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
   using G = Geo<N>;
   for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
@@ -177,7 +193,13 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
     const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
     double b = c_tab[N].E0[q] * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) + c_tab[N].F0[q] * lo[4] * c_tab[N].E0[r];
     b += c_tab[N].E1[q] * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) + c_tab[N].F1[q] * hi[4] * c_tab[N].E1[r];
-    g.Bf[cs][a][q * N + r] = area * b;
+    double t = area * b;
+    if constexpr (fold_volume<N>()) {
+      t = fma(g.vc[cs][a], c_tab[N].SG[q * N + r], t);
+      t = fma(-g.vb[cs][a], c_tab[N].CG[q * N + r], t);
+      if (a == 2 && q == r) t = fma(g.vc[cs][3], c_tab[N].w[q], t);
+    }
+    g.Bf[cs][a][q * N + r] = t;
   }
   __syncthreads();
 }
@@ -455,11 +477,18 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       ld<N, G::ZS>(SB + off, t);
       mv<N, 0>(t, U);
       const double Wl = g.tw[a] * g.tw[b];
-      const double sc = g.vc[cs][3];
+      constexpr bool FOLD = USEB && fold_volume<N>();
+      if constexpr (FOLD) {   // the whole z-line operator of D_T (volume + self faces) at once
 #pragma unroll
-      for (int q = 0; q < N; ++q) R[q] = GEN ? Wl * c_tab[N].w[q] * sc * U[q] : 0.0;
-      dir_term<N, GEN>(U, R, Wl, g.vc[cs][2], GEN ? sbk(cs, 2) : 0.0);
-      if constexpr (USEB) bterm<N>(g.Bf[cs][2], U, R, Wl);
+        for (int q = 0; q < N; ++q) R[q] = 0.0;
+        bterm<N>(g.Bf[cs][2], U, R, Wl);
+      } else {
+        const double sc = g.vc[cs][3];
+#pragma unroll
+        for (int q = 0; q < N; ++q) R[q] = GEN ? Wl * c_tab[N].w[q] * sc * U[q] : 0.0;
+        dir_term<N, GEN>(U, R, Wl, g.vc[cs][2], GEN ? sbk(cs, 2) : 0.0);
+        if constexpr (USEB) bterm<N>(g.Bf[cs][2], U, R, Wl);
+      }
       st<N, G::ZS>(SA + off, U);
       st<N, G::ZS>(SB + off, R);
     }
@@ -471,7 +500,8 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N];
       ld<N, 1>(SA + off, U);
       ld<N, 1>(SB + off, R);
-      dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], GEN ? sbk(cs, 0) : 0.0);
+      if constexpr (!(USEB && fold_volume<N>()))
+        dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][0], GEN ? sbk(cs, 0) : 0.0);
       if constexpr (USEB) bterm<N>(g.Bf[cs][0], U, R, g.tw[a] * g.tw[b]);
       st<N, 1>(SB + off, R);
     }
@@ -483,7 +513,8 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       double U[N], R[N], o[N];
       ld<N, G::YS>(SA + off, U);
       ld<N, G::YS>(SB + off, R);
-      dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], GEN ? sbk(cs, 1) : 0.0);
+      if constexpr (!(USEB && fold_volume<N>()))
+        dir_term<N, GEN>(U, R, g.tw[a] * g.tw[b], g.vc[cs][1], GEN ? sbk(cs, 1) : 0.0);
       if constexpr (USEB) bterm<N>(g.Bf[cs][1], U, R, g.tw[a] * g.tw[b]);
       mtv<N, 0>(R, o);
       st<N, G::YS>(SB + off, o);
@@ -1689,6 +1720,13 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
       d.AW[q * n + j] = t.A[q * n + j] * t.wq[q];
       d.GW[q * n + j] = t.G[q * n + j] * t.wq[q];
       d.DW[q * n + j] = t.D[q * n + j] * t.wq[q] / t.wq[j];
+    }
+  for (int q = 0; q < n; ++q)
+    for (int r = 0; r < n; ++r) {
+      double sg = 0.0;
+      for (int k = 0; k < n; ++k) sg += t.D[k * n + q] * t.wq[k] * t.D[k * n + r];
+      d.SG[q * n + r] = sg;
+      d.CG[q * n + r] = t.D[r * n + q] * t.wq[r];
     }
   for (int i = 0; i < n; ++i)
     for (int j = 0; j < n; ++j) {

@@ -15,10 +15,12 @@ from synth import Problem, uniform_pm1
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from kernel_times import PEAK, timed   # noqa: E402
 
-for p in ([int(a) for a in sys.argv[1:]] or range(1, 8)):
+for p in ([int(a) for a in sys.argv[1:] if not a.startswith('--')] or range(1, 8)):
     n = p + 1
     m = int(round((8e6 / n ** 3) ** (1 / 3)))
     P = Problem(m, m, m, p, K=np.ones(m ** 3))
+    if "--gen" in sys.argv:   # a zero reaction array: the general (convection / reaction) kernels
+        P.c = np.zeros(m ** 3)
     u, f = uniform_pm1(900 + p, 0, P.n_dof), uniform_pm1(910 + p, 0, P.n_dof)
     ctx = dg.DGContext(P)
     ut, ft = torch.from_numpy(u).cuda(), torch.from_numpy(f).cuda()
@@ -32,11 +34,21 @@ for p in ([int(a) for a in sys.argv[1:]] or range(1, 8)):
     t = timed(lambda: ctx.apply(ut, out))
     r["apply_us"], r["apply_frac"] = t, nc * (vol + 6 * sf + 6 * nf) / (t * 1e-6) / PEAK
     r["apply_gdof_s"] = P.n_dof / (t * 1e-6) / 1e9
-    uu = ut.clone()
-    t = timed(lambda: ctx.sweep(uu, ft, 1.0, 1e-12), calls=2)
+    uu = torch.empty_like(ut)
+    t = timed(lambda: ctx.sweep_to(ut, ft, uu, 1.0, 1e-12), calls=2)
     st = ctx.stats()
     fl = nc * (vol + 6 * sf + 6 * nf + 4 * n ** 3) + st["it_sum"] * (vol + 6 * sf + 12 * n ** 3)
     r["sweep_us"], r["sweep_frac"], r["it_mean"] = t, fl / (t * 1e-6) / PEAK, st["it_mean"]
     r["sweep_gdof_s"] = P.n_dof / (t * 1e-6) / 1e9
+    if "--conv" in sys.argv:
+        # convection-diffusion (K = 1e-2, b = (1, .5, .25)): local BiCGStab, 2 D_T per iteration
+        ctx.close()
+        Pc = Problem(m, m, m, p, K=np.full(m ** 3, 1e-2), b=(1.0, 0.5, 0.25))
+        ctx = dg.DGContext(Pc)
+        t = timed(lambda: ctx.sweep_to(ut, ft, uu, 1.0, 1e-12), calls=2)
+        st = ctx.stats()
+        volc = vol + 4 * n ** 3
+        fl = nc * (volc + 6 * sf + 6 * nf + 4 * n ** 3) + st["it_sum"] * 2 * (volc + 6 * sf + 10 * n ** 3)
+        r["conv_sweep_us"], r["conv_sweep_frac"], r["conv_it_mean"] = t, fl / (t * 1e-6) / PEAK, st["it_mean"]
     print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in r.items()}), flush=True)
     ctx.close()

@@ -17,7 +17,7 @@ Au = torch.empty_like(ut)
 for _ in range(3):
     ctx.apply(ut, Au)
 for _ in range(2):
-    ctx.sweep(ut, ft, 1.0, 1e-12)
+    ctx.sweep_to(ut, ft, Au, 1.0, 1e-12)
 torch.cuda.synchronize()
 print("ok", ctx.stats())
 # the volume kernel alone (dg_apply_parts, mask = volume)
