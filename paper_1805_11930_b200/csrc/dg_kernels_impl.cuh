@@ -47,6 +47,7 @@ struct DevTab {
   // Gauss-point line forms of the volume terms along one direction (collocation derivative D,
   // weights w): SG = D^T W D (stiffness), CG = D^T W (convection, test derivative)
   double SG[64], CG[64];
+  double SGW[64];                     // SG[r][s] / w_r: the plane kernels' unweighted residual form
 };
 __constant__ DevTab c_tab[kMaxN + 1];
 
@@ -1726,6 +1727,7 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
       double sg = 0.0;
       for (int k = 0; k < n; ++k) sg += t.D[k * n + q] * t.wq[k] * t.D[k * n + r];
       d.SG[q * n + r] = sg;
+      d.SGW[q * n + r] = sg / t.wq[q];
       d.CG[q * n + r] = t.D[r * n + q] * t.wq[r];
     }
   for (int i = 0; i < n; ++i)

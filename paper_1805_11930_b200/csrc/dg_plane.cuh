@@ -132,6 +132,7 @@ template <int N> __device__ __forceinline__ void load_rows(Rows<N>& r, int t) {
 template <int N> __device__ __forceinline__ double T_AW(int i) { return c_tab[N].AW[i]; }
 template <int N> __device__ __forceinline__ double T_GW(int i) { return c_tab[N].GW[i]; }
 template <int N> __device__ __forceinline__ double T_DW(int i) { return c_tab[N].DW[i]; }
+template <int N> __device__ __forceinline__ double T_SGW(int i) { return c_tab[N].SGW[i]; }
 
 // ---- coalesced tile staging: C cells x n^3 (contiguous in global) -> TB layout ---------
 // element (k, j, i) of cell slot cs at cs*CTB + k*KS + j*N + i
@@ -589,7 +590,9 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
 #pragma unroll
           for (int j = 0; j < N; ++j) {
             s = fma(T_A<N>(qy * N + j), a[j][qx], s);
-            sy = fma(T_G<N>(qy * N + j), a[j][qx], sy);
+            // GEN: the y derivative at the Gauss points; diffusion: the exact 1D stiffness
+            // along y (nodal to nodal, Shat = G^T W G) — index qy then stands for node j
+            sy = fma(GEN ? T_G<N>(qy * N + j) : c_tab[N].S[qy * N + j], a[j][qx], sy);
           }
           tb[k * G::KS + qy * N + qx] = s;
           if (vol) tb[G::ARR + k * G::KS + qy * N + qx] = sy;
@@ -657,26 +660,70 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           c0[k] = tb[k * G::KS + qy * N + qx];
           c1[k] = tb[G::ARR + k * G::KS + qy * N + qx];
         }
+        if constexpr (GEN) {
 #pragma unroll
-        for (int qz = 0; qz < N; ++qz) {
-          double s = 0.0, s1 = 0.0;
+          for (int qz = 0; qz < N; ++qz) {
+            double s = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              s = fma(T_A<N>(qz * N + k), c0[k], s);
+              s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
+            }
+            U[qz][qx] = s;
+            R[qz][qx] = cR * s;
+            fy_[qz] = fma(cK, s1, -vbc[1] * s);
+          }
 #pragma unroll
           for (int k = 0; k < N; ++k) {
-            s = fma(T_A<N>(qz * N + k), c0[k], s);
-            s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
+            double s = 0.0;
+#pragma unroll
+            for (int qz = 0; qz < N; ++qz) s = fma(T_AW<N>(qz * N + k), fy_[qz], s);
+            tb[G::ARR + k * G::KS + qy * N + qx] = s;
           }
-          U[qz][qx] = s;
-          R[qz][qx] = GEN ? cR * s : 0.0;
-          fy_[qz] = GEN ? fma(cK, s1, -vbc[1] * s) : cK * s1;
-        }
+        } else {
+          // diffusion: the y term is Ky (Mhat_z (x) Shat_y) on the x-Gauss / y,z-nodal values
+          // (constant coefficient on the affine cell: the y and z quadratures are the exact 1D
+          // mass and stiffness); c1 already holds Shat_y a, only the z mass is left, and Q3 adds
+          // the result without the G_y^T contraction
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          double s = 0.0;
+          for (int qz = 0; qz < N; ++qz) {
+            double s = 0.0;
 #pragma unroll
-          for (int qz = 0; qz < N; ++qz) s = fma(T_AW<N>(qz * N + k), fy_[qz], s);
-          tb[G::ARR + k * G::KS + qy * N + qx] = s;
+            for (int k = 0; k < N; ++k) s = fma(T_A<N>(qz * N + k), c0[k], s);
+            U[qz][qx] = s;
+            R[qz][qx] = 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double s = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < N; ++kk) s = fma(c_tab[N].M[k * N + kk], c1[kk], s);
+            tb[G::ARR + k * G::KS + qy * N + qx] = cK * s;
+          }
         }
       }
+      if constexpr (!GEN) {
+        // pure diffusion: the coefficient is constant along each line, so the derivative pair
+        // DW^T (sK D U) is one Gauss-point stiffness matvec sK (SGW U), SGW = DW^T D
+#pragma unroll
+        for (int qz = 0; qz < N; ++qz)
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s = fma(T_SGW<N>(r * N + q), U[qz][q], s);
+            R[qz][r] = fma(vcell[0], s, R[qz][r]);
+          }
+#pragma unroll
+        for (int qx = 0; qx < N; ++qx)
+#pragma unroll
+          for (int r = 0; r < N; ++r) {
+            double s = 0.0;
+#pragma unroll
+            for (int q = 0; q < N; ++q) s = fma(T_SGW<N>(r * N + q), U[q][qx], s);
+            R[r][qx] = fma(vcell[2], s, R[r][qx]);
+          }
+      } else {
       // x direction: rows qz;  R += DW^T (sK D U - sb U)
 #pragma unroll
       for (int qz = 0; qz < N; ++qz) {
@@ -686,7 +733,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[qz][r], du);
-          F[q] = GEN ? fma(vcell[0], du, -vbc[0] * U[qz][q]) : vcell[0] * du;
+          F[q] = fma(vcell[0], du, -vbc[0] * U[qz][q]);
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -705,7 +752,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           double du = 0.0;
 #pragma unroll
           for (int r = 0; r < N; ++r) du = fma(T_D<N>(q * N + r), U[r][qx], du);
-          F[q] = GEN ? fma(vcell[2], du, -vbc[2] * U[q][qx]) : vcell[2] * du;
+          F[q] = fma(vcell[2], du, -vbc[2] * U[q][qx]);
         }
 #pragma unroll
         for (int r = 0; r < N; ++r) {
@@ -714,6 +761,7 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           for (int q = 0; q < N; ++q) s = fma(T_DW<N>(q * N + r), F[q], s);
           R[r][qx] = s;
         }
+      }
       }
     } else {
       // faces only: U still needed for the traces
@@ -891,11 +939,11 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
-        double s = 0.0;
+        double s = GEN ? 0.0 : f[j];   // diffusion: the y term is already nodal in j
 #pragma unroll
         for (int qy = 0; qy < N; ++qy) {
           s = fma(T_AW<N>(qy * N + j), r[qy], s);
-          s = fma(T_GW<N>(qy * N + j), f[qy], s);
+          if constexpr (GEN) s = fma(T_GW<N>(qy * N + j), f[qy], s);
         }
         Vq[j][qx] = s;
       }
