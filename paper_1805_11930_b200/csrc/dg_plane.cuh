@@ -582,20 +582,24 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
           for (int i = 0; i < N; ++i) s = fma(T_A<N>(q * N + i), in[j][i], s);
           a[j][q] = s;
         }
+      // the y terms of the volume (constant coefficients on the affine cell): the exact 1D
+      // stiffness / convection matrices along y, nodal to nodal (Shat = G^T W G,
+      // Chat = G^T W A), scaled by the cell's |T| K_y / h_y^2 and |T| b_y / h_y; Q2 adds the
+      // z mass and Q3 the result without a G_y^T contraction (index qy stands for node j there)
+      const double cKy = cl.vc[L.cs][1], cBy = cl.vb[L.cs][1];
 #pragma unroll
       for (int qx = 0; qx < N; ++qx)
 #pragma unroll
         for (int qy = 0; qy < N; ++qy) {
-          double s = 0.0, sy = 0.0;
+          double s = 0.0, sy = 0.0, cy = 0.0;
 #pragma unroll
           for (int j = 0; j < N; ++j) {
             s = fma(T_A<N>(qy * N + j), a[j][qx], s);
-            // GEN: the y derivative at the Gauss points; diffusion: the exact 1D stiffness
-            // along y (nodal to nodal, Shat = G^T W G) — index qy then stands for node j
-            sy = fma(GEN ? T_G<N>(qy * N + j) : c_tab[N].S[qy * N + j], a[j][qx], sy);
+            sy = fma(c_tab[N].S[qy * N + j], a[j][qx], sy);
+            if constexpr (GEN) cy = fma(c_tab[N].Cm[qy * N + j], a[j][qx], cy);
           }
           tb[k * G::KS + qy * N + qx] = s;
-          if (vol) tb[G::ARR + k * G::KS + qy * N + qx] = sy;
+          if (vol) tb[G::ARR + k * G::KS + qy * N + qx] = GEN ? fma(cKy, sy, -cBy * cy) : cKy * sy;
         }
     }
     // y faces (normal y; tangential z = this lane, x): nodal S/T combos, then A_x
@@ -651,55 +655,32 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
     if (vol) {
       // U = A_z t2, Uy = A_z t2y; Stage 2 for the reaction and the y flux pointwise; the y flux
       // column goes straight through (A w)_z^T into TB (its t2y column has just been read)
-      const double cK = vcell[1], cR = vcell[3];
+      const double cR = vcell[3];
 #pragma unroll
       for (int qx = 0; qx < N; ++qx) {
-        double c0[N], c1[N], fy_[N];
+        double c0[N], c1[N];
 #pragma unroll
         for (int k = 0; k < N; ++k) {
           c0[k] = tb[k * G::KS + qy * N + qx];
           c1[k] = tb[G::ARR + k * G::KS + qy * N + qx];
         }
-        if constexpr (GEN) {
+        // U at the Gauss points (+ the reaction), and the y terms (c1: (K_y Shat - b_y Chat)_y a
+        // from Q1) through the exact z mass: (Mhat_z (x) (K_y Shat - b_y Chat)_y) on the
+        // x-Gauss / y,z-nodal values; Q3 adds them without a G_y^T contraction
 #pragma unroll
-          for (int qz = 0; qz < N; ++qz) {
-            double s = 0.0, s1 = 0.0;
+        for (int qz = 0; qz < N; ++qz) {
+          double s = 0.0;
 #pragma unroll
-            for (int k = 0; k < N; ++k) {
-              s = fma(T_A<N>(qz * N + k), c0[k], s);
-              s1 = fma(T_A<N>(qz * N + k), c1[k], s1);
-            }
-            U[qz][qx] = s;
-            R[qz][qx] = cR * s;
-            fy_[qz] = fma(cK, s1, -vbc[1] * s);
-          }
+          for (int k = 0; k < N; ++k) s = fma(T_A<N>(qz * N + k), c0[k], s);
+          U[qz][qx] = s;
+          R[qz][qx] = GEN ? cR * s : 0.0;
+        }
 #pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double s = 0.0;
+        for (int k = 0; k < N; ++k) {
+          double s = 0.0;
 #pragma unroll
-            for (int qz = 0; qz < N; ++qz) s = fma(T_AW<N>(qz * N + k), fy_[qz], s);
-            tb[G::ARR + k * G::KS + qy * N + qx] = s;
-          }
-        } else {
-          // diffusion: the y term is Ky (Mhat_z (x) Shat_y) on the x-Gauss / y,z-nodal values
-          // (constant coefficient on the affine cell: the y and z quadratures are the exact 1D
-          // mass and stiffness); c1 already holds Shat_y a, only the z mass is left, and Q3 adds
-          // the result without the G_y^T contraction
-#pragma unroll
-          for (int qz = 0; qz < N; ++qz) {
-            double s = 0.0;
-#pragma unroll
-            for (int k = 0; k < N; ++k) s = fma(T_A<N>(qz * N + k), c0[k], s);
-            U[qz][qx] = s;
-            R[qz][qx] = 0.0;
-          }
-#pragma unroll
-          for (int k = 0; k < N; ++k) {
-            double s = 0.0;
-#pragma unroll
-            for (int kk = 0; kk < N; ++kk) s = fma(c_tab[N].M[k * N + kk], c1[kk], s);
-            tb[G::ARR + k * G::KS + qy * N + qx] = cK * s;
-          }
+          for (int kk = 0; kk < N; ++kk) s = fma(c_tab[N].M[k * N + kk], c1[kk], s);
+          tb[G::ARR + k * G::KS + qy * N + qx] = s;
         }
       }
       if constexpr (!GEN) {
@@ -939,12 +920,9 @@ __device__ __forceinline__ void plane_op(const KParams& kp, const Cells<N, WB>& 
       }
 #pragma unroll
       for (int j = 0; j < N; ++j) {
-        double s = GEN ? 0.0 : f[j];   // diffusion: the y term is already nodal in j
+        double s = f[j];   // the y terms are already nodal in j
 #pragma unroll
-        for (int qy = 0; qy < N; ++qy) {
-          s = fma(T_AW<N>(qy * N + j), r[qy], s);
-          if constexpr (GEN) s = fma(T_GW<N>(qy * N + j), f[qy], s);
-        }
+        for (int qy = 0; qy < N; ++qy) s = fma(T_AW<N>(qy * N + j), r[qy], s);
         Vq[j][qx] = s;
       }
     }
