@@ -145,12 +145,25 @@ template <int N, int S> __device__ __forceinline__ void st(double* p, const doub
 
 // Stage 2 + the derivative half of stage 3 along one line of direction k:
 // R += D^T ( Wl * w_q * (sK * (D U)_q - sb * U_q) )
+// GEN = false (diffusion): the coefficient is constant along the line, so D^T W (sK D U) is the
+// Gauss-point stiffness matvec sK (SG U), SG = D^T W D: one contraction instead of two
 template <int N, bool GEN = true> __device__ __forceinline__ void dir_term(const double* U, double* R, double Wl,
                                                                            double sK, double sb) {
+  if constexpr (!GEN) {
+    const double f = Wl * sK;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) s = fma(c_tab[N].SG[r * N + q], U[q], s);
+      R[r] = fma(f, s, R[r]);
+    }
+    return;
+  }
   double du[N], F[N], t[N];
   mv<N, 1>(U, du);
 #pragma unroll
-  for (int q = 0; q < N; ++q) F[q] = Wl * c_tab[N].w[q] * (GEN ? fma(sK, du[q], -sb * U[q]) : sK * du[q]);
+  for (int q = 0; q < N; ++q) F[q] = Wl * c_tab[N].w[q] * fma(sK, du[q], -sb * U[q]);
   mtv<N, 1>(F, t);
 #pragma unroll
   for (int r = 0; r < N; ++r) R[r] += t[r];
@@ -644,7 +657,7 @@ __device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
 // =============================== kernels ========================================
 
 // FACES = false, USEB = true: D_T (self faces as Gauss-point operators, no face passes)
-template <int N, bool FACES = true, bool USEB = false>
+template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
   using G = Geo<N>;
@@ -660,7 +673,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   if constexpr (USEB) self_face_ops<N>(kp, g);
   const int nvalid = min(G::C, kp.ncells - cell0);
   double* o = out + (size_t)cell0 * G::N3;
-  cell_operator<N, FACES, USEB>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
+  cell_operator<N, FACES, USEB, false, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
                           [&](int cs, int j, int k, const double* v) {
                             if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
                           });
@@ -1618,7 +1631,10 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   if (grid == 0) return cudaSuccess;
   const size_t smem = smem_bytes<N>(3);
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point operators
-  auto kl = kp.mask == 1u ? k_apply<N, false> : (!with_nbr && kp.mask == 7u ? k_apply<N, false, true> : k_apply<N, true>);
+  const bool gen = gen_terms(kp);
+  auto kl = kp.mask == 1u ? (gen ? k_apply<N, false> : k_apply<N, false, false, false>)
+                          : (!with_nbr && kp.mask == 7u ? (gen ? k_apply<N, false, true> : k_apply<N, false, true, false>)
+                                                        : (gen ? k_apply<N, true> : k_apply<N, true, false, false>));
   cudaError_t e = set_smem(kl, smem);
   if (e != cudaSuccess) return e;
   kl<<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
