@@ -342,16 +342,19 @@ __device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncel
 
 // ---- faces, part 1: traces -> S/T arrays per face node (+ tangential mass) ------
 // face buffer: FB[((cs*3 + axis)*4 + arr)*N2 + l], arr: 0 S_lo, 1 T_lo, 2 S_hi, 3 T_hi
+// The neighbours' lines wlo / whi (the normal line through the face node, from the neighbour
+// below / above; loaded by the caller ahead of time, see cell_operator) enter through their end
+// value and end derivative. hlo / hhi: the neighbour exists (interior or ghost-layer face).
 template <int N, int AX>
 __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, double* FB,
-                                          int cs, int a, int b, double inv_h) {
+                                          int cs, int a, int b, double inv_h, const double* wlo,
+                                          const double* whi, bool hlo, bool hhi) {
   using G = Geo<N>;
-  int off, goff;
+  int off;
   constexpr int SS = AX == 0 ? 1 : (AX == 1 ? G::YS : G::ZS);   // smem stride along the line
-  constexpr int GS = AX == 0 ? 1 : (AX == 1 ? N : G::N2);       // global stride
-  if (AX == 0) { off = b * G::ZS + a * G::YS; goff = b * G::N2 + a * N; }
-  else if (AX == 1) { off = b * G::ZS + a; goff = b * G::N2 + a; }
-  else { off = b * G::YS + a; goff = b * N + a; }
+  if (AX == 0) off = b * G::ZS + a * G::YS;
+  else if (AX == 1) off = b * G::ZS + a;
+  else off = b * G::YS + a;
   double v[N];
   ld<N, SS>(src + cs * G::CS + off, v);
   double glo = 0.0, ghi = 0.0;
@@ -366,25 +369,19 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
   const double* chi = g.fc[cs][2 * AX + 1];
   double Slo = clo[0] * v[0] + clo[1] * glo, Tlo = clo[4] * v[0];
   double Shi = chi[0] * v[N - 1] + chi[1] * ghi, Thi = chi[4] * v[N - 1];
-  const double* nlo = g.nb[cs][2 * AX];
-  const double* nhi = g.nb[cs][2 * AX + 1];
-  if (nlo) {  // neighbour below: its hi trace (node N-1) and d1 derivative
-    double w[N];
-    ld<N, GS>(nlo + goff, w);
+  if (hlo) {  // neighbour below: its hi trace (node N-1) and d1 derivative
     double gn = 0.0;
 #pragma unroll
-    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
-    Slo += clo[2] * w[N - 1] + clo[3] * gn * inv_h;
-    Tlo += clo[5] * w[N - 1];
+    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], wlo[e], gn);
+    Slo += clo[2] * wlo[N - 1] + clo[3] * gn * inv_h;
+    Tlo += clo[5] * wlo[N - 1];
   }
-  if (nhi) {  // neighbour above: its lo trace (node 0) and d0 derivative
-    double w[N];
-    ld<N, GS>(nhi + goff, w);
+  if (hhi) {  // neighbour above: its lo trace (node 0) and d0 derivative
     double gn = 0.0;
 #pragma unroll
-    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
-    Shi += chi[2] * w[0] + chi[3] * gn * inv_h;
-    Thi += chi[5] * w[0];
+    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], whi[e], gn);
+    Shi += chi[2] * whi[0] + chi[3] * gn * inv_h;
+    Thi += chi[5] * whi[0];
   }
   double* fb = FB + (cs * 3 + AX) * 4 * G::N2 + a + N * b;
   fb[0 * G::N2] = Slo;
@@ -416,7 +413,6 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
   const int lb = WARP ? (tid >> 5) * N2 + (tid & 31) : tid;
   const int le = WARP ? ((tid >> 5) + 1) * N2 : LINES;
   constexpr int ls = WARP ? 32 : NT;
-  const double inv_h[3] = {1.0 / kp.h[0], 1.0 / kp.h[1], 1.0 / kp.h[2]};
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
   // advection scalings |T| b_k / h_k: in warp mode the warp's own cell's, read once (registers,
   // like the constant-b values they replace); otherwise per line item from shared memory
@@ -426,13 +422,31 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
     for (int a = 0; a < 3; ++a) sbw[a] = g.vb[tid >> 5][a];
   auto sbk = [&](int cs, int a) { return WARP ? sbw[a] : g.vb[cs][a]; };
 
-  // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src)
+  // pass 1: F1 (face traces, all axes) + P1 (x-lines: SA = A_x src); the neighbours' normal
+  // lines: x neighbours inside the group from the tile in shared memory, the others from global
+  // memory (prefetching them into registers cost more in occupancy than it saved in latency)
   for (int it = tid; FACES && it < 3 * LINES; it += NT) {
     const int ax = it / LINES, r = it % LINES, cs = r / N2, l = r % N2;
     const int a = l % N, b = l / N;
-    if (ax == 0) face_line<N, 0>(g, src, FB, cs, a, b, inv_h[0]);
-    else if (ax == 1) face_line<N, 1>(g, src, FB, cs, a, b, inv_h[1]);
-    else face_line<N, 2>(g, src, FB, cs, a, b, inv_h[2]);
+    const double* nlo = g.nb[cs][2 * ax];
+    const double* nhi = g.nb[cs][2 * ax + 1];
+    double wl[N], wh[N];
+    if (ax == 0) {
+      const int off = b * G::ZS + a * G::YS, goff = b * N2 + a * N;
+      if (nlo) { if (cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, wl); else ld<N, 1>(nlo + goff, wl); }
+      if (nhi) { if (cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, wh); else ld<N, 1>(nhi + goff, wh); }
+      face_line<N, 0>(g, src, FB, cs, a, b, kp.ih[0], wl, wh, nlo != nullptr, nhi != nullptr);
+    } else if (ax == 1) {
+      const int goff = b * N2 + a;
+      if (nlo) ld<N, N>(nlo + goff, wl);
+      if (nhi) ld<N, N>(nhi + goff, wh);
+      face_line<N, 1>(g, src, FB, cs, a, b, kp.ih[1], wl, wh, nlo != nullptr, nhi != nullptr);
+    } else {
+      const int goff = b * N + a;
+      if (nlo) ld<N, N2>(nlo + goff, wl);
+      if (nhi) ld<N, N2>(nhi + goff, wh);
+      face_line<N, 2>(g, src, FB, cs, a, b, kp.ih[2], wl, wh, nlo != nullptr, nhi != nullptr);
+    }
   }
   if (vol) {
     for (int it = lb; it < le; it += ls) {
@@ -656,7 +670,29 @@ __device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
 
 // =============================== kernels ========================================
 
-// FACES = false, USEB = true: D_T (self faces as Gauss-point operators, no face passes)
+// ---- asynchronous tile staging (cp.async: no registers held while the copies are in flight) --
+__device__ __forceinline__ void lcp_async8(double* dst, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void lcp_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+// the group's own tile (contiguous in global) into the padded CS layout, zero past the end
+template <int N>
+__device__ __forceinline__ void async_tile(double* dst, const double* src, int nvalid) {
+  using G = Geo<N>;
+  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+    const int cs = e / G::N3, r = e % G::N3;
+    const int i = r % N, j = (r / N) % N, k = r / G::N2;
+    lcp_async8(dst + cs * G::CS + k * G::ZS + j * G::YS + i, src + (cs < nvalid ? e : 0), cs < nvalid);
+  }
+}
+
+// FACES = false, USEB = true: D_T (self faces as Gauss-point operators, no face passes).
+// The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
+// lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
+// before the first read of u).
 template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
@@ -668,10 +704,14 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   double* SB = SA + G::TENSOR;
   double* FB = SB + G::TENSOR;
   const int cell0 = blockIdx.x * G::C;
-  load_tile<N>(g, cell0, kp.ncells, u, SRC);
-  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
-  if constexpr (USEB) self_face_ops<N>(kp, g);
   const int nvalid = min(G::C, kp.ncells - cell0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // pointers only; ends with __syncthreads
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  async_tile<N>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  if constexpr (USEB) self_face_ops<N>(kp, g);
+  lcp_wait_all();
+  __syncthreads();
   double* o = out + (size_t)cell0 * G::N3;
   cell_operator<N, FACES, USEB, false, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
                           [&](int cs, int j, int k, const double* v) {
@@ -1635,10 +1675,20 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   auto kl = kp.mask == 1u ? (gen ? k_apply<N, false> : k_apply<N, false, false, false>)
                           : (!with_nbr && kp.mask == 7u ? (gen ? k_apply<N, false, true> : k_apply<N, false, true, false>)
                                                         : (gen ? k_apply<N, true> : k_apply<N, true, false, false>));
-  cudaError_t e = set_smem(kl, smem);
+  const size_t smem_n = smem;
+  cudaError_t e = set_smem(kl, smem_n);
   if (e != cudaSuccess) return e;
-  kl<<<grid, G::NT, smem, s>>>(kp, u, out, with_nbr);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G::NT);
+  cfg.dynamicSmemBytes = smem_n;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kl, kp, u, out, with_nbr);
 }
 
 template <int N, bool SWEEP>
