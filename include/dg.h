@@ -104,7 +104,8 @@ dg_status dg_local_range(const dg_ctx* ctx, int32_t* z_begin, int32_t* z_end, in
 
 /* Au = A u, matrix-free: sum-factorised volume terms (Stages 1-3)
  * plus interior/boundary face terms. u, Au: device [n_local_dof], must not alias.
- * With nranks > 1 the z-boundary layers of u are exchanged first (NCCL or external). */
+ * With nranks > 1 the face traces of the z-boundary layers are exchanged first (NCCL send/recv
+ * of 2 n^2 doubles per column and side, or caller-filled in external mode). */
 dg_status dg_apply(dg_ctx* ctx, const double* u, double* Au, void* cuda_stream);
 
 /* One block-Jacobi sweep, Alg. 2 lines 2-4: d = f - A u; for every cell solve
@@ -159,13 +160,19 @@ dg_status dg_get_stats(dg_ctx* ctx, dg_stats* st);
 dg_status dg_apply_parts(dg_ctx* ctx, const double* u, double* out, uint32_t mask, void* cuda_stream);
 dg_status dg_block_diag_apply(dg_ctx* ctx, const double* u, double* Du, void* cuda_stream);
 
-/* External halo mode: device pointers of the ghost layers (nx*ny cells, n^3 DoF each, same
- * layout as u) that hold the neighbouring ranks' adjacent z-layer of u. Filled by the
- * caller before dg_apply / dg_block_jacobi_sweep; NULL where the slab touches the domain. */
-dg_status dg_ghost_layers(dg_ctx* ctx, double** ghost_lo, double** ghost_hi, int64_t* layer_dof);
+/* Ghost buffers (nranks > 1): per slab side the face traces of the neighbouring rank's adjacent
+ * z-layer, [nx*ny][2][n^2] doubles: per column the n^2 face values (node n-1 of the lower rank's
+ * top layer / node 0 of the upper rank's bottom layer, i + n j order) followed by the n^2 normal-
+ * derivative sums sum_k d[k] u_k (d = theta'(1) resp. theta'(0), unscaled). A neighbour enters the
+ * face terms only through these, so the halo is 2 n^2 instead of n^3 doubles per
+ * column. *ghost_len = nx*ny*2n^2; NULL pointers where the slab touches the domain boundary. */
+dg_status dg_ghost_layers(dg_ctx* ctx, double** ghost_lo, double** ghost_hi, int64_t* ghost_len);
 
-/* External halo mode: copies caller device buffers (each one layer: nx*ny cells, n^3 DoF) into
- * the ghost layers, stream ordered. lo / hi may be NULL when the slab has no such neighbour. */
+/* External halo mode: fills the ghost buffers from the neighbouring ranks' adjacent LAYERS
+ * (device, nx*ny cells of n^3 DoF each, the layout of u): lo = the lower rank's top layer,
+ * hi = the upper rank's bottom layer; their traces are packed by the same kernel (and the same
+ * arithmetic) the NCCL mode uses. Stream ordered; lo / hi may be NULL where there is no such
+ * neighbour. */
 dg_status dg_fill_ghosts(dg_ctx* ctx, const double* lo, const double* hi, void* cuda_stream);
 
 /* The 1D tables used by the kernels, for parity with the oracle's own: out receives

@@ -90,8 +90,10 @@ struct dg_ctx {
   double* d_bc = nullptr;      // per-cell b with ghost layers (or nullptr)
   bool has_b = false;          // any non-zero advection (selects BiCGStab for DG_LOCAL_AUTO)
   double* d_c = nullptr;
-  double* d_ghost_lo = nullptr;
-  double* d_ghost_hi = nullptr;
+  double* d_ghost_lo = nullptr;   // [nxy][2][n^2] trace records of the lower rank's top layer
+  double* d_ghost_hi = nullptr;   // ... of the upper rank's bottom layer
+  double* d_send = nullptr;       // NCCL mode: [2][nxy][2][n^2] this rank's bottom / top traces
+  int64_t ghost_len = 0;          // doubles per ghost buffer: nxy * 2 n^2
   double* d_unew = nullptr;
   int32_t* d_its = nullptr;
   int32_t* d_gperm = nullptr;  // solver CTA -> cell group, boundary-heavy groups first
@@ -157,6 +159,7 @@ void release(dg_ctx* c) {
   cudaFree(c->d_c);
   cudaFree(c->d_ghost_lo);
   cudaFree(c->d_ghost_hi);
+  cudaFree(c->d_send);
   cudaFree(c->d_unew);
   cudaFree(c->d_its);
   cudaFree(c->d_gperm);
@@ -171,17 +174,26 @@ void release(dg_ctx* c) {
   delete c;
 }
 
+// Halo exchange of the face traces (a neighbour enters the face terms only through
+// its trace and normal derivative): each rank packs its bottom and top layers' traces (2 n^2
+// doubles per column instead of the n^3 of the layer) and sends them to the ranks below / above.
 dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
   if (c->desc.nranks == 1 || c->desc.halo_mode == DG_HALO_EXTERNAL) return DG_OK;
   const int64_t* pl = c->plan;
-  const size_t L = (size_t)pl[2];
+  const size_t L = (size_t)c->ghost_len;
+  const int ncol = c->desc.nx * c->desc.ny;
+  cudaError_t ce = cudaSuccess;
+  if (pl[3] >= 0) ce = dg::launch_pack_traces(c->desc.p, c->tab, u + pl[0], ncol, 0, c->d_send, s);
+  if (ce == cudaSuccess && pl[4] >= 0)
+    ce = dg::launch_pack_traces(c->desc.p, c->tab, u + pl[1], ncol, 1, c->d_send + L, s);
+  if (ce != cudaSuccess) return cuda_fail(ce, "pack traces");
   ncclResult_t e = g_nccl.groupStart();
   if (pl[3] >= 0) {
-    e |= g_nccl.send(u + pl[0], L, ncclFloat64, (int)pl[3], c->comm, s);
+    e |= g_nccl.send(c->d_send, L, ncclFloat64, (int)pl[3], c->comm, s);
     e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, (int)pl[3], c->comm, s);
   }
   if (pl[4] >= 0) {
-    e |= g_nccl.send(u + pl[1], L, ncclFloat64, (int)pl[4], c->comm, s);
+    e |= g_nccl.send(c->d_send + L, L, ncclFloat64, (int)pl[4], c->comm, s);
     e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, (int)pl[4], c->comm, s);
   }
   e |= g_nccl.groupEnd();
@@ -279,11 +291,13 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
     if ((e = alloc((void**)&c->d_c, (size_t)c->ncells * 8)) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc c"); }
     if ((e = cudaMemcpy(c->d_c, desc->c + (size_t)c->z_begin * nxy, (size_t)c->ncells * 8, cudaMemcpyHostToDevice)) != cudaSuccess) { release(c); return cuda_fail(e, "copy c"); }
   }
+  c->ghost_len = nxy * 2 * c->n * c->n;
   if (G > 1) {
-    if (alloc((void**)&c->d_ghost_lo, (size_t)c->layer_dof * 8) != cudaSuccess ||
-        alloc((void**)&c->d_ghost_hi, (size_t)c->layer_dof * 8) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc ghosts"); }
-    cudaMemset(c->d_ghost_lo, 0, (size_t)c->layer_dof * 8);
-    cudaMemset(c->d_ghost_hi, 0, (size_t)c->layer_dof * 8);
+    if (alloc((void**)&c->d_ghost_lo, (size_t)c->ghost_len * 8) != cudaSuccess ||
+        alloc((void**)&c->d_ghost_hi, (size_t)c->ghost_len * 8) != cudaSuccess ||
+        alloc((void**)&c->d_send, (size_t)c->ghost_len * 2 * 8) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc ghosts"); }
+    cudaMemset(c->d_ghost_lo, 0, (size_t)c->ghost_len * 8);
+    cudaMemset(c->d_ghost_hi, 0, (size_t)c->ghost_len * 8);
   }
   if (alloc((void**)&c->d_unew, (size_t)c->ndof * 8) != cudaSuccess ||
       alloc((void**)&c->d_its, (size_t)c->ncells * 4) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc scratch"); }
@@ -385,11 +399,11 @@ dg_status dg_local_range(const dg_ctx* c, int32_t* zb, int32_t* ze, int64_t* nd)
   return DG_OK;
 }
 
-dg_status dg_ghost_layers(dg_ctx* c, double** lo, double** hi, int64_t* layer_dof) {
+dg_status dg_ghost_layers(dg_ctx* c, double** lo, double** hi, int64_t* ghost_len) {
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (lo) *lo = (double*)c->kp.ghost_lo;
   if (hi) *hi = (double*)c->kp.ghost_hi;
-  if (layer_dof) *layer_dof = c->layer_dof;
+  if (ghost_len) *ghost_len = c->ghost_len;
   return DG_OK;
 }
 
@@ -397,13 +411,14 @@ dg_status dg_fill_ghosts(dg_ctx* c, const double* lo, const double* hi, void* st
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (c->desc.halo_mode != DG_HALO_EXTERNAL) return fail(DG_ERR_STATE, "context is not in external halo mode");
   cudaStream_t s = (cudaStream_t)stream;
-  const size_t bytes = (size_t)c->layer_dof * 8;
+  const int ncol = c->desc.nx * c->desc.ny;
+  // the traces the neighbouring rank would send: the lower rank's top layer, the upper's bottom
   if (lo && c->kp.ghost_lo) {
-    cudaError_t e = cudaMemcpyAsync(c->d_ghost_lo, lo, bytes, cudaMemcpyDeviceToDevice, s);
+    cudaError_t e = dg::launch_pack_traces(c->desc.p, c->tab, lo, ncol, 1, c->d_ghost_lo, s);
     if (e != cudaSuccess) return cuda_fail(e, "fill ghost lo");
   }
   if (hi && c->kp.ghost_hi) {
-    cudaError_t e = cudaMemcpyAsync(c->d_ghost_hi, hi, bytes, cudaMemcpyDeviceToDevice, s);
+    cudaError_t e = dg::launch_pack_traces(c->desc.p, c->tab, hi, ncol, 0, c->d_ghost_hi, s);
     if (e != cudaSuccess) return cuda_fail(e, "fill ghost hi");
   }
   return DG_OK;

@@ -32,7 +32,44 @@ __global__ void __launch_bounds__(256) k_dfma(double* sink, int iters) {
   sink[blockIdx.x * 256 + threadIdx.x] = s;
 }
 
+struct DVec { double d[kMaxN]; };
+
+template <int N>
+__global__ void __launch_bounds__(256) k_pack_traces(const double* __restrict__ layer, int ncol, int top,
+                                                     DVec d, double* __restrict__ out) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;   // (col, face node)
+  if (e >= ncol * N2) return;
+  const int col = e / N2, node = e % N2;
+  const double* c = layer + (size_t)col * N3 + node;
+  double g = 0.0;
+#pragma unroll
+  for (int k = 0; k < N; ++k) g = fma(d.d[k], c[k * N2], g);   // the receivers' summation order
+  out[(size_t)col * 2 * N2 + node] = c[(top ? N - 1 : 0) * N2];
+  out[(size_t)col * 2 * N2 + N2 + node] = g;
+}
+
 }  // namespace
+
+cudaError_t launch_pack_traces(int p, const Tables1D& t, const double* layer, int ncol, int top,
+                               double* out, cudaStream_t s) {
+  DVec d{};
+  for (int i = 0; i < t.n; ++i) d.d[i] = top ? t.d1[i] : t.d0[i];
+  const int n = p + 1, items = ncol * n * n;
+  if (items == 0) return cudaSuccess;
+  const int blocks = (items + 255) / 256;
+  switch (p) {
+    case 1: k_pack_traces<2><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 2: k_pack_traces<3><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 3: k_pack_traces<4><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 4: k_pack_traces<5><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 5: k_pack_traces<6><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 6: k_pack_traces<7><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    case 7: k_pack_traces<8><<<blocks, 256, 0, s>>>(layer, ncol, top, d, out); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 cudaError_t launch_dfma_bench(double* sink, int blocks, int iters, cudaStream_t s) {
   k_dfma<<<blocks, 256, 0, s>>>(sink, iters);

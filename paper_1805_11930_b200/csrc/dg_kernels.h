@@ -25,8 +25,10 @@ struct KParams {
   const double* c;               // [ncells] reaction or nullptr
   const double* bc;              // [(nzl+2)*nx*ny][3] per-cell b (ghost layers as K) or nullptr:
                                  // constant kp.b; volume: the cell's b, faces: (b^- + b^+)/2 . nu
-  const double* ghost_lo;        // [nx*ny*n^3] neighbour rank's last layer (or nullptr)
-  const double* ghost_hi;        // [nx*ny*n^3] neighbour rank's first layer
+  const double* ghost_lo;        // [nx*ny][2][n^2] face traces of the lower rank's top layer (or nullptr)
+  const double* ghost_hi;        // [nx*ny][2][n^2] face traces of the upper rank's bottom layer
+                                 // (per column: the face values, then the normal-derivative sums
+                                 // sum_k d[k] u_k, unscaled; see ghost_trace / launch_pack_traces)
   uint32_t mask;                 // 1 volume, 2 interior faces, 4 boundary faces
   int32_t max_it;
   int32_t krestart;              // GMRES restart length (0: the compiled basis size)
@@ -42,6 +44,14 @@ struct KParams {
   int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
                                  // group_cell), the other colour is not touched
 };
+
+// The z-face of `cell` on side hi is a slab-boundary face whose neighbour is a ghost-layer
+// trace record (2 n^2 doubles: the neighbour's face values and normal-derivative sums).
+__host__ __device__ inline bool ghost_trace(const KParams& kp, int cell, int hi) {
+  const int nxy = kp.nx * kp.ny;
+  return hi ? (kp.slab_face[5] == FK_GHOST && cell >= kp.ncells - nxy)
+            : (kp.slab_face[4] == FK_GHOST && cell >= 0 && cell < nxy);
+}
 
 // the cell is outside the colour of a multicolour half-sweep (kp.colour >= 0, masked mode)
 __host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
@@ -82,6 +92,13 @@ cudaError_t launch_local_solve(int p, int method, const KParams& kp, const doubl
 // u_new = u + omega D^{-1}(f - A u).
 cudaError_t launch_sweep(int p, int method, const KParams& kp, const double* u, const double* f,
                          double* u_new, cudaStream_t s);
+
+// Face traces of a z-layer for the neighbouring rank (the neighbour enters a face
+// term only through its trace and its normal derivative): layer = ncol cells of n^3 DoF; out
+// [ncol][2][n^2]: top = 0: node-0 values and sum_k d0[k] u_k (for the rank below), top = 1:
+// node-(n-1) values and sum_k d1[k] u_k (for the rank above), summed in the kernels' order.
+cudaError_t launch_pack_traces(int p, const Tables1D& t, const double* layer, int ncol, int top,
+                               double* out, cudaStream_t s);
 
 // fp64 FMA peak microbenchmark: blocks x 256 threads, 16 chains x iters DFMA each.
 cudaError_t launch_dfma_bench(double* sink, int blocks, int iters, cudaStream_t s);

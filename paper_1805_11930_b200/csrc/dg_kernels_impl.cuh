@@ -277,7 +277,7 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*vb_)[3
           kind = 0;
           const int col = coord[0] + kp.nx * coord[1];
           kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
-          if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * N3;
+          if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * 2 * N * N;   // trace record
         } else {
           kind = (sk == FK_DIRICHLET) ? 1 : 2;
         }
@@ -345,10 +345,13 @@ __device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncel
 // The neighbours' lines wlo / whi (the normal line through the face node, from the neighbour
 // below / above; loaded by the caller ahead of time, see cell_operator) enter through their end
 // value and end derivative. hlo / hhi: the neighbour exists (interior or ghost-layer face).
+// tlo / thi: the neighbour is a ghost-layer trace record: w[0] is its face value and w[1] its
+// normal-derivative sum (the sender's arithmetic, bit for bit the value computed here otherwise).
 template <int N, int AX>
 __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, double* FB,
                                           int cs, int a, int b, double inv_h, const double* wlo,
-                                          const double* whi, bool hlo, bool hhi) {
+                                          const double* whi, bool hlo, bool hhi, bool tlo = false,
+                                          bool thi = false) {
   using G = Geo<N>;
   int off;
   constexpr int SS = AX == 0 ? 1 : (AX == 1 ? G::YS : G::ZS);   // smem stride along the line
@@ -370,18 +373,30 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
   double Slo = clo[0] * v[0] + clo[1] * glo, Tlo = clo[4] * v[0];
   double Shi = chi[0] * v[N - 1] + chi[1] * ghi, Thi = chi[4] * v[N - 1];
   if (hlo) {  // neighbour below: its hi trace (node N-1) and d1 derivative
-    double gn = 0.0;
+    double gn = 0.0, av;
+    if (tlo) {
+      av = wlo[0];
+      gn = wlo[1];
+    } else {
 #pragma unroll
-    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], wlo[e], gn);
-    Slo += clo[2] * wlo[N - 1] + clo[3] * gn * inv_h;
-    Tlo += clo[5] * wlo[N - 1];
+      for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], wlo[e], gn);
+      av = wlo[N - 1];
+    }
+    Slo += clo[2] * av + clo[3] * gn * inv_h;
+    Tlo += clo[5] * av;
   }
   if (hhi) {  // neighbour above: its lo trace (node 0) and d0 derivative
-    double gn = 0.0;
+    double gn = 0.0, av;
+    if (thi) {
+      av = whi[0];
+      gn = whi[1];
+    } else {
 #pragma unroll
-    for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], whi[e], gn);
-    Shi += chi[2] * whi[0] + chi[3] * gn * inv_h;
-    Thi += chi[5] * whi[0];
+      for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], whi[e], gn);
+      av = whi[0];
+    }
+    Shi += chi[2] * av + chi[3] * gn * inv_h;
+    Thi += chi[5] * av;
   }
   double* fb = FB + (cs * 3 + AX) * 4 * G::N2 + a + N * b;
   fb[0 * G::N2] = Slo;
@@ -442,10 +457,14 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       if (nhi) ld<N, N>(nhi + goff, wh);
       face_line<N, 1>(g, src, FB, cs, a, b, kp.ih[1], wl, wh, nlo != nullptr, nhi != nullptr);
     } else {
+      // slab-boundary faces: the neighbour is a ghost trace record (face values, derivative sums)
       const int goff = b * N + a;
-      if (nlo) ld<N, N2>(nlo + goff, wl);
-      if (nhi) ld<N, N2>(nhi + goff, wh);
-      face_line<N, 2>(g, src, FB, cs, a, b, kp.ih[2], wl, wh, nlo != nullptr, nhi != nullptr);
+      const bool tl = nlo && ghost_trace(kp, g.cell[cs], 0), th = nhi && ghost_trace(kp, g.cell[cs], 1);
+      if (tl) { wl[0] = nlo[goff]; wl[1] = nlo[N2 + goff]; }
+      else if (nlo) ld<N, N2>(nlo + goff, wl);
+      if (th) { wh[0] = nhi[goff]; wh[1] = nhi[N2 + goff]; }
+      else if (nhi) ld<N, N2>(nhi + goff, wh);
+      face_line<N, 2>(g, src, FB, cs, a, b, kp.ih[2], wl, wh, nlo != nullptr, nhi != nullptr, tl, th);
     }
   }
   if (vol) {

@@ -164,14 +164,19 @@ __device__ __forceinline__ void load_own(double (&v)[Geo<N>::PER], const double*
   }
 }
 // neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
+// (z faces at a slab boundary: the neighbour is a trace record of 2 n^2 doubles, which lands in
+// planes 0 and 1 of the staged tile)
 template <int N, bool WB>
-__device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N, WB>& cl, int f) {
+__device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N, WB>& cl, int f,
+                                         const KParams& kp) {
   using G = Geo<N>;
 #pragma unroll
   for (int m = 0; m < G::PER; ++m) {
     const int e = threadIdx.x + m * G::NT;
-    const double* p = (e < G::C * G::N3) ? cl.nb[e / G::N3][f] : nullptr;
-    v[m] = p ? __ldg(p + e % G::N3) : 0.0;
+    const int cs = e / G::N3, r = e % G::N3;
+    const double* p = (e < G::C * G::N3) ? cl.nb[cs][f] : nullptr;
+    if (p && f >= 4 && r >= 2 * G::N2 && ghost_trace(kp, cl.cell[cs], f & 1)) p = nullptr;
+    v[m] = p ? __ldg(p + r) : 0.0;
   }
 }
 template <int N>
@@ -271,8 +276,8 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N, WB>& cl, const La
     store_tile<N>(TB + G::ARR, pv1);
     __syncthreads();
     if (axis == 1) {
-      load_nbr<N>(pv0, cl, 4);
-      load_nbr<N>(pv1, cl, 5);
+      load_nbr<N>(pv0, cl, 4, kp);
+      load_nbr<N>(pv1, cl, 5, kp);
     }
     if (!L.active) continue;
 #pragma unroll
@@ -295,16 +300,22 @@ __device__ void nbr_prologue(const KParams& kp, const Cells<N, WB>& cl, const La
           fy[G::N2 + i] = ctn * a;
         }
       } else {
-        // lane t = y node j: the neighbour's z-lines (kk, i) at fixed j
+        // lane t = y node j: the neighbour's z-lines (kk, i) at fixed j (a ghost trace record:
+        // plane 0 the face values, plane 1 the normal-derivative sums)
         const int j = L.t;
+        const bool tr = ghost_trace(kp, cl.cell[L.cs], hi);
         double S[N], T[N];
 #pragma unroll
         for (int i = 0; i < N; ++i) {
           double g = 0.0;
+          if (tr) {
+            g = nb[G::KS + j * N + i];
+          } else {
 #pragma unroll
-          for (int kk = 0; kk < N; ++kk)
-            g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
-          const double a = nb[(hi ? 0 : N - 1) * G::KS + j * N + i];
+            for (int kk = 0; kk < N; ++kk)
+              g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::KS + j * N + i], g);
+          }
+          const double a = nb[(tr ? 0 : (hi ? 0 : N - 1)) * G::KS + j * N + i];
           S[i] = cna * a + cng * g * kp.ih[2];
           T[i] = ctn * a;
         }
@@ -408,6 +419,8 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
     if (e < G::C * G::N3) {
       const int cs = e / G::N3, r = e % G::N3;
       const double* p = cl.nb[cs][f];
+      // a ghost trace record (z faces at a slab boundary) holds 2 n^2 doubles: planes 0 and 1
+      if (p && f >= 4 && r >= 2 * G::N2 && ghost_trace(kp, cl.cell[cs], f & 1)) p = nullptr;
       cp_async8(dst + cs * CSX + (r / G::N2) * KSX + (r % G::N2), p ? p + r : any, p != nullptr);
     }
   }
@@ -430,17 +443,22 @@ __device__ __forceinline__ void ytrace(const double* nb, const double* c, double
   }
 }
 // z-face traces (lane t = y node j): rows (kk, i) of the neighbour at fixed j, interpolated in x
+// tr: nb is a ghost trace record (plane 0 the face values, plane 1 the derivative sums)
 template <int N, int KSX>
 __device__ __forceinline__ void ztrace(const double* nb, const double* c, double ih, int hi, int j,
-                                       double (&S)[N], double (&T)[N]) {
+                                       double (&S)[N], double (&T)[N], bool tr = false) {
   const double cna = c[2], cng = c[3], ctn = c[5];
   double s0[N], t0[N];
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     double g = 0.0;
+    if (tr) {
+      g = nb[KSX + j * N + i];
+    } else {
 #pragma unroll
-    for (int kk = 0; kk < N; ++kk) g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * KSX + j * N + i], g);
-    const double a = nb[(hi ? 0 : N - 1) * KSX + j * N + i];
+      for (int kk = 0; kk < N; ++kk) g = fma(hi ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * KSX + j * N + i], g);
+    }
+    const double a = nb[(tr ? 0 : (hi ? 0 : N - 1)) * KSX + j * N + i];
     s0[i] = cna * a + cng * g * ih;
     t0[i] = ctn * a;
   }
@@ -515,7 +533,7 @@ __device__ void nbr_prologue_async(const KParams& kp, const Cells<N, WB>& cl, co
         }
         xtrace<N>(plane, cl.fc[L.cs][hi], kp.ih[0], hi, xs[hi][0], xs[hi][1]);
         ztrace<N, G::N2>((hi ? FZ : FX) + L.cs * G::FS, cl.fc[L.cs][4 + hi], kp.ih[2], hi, t,
-                         zs[hi][0], zs[hi][1]);
+                         zs[hi][0], zs[hi][1], ghost_trace(kp, cl.cell[L.cs], hi));
       }
     }
     __syncthreads();   // z staging consumed
@@ -1084,7 +1102,7 @@ __device__ __forceinline__ void setup_issue(const KParams& kp, Cells<N, WB>& cl,
         kind = 0;
         const int col = cx + kp.nx * cy;
         kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
-        if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * G::N3;
+        if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * 2 * G::N2;   // trace record
       } else {
         kind = kp.slab_face[f] == FK_DIRICHLET ? 1 : 2;
       }
@@ -1451,8 +1469,8 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
-      load_nbr<N>(pv0, cl, 2);
-      load_nbr<N>(pv1, cl, 3);
+      load_nbr<N>(pv0, cl, 2, kp);
+      load_nbr<N>(pv1, cl, 3, kp);
       nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     }
     plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
@@ -1840,8 +1858,8 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
-      load_nbr<N>(pv0, cl, 2);
-      load_nbr<N>(pv1, cl, 3);
+      load_nbr<N>(pv0, cl, 2, kp);
+      load_nbr<N>(pv1, cl, 3, kp);
       nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     }
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
@@ -2192,8 +2210,8 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
-      load_nbr<N>(pv0, cl, 2);
-      load_nbr<N>(pv1, cl, 3);
+      load_nbr<N>(pv0, cl, 2, kp);
+      load_nbr<N>(pv1, cl, 3, kp);
       nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     }
     plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);

@@ -312,3 +312,50 @@ def test_partition_invariance_local_methods(p, method, b):
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("p", range(1, 8))
+@pytest.mark.parametrize("method", ["auto", "gmres-thomas"])
+def test_partition_invariance_every_degree(p, method):
+    """Trace halo (2 n^2 per column and side instead of the n^3 layer) through every kernel
+    family: apply (plane p <= 3, line p >= 4) and the sweeps' defects (plane solvers with staged
+    tiles p <= 3, register-staged plane solvers at p = 4 with GMRES, warp / CTA line solvers),
+    G = 3 virtual ranks on one GPU, bit for bit equal to one slab."""
+    if method != "auto" and p > 4:
+        pytest.skip("local GMRES exists for p <= 4")
+    nx, ny, nz = {1: (5, 3, 7), 2: (4, 3, 7), 3: (4, 3, 6), 4: (3, 3, 6), 5: (3, 2, 6), 6: (2, 2, 6),
+                  7: (2, 2, 4)}[p]
+    b = (0.6, -0.3, 0.4) if method != "auto" else (0.0, 0.0, 0.0)
+    P = random_problem(nx, ny, nz, p, seed=950 + p, spread=1.0, b=b, c=method != "auto")
+    u, f = vec(P, 97)
+    m = dg.DG_LOCAL_GMRES_THOMAS if method != "auto" else dg.DG_LOCAL_AUTO
+    with dg.DGContext(P) as one:
+        one.set_local_solver(m, 2000)
+        ut = cuda(u)
+        ref_A = torch.empty_like(ut)
+        one.apply(ut, ref_A)
+        one.sweep(ut, cuda(f), 0.9, 1e-12)
+        assert one.stats()["n_nonconverged"] == 0
+        ref_A, ref_S = host(ref_A), host(ut)
+    nd, nxy, G = P.nd, P.nx * P.ny, 3
+    ctxs = [dg.DGContext(P, rank=r, nranks=G, halo_mode=dg.DG_HALO_EXTERNAL) for r in range(G)]
+    try:
+        for c in ctxs:
+            c.set_local_solver(m, 2000)
+        parts_u = [cuda(u[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+        parts_f = [cuda(f[c.cell_begin * nd:c.cell_end * nd]) for c in ctxs]
+        for r, c in enumerate(ctxs):
+            c.fill_ghosts(parts_u[r - 1][-nxy * nd:] if r > 0 else None,
+                          parts_u[r + 1][:nxy * nd] if r < G - 1 else None)
+        outs = []
+        for r, c in enumerate(ctxs):
+            o = torch.empty_like(parts_u[r])
+            c.apply(parts_u[r], o)
+            outs.append(host(o))
+        assert np.array_equal(np.concatenate(outs), ref_A)
+        for r, c in enumerate(ctxs):
+            c.sweep(parts_u[r], parts_f[r], 0.9, 1e-12)
+        assert np.array_equal(np.concatenate([host(x) for x in parts_u]), ref_S)
+    finally:
+        for c in ctxs:
+            c.close()
