@@ -94,6 +94,8 @@ struct dg_ctx {
   double* d_ghost_hi = nullptr;   // ... of the upper rank's bottom layer
   double* d_send = nullptr;       // NCCL mode: [2][nxy][2][n^2] this rank's bottom / top traces
   int64_t ghost_len = 0;          // doubles per ghost buffer: nxy * 2 n^2
+  cudaStream_t comm_stream = nullptr;   // NCCL mode: the halo runs here, under the interior groups
+  cudaEvent_t ev_pack = nullptr, ev_halo = nullptr;
   double* d_unew = nullptr;
   int32_t* d_its = nullptr;
   int32_t* d_gperm = nullptr;  // solver CTA -> cell group, boundary-heavy groups first
@@ -154,6 +156,9 @@ dg_status validate(const dg_desc* d) {
 void release(dg_ctx* c) {
   if (!c) return;
   if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+  if (c->ev_pack) cudaEventDestroy(c->ev_pack);
+  if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   cudaFree(c->d_K);
   cudaFree(c->d_bc);
   cudaFree(c->d_c);
@@ -176,9 +181,10 @@ void release(dg_ctx* c) {
 
 // Halo exchange of the face traces (a neighbour enters the face terms only through
 // its trace and normal derivative): each rank packs its bottom and top layers' traces (2 n^2
-// doubles per column instead of the n^3 of the layer) and sends them to the ranks below / above.
-dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
-  if (c->desc.nranks == 1 || c->desc.halo_mode == DG_HALO_EXTERNAL) return DG_OK;
+// doubles per column instead of the n^3 of the layer) on the call's stream, and the NCCL
+// send/recv to the ranks below / above runs on the context's comm stream; the returned event
+// (ev_halo) marks the arrival of both ghost buffers.
+dg_status halo_start(dg_ctx* c, const double* u, cudaStream_t s) {
   const int64_t* pl = c->plan;
   const size_t L = (size_t)c->ghost_len;
   const int ncol = c->desc.nx * c->desc.ny;
@@ -186,18 +192,63 @@ dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
   if (pl[3] >= 0) ce = dg::launch_pack_traces(c->desc.p, c->tab, u + pl[0], ncol, 0, c->d_send, s);
   if (ce == cudaSuccess && pl[4] >= 0)
     ce = dg::launch_pack_traces(c->desc.p, c->tab, u + pl[1], ncol, 1, c->d_send + L, s);
+  if (ce == cudaSuccess) ce = cudaEventRecord(c->ev_pack, s);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(c->comm_stream, c->ev_pack, 0);
   if (ce != cudaSuccess) return cuda_fail(ce, "pack traces");
   ncclResult_t e = g_nccl.groupStart();
   if (pl[3] >= 0) {
-    e |= g_nccl.send(c->d_send, L, ncclFloat64, (int)pl[3], c->comm, s);
-    e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, (int)pl[3], c->comm, s);
+    e |= g_nccl.send(c->d_send, L, ncclFloat64, (int)pl[3], c->comm, c->comm_stream);
+    e |= g_nccl.recv(c->d_ghost_lo, L, ncclFloat64, (int)pl[3], c->comm, c->comm_stream);
   }
   if (pl[4] >= 0) {
-    e |= g_nccl.send(c->d_send + L, L, ncclFloat64, (int)pl[4], c->comm, s);
-    e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, (int)pl[4], c->comm, s);
+    e |= g_nccl.send(c->d_send + L, L, ncclFloat64, (int)pl[4], c->comm, c->comm_stream);
+    e |= g_nccl.recv(c->d_ghost_hi, L, ncclFloat64, (int)pl[4], c->comm, c->comm_stream);
   }
   e |= g_nccl.groupEnd();
   if (e != 0) return fail(DG_ERR_NCCL, "NCCL halo exchange failed");
+  ce = cudaEventRecord(c->ev_halo, c->comm_stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "halo event");
+  return DG_OK;
+}
+
+// A launch over the slab that reads neighbour data: with nranks > 1 the cell groups off the
+// ghost faces run first (while the halo is in flight, NCCL mode), then, once the ghost traces are
+// there, the slab-boundary groups. Per cell the arithmetic is that of one launch (bitwise).
+template <class F>
+dg_status run_split(dg_ctx* c, const double* u, cudaStream_t s, const dg::KParams& kp0, F&& launch,
+                    const char* what) {
+  dg::KParams kp = kp0;
+  if (c->desc.nranks == 1) {
+    kp.gsplit = 0;
+    cudaError_t e = launch(kp);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+    c->launches += 1;
+    return DG_OK;
+  }
+  const bool nccl = c->desc.halo_mode == DG_HALO_NCCL;
+  if (nccl) {
+    dg_status st = halo_start(c, u, s);
+    if (st != DG_OK) return st;
+  }
+  kp.gsplit = 1;
+  cudaError_t e = launch(kp);
+  if (e == cudaSuccess && nccl) e = cudaStreamWaitEvent(s, c->ev_halo, 0);
+  if (e == cudaSuccess) {
+    kp.gsplit = 2;
+    e = launch(kp);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  c->launches += 2 + (nccl ? 2 : 0);
+  return DG_OK;
+}
+
+// the whole halo before a launch (block SOR half-sweeps: one launch per colour)
+dg_status halo_exchange(dg_ctx* c, const double* u, cudaStream_t s) {
+  if (c->desc.nranks == 1 || c->desc.halo_mode == DG_HALO_EXTERNAL) return DG_OK;
+  dg_status st = halo_start(c, u, s);
+  if (st != DG_OK) return st;
+  cudaError_t e = cudaStreamWaitEvent(s, c->ev_halo, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "halo wait");
   return DG_OK;
 }
 
@@ -368,6 +419,12 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   if (G > 1 && desc->halo_mode == DG_HALO_NCCL) {
     std::string why;
     if (!g_nccl.load(&why)) { release(c); return fail(DG_ERR_NCCL, why); }
+    if ((e = cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming)) != cudaSuccess) {
+      release(c);
+      return cuda_fail(e, "comm stream");
+    }
     ncclUniqueId id;
     std::memcpy(&id, desc->nccl_id, sizeof(id));
     ncclResult_t ne = g_nccl.commInitRank(&c->comm, G, id, r);
@@ -470,14 +527,16 @@ dg_status dg_apply_parts(dg_ctx* c, const double* u, double* Au, uint32_t mask, 
   if (mask == 0 || mask > 7) return fail(DG_ERR_INVALID, "mask must be in 1..7");
   cudaStream_t s = (cudaStream_t)stream;
   c->launches = 0;
-  dg_status st = halo_exchange(c, u, s);
-  if (st != DG_OK) return st;
   dg::KParams kp = c->kp;
   kp.mask = mask;
-  cudaError_t e = dg::launch_apply(c->desc.p, kp, u, Au, s);
-  if (e != cudaSuccess) return cuda_fail(e, "apply");
-  c->launches = 1;
-  return DG_OK;
+  const int p = c->desc.p;
+  if (!(mask & 2u)) {   // no interior-face terms: no neighbour data, one launch
+    cudaError_t e = dg::launch_apply(p, kp, u, Au, s);
+    if (e != cudaSuccess) return cuda_fail(e, "apply");
+    c->launches = 1;
+    return DG_OK;
+  }
+  return run_split(c, u, s, kp, [&](const dg::KParams& k) { return dg::launch_apply(p, k, u, Au, s); }, "apply");
 }
 
 dg_status dg_apply(dg_ctx* c, const double* u, double* Au, void* stream) {
@@ -517,18 +576,17 @@ static dg_status sweep_impl(dg_ctx* c, const double* u, const double* f, double*
   if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
   if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
   c->launches = 0;
-  dg_status st = halo_exchange(c, u, s);
-  if (st != DG_OK) return st;
   dg::KParams kp = c->kp;
   kp.tol2 = tol * tol;
   kp.max_it = c->max_it;
   kp.krestart = c->krestart;
   kp.omega = omega;
-  cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, u_new, s);
-  if (e != cudaSuccess) return cuda_fail(e, "sweep");
+  const int p = c->desc.p, m = c->method;
+  dg_status st = run_split(c, u, s, kp,
+                           [&](const dg::KParams& k) { return dg::launch_sweep(p, m, k, u, f, u_new, s); }, "sweep");
+  if (st != DG_OK) return st;
   c->last_stream = s;
   c->have_stats = true;
-  c->launches = 1;
   return DG_OK;
 }
 

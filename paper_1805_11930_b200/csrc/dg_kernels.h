@@ -41,6 +41,9 @@ struct KParams {
   const int32_t* gperm;          // order in which the solver CTAs take the cell groups (longest
                                  // first: groups with Dirichlet faces), nullptr = in order
   uint32_t variant;              // VAR_* kernel variant bits (0 = the measured defaults)
+  int32_t gsplit;                // 0: every cell group; 1: the groups off the slab's ghost faces
+                                 // (launched before the halo arrives); 2: the others (after it)
+  int32_t gfirst, glast;         // the interior groups [gfirst, glast) of a split launch
   int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
                                  // group_cell), the other colour is not touched
 };
@@ -58,6 +61,37 @@ __host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
   if (kp.colour < 0 || kp.cmap) return false;
   const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / (kp.nx * kp.ny) + kp.zoff;
   return ((cx + cy + cz) & 1) != kp.colour;
+}
+
+// Cell group of this CTA: a split launch (interior groups, or the slab-boundary ones), else the
+// solvers' longest-first order (perm, plane solvers only), else blockIdx.x.
+#ifdef __CUDACC__
+__device__ inline int block_group(const KParams& kp, bool perm) {
+  const int b = blockIdx.x;
+  if (kp.gsplit == 1) return kp.gfirst + b;
+  if (kp.gsplit == 2) return b < kp.gfirst ? b : kp.glast + (b - kp.gfirst);
+  return (perm && kp.gperm) ? kp.gperm[b] : b;
+}
+#endif
+
+// Number of CTAs of a launch with C cells per group under kp.gsplit; sets gfirst / glast. The
+// interior groups hold no cell of a layer next to a ghost (slab-boundary) face.
+inline int split_groups(KParams& kp, int C) {
+  const int items = kp.cmap ? kp.ncells / 2 : kp.ncells;
+  const int ng = (items + C - 1) / C;
+  if (kp.gsplit == 0 || kp.cmap) {
+    kp.gsplit = 0;
+    return ng;
+  }
+  const int nxy = kp.nx * kp.ny;
+  const int b0 = kp.slab_face[4] == FK_GHOST ? nxy : 0;
+  const int b1 = kp.ncells - (kp.slab_face[5] == FK_GHOST ? nxy : 0);
+  int gf = (b0 + C - 1) / C, gl = b1 / C;
+  if (gl < gf) gl = gf;
+  if (gl > ng) gl = ng;
+  kp.gfirst = gf;
+  kp.glast = gl;
+  return kp.gsplit == 1 ? gl - gf : gf + (ng - gl);
 }
 
 // Cell of slot cs of the group starting at item g0: consecutive cells, or (kp.cmap) the

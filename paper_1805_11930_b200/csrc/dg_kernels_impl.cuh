@@ -722,7 +722,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   double* SA = SRC + G::TENSOR;
   double* SB = SA + G::TENSOR;
   double* FB = SB + G::TENSOR;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(G::C, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
   group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // pointers only; ends with __syncthreads
@@ -758,7 +758,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   // the face buffer is only used by the defect (the loop's D_T takes the self faces through
   // g.Bf), before Q and Dg are: it aliases them when it fits
   double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
@@ -927,7 +927,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
   double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
@@ -1126,7 +1126,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
   double* FB = fb_alias<N>() ? T : SB + G::TENSOR;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
@@ -1337,7 +1337,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
   double* FB = fb_alias<N>() ? T : SB + G::TENSOR;   // defect only: aliases T and Dg when it fits
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
@@ -1610,7 +1610,8 @@ inline bool gen_terms(const KParams& kp) {
 }
 
 template <int N>
-cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_t s, int with_nbr) {
+cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
+  KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
   if constexpr (N <= 5) {
 #ifndef DG_VOL_PERSIST
 #define DG_VOL_PERSIST 1
@@ -1661,7 +1662,7 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
   if constexpr (plane_apply<N>()) {
     if (!force_line(kp)) {
       using G = pk::Geo<N>;
-      const int grid = (kp.ncells + G::C - 1) / G::C;
+      const int grid = split_groups(kp, G::C);
       if (grid == 0) return cudaSuccess;
       const bool faces = kp.mask != 1u;   // mask = volume: the volume terms alone
       const size_t smem = pk::smem_apply<N>(with_nbr, faces);
@@ -1686,7 +1687,7 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
     }
   }
   using G = Geo<N>;
-  const int grid = (kp.ncells + G::C - 1) / G::C;
+  const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
   const size_t smem = smem_bytes<N>(3);
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point operators
@@ -1711,8 +1712,9 @@ cudaError_t apply_n(const KParams& kp, const double* u, double* out, cudaStream_
 }
 
 template <int N, bool SWEEP>
-cudaError_t solve_n(int method, const KParams& kp, const double* in, const double* f, double* out,
+cudaError_t solve_n(int method, const KParams& kp0, const double* in, const double* f, double* out,
                     cudaStream_t s) {
+  KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
   // plane solvers for n <= 4; at n = 5 the line solvers (self faces as Gauss-point operators,
   // two CTAs per SM) beat the register-starved plane ones (C3 sweep 32.7 -> 20.1 ms), except
   // for the tridiagonal preconditioner, which exists in the plane family only
@@ -1720,7 +1722,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
     if (!force_line(kp) && (N <= 4 || method == LM_BICGSTAB_THOMAS || method == LM_GMRES ||
                             method == LM_GMRES_THOMAS)) {
       using G = pk::Geo<N>;
-      const int grid = (group_items(kp) + G::C - 1) / G::C;
+      const int grid = split_groups(kp, G::C);
       if (grid == 0) return cudaSuccess;
       constexpr size_t cg_smem = pk::smem_solve<N>(2);
       // compact colour map (red-black SOR half-sweeps, n <= 4 sweeps only): own instantiations
@@ -1767,7 +1769,7 @@ cudaError_t solve_n(int method, const KParams& kp, const double* in, const doubl
     }
   }
   using G = Geo<N>;
-  const int grid = (kp.ncells + G::C - 1) / G::C;
+  const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
   if constexpr (N >= 5 && N <= 7) {

@@ -1211,7 +1211,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   double* FY = TB + G::TB;
   double* FX = FY + G::FY;
   double* FZ = FX + G::FX;
-  const int cell0 = blockIdx.x * G::C;
+  const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(G::C, kp.ncells - cell0);
   const Lane L = lane_id<N>();
   Rows<N> rw;
@@ -1446,7 +1446,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   double* DS = XS + G::C * G::PS;
   double* FX = XS;
   double* FZ = DS;
-  const int cell0 = (kp.gperm && !CMAP ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
+  const int cell0 = (CMAP ? (int)blockIdx.x : block_group(kp, true)) * G::C;
   const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
@@ -1835,7 +1835,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   double* FX = XS;
   double* FZ = XS + PLN;
   // TMEM: columns [0, 2N^2) x, [32, ...) p, [64, ...) v; this warp's lane quadrant
-  const int cell0 = (kp.gperm && !CMAP ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
+  const int cell0 = (CMAP ? (int)blockIdx.x : block_group(kp, true)) * G::C;
   const int nvalid = min(G::C, (CMAP ? kp.ncells / 2 : kp.ncells) - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
@@ -2189,7 +2189,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   double* SC = THOMAS ? CPM + PLN : XS + PLN;
   double* FX = XS;
   double* FZ = XS + PLN;
-  const int cell0 = (kp.gperm ? kp.gperm[blockIdx.x] : (int)blockIdx.x) * G::C;
+  const int cell0 = block_group(kp, true) * G::C;
   const int nvalid = min(G::C, kp.ncells - cell0);
   const Lane L = lane_id<N>();
   const bool valid = L.active && L.cs < nvalid;
