@@ -104,3 +104,99 @@ def test_slab_range_edges():
     assert sum(sizes) == 85 and set(sizes) <= {10, 11}
     with pytest.raises(Exception):
         dg.slab_range(4, 0, 5)
+
+
+def _trace_worker(rank, world, port, p, q):
+    """The trace-record contract of include/dg.h (dg_ghost_layers) over gloo: each rank packs its
+    bottom / top layers' face traces (face values at node 0 / n-1, normal-derivative sums with
+    theta'(0) / theta'(1) from the oracle's basis), exchanges them with the ranks below / above,
+    and rebuilds from the received records alone the coupling of its boundary cells to the other
+    rank's cells; that must equal the oracle's full neighbour blocks (tier B) applied to the
+    neighbours' complete n^3 data."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import paper_1805_11930_b200 as dg
+        from oracle.basis import lagrange_derivs, lobatto_nodes
+        from oracle.tier_b import TierB
+        from synth import make_vectors, random_problem
+        P = random_problem(3, 2, 2 * world + 1, p, seed=40 + p, b=(0.4, -0.2, 0.7), c=True)
+        n, nxy, nd = p + 1, P.nx * P.ny, P.nd
+        zb, ze = dg.slab_range(P.nz, rank, world)
+        plan = dg.halo_plan(P, rank, world)
+        u_glob, _ = make_vectors(P, seed=5)
+        u_loc = u_glob[zb * nxy * nd:ze * nxy * nd]
+        z = lobatto_nodes(p)
+        d0, d1 = lagrange_derivs(z, [0.0])[0], lagrange_derivs(z, [1.0])[0]
+
+        def pack(layer, top):
+            U = layer.reshape(nxy, n, n * n)          # [col][k][j*n + i]
+            vals = U[:, n - 1 if top else 0, :]
+            ders = np.einsum("k,ckf->cf", d1 if top else d0, U)
+            return np.concatenate([vals, ders], axis=1).reshape(-1)   # [col][2][n^2]
+
+        L = nxy * 2 * n * n
+        got_lo, got_hi = torch.zeros(L, dtype=torch.float64), torch.zeros(L, dtype=torch.float64)
+        reqs = []
+        if plan["peer_lo"] >= 0:
+            lay = u_loc[plan["send_lo_offset"]:plan["send_lo_offset"] + plan["layer_dof"]]
+            reqs.append(dist.isend(torch.from_numpy(pack(lay, top=False)), plan["peer_lo"]))
+            reqs.append(dist.irecv(got_lo, plan["peer_lo"]))
+        if plan["peer_hi"] >= 0:
+            lay = u_loc[plan["send_hi_offset"]:plan["send_hi_offset"] + plan["layer_dof"]]
+            reqs.append(dist.isend(torch.from_numpy(pack(lay, top=True)), plan["peer_hi"]))
+            reqs.append(dist.irecv(got_hi, plan["peer_hi"]))
+        for r_ in reqs:
+            r_.wait()
+        tb = TierB(P)
+        U = u_glob.reshape(-1, nd)
+        Mx, My = tb.M1(0), tb.M1(1)
+        MM = np.kron(My, Mx)                             # tangential face mass of a z face
+        e0, e1 = np.eye(n)[0], np.eye(n)[n - 1]
+        hz = tb.h[2]
+        for hi, rec in ((False, got_lo.numpy()), (True, got_hi.numpy())):
+            if (not hi and plan["peer_lo"] < 0) or (hi and plan["peer_hi"] < 0):
+                continue
+            R = rec.reshape(nxy, 2, n * n)
+            zc = zb if not hi else ze - 1                # the slab's boundary layer
+            for col in range(nxy):
+                c = zc * nxy + col
+                kind, wT, wN, g, bn, KT, KN, nb = tb.face_params(c, 2, hi)
+                V, D = R[col, 0], R[col, 1]              # neighbour face values, derivative sums
+                if hi:   # neighbour above: F_z (x) [min(bn,0) e1 e0' - wN KN e1 d0'/h + wT KT d1 e0'/h - g e1 e0']
+                    a = MM @ ((min(bn, 0.0) - g) * V - wN * KN * D / hz)
+                    b = MM @ (wT * KT * V / hz)
+                    got = np.outer(e1, a) + np.outer(d1, b)
+                else:    # neighbour below: F_z (x) [min(-bn,0) e0 e1' + wN KN e0 d1'/h - wT KT d0 e1'/h - g e0 e1']
+                    a = MM @ ((min(-bn, 0.0) - g) * V + wN * KN * D / hz)
+                    b = MM @ (-wT * KT * V / hz)
+                    got = np.outer(e0, a) + np.outer(d0, b)
+                nb2, B = tb.nbr_face_1d(c, 2, hi)
+                ref = tb.embed(2, B) @ U[nb2]
+                err = np.abs(got.reshape(-1) - ref).max() / max(np.abs(ref).max(), 1e-300)
+                assert err < 1e-12, (rank, hi, col, err)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("world,p", [(2, 1), (2, 3), (3, 2)])
+def test_trace_halo_contract_gloo(world, p):
+    from paper_1805_11930_b200.build import build
+    build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_trace_worker, args=(r, world, port, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    assert sorted(res) == [(r, "ok") for r in range(world)], res
