@@ -344,11 +344,13 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   }
   c->ghost_len = nxy * 2 * c->n * c->n;
   if (G > 1) {
-    if (alloc((void**)&c->d_ghost_lo, (size_t)c->ghost_len * 8) != cudaSuccess ||
-        alloc((void**)&c->d_ghost_hi, (size_t)c->ghost_len * 8) != cudaSuccess ||
+    // + n^3 doubles of padding: the kernels stage a neighbour as n^3 doubles from its record
+    const size_t gbytes = ((size_t)c->ghost_len + (size_t)c->nd) * 8;
+    if (alloc((void**)&c->d_ghost_lo, gbytes) != cudaSuccess ||
+        alloc((void**)&c->d_ghost_hi, gbytes) != cudaSuccess ||
         alloc((void**)&c->d_send, (size_t)c->ghost_len * 2 * 8) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc ghosts"); }
-    cudaMemset(c->d_ghost_lo, 0, (size_t)c->ghost_len * 8);
-    cudaMemset(c->d_ghost_hi, 0, (size_t)c->ghost_len * 8);
+    cudaMemset(c->d_ghost_lo, 0, gbytes);
+    cudaMemset(c->d_ghost_hi, 0, gbytes);
   }
   if (alloc((void**)&c->d_unew, (size_t)c->ndof * 8) != cudaSuccess ||
       alloc((void**)&c->d_its, (size_t)c->ncells * 4) != cudaSuccess) { release(c); return fail(DG_ERR_NOMEM, "cudaMalloc scratch"); }

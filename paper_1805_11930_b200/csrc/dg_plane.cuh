@@ -165,7 +165,8 @@ __device__ __forceinline__ void load_own(double (&v)[Geo<N>::PER], const double*
 }
 // neighbour tile: per-cell base pointers (nullptr -> zeros), loaded into registers
 // (z faces at a slab boundary: the neighbour is a trace record of 2 n^2 doubles, which lands in
-// planes 0 and 1 of the staged tile)
+// planes 0 and 1 of the staged tile; the ghost buffers are padded so the full n^3 read stays in
+// bounds)
 template <int N, bool WB>
 __device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N, WB>& cl, int f,
                                          const KParams& kp) {
@@ -175,7 +176,6 @@ __device__ __forceinline__ void load_nbr(double (&v)[Geo<N>::PER], const Cells<N
     const int e = threadIdx.x + m * G::NT;
     const int cs = e / G::N3, r = e % G::N3;
     const double* p = (e < G::C * G::N3) ? cl.nb[cs][f] : nullptr;
-    if (p && f >= 4 && r >= 2 * G::N2 && ghost_trace(kp, cl.cell[cs], f & 1)) p = nullptr;
     v[m] = p ? __ldg(p + r) : 0.0;
   }
 }
@@ -418,9 +418,9 @@ __device__ __forceinline__ void async_nbr(double* dst, const Cells<N, WB>& cl, i
     const int e = threadIdx.x + m * G::NT;
     if (e < G::C * G::N3) {
       const int cs = e / G::N3, r = e % G::N3;
+      // (a ghost trace record, z faces at a slab boundary, fills planes 0 and 1; the rest of the
+      // n^3 copy reads the next record or the buffer's padding and is never used)
       const double* p = cl.nb[cs][f];
-      // a ghost trace record (z faces at a slab boundary) holds 2 n^2 doubles: planes 0 and 1
-      if (p && f >= 4 && r >= 2 * G::N2 && ghost_trace(kp, cl.cell[cs], f & 1)) p = nullptr;
       cp_async8(dst + cs * CSX + (r / G::N2) * KSX + (r % G::N2), p ? p + r : any, p != nullptr);
     }
   }
@@ -443,7 +443,8 @@ __device__ __forceinline__ void ytrace(const double* nb, const double* c, double
   }
 }
 // z-face traces (lane t = y node j): rows (kk, i) of the neighbour at fixed j, interpolated in x
-// tr: nb is a ghost trace record (plane 0 the face values, plane 1 the derivative sums)
+// tr: nb is a ghost trace record (plane 0 the face values, plane 1 the derivative sums); both
+// paths share the flux arithmetic below, so a slab-boundary face is bitwise the in-slab one
 template <int N, int KSX>
 __device__ __forceinline__ void ztrace(const double* nb, const double* c, double ih, int hi, int j,
                                        double (&S)[N], double (&T)[N], bool tr = false) {
@@ -509,7 +510,7 @@ __device__ __forceinline__ void xtrace(const double* plane, const double* c, dou
 // y-hi / z-lo / z-hi in the FY / FX / FZ regions (cell stride FS, plane stride N2). The z and x
 // traces are taken first and written over the z staging, then the y traces over the y-hi
 // staging. Leaves TB free. All threads must call it (three barriers).
-template <int N, bool WB>
+template <int N, bool GH, bool WB>
 __device__ void nbr_prologue_async(const KParams& kp, const Cells<N, WB>& cl, const Lane& L,
                                    double* TB, double* FY, double* FX, double* FZ, const double* tile) {
   using G = Geo<N>;
@@ -533,7 +534,7 @@ __device__ void nbr_prologue_async(const KParams& kp, const Cells<N, WB>& cl, co
         }
         xtrace<N>(plane, cl.fc[L.cs][hi], kp.ih[0], hi, xs[hi][0], xs[hi][1]);
         ztrace<N, G::N2>((hi ? FZ : FX) + L.cs * G::FS, cl.fc[L.cs][4 + hi], kp.ih[2], hi, t,
-                         zs[hi][0], zs[hi][1], ghost_trace(kp, cl.cell[L.cs], hi));
+                         zs[hi][0], zs[hi][1], GH && ghost_trace(kp, cl.cell[L.cs], hi));
       }
     }
     __syncthreads();   // z staging consumed
@@ -1239,7 +1240,7 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   __syncthreads();
   double in[N][N], o[N][N];
   read_plane<N>(TB, L, in);
-  if (NBR) nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, tile);
+  if (NBR) nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, tile);
   else __syncthreads();
   plane_op<N, NBR, false, FACES, GEN>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
@@ -1466,7 +1467,7 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   if (SWEEP) {
     double Q[N][N];
     if constexpr (ASYNC) {
-      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
+      nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
       load_nbr<N>(pv0, cl, 2, kp);
@@ -1855,7 +1856,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   if (SWEEP) {
     double T[N][N];
     if constexpr (ASYNC) {
-      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
+      nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, CMAP ? nullptr : in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
       load_nbr<N>(pv0, cl, 2, kp);
@@ -2207,7 +2208,7 @@ k_gmres(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   read_plane<N>(TB, L, W);
   if (SWEEP) {
     if constexpr (ASYNC) {
-      nbr_prologue_async<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
+      nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3);
     } else {
       double pv0[G::PER], pv1[G::PER];
       load_nbr<N>(pv0, cl, 2, kp);
