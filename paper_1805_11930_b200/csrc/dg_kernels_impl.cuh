@@ -99,7 +99,10 @@ template <int N> struct Group {
   double red[2][C * N * N];     // per-line partial sums
   // self-face operators of D_T at the Gauss points, weighted residual form, per axis (x, y, z):
   // R_line += w_t1 w_t2 Bf U_line (the local solvers' D_T applications, no face passes)
-  double Bf[C][3][N * N];
+  // rows padded to an even length (zero pad): the 16-byte aligned pairs are read with one
+  // 128-bit broadcast load each (bterm)
+  static constexpr int BR = (N + 1) & ~1;
+  alignas(16) double Bf[C][3][N * BR];
   double sc[8][C];              // per-cell solver scalars
   int conv[C], its[C], rst[C];
 };
@@ -169,13 +172,19 @@ template <int N, bool GEN = true> __device__ __forceinline__ void dir_term(const
   for (int r = 0; r < N; ++r) R[r] += t[r];
 }
 
-// R += Wl B U (B: a cell's self-face operator along the line direction, from shared memory)
+// R += Wl B U (B: a cell's D_T line operator along the line direction, from shared memory, rows
+// of even stride BR, 16-byte aligned: read as pairs, one 128-bit broadcast load per pair)
 template <int N> __device__ __forceinline__ void bterm(const double* B, const double* U, double* R, double Wl) {
+  constexpr int BR = (N + 1) & ~1;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
     double s = 0.0;
 #pragma unroll
-    for (int r = 0; r < N; ++r) s = fma(B[q * N + r], U[r], s);
+    for (int r = 0; r < N; r += 2) {
+      const double2 b2 = *reinterpret_cast<const double2*>(B + q * BR + r);
+      s = fma(b2.x, U[r], s);
+      if (r + 1 < N) s = fma(b2.y, U[r + 1], s);
+    }
     R[q] = fma(Wl, s, R[q]);
   }
 }
@@ -213,7 +222,8 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
       t = fma(-g.vb[cs][a], c_tab[N].CG[q * N + r], t);
       if (a == 2 && q == r) t = fma(g.vc[cs][3], c_tab[N].w[q], t);
     }
-    g.Bf[cs][a][q * N + r] = t;
+    g.Bf[cs][a][q * Group<N>::BR + r] = t;
+    if (r == N - 1 && (N & 1)) g.Bf[cs][a][q * Group<N>::BR + N] = 0.0;   // the pad
   }
   __syncthreads();
 }
