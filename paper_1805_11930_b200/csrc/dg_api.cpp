@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
 
 #include <algorithm>
 #include <cmath>
@@ -21,6 +22,12 @@
 #include "dg_tables.h"
 
 namespace {
+
+// NVTX range over one ABI call (the host-side enqueue of its kernels; SURVEY §5 phase tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 bool getenv_flag(const char* name) {
   const char* v = std::getenv(name);
@@ -185,6 +192,7 @@ void release(dg_ctx* c) {
 // send/recv to the ranks below / above runs on the context's comm stream; the returned event
 // (ev_halo) marks the arrival of both ghost buffers.
 dg_status halo_start(dg_ctx* c, const double* u, cudaStream_t s) {
+  NvtxRange nv("halo_traces");
   const int64_t* pl = c->plan;
   const size_t L = (size_t)c->ghost_len;
   const int ncol = c->desc.nx * c->desc.ny;
@@ -523,6 +531,7 @@ static dg_status check_vec(const void* p, const char* name) {
 }
 
 dg_status dg_apply_parts(dg_ctx* c, const double* u, double* Au, uint32_t mask, void* stream) {
+  NvtxRange nv("dg_apply");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(Au, "Au")) return DG_ERR_INVALID;
   if (u == Au) return fail(DG_ERR_INVALID, "u and Au must not alias");
@@ -546,6 +555,7 @@ dg_status dg_apply(dg_ctx* c, const double* u, double* Au, void* stream) {
 }
 
 dg_status dg_block_diag_apply(dg_ctx* c, const double* u, double* Du, void* stream) {
+  NvtxRange nv("dg_block_diag_apply");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(Du, "Du")) return DG_ERR_INVALID;
   if (u == Du) return fail(DG_ERR_INVALID, "u and Du must not alias");
@@ -556,6 +566,7 @@ dg_status dg_block_diag_apply(dg_ctx* c, const double* u, double* Du, void* stre
 }
 
 dg_status dg_local_block_solve(dg_ctx* c, const double* d, double* du, double tol, void* stream) {
+  NvtxRange nv("dg_local_block_solve");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(d, "d") || check_vec(du, "du")) return DG_ERR_INVALID;
   if (d == du) return fail(DG_ERR_INVALID, "d and du must not alias");
@@ -575,6 +586,7 @@ dg_status dg_local_block_solve(dg_ctx* c, const double* d, double* du, double to
 
 static dg_status sweep_impl(dg_ctx* c, const double* u, const double* f, double* u_new, double omega,
                             double tol, cudaStream_t s) {
+  NvtxRange nv("dg_block_jacobi_sweep");
   if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
   if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
   c->launches = 0;
@@ -615,6 +627,7 @@ dg_status dg_block_jacobi_sweep_to(dg_ctx* c, const double* u, const double* f, 
 
 dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega, double tol,
                              int32_t symmetric, void* stream) {
+  NvtxRange nv("dg_block_sor_sweep");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
   if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
@@ -841,6 +854,7 @@ dg_status dg_coarse_matrix(dg_ctx* c, double* Ah_host) {
 }
 
 dg_status dg_hybrid_vcycle(dg_ctx* c, const double* r, double* z, const dg_hybrid_params* p, void* stream) {
+  NvtxRange nv("dg_hybrid_vcycle");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(r, "r") || check_vec(z, "z")) return DG_ERR_INVALID;
   if (r == z) return fail(DG_ERR_INVALID, "r and z must not alias");
@@ -853,6 +867,7 @@ dg_status dg_hybrid_vcycle(dg_ctx* c, const double* r, double* z, const dg_hybri
 
 dg_status dg_hybrid_solve(dg_ctx* c, double* u, const double* f, const dg_hybrid_params* p,
                           dg_hybrid_stats* out, void* stream) {
+  NvtxRange nv("dg_hybrid_solve");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
   if ((const double*)u == f) return fail(DG_ERR_INVALID, "u and f must not alias");
@@ -961,6 +976,7 @@ dg_status dg_pmf_setup(dg_ctx* c) {
 }
 
 dg_status dg_pmf_sweep(dg_ctx* c, double* u, const double* f, double omega, void* stream) {
+  NvtxRange nv("dg_pmf_sweep");
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
   if (check_vec(u, "u") || check_vec(f, "f")) return DG_ERR_INVALID;
   if (!c->d_pmf) return fail(DG_ERR_STATE, "dg_pmf_setup has not run");

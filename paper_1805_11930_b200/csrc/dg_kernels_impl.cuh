@@ -1612,7 +1612,12 @@ inline bool force_line(const KParams& kp) { return (kp.variant & VAR_LINE) != 0;
 #ifndef DG_PLANE_APPLY3
 #define DG_PLANE_APPLY3 1   // n = 3: plane kernels (C5: D_T 832 -> 351 us, A 900 -> 847 us)
 #endif
-template <int N> constexpr bool plane_apply() { return N == 2 || N == 4 || (N == 3 && DG_PLANE_APPLY3); }
+#ifndef DG_PLANE_APPLY5
+#define DG_PLANE_APPLY5 0
+#endif
+template <int N> constexpr bool plane_apply() {
+  return N == 2 || N == 4 || (N == 3 && DG_PLANE_APPLY3) || (N == 5 && DG_PLANE_APPLY5);
+}
 
 // convective or reaction terms present (else the pure-diffusion instantiations, GEN = false)
 inline bool gen_terms(const KParams& kp) {

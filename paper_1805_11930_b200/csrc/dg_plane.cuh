@@ -25,6 +25,9 @@
 #endif
 namespace pk {
 
+#ifndef DG_PLANE5_ASYNC
+#define DG_PLANE5_ASYNC 0
+#endif
 #ifndef DG_VOL_MINB
 #define DG_VOL_MINB 3   // resident CTAs per SM the persistent volume kernel is compiled for
 #endif
@@ -55,7 +58,8 @@ template <int N_> struct Geo {
   static constexpr int KS = PL<N>::KS, ARR = N * KS, CTB = PL<N>::CTB;
   // per-cell stride of a block of 4 face arrays; even at n = 4 so that staged neighbour tiles
   // can be copied with 16-byte cp.async (see async_nbr)
-  static constexpr int FS = 4 * N2 + (N == 4 ? 2 : 1);
+  // DG_PLANE5_ASYNC: at n = 5 too a face region holds a whole neighbour tile (cp.async staging)
+  static constexpr int FS = (N == 5 && DG_PLANE5_ASYNC) ? N3 : 4 * N2 + (N == 4 ? 2 : 1);
   static constexpr int QS = PL<N>::QS, PS = PL<N>::PS;  // plane storage (X, Dg, ...)
   static_assert(PS >= N * QS && PS >= FS, "plane storage must hold a cell and a face block");
   static constexpr int PER = (C * N3 + NT - 1) / NT;      // tile elements per thread
