@@ -15,7 +15,8 @@ from synth import Problem, uniform_pm1
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from kernel_times import PEAK, timed   # noqa: E402
 
-for p in ([int(a) for a in sys.argv[1:] if not a.startswith('--')] or range(1, 8)):
+ARGS = [a for i, a in enumerate(sys.argv[1:]) if not a.startswith('--') and sys.argv[i] != '--variant']
+for p in ([int(a) for a in ARGS] or range(1, 8)):
     n = p + 1
     m = int(round((8e6 / n ** 3) ** (1 / 3)))
     P = Problem(m, m, m, p, K=np.ones(m ** 3))
@@ -23,6 +24,8 @@ for p in ([int(a) for a in sys.argv[1:] if not a.startswith('--')] or range(1, 8
         P.c = np.zeros(m ** 3)
     u, f = uniform_pm1(900 + p, 0, P.n_dof), uniform_pm1(910 + p, 0, P.n_dof)
     ctx = dg.DGContext(P)
+    VAR = int(sys.argv[sys.argv.index("--variant") + 1]) if "--variant" in sys.argv else 0
+    ctx.set_kernel_variant(VAR)
     ut, ft = torch.from_numpy(u).cuda(), torch.from_numpy(f).cuda()
     out = torch.empty_like(ut)
     nc = P.n_cells
@@ -45,6 +48,7 @@ for p in ([int(a) for a in sys.argv[1:] if not a.startswith('--')] or range(1, 8
         ctx.close()
         Pc = Problem(m, m, m, p, K=np.full(m ** 3, 1e-2), b=(1.0, 0.5, 0.25))
         ctx = dg.DGContext(Pc)
+        ctx.set_kernel_variant(VAR)
         t = timed(lambda: ctx.sweep_to(ut, ft, uu, 1.0, 1e-12), calls=2)
         st = ctx.stats()
         volc = vol + 4 * n ** 3
