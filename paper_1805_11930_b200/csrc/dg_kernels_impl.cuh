@@ -482,7 +482,7 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
       const int cs = it / N2, l = it % N2, a = l % N, b = l / N;
       const int off = cs * G::CS + b * G::ZS + a * G::YS;
       double v[N], o[N];
-      if (WARP && pin) {
+      if ((WARP || LINES <= NT) && pin) {   // one line per thread: its own line, from registers
 #pragma unroll
         for (int e = 0; e < N; ++e) v[e] = pin[e];
       } else {
@@ -791,19 +791,27 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   }
   diag_setup<N>(kp, g, Dg);
   __syncthreads();
-  // r0 = d, p = M^-1 r, x = 0
-  DG_FOR_XLINES({
-    double r[N], dg[N], z[N], zero[N] = {};
-    ld<N, 1>(R + off, r);
-    ld<N, 1>(Dg + off, dg);
-    double rr = 0.0, rz = 0.0;
+  // Each thread owns one x-line of the group (LINES <= NT): the operator's first pass reads that
+  // line of p and its last pass produces that line of q = D_T p, so r, p, x and diag(D_T)^-1 stay
+  // in registers; only the per-cell scalars go through shared memory (reductions, alpha, beta).
+  static_assert(G::LINES <= G::NT, "one line per thread");
+  const bool own = tid < G::LINES;
+  const int lcs = own ? tid / G::N2 : 0, ll = tid % G::N2;
+  const int loff = lcs * G::CS + (ll / N) * G::ZS + (ll % N) * G::YS;
+  double r[N], p[N], x[N], dgi[N];
 #pragma unroll
-    for (int e = 0; e < N; ++e) { z[e] = r[e] * dg[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], z[e], rz); }
-    st<N, 1>(P + off, z);
-    st<N, 1>(X + off, zero);
-    g.red[0][it] = rr;
-    g.red[1][it] = rz;
-  })
+  for (int e = 0; e < N; ++e) r[e] = p[e] = x[e] = dgi[e] = 0.0;
+  {  // r0 = d, p = M^-1 r, x = 0
+    double rr = 0.0, rz = 0.0;
+    if (own) {
+      ld<N, 1>(R + loff, r);
+      ld<N, 1>(Dg + loff, dgi);
+#pragma unroll
+      for (int e = 0; e < N; ++e) { p[e] = r[e] * dgi[e]; rr = fma(r[e], r[e], rr); rz = fma(r[e], p[e], rz); }
+      g.red[0][tid] = rr;
+      g.red[1][tid] = rz;
+    }
+  }
   __syncthreads();
   if (tid < C) {
     const double rr0 = cell_sum<N>(g, 0, tid);
@@ -815,20 +823,20 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   for (int iter = 0;; ++iter) {
     const int done = __syncthreads_and(tid >= C || g.conv[tid]);
     if (done || iter >= kp.max_it) break;
-    // q = D_T p
-    cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
-      st<N, 1>(Q + cs * G::CS + k * G::ZS + j * G::YS, v);
-    });
-    __syncthreads();
-    DG_FOR_XLINES({
-      double p[N], q[N];
-      ld<N, 1>(P + off, p);
-      ld<N, 1>(Q + off, q);
-      double s = 0.0;
+    // q = D_T p (the thread's own line, in registers)
+    double q[N];
 #pragma unroll
-      for (int e = 0; e < N; ++e) s = fma(p[e], q[e], s);
-      g.red[0][it] = s;
-    })
+    for (int e = 0; e < N; ++e) q[e] = 0.0;
+    cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
+#pragma unroll
+      for (int e = 0; e < N; ++e) q[e] = v[e];
+    }, p);
+    if (own) {
+      double sp = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) sp = fma(p[e], q[e], sp);
+      g.red[0][tid] = sp;
+    }
     __syncthreads();
     if (tid < C) {
       const double pq = cell_sum<N>(g, 0, tid);
@@ -840,27 +848,23 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       g.sc[S_ALPHA][tid] = alpha;
     }
     __syncthreads();
-    DG_FOR_XLINES({
-      const double alpha = g.sc[S_ALPHA][cs];
-      double x[N], r[N], p[N], q[N], dg[N];
-      ld<N, 1>(X + off, x);
-      ld<N, 1>(R + off, r);
-      ld<N, 1>(P + off, p);
-      ld<N, 1>(Q + off, q);
-      ld<N, 1>(Dg + off, dg);
+    double z[N];
+    {
+      const double alpha = g.sc[S_ALPHA][lcs];
       double rr = 0.0, rz = 0.0;
 #pragma unroll
       for (int e = 0; e < N; ++e) {
         x[e] = fma(alpha, p[e], x[e]);
         r[e] = fma(-alpha, q[e], r[e]);
         rr = fma(r[e], r[e], rr);
-        rz = fma(r[e], r[e] * dg[e], rz);
+        z[e] = r[e] * dgi[e];
+        rz = fma(r[e], z[e], rz);
       }
-      st<N, 1>(X + off, x);
-      st<N, 1>(R + off, r);
-      g.red[0][it] = rr;
-      g.red[1][it] = rz;
-    })
+      if (own) {
+        g.red[0][tid] = rr;
+        g.red[1][tid] = rz;
+      }
+    }
     __syncthreads();
     if (tid < C && !g.conv[tid]) {
       const double rr = cell_sum<N>(g, 0, tid), rzn = cell_sum<N>(g, 1, tid);
@@ -870,19 +874,14 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       g.sc[S_RZ][tid] = rzn;
     }
     __syncthreads();
-    DG_FOR_XLINES({
-      if (!g.conv[cs]) {
-        const double beta = g.sc[S_BETA][cs];
-        double r[N], p[N], dg[N];
-        ld<N, 1>(R + off, r);
-        ld<N, 1>(P + off, p);
-        ld<N, 1>(Dg + off, dg);
+    if (!g.conv[lcs]) {
+      const double beta = g.sc[S_BETA][lcs];
 #pragma unroll
-        for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], r[e] * dg[e]);
-        st<N, 1>(P + off, p);
-      }
-    })
+      for (int e = 0; e < N; ++e) p[e] = fma(beta, p[e], z[e]);
+    }
   }
+  if (own) st<N, 1>(X + loff, x);
+  __syncthreads();
   // write result (u + omega du for a sweep, du for a solve)
   const double* ib = in + (size_t)cell0 * G::N3;
   double* ob = out + (size_t)cell0 * G::N3;
