@@ -61,8 +61,9 @@ enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
  * 0 = the measured defaults. DG_VARIANT_VOLUME_PREFETCH: the register-prefetch persistent volume
  * kernel at p = 3 (default: the slim one); DG_VARIANT_LINE: line-per-thread kernels at every
  * degree; DG_VARIANT_NO_TMEM: shared-memory p = 3 BiCGStab (default: Krylov vectors in tensor
- * memory); DG_VARIANT_LINE_CG_CTA: the other line-solver kernel at p = 4..6 (defaults: one warp
- * per cell at p = 4 and p = 6, CTA-wide at p = 5; the flag swaps them). */
+ * memory); DG_VARIANT_LINE_CG_CTA: the other line-solver kernel at p = 4..6 (defaults: CG one
+ * warp per cell at p = 4, CTA-wide at p = 5, 6; BiCGStab one warp per cell at p = 4, 6, CTA-wide
+ * at p = 5; the flag swaps them). */
 enum { DG_VARIANT_VOLUME_PREFETCH = 1, DG_VARIANT_LINE = 2, DG_VARIANT_NO_TMEM = 4,
        DG_VARIANT_LINE_CG_CTA = 8 };
 

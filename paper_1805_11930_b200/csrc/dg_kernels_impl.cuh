@@ -1786,11 +1786,12 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
   const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
   if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
-  // line solvers per degree (measured after the D_T fold, profiles/r02_ab.md): one warp per cell
-  // at n = 5 and 7, CTA-wide at n = 6 and 8; VAR_LINE_CG_CTA selects the other kernel (A/B)
-  constexpr bool warp_default = N == 5 || N == 7;
+  // line solvers per degree (measured after the D_T fold and the register-resident CTA CG,
+  // profiles/r02_ab.md): CG one warp per cell at n = 5, CTA-wide at n = 6..8; BiCGStab one warp
+  // per cell at n = 5 and 7, CTA-wide at n = 6 and 8; VAR_LINE_CG_CTA selects the other kernel
+  constexpr bool warp_cg = N == 5, warp_bicg = N == 5 || N == 7;
   if constexpr (N >= 5 && N <= 7) {
-    const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_default;
+    const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_bicg;
     if (method == LM_BICGSTAB && !cta)
       return launch(k_bicgstab_w<N, SWEEP>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
@@ -1799,7 +1800,7 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
   if constexpr (N >= 5 && N <= 7) {   // n = 8: 255 registers with spills, the CTA version is faster
-    const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_default;
+    const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_cg;
     if (!cta)
       return launch(gen_terms(kp) ? k_cg_w<N, SWEEP, true> : k_cg_w<N, SWEEP, false>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 7 * (size_t)G::TENSOR : smem_bytes<N>(7), s, kp, in, f, out);
