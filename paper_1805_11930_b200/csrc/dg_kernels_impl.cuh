@@ -22,6 +22,9 @@
 //  Local solves: Jacobi-preconditioned CG or BiCGStab per
 //    cell, all C cells of a CTA iterating together with per-cell convergence masks
 //    and deterministic per-cell reductions (no atomics).
+#ifndef DG_NODAL_DT
+#define DG_NODAL_DT 1   // warp-per-cell CG at n = 5: D_T in the nodal Kronecker-sum form
+#endif
 #ifndef DG_PDL
 #define DG_PDL 1
 #endif
@@ -226,6 +229,108 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
     if (r == N - 1 && (N & 1)) g.Bf[cs][a][q * Group<N>::BR + N] = 0.0;   // the pad
   }
   __syncthreads();
+}
+
+// Nodal D_T factors (warp-per-cell CG at n = 5): with per-cell constant coefficients on the
+// affine cell, D_T = Kx (x) Mhat (x) Mhat + Mhat (x) Ky (x) Mhat + Mhat (x) Mhat (x) Kz (the
+// Kronecker-sum form of the volume and self-face terms, P:343-357 restricted to T; tier B's
+// diag_block), with the 1D matrices per cell and direction
+//   K_a = |T|K_a/h_a^2 Shat - |T|b_a/h_a Chat + [a = z] |T| c Mhat
+//       + |F_a| (e0 (s_a e0' + s_g/h d0') + t_a d0 e0' + e1 (.. hi ..))       (self faces)
+// i.e. A^T Bf_a A of the Gauss-point line operators. Stored in g.Bf (rows of stride BR).
+template <int N, int NTH = Geo<N>::NT> __device__ void nodal_face_ops(const KParams& kp, Group<N>& g) {
+  using G = Geo<N>;
+  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
+    const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
+    const int i = (rem % (N * N)) / N, ip = rem % N;
+    const double* lo = g.fc[cs][2 * a];
+    const double* hi = g.fc[cs][2 * a + 1];
+    const double ih = kp.ih[a];
+    const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
+    const double e0i = i == 0, e0p = ip == 0, e1i = i == N - 1, e1p = ip == N - 1;
+    double f = e0i * (lo[0] * e0p + lo[1] * ih * c_tab[N].d0[ip]) + lo[4] * c_tab[N].d0[i] * e0p;
+    f += e1i * (hi[0] * e1p + hi[1] * ih * c_tab[N].d1[ip]) + hi[4] * c_tab[N].d1[i] * e1p;
+    double t = area * f;
+    t = fma(g.vc[cs][a], c_tab[N].S[i * N + ip], t);
+    t = fma(-g.vb[cs][a], c_tab[N].Cm[i * N + ip], t);
+    if (a == 2) t = fma(g.vc[cs][3], c_tab[N].M[i * N + ip], t);
+    g.Bf[cs][a][i * Group<N>::BR + ip] = t;
+    if (ip == N - 1 && (N & 1)) g.Bf[cs][a][i * Group<N>::BR + N] = 0.0;
+  }
+  __syncthreads();
+}
+
+// v = K u along a line with K a per-cell nodal factor (rows of stride BR in shared memory, read
+// as 128-bit broadcast pairs)
+template <int N> __device__ __forceinline__ void kmv(const double* K, const double* u, double* v) {
+  constexpr int BR = (N + 1) & ~1;
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double s = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; r += 2) {
+      const double2 b2 = *reinterpret_cast<const double2*>(K + q * BR + r);
+      s = fma(b2.x, u[r], s);
+      if (r + 1 < N) s = fma(b2.y, u[r + 1], s);
+    }
+    v[q] = s;
+  }
+}
+
+// D_T p for the warp's own cell (one x-line per lane, LPL = 1) in the nodal Kronecker-sum form:
+// x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
+// q = Mhat g + Kz d -> back to the lane's x-line. 7 one-direction contractions and 3 transposes
+// (the Gauss-point form: 9 contractions, 6 transposes). pin: the lane's x-line of p.
+template <int N>
+__device__ __forceinline__ void dt_nodal_warp(const Group<N>& g, double* SA, double* SB, const double* pin,
+                                              double* q) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2;
+  const int tid = threadIdx.x, cs = tid >> 5, lane = tid & 31;
+  const bool act = lane < N2;
+  const int a = lane % N, b = lane / N;
+  const double* Kx = g.Bf[cs][0];
+  const double* Ky = g.Bf[cs][1];
+  const double* Kz = g.Bf[cs][2];
+  const int base = cs * G::CS;
+  if (act) {   // x-lines (j = a, k = b)
+    double bv[N], cv[N];
+    mv<N, 2>(pin, bv);
+    kmv<N>(Kx, pin, cv);
+    st<N, 1>(SA + base + b * G::ZS + a * G::YS, bv);
+    st<N, 1>(SB + base + b * G::ZS + a * G::YS, cv);
+  }
+  __syncwarp();
+  if (act) {   // y-lines (i = a, k = b)
+    const int off = base + b * G::ZS + a;
+    double bv[N], cv[N], dv[N], ev[N], fv[N];
+    ld<N, G::YS>(SA + off, bv);
+    ld<N, G::YS>(SB + off, cv);
+    mv<N, 2>(bv, dv);
+    kmv<N>(Ky, bv, ev);
+    mv<N, 2>(cv, fv);
+#pragma unroll
+    for (int e = 0; e < N; ++e) ev[e] += fv[e];
+    st<N, G::YS>(SA + off, dv);
+    st<N, G::YS>(SB + off, ev);
+  }
+  __syncwarp();
+  if (act) {   // z-lines (i = a, j = b)
+    const int off = base + b * G::YS + a;
+    double dv[N], gv[N], o1[N], o2[N];
+    ld<N, G::ZS>(SA + off, dv);
+    ld<N, G::ZS>(SB + off, gv);
+    mv<N, 2>(gv, o1);
+    kmv<N>(Kz, dv, o2);
+#pragma unroll
+    for (int e = 0; e < N; ++e) o1[e] += o2[e];
+    st<N, G::ZS>(SA + off, o1);
+  }
+  __syncwarp();
+  if (act) ld<N, 1>(SA + base + b * G::ZS + a * G::YS, q);
+  else
+#pragma unroll
+    for (int e = 0; e < N; ++e) q[e] = 0.0;
 }
 
 // ---- group setup: coefficients, face parameters, neighbour pointers ------------
@@ -942,7 +1047,10 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N, G::NTW>(kq, g);
+  constexpr int LPL0 = (G::N2 + 31) / 32;
+  constexpr bool NODAL = DG_NODAL_DT && LPL0 == 1;   // D_T in the nodal Kronecker-sum form
+  if constexpr (NODAL) nodal_face_ops<N, G::NTW>(kq, g);
+  else self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2), CTA-wide
     const double* fb = f + (size_t)cell0 * G::N3;
     cell_operator<N, true, false, false, G::NTW, GEN>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
@@ -1003,11 +1111,15 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       double q[N];
 #pragma unroll
       for (int e = 0; e < N; ++e) q[e] = 0.0;
-      cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
-                                                           [&](int, int, int, const double* v) {
+      if constexpr (NODAL) {
+        dt_nodal_warp<N>(g, SA, SB, p, q);
+      } else {
+        cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
+                                                             [&](int, int, int, const double* v) {
 #pragma unroll
-        for (int e = 0; e < N; ++e) q[e] = v[e];
-      }, p);
+          for (int e = 0; e < N; ++e) q[e] = v[e];
+        }, p);
+      }
       double pq = 0.0;
 #pragma unroll
       for (int e = 0; e < N; ++e) pq = fma(p[e], q[e], pq);
