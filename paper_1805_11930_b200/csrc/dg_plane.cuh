@@ -73,7 +73,9 @@ template <int N_> struct Geo {
 // WB: with the per-cell self-face operators B (local solvers); the apply kernels omit them.
 template <int N, bool WB = true> struct Cells {
   static constexpr int C = Geo<N>::C;
-  static constexpr int BS = 2 * N * N + 1;   // odd stride: the cells of a half-warp hit distinct banks
+  // odd stride (the cells of a half-warp hit distinct banks), room for the x / z Gauss-point
+  // self-face operators (2 n^2) or the three nodal D_T factors (3 n^2, setup_K3)
+  static constexpr int BS = 3 * N * N + (N % 2 == 0 ? 1 : 2);
   double vc[C][4];
   double vb[C][3];   // |T| b_k / h_k of the cell (volume advection)
   double fc[C][6][6];
@@ -1292,7 +1294,113 @@ __device__ __forceinline__ void unstage_tile_map(const double* TB, double* __res
 
 // Solver prologue: coefficients, self-face operators and (SWEEP) the defect's neighbour tiles
 // staged with cp.async exactly as in the apply kernel; the own tile lands in TB half 0.
-template <int N, bool SWEEP, bool CMAP, bool WB>
+// The nodal D_T factors of every cell (the Kronecker-sum form, see plane_dt_nodal): per direction
+//   K_a = |T|K_a/h_a^2 Shat - |T|b_a/h_a Chat + [a = z] |T| c Mhat + |F_a| (self-face 1D terms)
+// in cl.B[cs][a n^2 + i n + i']. Needs fc, vc, vb complete; ends with a barrier.
+template <int N, bool WB> __device__ __forceinline__ void setup_K3(const KParams& kp, Cells<N, WB>& cl) {
+  using G = Geo<N>;
+  for (int it = threadIdx.x; it < G::C * 3 * G::N2; it += G::NT) {
+    const int cs = it / (3 * G::N2), rem = it % (3 * G::N2), a = rem / G::N2;
+    const int i = (rem % G::N2) / N, ip = rem % N;
+    const double* lo = cl.fc[cs][2 * a];
+    const double* hi = cl.fc[cs][2 * a + 1];
+    const double ih = kp.ih[a];
+    const double e0i = i == 0, e0p = ip == 0, e1i = i == N - 1, e1p = ip == N - 1;
+    double f = e0i * (lo[0] * e0p + lo[1] * ih * c_tab[N].d0[ip]) + lo[4] * c_tab[N].d0[i] * e0p;
+    f += e1i * (hi[0] * e1p + hi[1] * ih * c_tab[N].d1[ip]) + hi[4] * c_tab[N].d1[i] * e1p;
+    double t = kp.fa[a] * f;
+    t = fma(cl.vc[cs][a], c_tab[N].S[i * N + ip], t);
+    t = fma(-cl.vb[cs][a], c_tab[N].Cm[i * N + ip], t);
+    if (a == 2) t = fma(cl.vc[cs][3], c_tab[N].M[i * N + ip], t);
+    cl.B[cs][a * G::N2 + i * N + ip] = t;
+  }
+  __syncthreads();
+}
+
+// out = D_T in for the lane's plane in the nodal Kronecker-sum form
+//   D_T = Kx (x) Mhat (x) Mhat + Mhat (x) Ky (x) Mhat + Mhat (x) Mhat (x) Kz
+// (per-cell constant coefficients on the affine cell): in the plane (lane = z node k)
+// b = Mhat_x p, c = Kx p, d = Mhat_y b, g = Ky b + Mhat_y c; one transpose; (lane = y node j)
+// q = Mhat_z g + Kz d; one transpose back. 7 contractions per lane (the Gauss-point form: ~14).
+template <int N, bool WB>
+__device__ __forceinline__ void plane_dt_nodal(const Cells<N, WB>& cl, const Lane& L, const double (&in)[N][N],
+                                               double (&out)[N][N], double* TB) {
+  using G = Geo<N>;
+  double* tb = TB + L.cs * G::CTB;
+  const double* K = cl.B[L.cs];
+  __syncwarp();   // the previous call's reads of TB (other lanes of the cell) are done
+  if (L.active) {
+    const int k = L.t;
+    double b[N][N], c[N][N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double kr[N];
+#pragma unroll
+      for (int ip = 0; ip < N; ++ip) kr[ip] = K[i * N + ip];
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double sb = 0.0, sc = 0.0;
+#pragma unroll
+        for (int ip = 0; ip < N; ++ip) {
+          sb = fma(c_tab[N].M[i * N + ip], in[j][ip], sb);
+          sc = fma(kr[ip], in[j][ip], sc);
+        }
+        b[j][i] = sb;
+        c[j][i] = sc;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double kr[N];
+#pragma unroll
+      for (int jp = 0; jp < N; ++jp) kr[jp] = K[G::N2 + j * N + jp];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double sd = 0.0, sg = 0.0;
+#pragma unroll
+        for (int jp = 0; jp < N; ++jp) {
+          sd = fma(c_tab[N].M[j * N + jp], b[jp][i], sd);
+          sg = fma(kr[jp], b[jp][i], sg);
+          sg = fma(c_tab[N].M[j * N + jp], c[jp][i], sg);
+        }
+        tb[k * G::KS + j * N + i] = sd;
+        tb[G::ARR + k * G::KS + j * N + i] = sg;
+      }
+    }
+  }
+  __syncwarp();
+  if (L.active) {
+    const int j = L.t;
+    double dz[N][N], gz[N][N];   // [k][i]
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        dz[kk][i] = tb[kk * G::KS + j * N + i];
+        gz[kk][i] = tb[G::ARR + kk * G::KS + j * N + i];
+      }
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double kr[N];
+#pragma unroll
+      for (int kk = 0; kk < N; ++kk) kr[kk] = K[2 * G::N2 + k * N + kk];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < N; ++kk) {
+          s = fma(c_tab[N].M[k * N + kk], gz[kk][i], s);
+          s = fma(kr[kk], dz[kk][i], s);
+        }
+        tb[k * G::KS + j * N + i] = s;
+      }
+    }
+  }
+  __syncwarp();
+  if (L.active) read_plane<N>(TB, L, out);
+}
+
+template <int N, bool SWEEP, bool CMAP, bool WB, bool NODAL = false>
 __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl, double* TB, double* FY,
                                              double* FX, double* FZ, const double* in, int cell0, int nvalid) {
   using G = Geo<N>;
@@ -1315,7 +1423,8 @@ __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl
   }
   setup_finish<N>(kp, cl, sr);
   __syncthreads();   // fc of every cell
-  setup_B<N>(kp, cl);
+  if constexpr (NODAL) setup_K3<N>(kp, cl);
+  else setup_B<N>(kp, cl);
   cp_async_wait_all();
   __syncthreads();
 }
@@ -1460,8 +1569,12 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   // n <= 4: neighbour tiles staged with cp.async (a face region holds a tile); n = 5: through
   // registers, one pair of tiles at a time
   constexpr bool ASYNC = G::FS >= G::N3;
+  // D_T of the iterations in the nodal Kronecker-sum form (plane_dt_nodal) at n <= 3 (C5 sweep
+  // 5339 -> 3960 us); at n = 4 it measured equal (C2 339 vs 342 us) and the Gauss-point form,
+  // tuned to the instruction cache, stays
+  constexpr bool NODAL = DG_NODAL_DT && ASYNC && N <= 3;
   if constexpr (ASYNC) {
-    solver_setup<N, SWEEP, CMAP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+    solver_setup<N, SWEEP, CMAP, true, NODAL>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
   } else {
     stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
     setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
@@ -1478,7 +1591,8 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
       load_nbr<N>(pv1, cl, 3, kp);
       nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     }
-    plane_op<N, true, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);   // Q = A u
+    // Q = A u (with the nodal D_T factors in cl.B, the self faces come from the traces)
+    plane_op<N, true, !NODAL, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);
     __syncthreads();
     if (CMAP) stage_tile_map<N>(TB, f, cl);
     else stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
@@ -1528,7 +1642,8 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
     const int done = __all_sync(0xffffffffu, conv || !L.active);  // per-warp lock-step
     if (done || iter >= kp.max_it) break;
     double Q[N][N];
-    plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);  // Q = D_T P
+    if constexpr (NODAL) plane_dt_nodal<N>(cl, L, P, Q, TB);                       // Q = D_T P
+    else plane_op<N, false, true, true, GEN>(kp, cl, L, rw, true, P, Q, TB, FY, FX, FZ);
     double pq = 0.0;
 #pragma unroll
     for (int j = 0; j < N; ++j)
