@@ -277,22 +277,25 @@ template <int N> __device__ __forceinline__ void kmv(const double* K, const doub
   }
 }
 
-// D_T p for the warp's own cell (one x-line per lane, LPL = 1) in the nodal Kronecker-sum form:
+// D_T p in the nodal Kronecker-sum form, one x-line per thread: WARP = the warp's own cell (lane
+// l < n^2 owns x-line l), else the CTA's group (thread t < C n^2 owns x-line t):
 // x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
-// q = Mhat g + Kz d -> back to the lane's x-line. 7 one-direction contractions and 3 transposes
-// (the Gauss-point form: 9 contractions, 6 transposes). pin: the lane's x-line of p.
-template <int N>
-__device__ __forceinline__ void dt_nodal_warp(const Group<N>& g, double* SA, double* SB, const double* pin,
-                                              double* q) {
+// q = Mhat g + Kz d -> back to the thread's x-line. 7 one-direction contractions and 3 transposes
+// (the Gauss-point form: 9 contractions, 6 transposes). pin: the thread's x-line of p.
+template <int N, bool WARP>
+__device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* SB, const double* pin,
+                                         double* q) {
   using G = Geo<N>;
   constexpr int N2 = G::N2;
-  const int tid = threadIdx.x, cs = tid >> 5, lane = tid & 31;
-  const bool act = lane < N2;
-  const int a = lane % N, b = lane / N;
-  const double* Kx = g.Bf[cs][0];
-  const double* Ky = g.Bf[cs][1];
-  const double* Kz = g.Bf[cs][2];
+  const int tid = threadIdx.x;
+  const int cs = WARP ? tid >> 5 : tid / N2, l = WARP ? (tid & 31) : tid % N2;
+  const bool act = WARP ? l < N2 : tid < G::LINES;
+  const int a = l % N, b = l / N;
+  const double* Kx = g.Bf[act ? cs : 0][0];
+  const double* Ky = g.Bf[act ? cs : 0][1];
+  const double* Kz = g.Bf[act ? cs : 0][2];
   const int base = cs * G::CS;
+  auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
   if (act) {   // x-lines (j = a, k = b)
     double bv[N], cv[N];
     mv<N, 2>(pin, bv);
@@ -300,7 +303,7 @@ __device__ __forceinline__ void dt_nodal_warp(const Group<N>& g, double* SA, dou
     st<N, 1>(SA + base + b * G::ZS + a * G::YS, bv);
     st<N, 1>(SB + base + b * G::ZS + a * G::YS, cv);
   }
-  __syncwarp();
+  sync();
   if (act) {   // y-lines (i = a, k = b)
     const int off = base + b * G::ZS + a;
     double bv[N], cv[N], dv[N], ev[N], fv[N];
@@ -314,7 +317,7 @@ __device__ __forceinline__ void dt_nodal_warp(const Group<N>& g, double* SA, dou
     st<N, G::YS>(SA + off, dv);
     st<N, G::YS>(SB + off, ev);
   }
-  __syncwarp();
+  sync();
   if (act) {   // z-lines (i = a, j = b)
     const int off = base + b * G::YS + a;
     double dv[N], gv[N], o1[N], o2[N];
@@ -326,7 +329,7 @@ __device__ __forceinline__ void dt_nodal_warp(const Group<N>& g, double* SA, dou
     for (int e = 0; e < N; ++e) o1[e] += o2[e];
     st<N, G::ZS>(SA + off, o1);
   }
-  __syncwarp();
+  sync();
   if (act) ld<N, 1>(SA + base + b * G::ZS + a * G::YS, q);
   else
 #pragma unroll
@@ -879,7 +882,9 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
+  constexpr bool NODAL = DG_NODAL_DT;   // D_T of the iterations in the nodal Kronecker-sum form
+  if constexpr (NODAL) nodal_face_ops<N>(kq, g);
+  else self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
     const double* fb = f + (size_t)cell0 * G::N3;
     cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
@@ -932,10 +937,14 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     double q[N];
 #pragma unroll
     for (int e = 0; e < N; ++e) q[e] = 0.0;
-    cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
+    if constexpr (NODAL) {
+      dt_nodal<N, false>(g, SA, SB, p, q);
+    } else {
+      cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
 #pragma unroll
-      for (int e = 0; e < N; ++e) q[e] = v[e];
-    }, p);
+        for (int e = 0; e < N; ++e) q[e] = v[e];
+      }, p);
+    }
     if (own) {
       double sp = 0.0;
 #pragma unroll
@@ -1112,7 +1121,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
       for (int e = 0; e < N; ++e) q[e] = 0.0;
       if constexpr (NODAL) {
-        dt_nodal_warp<N>(g, SA, SB, p, q);
+        dt_nodal<N, true>(g, SA, SB, p, q);
       } else {
         cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
                                                              [&](int, int, int, const double* v) {
