@@ -25,6 +25,9 @@
 #endif
 namespace pk {
 
+#ifndef DG_NODAL_BICG
+#define DG_NODAL_BICG 1
+#endif
 #ifndef DG_PLANE5_ASYNC
 #define DG_PLANE5_ASYNC 0
 #endif
@@ -1569,10 +1572,10 @@ k_cg(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ f,
   // n <= 4: neighbour tiles staged with cp.async (a face region holds a tile); n = 5: through
   // registers, one pair of tiles at a time
   constexpr bool ASYNC = G::FS >= G::N3;
-  // D_T of the iterations in the nodal Kronecker-sum form (plane_dt_nodal) at n <= 3 (C5 sweep
-  // 5339 -> 3960 us); at n = 4 it measured equal (C2 339 vs 342 us) and the Gauss-point form,
-  // tuned to the instruction cache, stays
-  constexpr bool NODAL = DG_NODAL_DT && ASYNC && N <= 3;
+  // D_T of the iterations in the nodal Kronecker-sum form (plane_dt_nodal): C5 sweep
+  // 5339 -> 3960 us; at n = 4 equal to the Gauss-point form (C2 339 vs 342 us), which with the
+  // cell block sized for the nodal factors (BiCGStab) loses occupancy (437 us)
+  constexpr bool NODAL = DG_NODAL_DT && ASYNC;
   if constexpr (ASYNC) {
     solver_setup<N, SWEEP, CMAP, true, NODAL>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
   } else {
@@ -1964,8 +1967,10 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
   // n <= 4: neighbour tiles staged with cp.async (a face region holds a tile); n = 5: through
   // registers, one pair of tiles at a time
   constexpr bool ASYNC = G::FS >= G::N3;
+  // D_T of the iterations in the nodal Kronecker-sum form (plane_dt_nodal)
+  constexpr bool NODAL = DG_NODAL_DT && DG_NODAL_BICG && ASYNC;
   if constexpr (ASYNC) {
-    solver_setup<N, SWEEP, CMAP>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
+    solver_setup<N, SWEEP, CMAP, true, NODAL>(kp, cl, TB, FY, FX, FZ, in, cell0, nvalid);
   } else {
     stage_tile<N>(TB, in + (size_t)cell0 * G::N3, nvalid);
     setup<N>(kp, cl, cell0, SWEEP ? in : nullptr);
@@ -1982,7 +1987,7 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       load_nbr<N>(pv1, cl, 3, kp);
       nbr_prologue<N>(kp, cl, L, TB, FY, FX, FZ, in + (size_t)cell0 * G::N3, pv0, pv1);
     }
-    plane_op<N, true, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
+    plane_op<N, true, !NODAL>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // A u
     __syncthreads();
     if (CMAP) stage_tile_map<N>(TB, f, cl);
     else stage_tile_s<N>(TB, f + (size_t)cell0 * G::N3, nvalid);
@@ -2132,7 +2137,8 @@ k_bicgstab(KParams kp, const double* DG_RESTRICT in, const double* __restrict__ 
       rst = false;
     }
     park(R);
-    plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);   // v = D_T p^ / t = D_T s^
+    if constexpr (NODAL) plane_dt_nodal<N>(cl, L, W, T, TB);                  // v = D_T p^ / t = D_T s^
+    else plane_op<N, false, true>(kp, cl, L, rw, true, W, T, TB, FY, FX, FZ);
     unpark(R);
     if (!half) {
       double rv = 0.0;
