@@ -23,7 +23,10 @@
 //    cell, all C cells of a CTA iterating together with per-cell convergence masks
 //    and deterministic per-cell reductions (no atomics).
 #ifndef DG_NODAL_DT
-#define DG_NODAL_DT 1   // warp-per-cell CG at n = 5: D_T in the nodal Kronecker-sum form
+#define DG_NODAL_DT 1   // local solvers: D_T in the nodal Kronecker-sum form
+#endif
+#ifndef DG_NODAL_APPLY
+#define DG_NODAL_APPLY 1   // line-family A u in the nodal Kronecker-sum form (apply_nodal)
 #endif
 #ifndef DG_PDL
 #define DG_PDL 1
@@ -334,6 +337,258 @@ __device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* 
   else
 #pragma unroll
     for (int e = 0; e < N; ++e) q[e] = 0.0;
+}
+
+// v = K_a u along a line with the nodal D_T factor of direction a (see nodal_face_ops) formed on
+// the fly from the constant 1D tables (Shat, Chat, Mhat: constant-bank operands) and the cell's
+// scalars: K_a = vc_a Shat - vb_a Chat + [a = z] vc_3 Mhat + |F_a| (self-face rank-2 terms)
+template <int N, bool GEN>
+__device__ __forceinline__ void kfly(const KParams& kp, const Group<N>& g, int cs, int a, const double* u,
+                                     double* v) {
+  const double* lo = g.fc[cs][2 * a];
+  const double* hi = g.fc[cs][2 * a + 1];
+  const double vk = g.vc[cs][a];
+  double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    g0 = fma(c_tab[N].d0[r], u[r], g0);
+    g1 = fma(c_tab[N].d1[r], u[r], g1);
+  }
+  const double ih = kp.ih[a], fa = kp.fa[a];
+  const double sl = fa * (lo[0] * u[0] + lo[1] * ih * g0), tl = fa * lo[4] * u[0];
+  const double sh = fa * (hi[0] * u[N - 1] + hi[1] * ih * g1), th = fa * hi[4] * u[N - 1];
+  double vb = 0.0, vr = 0.0;
+  if constexpr (GEN) {
+    vb = g.vb[cs][a];
+    vr = a == 2 ? g.vc[cs][3] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double ss = 0.0, cc = 0.0, mm = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      ss = fma(c_tab[N].S[q * N + r], u[r], ss);
+      if constexpr (GEN) {
+        cc = fma(c_tab[N].Cm[q * N + r], u[r], cc);
+        mm = fma(c_tab[N].M[q * N + r], u[r], mm);
+      }
+    }
+    double o = vk * ss;
+    if constexpr (GEN) o = fma(-vb, cc, fma(vr, mm, o));
+    o = fma(c_tab[N].d0[q], tl, fma(c_tab[N].d1[q], th, o));
+    if (q == 0) o += sl;
+    if (q == N - 1) o += sh;
+    v[q] = o;
+  }
+}
+
+// A u (or the parts selected by kp.mask) for the CTA's group in the nodal Kronecker-sum form,
+// one x-line per thread (C n^2 <= NTH):
+//   (A u)_T = D_T u_T + sum over the interior faces F of (B_F (x) Mhat (x) Mhat) u_N
+// D_T in the factored form of dt_nodal (K_a = g.Bf, nodal_face_ops: volume + self faces); the
+// neighbour's face term depends on u_N only through its face values and normal-derivative sums
+// (P:345-350), combined per face node into the value-test and derivative-test coefficients
+// S, T (the fc neighbour coefficients, as face_line) and injected where the pipeline still
+// applies the tangential masses: x faces into c = Kx u at the x stage (then Mhat_y, Mhat_z),
+// y faces into g at the y stage after their Mhat_x (then Mhat_z), z faces at the z stage after
+// Mhat_x and Mhat_y. Four barriers; no face passes. src: the group's tile (CS layout, shared),
+// SA, SB: scratch tensors, FA: 12 C n^2 doubles (face arrays; the face buffer of cell_operator). out(cs, j, k, v[N]) receives x-line
+// (j, k) of slot cs.
+template <int N, int NTH, bool GEN, class Out>
+__device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g, const double* src,
+                                            double* SA, double* SB, double* FA, Out out) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2, C = G::C;
+  static_assert(G::LINES <= NTH, "one x-line per thread");
+  const int t = threadIdx.x;
+  const bool act = t < G::LINES;
+  const int cs = act ? t / N2 : 0, l = t % N2, a = l % N, bb = l / N;
+  double* FY = FA;                  // [C][4][n^2]: y faces S_lo, T_lo, S_hi, T_hi at (i, k)
+  double* FZ = FA + 4 * C * N2;     // [C][4][n^2]: z faces at (i, j); reused after Mhat_y
+  double* FZb = FA + 8 * C * N2;    // [C][4][n^2]: z faces after Mhat_x
+  const int base = cs * G::CS;
+  double sxl = 0.0, txl = 0.0, sxh = 0.0, txh = 0.0;
+  // ---- stage 0: the neighbours' face data at this thread's face nodes
+  if (act) {
+    // x faces at (j = a, k = bb): the neighbours' x-lines (in the group: from the tile)
+    {
+      const double* nlo = g.nb[cs][0];
+      const double* nhi = g.nb[cs][1];
+      const double* clo = g.fc[cs][0];
+      const double* chi = g.fc[cs][1];
+      const int off = bb * G::ZS + a * G::YS, goff = bb * N2 + a * N;
+      if (nlo) {
+        double w[N];
+        if (cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, w); else ld<N, 1>(nlo + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+        sxl = clo[2] * w[N - 1] + clo[3] * gn * kp.ih[0];
+        txl = clo[5] * w[N - 1];
+      }
+      if (nhi) {
+        double w[N];
+        if (cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, w); else ld<N, 1>(nhi + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+        sxh = chi[2] * w[0] + chi[3] * gn * kp.ih[0];
+        txh = chi[5] * w[0];
+      }
+    }
+    // y faces at (i = a, k = bb)
+    {
+      const double* nlo = g.nb[cs][2];
+      const double* nhi = g.nb[cs][3];
+      const double* clo = g.fc[cs][2];
+      const double* chi = g.fc[cs][3];
+      const int goff = bb * N2 + a;
+      double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+      if (nlo) {
+        double w[N];
+        ld<N, N>(nlo + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+        s0 = clo[2] * w[N - 1] + clo[3] * gn * kp.ih[1];
+        t0 = clo[5] * w[N - 1];
+      }
+      if (nhi) {
+        double w[N];
+        ld<N, N>(nhi + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+        s1 = chi[2] * w[0] + chi[3] * gn * kp.ih[1];
+        t1 = chi[5] * w[0];
+      }
+      double* fy = FY + cs * 4 * N2 + bb * N + a;
+      fy[0] = s0; fy[N2] = t0; fy[2 * N2] = s1; fy[3 * N2] = t1;
+    }
+    // z faces at (i = a, j = bb); at a slab boundary the neighbour is a ghost trace record
+    {
+      const double* nlo = g.nb[cs][4];
+      const double* nhi = g.nb[cs][5];
+      const double* clo = g.fc[cs][4];
+      const double* chi = g.fc[cs][5];
+      const int goff = bb * N + a;
+      double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
+      if (nlo) {
+        double av, gn = 0.0;
+        if (ghost_trace(kp, g.cell[cs], 0)) {
+          av = nlo[goff];
+          gn = nlo[N2 + goff];
+        } else {
+          double w[N];
+          ld<N, N2>(nlo + goff, w);
+#pragma unroll
+          for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+          av = w[N - 1];
+        }
+        s0 = clo[2] * av + clo[3] * gn * kp.ih[2];
+        t0 = clo[5] * av;
+      }
+      if (nhi) {
+        double av, gn = 0.0;
+        if (ghost_trace(kp, g.cell[cs], 1)) {
+          av = nhi[goff];
+          gn = nhi[N2 + goff];
+        } else {
+          double w[N];
+          ld<N, N2>(nhi + goff, w);
+#pragma unroll
+          for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+          av = w[0];
+        }
+        s1 = chi[2] * av + chi[3] * gn * kp.ih[2];
+        t1 = chi[5] * av;
+      }
+      double* fz = FZ + cs * 4 * N2 + bb * N + a;
+      fz[0] = s0; fz[N2] = t0; fz[2 * N2] = s1; fz[3 * N2] = t1;
+    }
+  }
+  __syncthreads();
+  // ---- x stage (x-line j = a, k = bb): b = Mhat u, c = Kx u + x faces; z faces: Mhat_x
+  if (act) {
+    double u[N], bv[N], cv[N];
+    ld<N, 1>(src + base + bb * G::ZS + a * G::YS, u);
+    mv<N, 2>(u, bv);
+    kfly<N, GEN>(kp, g, cs, 0, u, cv);
+    const double fa = kp.fa[0];
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+      cv[e] = fma(fa, fma(c_tab[N].d0[e], txl, fma(c_tab[N].d1[e], txh, (e == 0 ? sxl : 0.0) + (e == N - 1 ? sxh : 0.0))), cv[e]);
+    st<N, 1>(SA + base + bb * G::ZS + a * G::YS, bv);
+    st<N, 1>(SB + base + bb * G::ZS + a * G::YS, cv);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {   // z-face arrays along x: entry (i = a, j = bb)
+      const double* row = FZ + cs * 4 * N2 + q * N2 + bb * N;
+      double zs = 0.0;
+#pragma unroll
+      for (int ip = 0; ip < N; ++ip) zs = fma(c_tab[N].M[a * N + ip], row[ip], zs);
+      FZb[cs * 4 * N2 + q * N2 + bb * N + a] = zs;
+    }
+  }
+  __syncthreads();
+  // ---- y stage (y-line i = a, k = bb): d = Mhat b, g = Ky b + Mhat c + y faces (after Mhat_x);
+  // z faces: Mhat_y
+  if (act) {
+    const int off = base + bb * G::ZS + a;
+    double bv[N], cv[N], dv[N], ev[N], fv[N];
+    ld<N, G::YS>(SA + off, bv);
+    ld<N, G::YS>(SB + off, cv);
+    mv<N, 2>(bv, dv);
+    kfly<N, GEN>(kp, g, cs, 1, bv, ev);
+    mv<N, 2>(cv, fv);
+    double yq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double* row = FY + cs * 4 * N2 + q * N2 + bb * N;
+      double s = 0.0;
+#pragma unroll
+      for (int ip = 0; ip < N; ++ip) s = fma(c_tab[N].M[a * N + ip], row[ip], s);
+      yq[q] = s;
+    }
+    const double fa = kp.fa[1];
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+      ev[e] += fv[e] + fa * (c_tab[N].d0[e] * yq[1] + c_tab[N].d1[e] * yq[3] + (e == 0 ? yq[0] : 0.0) +
+                             (e == N - 1 ? yq[2] : 0.0));
+    // z-face arrays along y (entry (i = a, j = bb)) -> FZ (free again)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0;
+#pragma unroll
+      for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[bb * N + jp], FZb[cs * 4 * N2 + q * N2 + jp * N + a], s);
+      FZ[cs * 4 * N2 + q * N2 + bb * N + a] = s;
+    }
+    st<N, G::YS>(SA + off, dv);
+    st<N, G::YS>(SB + off, ev);
+  }
+  __syncthreads();
+  // ---- z stage (z-line i = a, j = bb): q = Mhat g + Kz d + z faces (after Mhat_x, Mhat_y)
+  if (act) {
+    const int off = base + bb * G::YS + a;
+    double dv[N], gv[N], o1[N], o2[N];
+    ld<N, G::ZS>(SA + off, dv);
+    ld<N, G::ZS>(SB + off, gv);
+    mv<N, 2>(gv, o1);
+    kfly<N, GEN>(kp, g, cs, 2, dv, o2);
+    const double* fz = FZ + cs * 4 * N2 + bb * N + a;
+    const double z0 = fz[0], z1 = fz[N2], z2 = fz[2 * N2], z3 = fz[3 * N2];
+    const double fa = kp.fa[2];
+#pragma unroll
+    for (int e = 0; e < N; ++e)
+      o1[e] += o2[e] + fa * (c_tab[N].d0[e] * z1 + c_tab[N].d1[e] * z3 + (e == 0 ? z0 : 0.0) +
+                             (e == N - 1 ? z2 : 0.0));
+    st<N, G::ZS>(SA + off, o1);
+  }
+  __syncthreads();
+  if (act) {
+    double v[N];
+    ld<N, 1>(SA + base + bb * G::ZS + a * G::YS, v);
+    out(cs, a, bb, v);
+  }
 }
 
 // ---- group setup: coefficients, face parameters, neighbour pointers ------------
@@ -846,10 +1101,18 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // pointers only; ends with __syncthreads
   asm volatile("griddepcontrol.wait;" ::: "memory");
   async_tile<N>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  // A u (faces, not the D_T hook) in the nodal Kronecker-sum form
+  constexpr bool NODAL = DG_NODAL_APPLY && FACES && !USEB;
   if constexpr (USEB) self_face_ops<N>(kp, g);
   lcp_wait_all();
   __syncthreads();
   double* o = out + (size_t)cell0 * G::N3;
+  if constexpr (NODAL) {
+    apply_nodal<N, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
+      if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, w);
+    });
+    return;
+  }
   cell_operator<N, FACES, USEB, false, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
                           [&](int cs, int j, int k, const double* v) {
                             if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
