@@ -25,6 +25,9 @@
 #ifndef DG_NODAL_DT
 #define DG_NODAL_DT 1   // local solvers: D_T in the nodal Kronecker-sum form
 #endif
+#ifndef DG_NODAL_FLY
+#define DG_NODAL_FLY 0   // local solvers: nodal factors from shared memory (1) or formed on the fly
+#endif
 #ifndef DG_NODAL_APPLY
 #define DG_NODAL_APPLY 1   // line-family A u in the nodal Kronecker-sum form (apply_nodal)
 #endif
@@ -280,65 +283,6 @@ template <int N> __device__ __forceinline__ void kmv(const double* K, const doub
   }
 }
 
-// D_T p in the nodal Kronecker-sum form, one x-line per thread: WARP = the warp's own cell (lane
-// l < n^2 owns x-line l), else the CTA's group (thread t < C n^2 owns x-line t):
-// x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
-// q = Mhat g + Kz d -> back to the thread's x-line. 7 one-direction contractions and 3 transposes
-// (the Gauss-point form: 9 contractions, 6 transposes). pin: the thread's x-line of p.
-template <int N, bool WARP>
-__device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* SB, const double* pin,
-                                         double* q) {
-  using G = Geo<N>;
-  constexpr int N2 = G::N2;
-  const int tid = threadIdx.x;
-  const int cs = WARP ? tid >> 5 : tid / N2, l = WARP ? (tid & 31) : tid % N2;
-  const bool act = WARP ? l < N2 : tid < G::LINES;
-  const int a = l % N, b = l / N;
-  const double* Kx = g.Bf[act ? cs : 0][0];
-  const double* Ky = g.Bf[act ? cs : 0][1];
-  const double* Kz = g.Bf[act ? cs : 0][2];
-  const int base = cs * G::CS;
-  auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
-  if (act) {   // x-lines (j = a, k = b)
-    double bv[N], cv[N];
-    mv<N, 2>(pin, bv);
-    kmv<N>(Kx, pin, cv);
-    st<N, 1>(SA + base + b * G::ZS + a * G::YS, bv);
-    st<N, 1>(SB + base + b * G::ZS + a * G::YS, cv);
-  }
-  sync();
-  if (act) {   // y-lines (i = a, k = b)
-    const int off = base + b * G::ZS + a;
-    double bv[N], cv[N], dv[N], ev[N], fv[N];
-    ld<N, G::YS>(SA + off, bv);
-    ld<N, G::YS>(SB + off, cv);
-    mv<N, 2>(bv, dv);
-    kmv<N>(Ky, bv, ev);
-    mv<N, 2>(cv, fv);
-#pragma unroll
-    for (int e = 0; e < N; ++e) ev[e] += fv[e];
-    st<N, G::YS>(SA + off, dv);
-    st<N, G::YS>(SB + off, ev);
-  }
-  sync();
-  if (act) {   // z-lines (i = a, j = b)
-    const int off = base + b * G::YS + a;
-    double dv[N], gv[N], o1[N], o2[N];
-    ld<N, G::ZS>(SA + off, dv);
-    ld<N, G::ZS>(SB + off, gv);
-    mv<N, 2>(gv, o1);
-    kmv<N>(Kz, dv, o2);
-#pragma unroll
-    for (int e = 0; e < N; ++e) o1[e] += o2[e];
-    st<N, G::ZS>(SA + off, o1);
-  }
-  sync();
-  if (act) ld<N, 1>(SA + base + b * G::ZS + a * G::YS, q);
-  else
-#pragma unroll
-    for (int e = 0; e < N; ++e) q[e] = 0.0;
-}
-
 // v = K_a u along a line with the nodal D_T factor of direction a (see nodal_face_ops) formed on
 // the fly from the constant 1D tables (Shat, Chat, Mhat: constant-bank operands) and the cell's
 // scalars: K_a = vc_a Shat - vb_a Chat + [a = z] vc_3 Mhat + |F_a| (self-face rank-2 terms)
@@ -380,6 +324,65 @@ __device__ __forceinline__ void kfly(const KParams& kp, const Group<N>& g, int c
     if (q == N - 1) o += sh;
     v[q] = o;
   }
+}
+
+// D_T p in the nodal Kronecker-sum form, one x-line per thread: WARP = the warp's own cell (lane
+// l < n^2 owns x-line l), else the CTA's group (thread t < C n^2 owns x-line t):
+// x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
+// q = Mhat g + Kz d -> back to the thread's x-line. 7 one-direction contractions and 3 transposes
+// (the Gauss-point form: 9 contractions, 6 transposes). pin: the thread's x-line of p.
+template <int N, bool WARP, bool FLY = false, bool GEN = true>
+__device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* SB, const double* pin,
+                                         double* q, const KParams* kpp = nullptr) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2;
+  const int tid = threadIdx.x;
+  const int cs = WARP ? tid >> 5 : tid / N2, l = WARP ? (tid & 31) : tid % N2;
+  const bool act = WARP ? l < N2 : tid < G::LINES;
+  const int a = l % N, b = l / N;
+  const double* Kx = g.Bf[act ? cs : 0][0];
+  const double* Ky = g.Bf[act ? cs : 0][1];
+  const double* Kz = g.Bf[act ? cs : 0][2];
+  const int base = cs * G::CS;
+  auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
+  if (act) {   // x-lines (j = a, k = b)
+    double bv[N], cv[N];
+    mv<N, 2>(pin, bv);
+    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 0, pin, cv); else kmv<N>(Kx, pin, cv);
+    st<N, 1>(SA + base + b * G::ZS + a * G::YS, bv);
+    st<N, 1>(SB + base + b * G::ZS + a * G::YS, cv);
+  }
+  sync();
+  if (act) {   // y-lines (i = a, k = b)
+    const int off = base + b * G::ZS + a;
+    double bv[N], cv[N], dv[N], ev[N], fv[N];
+    ld<N, G::YS>(SA + off, bv);
+    ld<N, G::YS>(SB + off, cv);
+    mv<N, 2>(bv, dv);
+    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 1, bv, ev); else kmv<N>(Ky, bv, ev);
+    mv<N, 2>(cv, fv);
+#pragma unroll
+    for (int e = 0; e < N; ++e) ev[e] += fv[e];
+    st<N, G::YS>(SA + off, dv);
+    st<N, G::YS>(SB + off, ev);
+  }
+  sync();
+  if (act) {   // z-lines (i = a, j = b)
+    const int off = base + b * G::YS + a;
+    double dv[N], gv[N], o1[N], o2[N];
+    ld<N, G::ZS>(SA + off, dv);
+    ld<N, G::ZS>(SB + off, gv);
+    mv<N, 2>(gv, o1);
+    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 2, dv, o2); else kmv<N>(Kz, dv, o2);
+#pragma unroll
+    for (int e = 0; e < N; ++e) o1[e] += o2[e];
+    st<N, G::ZS>(SA + off, o1);
+  }
+  sync();
+  if (act) ld<N, 1>(SA + base + b * G::ZS + a * G::YS, q);
+  else
+#pragma unroll
+    for (int e = 0; e < N; ++e) q[e] = 0.0;
 }
 
 // A u (or the parts selected by kp.mask) for the CTA's group in the nodal Kronecker-sum form,
@@ -1201,7 +1204,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
     for (int e = 0; e < N; ++e) q[e] = 0.0;
     if constexpr (NODAL) {
-      dt_nodal<N, false>(g, SA, SB, p, q);
+      dt_nodal<N, false, DG_NODAL_FLY, true>(g, SA, SB, p, q, &kq);
     } else {
       cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
 #pragma unroll
@@ -1384,7 +1387,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 #pragma unroll
       for (int e = 0; e < N; ++e) q[e] = 0.0;
       if constexpr (NODAL) {
-        dt_nodal<N, true>(g, SA, SB, p, q);
+        dt_nodal<N, true, DG_NODAL_FLY, GEN>(g, SA, SB, p, q, &kq);
       } else {
         cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
                                                              [&](int, int, int, const double* v) {
