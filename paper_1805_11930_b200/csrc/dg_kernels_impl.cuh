@@ -1153,14 +1153,17 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   else self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    auto defect = [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
 #pragma unroll
       for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
-    });
+    };
+    // d = f - A u: nodal form at n <= 6 (n = 7, 8: the Gauss-point passes measured faster)
+    if constexpr (DG_NODAL_APPLY && N <= 6) apply_nodal<N, G::NT, true>(kq, g, P, SA, SB, FB, defect);
+    else cell_operator<N>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     // D_T uses self faces only
     for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
@@ -1328,14 +1331,16 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   else self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2), CTA-wide
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N, true, false, false, G::NTW, GEN>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    auto defect = [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
 #pragma unroll
       for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
-    });
+    };
+    if constexpr (DG_NODAL_APPLY && G::LINES <= G::NTW) apply_nodal<N, G::NTW, GEN>(kq, g, P, SA, SB, FB, defect);
+    else cell_operator<N, true, false, false, G::NTW, GEN>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     for (int it = tid; it < C * 6; it += G::NTW) g.nb[it / 6][it % 6] = nullptr;
   }
@@ -1742,14 +1747,17 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    auto defect = [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
 #pragma unroll
       for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
-    });
+    };
+    // d = f - A u: nodal form at n <= 6 (n = 7, 8: the Gauss-point passes measured faster)
+    if constexpr (DG_NODAL_APPLY && N <= 6) apply_nodal<N, G::NT, true>(kq, g, P, SA, SB, FB, defect);
+    else cell_operator<N>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
   }
