@@ -286,8 +286,8 @@ template <int N> __device__ __forceinline__ void kmv(const double* K, const doub
 // v = K_a u along a line with the nodal D_T factor of direction a (see nodal_face_ops) formed on
 // the fly from the constant 1D tables (Shat, Chat, Mhat: constant-bank operands) and the cell's
 // scalars: K_a = vc_a Shat - vb_a Chat + [a = z] vc_3 Mhat + |F_a| (self-face rank-2 terms)
-template <int N, bool GEN>
-__device__ __forceinline__ void kfly(const KParams& kp, const Group<N>& g, int cs, int a, const double* u,
+template <int N, bool GEN, class CB>
+__device__ __forceinline__ void kfly(const KParams& kp, const CB& g, int cs, int a, const double* u,
                                      double* v) {
   const double* lo = g.fc[cs][2 * a];
   const double* hi = g.fc[cs][2 * a + 1];

@@ -25,6 +25,9 @@
 #endif
 namespace pk {
 
+#ifndef DG_PLANE_NODAL_APPLY
+#define DG_PLANE_NODAL_APPLY 1   // plane-family A u in the nodal Kronecker-sum form
+#endif
 #ifndef DG_NODAL_BICG
 #define DG_NODAL_BICG 1
 #endif
@@ -1211,6 +1214,216 @@ __device__ __forceinline__ void setup_B(const KParams& kp, Cells<N, WB>& cl) {
 
 // out = A u (with_nbr) or D_T u, selected parts by kp.mask
 // FACES = false: the volume terms alone (dg_apply_parts with mask = volume), no face code.
+// A u (kp.mask parts) for the lane's plane in the nodal Kronecker-sum form:
+//   (A u)_T = Kx (x) Mhat (x) Mhat u_T + Mhat (x) Ky (x) Mhat u_T + Mhat (x) Mhat (x) Kz u_T
+//           + sum over the interior faces of (B_F (x) Mhat (x) Mhat) u_N
+// (K_a: volume + self faces, formed on the fly by kfly; B_F: the neighbour coupling, through the
+// neighbour's face values and normal-derivative sums). In the plane (lane = z node
+// k): b = Mhat_x u, c = Kx u + x faces, d = Mhat_y b, g = Ky b + Mhat_y c + y faces (after
+// Mhat_x); transpose; (lane = y node j) q = Mhat_z g + Kz d + z faces (after Mhat_x, Mhat_y);
+// transpose back. The neighbours come from the tiles staged by the caller (TB half 1: y-lo,
+// FY: y-hi, FX: z-lo, FZ: z-hi; x: the group's own tile or global memory); FX then holds the
+// contracted z-face arrays. res: the lane's plane of the result.
+template <int N, bool GEN, bool WB>
+__device__ __forceinline__ void plane_apply_nodal(const KParams& kp, const Cells<N, WB>& cl, const Lane& L,
+                                                  double* TB, double* FY, double* FX, double* FZ,
+                                                  const double* tile, double (&res)[N][N]) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2;
+  static_assert(G::FS >= 4 * G::N2, "a face region holds the four contracted z-face arrays");
+  constexpr int ZQ = (4 + N - 1) / N;   // z-face arrays per lane
+  const int k = L.t, cs = L.cs;
+  double u[N][N], xs[4][N], ys[4][N], zs[ZQ][N][N];
+  if (L.active) {
+    read_plane<N>(TB, L, u);
+    // x faces at (j, k): the neighbours' plane k (in the group: the own tile; else global)
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const double* c = cl.fc[cs][hi];
+      const double* nbp = cl.nb[cs][hi];
+      const int ncs = cs + (hi ? 1 : -1);
+      const double* plane = nullptr;
+      if (nbp) plane = (ncs >= 0 && ncs < G::C && nbp == tile + (size_t)ncs * G::N3) ? TB + ncs * G::CTB + k * G::KS
+                                                                                     : nbp + k * G::N2;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double row[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) row[i] = plane ? plane[j * N + i] : 0.0;
+        double gn = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) gn = fma(hi ? c_tab[N].d0[i] : c_tab[N].d1[i], row[i], gn);
+        const double av = hi ? row[0] : row[N - 1];
+        xs[2 * hi][j] = c[2] * av + c[3] * gn * kp.ih[0];
+        xs[2 * hi + 1][j] = c[5] * av;
+      }
+    }
+    // y faces at (i, k): the staged y tiles' plane k, then Mhat_x along i
+#pragma unroll
+    for (int hi = 0; hi < 2; ++hi) {
+      const double* c = cl.fc[cs][2 + hi];
+      double S[N], T[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double gn = 0.0, av;
+        if (hi) {
+          const double* nb = FY + cs * G::FS + k * G::N2;
+#pragma unroll
+          for (int j = 0; j < N; ++j) gn = fma(c_tab[N].d0[j], nb[j * N + i], gn);
+          av = nb[i];
+        } else {
+          const double* nb = TB + cs * G::CTB + G::ARR + k * G::KS;
+#pragma unroll
+          for (int j = 0; j < N; ++j) gn = fma(c_tab[N].d1[j], nb[j * N + i], gn);
+          av = nb[(N - 1) * N + i];
+        }
+        S[i] = c[2] * av + c[3] * gn * kp.ih[1];
+        T[i] = c[5] * av;
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0, t = 0.0;
+#pragma unroll
+        for (int ip = 0; ip < N; ++ip) {
+          s = fma(c_tab[N].M[i * N + ip], S[ip], s);
+          t = fma(c_tab[N].M[i * N + ip], T[ip], t);
+        }
+        ys[2 * hi][i] = s;
+        ys[2 * hi + 1][i] = t;
+      }
+    }
+    // z faces: array q = k + N qq (S_lo, T_lo, S_hi, T_hi) over (j, i), then Mhat_x, Mhat_y
+#pragma unroll
+    for (int qq = 0; qq < ZQ; ++qq) {
+      const int q = k + N * qq;
+      if (q < 4) {
+        const int side = q >> 1, isT = q & 1;
+        const double* c = cl.fc[cs][4 + side];
+        const double* nb = (side ? FZ : FX) + cs * G::FS;   // layout kk*N2 + j*N + i
+        const bool tr = ghost_trace(kp, cl.cell[cs], side);
+        double A[N][N];
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double gn = 0.0, av;
+            if (tr) {
+              av = nb[j * N + i];
+              gn = nb[G::N2 + j * N + i];
+            } else {
+#pragma unroll
+              for (int kk = 0; kk < N; ++kk) gn = fma(side ? c_tab[N].d0[kk] : c_tab[N].d1[kk], nb[kk * G::N2 + j * N + i], gn);
+              av = nb[(side ? 0 : N - 1) * G::N2 + j * N + i];
+            }
+            A[j][i] = isT ? c[5] * av : c[2] * av + c[3] * gn * kp.ih[2];
+          }
+        double B[N][N];
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int ip = 0; ip < N; ++ip) s = fma(c_tab[N].M[i * N + ip], A[j][ip], s);
+            B[j][i] = s;
+          }
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[j * N + jp], B[jp][i], s);
+            zs[qq][j][i] = s;
+          }
+      }
+    }
+  }
+  __syncthreads();   // every read of the staged tiles and of the own tile is done
+  double* tb = TB + cs * G::CTB;
+  if (L.active) {
+    double b[N][N], c[N][N];
+    const double fa0 = kp.fa[0];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int ip = 0; ip < N; ++ip) s = fma(c_tab[N].M[i * N + ip], u[j][ip], s);
+        b[j][i] = s;
+      }
+      kfly<N, GEN>(kp, cl, cs, 0, u[j], c[j]);
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        c[j][i] = fma(fa0, fma(c_tab[N].d0[i], xs[1][j], fma(c_tab[N].d1[i], xs[3][j],
+                               (i == 0 ? xs[0][j] : 0.0) + (i == N - 1 ? xs[2][j] : 0.0))), c[j][i]);
+    }
+    const double fa1 = kp.fa[1];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double cb[N], cc[N], e[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) { cb[j] = b[j][i]; cc[j] = c[j][i]; }
+      kfly<N, GEN>(kp, cl, cs, 1, cb, e);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        double sd = 0.0, sf = 0.0;
+#pragma unroll
+        for (int jp = 0; jp < N; ++jp) {
+          sd = fma(c_tab[N].M[j * N + jp], cb[jp], sd);
+          sf = fma(c_tab[N].M[j * N + jp], cc[jp], sf);
+        }
+        const double yf = c_tab[N].d0[j] * ys[1][i] + c_tab[N].d1[j] * ys[3][i] +
+                          (j == 0 ? ys[0][i] : 0.0) + (j == N - 1 ? ys[2][i] : 0.0);
+        tb[k * G::KS + j * N + i] = sd;
+        tb[G::ARR + k * G::KS + j * N + i] = e[j] + sf + fa1 * yf;
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < ZQ; ++qq) {
+      const int q = k + N * qq;
+      if (q < 4)
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+#pragma unroll
+          for (int i = 0; i < N; ++i) FX[cs * G::FS + q * G::N2 + j * N + i] = zs[qq][j][i];
+    }
+  }
+  __syncwarp();
+  if (L.active) {   // lane = y node j
+    const int j = k;
+    const double fa2 = kp.fa[2];
+    double dz[N][N], gz[N][N];   // [kk][i]
+#pragma unroll
+    for (int kk = 0; kk < N; ++kk)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        dz[kk][i] = tb[kk * G::KS + j * N + i];
+        gz[kk][i] = tb[G::ARR + kk * G::KS + j * N + i];
+      }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double cd[N], o[N];
+#pragma unroll
+      for (int kk = 0; kk < N; ++kk) cd[kk] = dz[kk][i];
+      kfly<N, GEN>(kp, cl, cs, 2, cd, o);
+      const double* z = FX + cs * G::FS + j * N + i;
+      const double z0 = z[0], z1 = z[G::N2], z2 = z[2 * G::N2], z3 = z[3 * G::N2];
+#pragma unroll
+      for (int kk = 0; kk < N; ++kk) {
+        double s = o[kk];
+#pragma unroll
+        for (int kp2 = 0; kp2 < N; ++kp2) s = fma(c_tab[N].M[kk * N + kp2], gz[kp2][i], s);
+        s += fa2 * (c_tab[N].d0[kk] * z1 + c_tab[N].d1[kk] * z3 + (kk == 0 ? z0 : 0.0) + (kk == N - 1 ? z2 : 0.0));
+        tb[kk * G::KS + j * N + i] = s;
+      }
+    }
+  }
+  __syncwarp();
+  if (L.active) read_plane<N>(TB, L, res);
+}
+
 template <int N, bool NBR, bool FACES = true, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
@@ -1248,10 +1461,16 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   cp_async_wait_all();
   __syncthreads();
   double in[N][N], o[N][N];
-  read_plane<N>(TB, L, in);
-  if (NBR) nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, tile);
-  else __syncthreads();
-  plane_op<N, NBR, false, FACES, GEN>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
+  // nodal form (C5 apply 815 -> 739 us, C2 37.8 -> 36.3 us); at n = 4 with convection it spills
+  // (C4 301 -> 330 us) and the Gauss-point form stays
+  if constexpr (DG_PLANE_NODAL_APPLY && NBR && FACES && !(N == 4 && GEN)) {
+    plane_apply_nodal<N, GEN>(kp, cl, L, TB, FY, FX, FZ, tile, o);
+  } else {
+    read_plane<N>(TB, L, in);
+    if (NBR) nbr_prologue_async<N, true>(kp, cl, L, TB, FY, FX, FZ, tile);
+    else __syncthreads();
+    plane_op<N, NBR, false, FACES, GEN>(kp, cl, L, rw, FACES ? (kp.mask & 1u) != 0 : true, in, o, TB, FY, FX, FZ);
+  }
   if (L.active) write_plane<N>(TB, L, o);  // same TB slots this lane read in Q3
   __syncthreads();
   unstage_tile<N>(TB, out + (size_t)cell0 * G::N3, nvalid);
