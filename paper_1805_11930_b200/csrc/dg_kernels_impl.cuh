@@ -97,6 +97,18 @@ template <int N_> struct Geo {
 // the solvers' face buffer fits in two tensors (it then aliases two the defect does not use)
 template <int N> __host__ __device__ constexpr bool fb_alias() { return 2 * Geo<N>::TENSOR >= Geo<N>::FACE; }
 
+// The leading members of Group (coefficients, face data, neighbour pointers, 1D rows): all the
+// nodal apply uses, without the solvers' reduction and operator arrays (less static shared
+// memory, one more resident CTA per SM at n = 5)
+template <int N> struct GroupHead {
+  static constexpr int C = Cells<N>::C;
+  int cell[C];
+  double vc[C][4];
+  double vb[C][3];
+  double fc[C][6][6];
+  const double* nb[C][6];
+  double tw[N], td0[N], td1[N];
+};
 template <int N> struct Group {
   static constexpr int C = Cells<N>::C;
   int cell[C];
@@ -1088,12 +1100,11 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 // The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
 // lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
 // before the first read of u).
-template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
-__global__ void __launch_bounds__(Geo<N>::NT)
-k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
+template <int N, bool FACES, bool USEB, bool GEN>
+__device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __restrict__ u,
+                                             double* __restrict__ out, int with_nbr, Group<N>& g) {
   using G = Geo<N>;
   extern __shared__ double sm[];
-  __shared__ Group<N> g;
   double* SRC = sm;
   double* SA = SRC + G::TENSOR;
   double* SB = SA + G::TENSOR;
@@ -1120,6 +1131,20 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
                           [&](int cs, int j, int k, const double* v) {
                             if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
                           });
+}
+
+template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
+  if constexpr (DG_NODAL_APPLY && FACES && !USEB) {
+    // the nodal apply touches only the head of the group block
+    static_assert(offsetof(Group<N>, td1) == offsetof(GroupHead<N>, td1), "GroupHead is a prefix of Group");
+    __shared__ GroupHead<N> gh;
+    k_apply_body<N, FACES, USEB, GEN>(kp, u, out, with_nbr, *reinterpret_cast<Group<N>*>(&gh));
+  } else {
+    __shared__ Group<N> g;
+    k_apply_body<N, FACES, USEB, GEN>(kp, u, out, with_nbr, g);
+  }
 }
 
 // Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
