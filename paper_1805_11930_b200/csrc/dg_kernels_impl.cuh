@@ -25,6 +25,9 @@
 #ifndef DG_NODAL_DT
 #define DG_NODAL_DT 1   // local solvers: D_T in the nodal Kronecker-sum form
 #endif
+#ifndef DG_APPLY_SETUP_FIRST
+#define DG_APPLY_SETUP_FIRST 0   // line apply: coefficient setup before the PDL wait (A/B)
+#endif
 #ifndef DG_NODAL_FLY
 #define DG_NODAL_FLY 0   // local solvers: nodal factors from shared memory (1) or formed on the fly
 #endif
@@ -1112,9 +1115,16 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
   const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(G::C, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
+#if DG_APPLY_SETUP_FIRST
   group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // pointers only; ends with __syncthreads
   asm volatile("griddepcontrol.wait;" ::: "memory");
   async_tile<N>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+#else
+  // the tile copy is in flight while the setup's coefficient loads wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  async_tile<N>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
+#endif
   // A u (faces, not the D_T hook) in the nodal Kronecker-sum form
   constexpr bool NODAL = DG_NODAL_APPLY && FACES && !USEB;
   if constexpr (USEB) self_face_ops<N>(kp, g);
