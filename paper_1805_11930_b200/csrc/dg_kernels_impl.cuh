@@ -400,6 +400,25 @@ __device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* 
     for (int e = 0; e < N; ++e) q[e] = 0.0;
 }
 
+// dst = D_T src in the nodal form for tensors in shared memory (CS layout), one x-line per thread
+// (WARP: the warp's own cell); the callers synchronise around it
+template <int N, bool WARP>
+__device__ __forceinline__ void dt_nodal_smem(const Group<N>& g, double* SA, double* SB, const double* src,
+                                              double* dst) {
+  using G = Geo<N>;
+  const int tid = threadIdx.x;
+  const int cs = WARP ? tid >> 5 : tid / G::N2, l = WARP ? (tid & 31) : tid % G::N2;
+  const bool act = WARP ? l < G::N2 : tid < G::LINES;
+  const int off = cs * G::CS + (l / N) * G::ZS + (l % N) * G::YS;
+  double pin[N], q[N];
+  if (act) ld<N, 1>(src + off, pin);
+  else
+#pragma unroll
+    for (int e = 0; e < N; ++e) pin[e] = 0.0;
+  dt_nodal<N, WARP>(g, SA, SB, pin, q);
+  if (act) st<N, 1>(dst + off, q);
+}
+
 // A u (or the parts selected by kp.mask) for the CTA's group in the nodal Kronecker-sum form,
 // one x-line per thread (C n^2 <= NTH):
 //   (A u)_T = D_T u_T + sum over the interior faces F of (B_F (x) Mhat (x) Mhat) u_N
@@ -1568,7 +1587,9 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   load_tile<N, G::NTW>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N, G::NTW>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N, G::NTW>(kq, g);
+  constexpr bool NODAL = DG_NODAL_DT && G::N2 <= 32;   // one line per lane: D_T in the nodal form
+  if constexpr (NODAL) nodal_face_ops<N, G::NTW>(kq, g);
+  else self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
     cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
@@ -1596,9 +1617,13 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   }
   auto op = [&](double* dst) {   // dst = D_T PS on this warp's cell
     __syncwarp();
-    cell_operator<N, false, true, true>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
-      st<N, 1>(dst + c * G::CS + k * G::ZS + j * G::YS, v);
-    });
+    if constexpr (NODAL) {
+      dt_nodal_smem<N, true>(g, SA, SB, PS, dst);
+    } else {
+      cell_operator<N, false, true, true>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+        st<N, 1>(dst + c * G::CS + k * G::ZS + j * G::YS, v);
+      });
+    }
     __syncwarp();
   };
   double rr = 0.0;
@@ -1779,7 +1804,9 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
   group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
-  self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
+  constexpr bool NODAL = DG_NODAL_DT;   // D_T of the iterations in the nodal form
+  if constexpr (NODAL) nodal_face_ops<N>(kq, g);
+  else self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
     auto defect = [&](int cs, int j, int k, const double* v) {
@@ -1868,9 +1895,13 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       }
     })
     __syncthreads();
-    cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
-      st<N, 1>(V + cs * G::CS + k * G::ZS + j * G::YS, v);
-    });
+    if constexpr (NODAL) {
+      dt_nodal_smem<N, false>(g, SA, SB, PS, V);
+    } else {
+      cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+        st<N, 1>(V + cs * G::CS + k * G::ZS + j * G::YS, v);
+      });
+    }
     __syncthreads();
     DG_FOR_XLINES({
       double rh[N], v[N];
@@ -1925,9 +1956,13 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
       if (ss <= kp.tol2 * g.sc[S_RR0][tid]) { g.conv[tid] = 1; g.its[tid] += 1; }
     }
     __syncthreads();
-    cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
-      st<N, 1>(T + cs * G::CS + k * G::ZS + j * G::YS, v);
-    });
+    if constexpr (NODAL) {
+      dt_nodal_smem<N, false>(g, SA, SB, PS, T);
+    } else {
+      cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+        st<N, 1>(T + cs * G::CS + k * G::ZS + j * G::YS, v);
+      });
+    }
     __syncthreads();
     DG_FOR_XLINES({
       double t[N], s[N];
