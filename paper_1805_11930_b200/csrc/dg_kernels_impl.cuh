@@ -1165,8 +1165,8 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
 template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
 __global__ void __launch_bounds__(Geo<N>::NT)
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
-  if constexpr (DG_NODAL_APPLY && FACES && !USEB) {
-    // the nodal apply touches only the head of the group block
+  if constexpr ((DG_NODAL_APPLY && FACES && !USEB) || (!FACES && !USEB)) {
+    // the nodal apply and the volume terms alone touch only the head of the group block
     static_assert(offsetof(Group<N>, td1) == offsetof(GroupHead<N>, td1), "GroupHead is a prefix of Group");
     __shared__ GroupHead<N> gh;
     k_apply_body<N, FACES, USEB, GEN>(kp, u, out, with_nbr, *reinterpret_cast<Group<N>*>(&gh));
@@ -2091,10 +2091,36 @@ inline bool gen_terms(const KParams& kp) {
 template <int N>
 cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
   KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
-  if constexpr (N <= 5) {
 #ifndef DG_VOL_PERSIST
 #define DG_VOL_PERSIST 1
 #endif
+#ifndef DG_PLANE_VOL67
+#define DG_PLANE_VOL67 0   // measured slower: p = 6 volume 105 -> 130 us (255 registers, 8 warps per SM)
+#endif
+  if constexpr (N >= 6 && N <= 7 && DG_PLANE_VOL67) {
+    // n = 6, 7: the plane-per-lane volume kernel without register prefetch (k_volume_s)
+    if (kp.mask == 1u && !force_line(kp)) {
+      using G = pk::Geo<N>;
+      const int grid = (kp.ncells + G::C - 1) / G::C;
+      if (grid == 0) return cudaSuccess;
+      static int sslots = 0;
+      const size_t ssm = sizeof(double) * (size_t)G::TB;
+      if (sslots == 0) {
+        cudaError_t e = set_smem(pk::k_volume_s<N, true>, ssm);
+        if (e == cudaSuccess) e = set_smem(pk::k_volume_s<N, false>, ssm);
+        int per_sm = 0, dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk::k_volume_s<N>, G::NT, ssm);
+        if (e != cudaSuccess) return e;
+        sslots = max(1, per_sm) * nsm;
+      }
+      if (gen_terms(kp)) pk::k_volume_s<N, true><<<min(grid, sslots), G::NT, ssm, s>>>(kp, u, out);
+      else pk::k_volume_s<N, false><<<min(grid, sslots), G::NT, ssm, s>>>(kp, u, out);
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (N <= 5) {
     if (kp.mask == 1u && DG_VOL_PERSIST && N <= 5) {
       using G = pk::Geo<N>;
       const int grid = (kp.ncells + G::C - 1) / G::C;
@@ -2168,8 +2194,10 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   using G = Geo<N>;
   const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
-  const size_t smem = smem_bytes<N>(3);
-  // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point operators
+  // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point
+  // operators. Neither has face passes, so neither gets the face buffer (more resident CTAs)
+  const bool nofb = kp.mask == 1u || (!with_nbr && kp.mask == 7u);   // kernels without face passes
+  const size_t smem = nofb ? sizeof(double) * 3 * (size_t)G::TENSOR : smem_bytes<N>(3);
   const bool gen = gen_terms(kp);
   auto kl = kp.mask == 1u ? (gen ? k_apply<N, false> : k_apply<N, false, false, false>)
                           : (!with_nbr && kp.mask == 7u ? (gen ? k_apply<N, false, true> : k_apply<N, false, true, false>)

@@ -57,6 +57,11 @@ template <> struct PL<2> { static constexpr int WARPS = DG_PL_WARPS2, KS = 5, CT
 template <> struct PL<3> { static constexpr int WARPS = DG_PL_WARPS3, KS = 19, CTB = 121, QS = 13, PS = 39; };
 template <> struct PL<4> { static constexpr int WARPS = DG_PL_WARPS4, KS = 20, CTB = 161, QS = 17, PS = 68; };
 template <> struct PL<5> { static constexpr int WARPS = DG_PL_WARPS5, KS = 25, CTB = 253, QS = 25, PS = 125; };
+// n = 6, 7: the volume-only kernel k_volume_s alone (one n x n plane per lane, 5 / 4 cells per
+// warp); strides from the same search restricted to its two lane patterns (read_plane and the
+// Q2 columns): 2 + 3 and 2 + 2 wavefronts per warp-wide 8-byte access
+template <> struct PL<6> { static constexpr int WARPS = 2, KS = 37, CTB = 447, QS = 36, PS = 216; };
+template <> struct PL<7> { static constexpr int WARPS = 2, KS = 49, CTB = 692, QS = 49, PS = 343; };
 
 template <int N_> struct Geo {
   static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
