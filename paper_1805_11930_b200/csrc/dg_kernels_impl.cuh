@@ -431,7 +431,9 @@ __device__ __forceinline__ void dt_nodal_smem(const Group<N>& g, double* SA, dou
 // Mhat_x and Mhat_y. Four barriers; no face passes. src: the group's tile (CS layout, shared),
 // SA, SB: scratch tensors, FA: 12 C n^2 doubles (face arrays; the face buffer of cell_operator). out(cs, j, k, v[N]) receives x-line
 // (j, k) of slot cs.
-template <int N, int NTH, bool GEN, class Out>
+// INPLACE: src may be overwritten (A u alone): after the x stage has read a thread's own line, the
+// z-face arrays after Mhat_x go there (4 < n entries per line) and FA shrinks to 8 C n^2
+template <int N, int NTH, bool GEN, bool INPLACE = false, class Out>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out) {
   using G = Geo<N>;
@@ -442,7 +444,14 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
   const int cs = act ? t / N2 : 0, l = t % N2, a = l % N, bb = l / N;
   double* FY = FA;                  // [C][4][n^2]: y faces S_lo, T_lo, S_hi, T_hi at (i, k)
   double* FZ = FA + 4 * C * N2;     // [C][4][n^2]: z faces at (i, j); reused after Mhat_y
-  double* FZb = FA + 8 * C * N2;    // [C][4][n^2]: z faces after Mhat_x
+  double* FZb = FA + 8 * C * N2;    // [C][4][n^2]: z faces after Mhat_x (not with INPLACE)
+  static_assert(!INPLACE || N > 4, "INPLACE: the four face arrays fit in an x-line");
+  // z-face entry (i, j) of array q after Mhat_x: in FZb, or (INPLACE) in the tile's x-line
+  // (j' = i, k' = j), i.e. the line of the thread that produces the entry
+  auto fzb = [&](int cs_, int q, int j, int i) -> double& {
+    if constexpr (INPLACE) return const_cast<double*>(src)[cs_ * G::CS + j * G::ZS + i * G::YS + q];
+    else return FZb[cs_ * 4 * N2 + q * N2 + j * N + i];
+  };
   const int base = cs * G::CS;
   double sxl = 0.0, txl = 0.0, sxh = 0.0, txh = 0.0;
   // ---- stage 0: the neighbours' face data at this thread's face nodes
@@ -563,7 +572,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
       double zs = 0.0;
 #pragma unroll
       for (int ip = 0; ip < N; ++ip) zs = fma(c_tab[N].M[a * N + ip], row[ip], zs);
-      FZb[cs * 4 * N2 + q * N2 + bb * N + a] = zs;
+      fzb(cs, q, bb, a) = zs;
     }
   }
   __syncthreads();
@@ -596,7 +605,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
     for (int q = 0; q < 4; ++q) {
       double s = 0.0;
 #pragma unroll
-      for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[bb * N + jp], FZb[cs * 4 * N2 + q * N2 + jp * N + a], s);
+      for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[bb * N + jp], fzb(cs, q, jp, a), s);
       FZ[cs * 4 * N2 + q * N2 + bb * N + a] = s;
     }
     st<N, G::YS>(SA + off, dv);
@@ -1122,6 +1131,12 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 // The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
 // lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
 // before the first read of u).
+#ifndef DG_APPLY_INPLACE
+#define DG_APPLY_INPLACE 1   // nodal A u: z-face arrays in the consumed tile (8 C n^2 face buffer)
+#endif
+template <int N> constexpr size_t apply_fb_doubles() {
+  return (DG_APPLY_INPLACE && N > 4 ? 8 : 12) * (size_t)Geo<N>::C * Geo<N>::N2;
+}
 template <int N, bool FACES, bool USEB, bool GEN>
 __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __restrict__ u,
                                              double* __restrict__ out, int with_nbr, Group<N>& g) {
@@ -1151,7 +1166,7 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
   __syncthreads();
   double* o = out + (size_t)cell0 * G::N3;
   if constexpr (NODAL) {
-    apply_nodal<N, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
+    apply_nodal<N, Geo<N>::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
       if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, w);
     });
     return;
@@ -2197,7 +2212,8 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point
   // operators. Neither has face passes, so neither gets the face buffer (more resident CTAs)
   const bool nofb = kp.mask == 1u || (!with_nbr && kp.mask == 7u);   // kernels without face passes
-  const size_t smem = nofb ? sizeof(double) * 3 * (size_t)G::TENSOR : smem_bytes<N>(3);
+  const size_t smem = sizeof(double) * (3 * (size_t)G::TENSOR +
+                                        (nofb ? 0 : (DG_NODAL_APPLY ? apply_fb_doubles<N>() : (size_t)G::FACE)));
   const bool gen = gen_terms(kp);
   auto kl = kp.mask == 1u ? (gen ? k_apply<N, false> : k_apply<N, false, false, false>)
                           : (!with_nbr && kp.mask == 7u ? (gen ? k_apply<N, false, true> : k_apply<N, false, true, false>)

@@ -53,8 +53,12 @@ template <int N> struct PL;
 #ifndef DG_PL_WARPS5
 #define DG_PL_WARPS5 2
 #endif
+#ifndef DG_PL3_KS
+#define DG_PL3_KS 10    // n = 3: conflict-free for the plane (t KS) and column (t N) lane patterns
+#define DG_PL3_CTB 71   // with 71 instead of 121 doubles per cell (apply: 3 instead of 2 CTAs per SM)
+#endif
 template <> struct PL<2> { static constexpr int WARPS = DG_PL_WARPS2, KS = 5, CTB = 22, QS = 8, PS = 17; };
-template <> struct PL<3> { static constexpr int WARPS = DG_PL_WARPS3, KS = 19, CTB = 121, QS = 13, PS = 39; };
+template <> struct PL<3> { static constexpr int WARPS = DG_PL_WARPS3, KS = DG_PL3_KS, CTB = DG_PL3_CTB, QS = 13, PS = 39; };
 template <> struct PL<4> { static constexpr int WARPS = DG_PL_WARPS4, KS = 20, CTB = 161, QS = 17, PS = 68; };
 template <> struct PL<5> { static constexpr int WARPS = DG_PL_WARPS5, KS = 25, CTB = 253, QS = 25, PS = 125; };
 // n = 6, 7: the volume-only kernel k_volume_s alone (one n x n plane per lane, 5 / 4 cells per
