@@ -1177,8 +1177,14 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
                           });
 }
 
+// resident CTAs the line apply is compiled for (n = 5: five by shared memory after INPLACE,
+// registers capped at 56 so that the register file allows them too)
+#ifndef DG_APPLY5_MINB
+#define DG_APPLY5_MINB 5
+#endif
+template <int N> constexpr int apply_minb() { return N == 5 ? DG_APPLY5_MINB : 0; }   // 0: no .minnctapersm
 template <int N, bool FACES = true, bool USEB = false, bool GEN = true>
-__global__ void __launch_bounds__(Geo<N>::NT)
+__global__ void __launch_bounds__(Geo<N>::NT, apply_minb<N>())
 k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int with_nbr) {
   if constexpr ((DG_NODAL_APPLY && FACES && !USEB) || (!FACES && !USEB)) {
     // the nodal apply and the volume terms alone touch only the head of the group block

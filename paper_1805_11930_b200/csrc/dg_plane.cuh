@@ -54,8 +54,10 @@ template <int N> struct PL;
 #define DG_PL_WARPS5 2
 #endif
 #ifndef DG_PL3_KS
-#define DG_PL3_KS 10    // n = 3: conflict-free for the plane (t KS) and column (t N) lane patterns
-#define DG_PL3_CTB 71   // with 71 instead of 121 doubles per cell (apply: 3 instead of 2 CTAs per SM)
+// n = 3 transpose strides (A/B: KS = 10, CTB = 71 gives the apply 3 instead of 2 CTAs per SM,
+// C5 apply 739 -> 662 us, but 2-way half-warp conflicts cost the sweep 3960 -> 4264 us)
+#define DG_PL3_KS 19
+#define DG_PL3_CTB 121
 #endif
 template <> struct PL<2> { static constexpr int WARPS = DG_PL_WARPS2, KS = 5, CTB = 22, QS = 8, PS = 17; };
 template <> struct PL<3> { static constexpr int WARPS = DG_PL_WARPS3, KS = DG_PL3_KS, CTB = DG_PL3_CTB, QS = 13, PS = 39; };
