@@ -419,6 +419,47 @@ __device__ __forceinline__ void dt_nodal_smem(const Group<N>& g, double* SA, dou
   if (act) st<N, 1>(dst + off, q);
 }
 
+// The y / z neighbours' lines through this thread's face nodes, loaded before the group setup:
+// their addresses are integer arithmetic on the cell index (no coefficient), so their latency
+// overlaps that of the setup's coefficient loads instead of following it. w[0], w[1]: y lo / hi
+// (line (i = a, k = bb), stride n), w[2], w[3]: z lo / hi (line (i = a, j = bb), stride n^2); at a
+// slab-boundary z face the ghost trace record's face value and derivative sum in w[.][0], w[.][1].
+// Which faces have a neighbour is still read from the setup's pointers (the same decision).
+template <int N> struct NbrLines { double w[4][N]; };
+template <int N>
+__device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const double* u, int cell0,
+                                                   NbrLines<N>& W) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2, N3 = G::N3;
+  const int t = threadIdx.x;
+  const int cs = t / N2, l = t % N2, a = l % N, bb = l / N;
+  const int cell = cell0 + cs;
+#pragma unroll
+  for (int f = 0; f < 4; ++f)
+#pragma unroll
+    for (int e = 0; e < N; ++e) W.w[f][e] = 0.0;
+  if (u == nullptr || t >= G::LINES || cell >= kp.ncells) return;
+  const int nxy = kp.nx * kp.ny;
+  const int cy = (cell / kp.nx) % kp.ny, cz = cell / nxy;
+  if (cy > 0) ld<N, N>(u + (size_t)(cell - kp.nx) * N3 + bb * N2 + a, W.w[0]);
+  if (cy < kp.ny - 1) ld<N, N>(u + (size_t)(cell + kp.nx) * N3 + bb * N2 + a, W.w[1]);
+  const int col = cell - cz * nxy, zo = bb * N + a;
+  if (cz > 0) {
+    ld<N, N2>(u + (size_t)(cell - nxy) * N3 + zo, W.w[2]);
+  } else if (kp.slab_face[4] == FK_GHOST) {
+    const double* rec = kp.ghost_lo + (size_t)col * 2 * N2;
+    W.w[2][0] = rec[zo];
+    W.w[2][1] = rec[N2 + zo];
+  }
+  if (cz < kp.nzl - 1) {
+    ld<N, N2>(u + (size_t)(cell + nxy) * N3 + zo, W.w[3]);
+  } else if (kp.slab_face[5] == FK_GHOST) {
+    const double* rec = kp.ghost_hi + (size_t)col * 2 * N2;
+    W.w[3][0] = rec[zo];
+    W.w[3][1] = rec[N2 + zo];
+  }
+}
+
 // A u (or the parts selected by kp.mask) for the CTA's group in the nodal Kronecker-sum form,
 // one x-line per thread (C n^2 <= NTH):
 //   (A u)_T = D_T u_T + sum over the interior faces F of (B_F (x) Mhat (x) Mhat) u_N
@@ -433,9 +474,11 @@ __device__ __forceinline__ void dt_nodal_smem(const Group<N>& g, double* SA, dou
 // (j, k) of slot cs.
 // INPLACE: src may be overwritten (A u alone): after the x stage has read a thread's own line, the
 // z-face arrays after Mhat_x go there (4 < n entries per line) and FA shrinks to 8 C n^2
+// W (optional): the y / z neighbour lines prefetched by nbr_lines_prefetch
 template <int N, int NTH, bool GEN, bool INPLACE = false, class Out>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g, const double* src,
-                                            double* SA, double* SB, double* FA, Out out) {
+                                            double* SA, double* SB, double* FA, Out out,
+                                            const NbrLines<N>* W = nullptr) {
   using G = Geo<N>;
   constexpr int N2 = G::N2, C = G::C;
   static_assert(G::LINES <= NTH, "one x-line per thread");
@@ -492,7 +535,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
       double s0 = 0.0, t0 = 0.0, s1 = 0.0, t1 = 0.0;
       if (nlo) {
         double w[N];
-        ld<N, N>(nlo + goff, w);
+        if (W) {
+#pragma unroll
+          for (int e = 0; e < N; ++e) w[e] = W->w[0][e];
+        } else {
+          ld<N, N>(nlo + goff, w);
+        }
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
@@ -501,7 +549,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
       }
       if (nhi) {
         double w[N];
-        ld<N, N>(nhi + goff, w);
+        if (W) {
+#pragma unroll
+          for (int e = 0; e < N; ++e) w[e] = W->w[1][e];
+        } else {
+          ld<N, N>(nhi + goff, w);
+        }
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
@@ -522,11 +575,16 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
       if (nlo) {
         double av, gn = 0.0;
         if (ghost_trace(kp, g.cell[cs], 0)) {
-          av = nlo[goff];
-          gn = nlo[N2 + goff];
+          av = W ? W->w[2][0] : nlo[goff];
+          gn = W ? W->w[2][1] : nlo[N2 + goff];
         } else {
           double w[N];
-          ld<N, N2>(nlo + goff, w);
+          if (W) {
+#pragma unroll
+            for (int e = 0; e < N; ++e) w[e] = W->w[2][e];
+          } else {
+            ld<N, N2>(nlo + goff, w);
+          }
 #pragma unroll
           for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
           av = w[N - 1];
@@ -537,11 +595,16 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g
       if (nhi) {
         double av, gn = 0.0;
         if (ghost_trace(kp, g.cell[cs], 1)) {
-          av = nhi[goff];
-          gn = nhi[N2 + goff];
+          av = W ? W->w[3][0] : nhi[goff];
+          gn = W ? W->w[3][1] : nhi[N2 + goff];
         } else {
           double w[N];
-          ld<N, N2>(nhi + goff, w);
+          if (W) {
+#pragma unroll
+            for (int e = 0; e < N; ++e) w[e] = W->w[3][e];
+          } else {
+            ld<N, N2>(nhi + goff, w);
+          }
 #pragma unroll
           for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
           av = w[0];
@@ -1131,6 +1194,12 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 // The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
 // lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
 // before the first read of u).
+#ifndef DG_APPLY_NBR_PREFETCH
+// bit n: the nodal apply at n prefetches the neighbours' face lines (p = 6: 221 -> 200 us; at
+// n = 5, 6, 8 the registers held across the setup cost more occupancy than they save: C3
+// 596 -> 635 us with 4 CTAs per SM, 685 us with spills at 5; p = 5 136 -> 142; p = 7 142 -> 161)
+#define DG_APPLY_NBR_PREFETCH 0x80
+#endif
 #ifndef DG_APPLY_INPLACE
 #define DG_APPLY_INPLACE 1   // nodal A u: z-face arrays in the consumed tile (8 C n^2 face buffer)
 #endif
@@ -1157,10 +1226,16 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
   // the tile copy is in flight while the setup's coefficient loads wait
   asm volatile("griddepcontrol.wait;" ::: "memory");
   async_tile<N>(SRC, u + (size_t)cell0 * G::N3, nvalid);
-  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
 #endif
   // A u (faces, not the D_T hook) in the nodal Kronecker-sum form
   constexpr bool NODAL = DG_NODAL_APPLY && FACES && !USEB;
+  // the neighbours' face lines in flight together with the setup's coefficient loads
+  constexpr bool PRE = NODAL && ((DG_APPLY_NBR_PREFETCH >> N) & 1);
+  NbrLines<N> W;
+  if constexpr (PRE) nbr_lines_prefetch<N>(kp, with_nbr ? u : nullptr, cell0, W);
+#if !DG_APPLY_SETUP_FIRST
+  group_setup<N>(kp, g, cell0, with_nbr ? u : nullptr);  // ends with __syncthreads
+#endif
   if constexpr (USEB) self_face_ops<N>(kp, g);
   lcp_wait_all();
   __syncthreads();
@@ -1168,7 +1243,7 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
   if constexpr (NODAL) {
     apply_nodal<N, Geo<N>::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
       if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, w);
-    });
+    }, PRE ? &W : nullptr);
     return;
   }
   cell_operator<N, FACES, USEB, false, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
