@@ -84,9 +84,10 @@ template <> struct Cells<6> { static constexpr int C = 4; };
 template <> struct Cells<7> { static constexpr int C = 4; };
 template <> struct Cells<8> { static constexpr int C = 2; };
 
-template <int N_> struct Geo {
+// C_: cells per CTA (Cells<N>::C; the warp-per-cell solvers can run one cell per CTA)
+template <int N_, int C_ = Cells<N_>::C> struct Geo {
   static constexpr int N = N_, N2 = N * N, N3 = N * N * N;
-  static constexpr int C = Cells<N>::C;
+  static constexpr int C = C_;
   static constexpr int YS = Lay<N>::YS, ZS = Lay<N>::ZS, CS = Lay<N>::CS;
   static constexpr int LINES = C * N2;
   static constexpr int NT = ((LINES + 31) / 32) * 32;
@@ -98,13 +99,15 @@ template <int N_> struct Geo {
 };
 
 // the solvers' face buffer fits in two tensors (it then aliases two the defect does not use)
-template <int N> __host__ __device__ constexpr bool fb_alias() { return 2 * Geo<N>::TENSOR >= Geo<N>::FACE; }
+template <int N, int CC = Cells<N>::C> __host__ __device__ constexpr bool fb_alias() {
+  return 2 * Geo<N, CC>::TENSOR >= Geo<N, CC>::FACE;
+}
 
 // The leading members of Group (coefficients, face data, neighbour pointers, 1D rows): all the
 // nodal apply uses, without the solvers' reduction and operator arrays (less static shared
 // memory, one more resident CTA per SM at n = 5)
-template <int N> struct GroupHead {
-  static constexpr int C = Cells<N>::C;
+template <int N, int C_ = Cells<N>::C> struct GroupHead {
+  static constexpr int C = C_;
   int cell[C];
   double vc[C][4];
   double vb[C][3];
@@ -112,8 +115,8 @@ template <int N> struct GroupHead {
   const double* nb[C][6];
   double tw[N], td0[N], td1[N];
 };
-template <int N> struct Group {
-  static constexpr int C = Cells<N>::C;
+template <int N, int C_ = Cells<N>::C> struct Group {
+  static constexpr int C = C_;
   int cell[C];
   double vc[C][4];              // |T|K_x/h_x^2, |T|K_y/h_y^2, |T|K_z/h_z^2, |T|c
   double vb[C][3];              // |T| b_k / h_k (the cell's advection)
@@ -229,8 +232,8 @@ template <int N> __host__ __device__ constexpr bool fold_volume() { return (DG_F
 // (self faces: traces of a Gauss-value line u(s) = E_s.U, u'(s) = F_s.U, and the injection of
 // the value- and derivative-test fluxes into the weighted Gauss residual).
 // Needs g.fc, g.vc, g.vb; ends with a barrier.
-template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KParams& kp, Group<N>& g) {
-  using G = Geo<N>;
+template <int N, int NTH = Geo<N>::NT, int CC> __device__ void self_face_ops(const KParams& kp, Group<N, CC>& g) {
+  using G = Geo<N, CC>;
   for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
     const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
     const int q = (rem % (N * N)) / N, r = rem % N;
@@ -246,8 +249,8 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
       t = fma(-g.vb[cs][a], c_tab[N].CG[q * N + r], t);
       if (a == 2 && q == r) t = fma(g.vc[cs][3], c_tab[N].w[q], t);
     }
-    g.Bf[cs][a][q * Group<N>::BR + r] = t;
-    if (r == N - 1 && (N & 1)) g.Bf[cs][a][q * Group<N>::BR + N] = 0.0;   // the pad
+    g.Bf[cs][a][q * Group<N, CC>::BR + r] = t;
+    if (r == N - 1 && (N & 1)) g.Bf[cs][a][q * Group<N, CC>::BR + N] = 0.0;   // the pad
   }
   __syncthreads();
 }
@@ -259,8 +262,8 @@ template <int N, int NTH = Geo<N>::NT> __device__ void self_face_ops(const KPara
 //   K_a = |T|K_a/h_a^2 Shat - |T|b_a/h_a Chat + [a = z] |T| c Mhat
 //       + |F_a| (e0 (s_a e0' + s_g/h d0') + t_a d0 e0' + e1 (.. hi ..))       (self faces)
 // i.e. A^T Bf_a A of the Gauss-point line operators. Stored in g.Bf (rows of stride BR).
-template <int N, int NTH = Geo<N>::NT> __device__ void nodal_face_ops(const KParams& kp, Group<N>& g) {
-  using G = Geo<N>;
+template <int N, int NTH = Geo<N>::NT, int CC> __device__ void nodal_face_ops(const KParams& kp, Group<N, CC>& g) {
+  using G = Geo<N, CC>;
   for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
     const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
     const int i = (rem % (N * N)) / N, ip = rem % N;
@@ -275,8 +278,8 @@ template <int N, int NTH = Geo<N>::NT> __device__ void nodal_face_ops(const KPar
     t = fma(g.vc[cs][a], c_tab[N].S[i * N + ip], t);
     t = fma(-g.vb[cs][a], c_tab[N].Cm[i * N + ip], t);
     if (a == 2) t = fma(g.vc[cs][3], c_tab[N].M[i * N + ip], t);
-    g.Bf[cs][a][i * Group<N>::BR + ip] = t;
-    if (ip == N - 1 && (N & 1)) g.Bf[cs][a][i * Group<N>::BR + N] = 0.0;
+    g.Bf[cs][a][i * Group<N, CC>::BR + ip] = t;
+    if (ip == N - 1 && (N & 1)) g.Bf[cs][a][i * Group<N, CC>::BR + N] = 0.0;
   }
   __syncthreads();
 }
@@ -346,10 +349,10 @@ __device__ __forceinline__ void kfly(const KParams& kp, const CB& g, int cs, int
 // x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
 // q = Mhat g + Kz d -> back to the thread's x-line. 7 one-direction contractions and 3 transposes
 // (the Gauss-point form: 9 contractions, 6 transposes). pin: the thread's x-line of p.
-template <int N, bool WARP, bool FLY = false, bool GEN = true>
-__device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* SB, const double* pin,
+template <int N, bool WARP, bool FLY = false, bool GEN = true, int CC>
+__device__ __forceinline__ void dt_nodal(const Group<N, CC>& g, double* SA, double* SB, const double* pin,
                                          double* q, const KParams* kpp = nullptr) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int N2 = G::N2;
   const int tid = threadIdx.x;
   const int cs = WARP ? tid >> 5 : tid / N2, l = WARP ? (tid & 31) : tid % N2;
@@ -402,10 +405,10 @@ __device__ __forceinline__ void dt_nodal(const Group<N>& g, double* SA, double* 
 
 // dst = D_T src in the nodal form for tensors in shared memory (CS layout), one x-line per thread
 // (WARP: the warp's own cell); the callers synchronise around it
-template <int N, bool WARP>
-__device__ __forceinline__ void dt_nodal_smem(const Group<N>& g, double* SA, double* SB, const double* src,
+template <int N, bool WARP, int CC>
+__device__ __forceinline__ void dt_nodal_smem(const Group<N, CC>& g, double* SA, double* SB, const double* src,
                                               double* dst) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   const int tid = threadIdx.x;
   const int cs = WARP ? tid >> 5 : tid / G::N2, l = WARP ? (tid & 31) : tid % G::N2;
   const bool act = WARP ? l < G::N2 : tid < G::LINES;
@@ -475,11 +478,11 @@ __device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const doub
 // INPLACE: src may be overwritten (A u alone): after the x stage has read a thread's own line, the
 // z-face arrays after Mhat_x go there (4 < n entries per line) and FA shrinks to 8 C n^2
 // W (optional): the y / z neighbour lines prefetched by nbr_lines_prefetch
-template <int N, int NTH, bool GEN, bool INPLACE = false, class Out>
-__device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N>& g, const double* src,
+template <int N, int NTH, bool GEN, bool INPLACE = false, class Out, int CC>
+__device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out,
                                             const NbrLines<N>* W = nullptr) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int N2 = G::N2, C = G::C;
   static_assert(G::LINES <= NTH, "one x-line per thread");
   const int t = threadIdx.x;
@@ -796,9 +799,9 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*vb_)[3
   __syncthreads();
 }
 
-template <int N, int NTH = Geo<N>::NT>
-__device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const double* u) {
-  using G = Geo<N>;
+template <int N, int NTH = Geo<N>::NT, int CC>
+__device__ void group_setup(const KParams& kp, Group<N, CC>& g, int cell0, const double* u) {
+  using G = Geo<N, CC>;
   const int t = threadIdx.x;
   if (t < N) {
     g.tw[t] = c_tab[N].w[t];
@@ -809,10 +812,10 @@ __device__ void group_setup(const KParams& kp, Group<N>& g, int cell0, const dou
 }
 
 // ---- tiles ---------------------------------------------------------------------
-template <int N, int NTH = Geo<N>::NT>
-__device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncells,
+template <int N, int NTH = Geo<N>::NT, int CC>
+__device__ __forceinline__ void load_tile(const Group<N, CC>& g, int cell0, int ncells,
                                           const double* __restrict__ src, double* dst) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   const int nvalid = min(G::C, ncells - cell0);
   const double* s = src + (size_t)cell0 * G::N3;
   for (int e = threadIdx.x; e < G::C * G::N3; e += NTH) {
@@ -829,12 +832,12 @@ __device__ __forceinline__ void load_tile(const Group<N>& g, int cell0, int ncel
 // value and end derivative. hlo / hhi: the neighbour exists (interior or ghost-layer face).
 // tlo / thi: the neighbour is a ghost-layer trace record: w[0] is its face value and w[1] its
 // normal-derivative sum (the sender's arithmetic, bit for bit the value computed here otherwise).
-template <int N, int AX>
-__device__ __forceinline__ void face_line(const Group<N>& g, const double* src, double* FB,
+template <int N, int AX, int CC>
+__device__ __forceinline__ void face_line(const Group<N, CC>& g, const double* src, double* FB,
                                           int cs, int a, int b, double inv_h, const double* wlo,
                                           const double* whi, bool hlo, bool hhi, bool tlo = false,
                                           bool thi = false) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   int off;
   constexpr int SS = AX == 0 ? 1 : (AX == 1 ? G::YS : G::ZS);   // smem stride along the line
   if (AX == 0) off = b * G::ZS + a * G::YS;
@@ -894,14 +897,14 @@ __device__ __forceinline__ void face_line(const Group<N>& g, const double* src, 
 // plus the self-face terms through g.Bf inside the Gauss-point passes (D_T without face passes)
 // GEN = false: pure diffusion (b = 0, no reaction) with the convective and reaction terms compiled out
 template <int N, bool FACES = true, bool USEB = false, bool WARP = false, int NTH = Geo<N>::NT,
-          bool GEN = true, class Out>
-__device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>& g,
+          bool GEN = true, class Out, int CC>
+__device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N, CC>& g,
                                               const double* src, double* SA, double* SB,
                                               double* FB, bool vol, Out out,
                                               const double* pin = nullptr) {
   // pin (warp mode, one line per lane): the lane's own x-line of the input, from registers
   // instead of src
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int C = G::C, N2 = G::N2, LINES = G::LINES, NT = NTH;   // NTH: the launch's thread count
   const int tid = threadIdx.x;
   static_assert(!WARP || !FACES, "warp mode: one cell per warp, no face passes");
@@ -1111,9 +1114,9 @@ __device__ __forceinline__ void cell_operator(const KParams& kp, const Group<N>&
 }
 
 // ---- diag(D_T) from 1D diagonals (Jacobi preconditioner) --------------
-template <int N, int NTH = Geo<N>::NT>
-__device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
-  using G = Geo<N>;
+template <int N, int NTH = Geo<N>::NT, int CC>
+__device__ void diag_setup(const KParams& kp, const Group<N, CC>& g, double* Dg) {
+  using G = Geo<N, CC>;
   const double area[3] = {kp.h[1] * kp.h[2], kp.h[0] * kp.h[2], kp.h[0] * kp.h[1]};
   for (int e = threadIdx.x; e < G::C * G::N3; e += NTH) {
     const int cs = e / G::N3, r = e % G::N3;
@@ -1152,8 +1155,8 @@ __device__ void diag_setup(const KParams& kp, const Group<N>& g, double* Dg) {
 }
 
 // per-cell sum of the per-line partials red[q][cs*N2 + l] -> result[q][cs]
-template <int N>
-__device__ __forceinline__ double cell_sum(const Group<N>& g, int q, int cs) {
+template <int N, int CC>
+__device__ __forceinline__ double cell_sum(const Group<N, CC>& g, int q, int cs) {
   constexpr int N2 = N * N;
   double s = 0.0;
   for (int l = 0; l < N2; ++l) s += g.red[q][cs * N2 + l];
@@ -1194,6 +1197,9 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 // The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
 // lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
 // before the first read of u).
+#ifndef DG_CGW_CELLS
+#define DG_CGW_CELLS 1   // cells per CTA of the warp-per-cell CG at n = 5
+#endif
 #ifndef DG_APPLY_NBR_PREFETCH
 // bit n: the nodal apply at n prefetches the neighbours' face lines (p = 6: 221 -> 200 us; at
 // n = 5, 6, 8 the registers held across the setup cost more occupancy than they save: C3
@@ -1453,14 +1459,17 @@ __device__ __forceinline__ double warp_sum(double v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-template <int N, bool SWEEP, bool GEN = true>
-__global__ void __launch_bounds__(Geo<N>::NTW, 2)
+// CC: cells (warps) per CTA. A CTA holds its registers until its slowest cell has converged, so
+// with CC = 8 the warp slots of the early finishers idle (local iterations vary +-12 %, up to 1.8x
+// the mean); CC = 1 releases each cell's slot as soon as that cell is done.
+template <int N, bool SWEEP, bool GEN = true, int CC = Cells<N>::C>
+__global__ void __launch_bounds__(Geo<N, CC>::NTW, (CC > 1 ? 2 : 0))
 k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
        double* __restrict__ out) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int C = G::C;
   extern __shared__ double sm[];
-  __shared__ Group<N> g;
+  __shared__ Group<N, CC> g;
   double* X = sm;
   double* R = X + G::TENSOR;
   double* P = R + G::TENSOR;
@@ -1468,7 +1477,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   double* Dg = Q + G::TENSOR;
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
-  double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
+  double* FB = fb_alias<N, CC>() ? Q : SB + G::TENSOR;
   const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
@@ -1544,7 +1553,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
       if constexpr (NODAL) {
         dt_nodal<N, true, DG_NODAL_FLY, GEN>(g, SA, SB, p, q, &kq);
       } else {
-        cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true,
+        cell_operator<N, false, true, true, G::NT, GEN>(kq, g, P, SA, SB, FB, true,
                                                              [&](int, int, int, const double* v) {
 #pragma unroll
           for (int e = 0; e < N; ++e) q[e] = v[e];
@@ -1581,7 +1590,7 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   } else {
   for (int iter = 0; !conv && iter < kp.max_it; ++iter) {   // conv is warp-uniform
     __syncwarp();
-    cell_operator<N, false, true, true, Geo<N>::NT, GEN>(kq, g, P, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+    cell_operator<N, false, true, true, G::NT, GEN>(kq, g, P, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
       st<N, 1>(Q + c * G::CS + k * G::ZS + j * G::YS, v);
     });
     __syncwarp();
@@ -2372,10 +2381,22 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
       }
     }
   }
+  if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
+  if constexpr (N == 5 && DG_CGW_CELLS != Cells<N>::C) {
+    // warp-per-cell CG with DG_CGW_CELLS cells per CTA (its own group size, hence its own split)
+    if (method == LM_CG && !(kp.variant & VAR_LINE_CG_CTA)) {
+      constexpr int CC = DG_CGW_CELLS;
+      using G1 = Geo<N, CC>;
+      const int grid1 = split_groups(kp, CC);
+      if (grid1 == 0) return cudaSuccess;
+      const size_t sm1 = sizeof(double) * (7 * (size_t)G1::TENSOR + (fb_alias<N, CC>() ? 0 : (size_t)G1::FACE));
+      return launch(gen_terms(kp) ? k_cg_w<N, SWEEP, true, CC> : k_cg_w<N, SWEEP, false, CC>, grid1, G1::NTW,
+                    sm1, s, kp, in, f, out);
+    }
+  }
   using G = Geo<N>;
   const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
-  if (method == LM_BICGSTAB_THOMAS) return cudaErrorInvalidValue;   // plane kernels (p <= 4) only
   // line solvers per degree (measured after the D_T fold and the register-resident CTA CG,
   // profiles/r02_ab.md): CG one warp per cell at n = 5, CTA-wide at n = 6..8; BiCGStab one warp
   // per cell at n = 5 and 7, CTA-wide at n = 6 and 8; VAR_LINE_CG_CTA selects the other kernel
