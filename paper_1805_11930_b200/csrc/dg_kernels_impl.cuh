@@ -1197,6 +1197,23 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 // The own tile is staged with cp.async while the face setup runs; programmatic dependent launch
 // lets the setup (coefficients only) overlap the previous kernel's tail (griddepcontrol.wait
 // before the first read of u).
+// cells per CTA of the CTA-wide line CG at n = 6, 7, 8 (the group size Cells<N>::C = 4, 4, 2 of
+// the other line kernels). Fewer cells: a CTA runs until its slowest cell has converged, so small
+// groups idle less; at n = 6 one cell leaves 28 of 64 threads without a line. Poisson sweeps
+// (~8M DoF): n = 6 2413 (4 cells) / 2091 (3) / 1985 (2) / 2465 us (1); n = 7 3568 (4) / 3814
+// (2) / 3519 us (1); n = 8 3806 (2) / 3479 us (1)
+#ifndef DG_CG_CELLS6
+#define DG_CG_CELLS6 2
+#endif
+#ifndef DG_CG_CELLS7
+#define DG_CG_CELLS7 1
+#endif
+#ifndef DG_CG_CELLS8
+#define DG_CG_CELLS8 1
+#endif
+template <int N> constexpr int line_cg_cells() {
+  return N == 6 ? DG_CG_CELLS6 : (N == 7 ? DG_CG_CELLS7 : (N == 8 ? DG_CG_CELLS8 : Cells<N>::C));
+}
 #ifndef DG_CGW_CELLS
 #define DG_CGW_CELLS 1   // cells per CTA of the warp-per-cell CG at n = 5
 #endif
@@ -1280,14 +1297,14 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
 
 // Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
 // SWEEP: in = u (defect d = f - A u formed first), result u + omega du; else in = d, result du.
-template <int N, bool SWEEP>
-__global__ void __launch_bounds__(Geo<N>::NT, 2)   // two CTAs per SM (n = 7: <= 146 registers)
+template <int N, bool SWEEP, int CC = Cells<N>::C>
+__global__ void __launch_bounds__(Geo<N, CC>::NT, (CC == Cells<N>::C ? 2 : 0))   // two CTAs per SM (n = 7: <= 146 registers)
 k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
      double* __restrict__ out) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int C = G::C;
   extern __shared__ double sm[];
-  __shared__ Group<N> g;
+  __shared__ Group<N, CC> g;
   double* X = sm;
   double* R = X + G::TENSOR;
   double* P = R + G::TENSOR;
@@ -1297,16 +1314,16 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
   double* SB = SA + G::TENSOR;
   // the face buffer is only used by the defect (the loop's D_T takes the self faces through
   // g.Bf), before Q and Dg are: it aliases them when it fits
-  double* FB = fb_alias<N>() ? Q : SB + G::TENSOR;
+  double* FB = fb_alias<N, CC>() ? Q : SB + G::TENSOR;
   const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
-  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  load_tile<N, G::NT>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
-  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  group_setup<N, G::NT>(kq, g, cell0, SWEEP ? in : nullptr);
   constexpr bool NODAL = DG_NODAL_DT;   // D_T of the iterations in the nodal Kronecker-sum form
-  if constexpr (NODAL) nodal_face_ops<N>(kq, g);
-  else self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
+  if constexpr (NODAL) nodal_face_ops<N, G::NT>(kq, g);
+  else self_face_ops<N, G::NT>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {  // d = f - A u  (Alg. 2 line 2)
     const double* fb = f + (size_t)cell0 * G::N3;
     auto defect = [&](int cs, int j, int k, const double* v) {
@@ -1319,12 +1336,12 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     };
     // d = f - A u: nodal form at n <= 6 (n = 7, 8: the Gauss-point passes measured faster)
     if constexpr (DG_NODAL_APPLY && N <= 6) apply_nodal<N, G::NT, true>(kq, g, P, SA, SB, FB, defect);
-    else cell_operator<N>(kq, g, P, SA, SB, FB, true, defect);
+    else cell_operator<N, true, false, false, G::NT>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     // D_T uses self faces only
     for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
   }
-  diag_setup<N>(kp, g, Dg);
+  diag_setup<N, G::NT>(kp, g, Dg);
   __syncthreads();
   // Each thread owns one x-line of the group (LINES <= NT): the operator's first pass reads that
   // line of p and its last pass produces that line of q = D_T p, so r, p, x and diag(D_T)^-1 stay
@@ -1365,7 +1382,7 @@ k_cg(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
     if constexpr (NODAL) {
       dt_nodal<N, false, DG_NODAL_FLY, true>(g, SA, SB, p, q, &kq);
     } else {
-      cell_operator<N, false, true>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
+      cell_operator<N, false, true, false, G::NT>(kq, g, P, SA, SB, FB, true, [&](int, int, int, const double* v) {
 #pragma unroll
         for (int e = 0; e < N; ++e) q[e] = v[e];
       }, p);
@@ -2392,6 +2409,17 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
       const size_t sm1 = sizeof(double) * (7 * (size_t)G1::TENSOR + (fb_alias<N, CC>() ? 0 : (size_t)G1::FACE));
       return launch(gen_terms(kp) ? k_cg_w<N, SWEEP, true, CC> : k_cg_w<N, SWEEP, false, CC>, grid1, G1::NTW,
                     sm1, s, kp, in, f, out);
+    }
+  }
+  if constexpr (N >= 6 && line_cg_cells<N>() != Cells<N>::C) {
+    // CTA-wide CG with its own group size (hence its own split), n >= 6
+    if (method == LM_CG && !(N <= 7 && (kp.variant & VAR_LINE_CG_CTA))) {
+      constexpr int CC = line_cg_cells<N>();
+      using G1 = Geo<N, CC>;
+      const int grid1 = split_groups(kp, CC);
+      if (grid1 == 0) return cudaSuccess;
+      const size_t sm1 = sizeof(double) * (7 * (size_t)G1::TENSOR + (fb_alias<N, CC>() ? 0 : (size_t)G1::FACE));
+      return launch(k_cg<N, SWEEP, CC>, grid1, G1::NT, sm1, s, kp, in, f, out);
     }
   }
   using G = Geo<N>;
