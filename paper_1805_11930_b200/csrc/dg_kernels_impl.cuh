@@ -1214,6 +1214,17 @@ __device__ __forceinline__ void async_tile(double* dst, const double* src, int n
 template <int N> constexpr int line_cg_cells() {
   return N == 6 ? DG_CG_CELLS6 : (N == 7 ? DG_CG_CELLS7 : (N == 8 ? DG_CG_CELLS8 : Cells<N>::C));
 }
+// cells per CTA of the warp-per-cell BiCGStab at n = 5, 7 (convection sweeps, ~8M DoF: n = 5
+// 2834 (8 cells) / 2807 (2) / 2795 us (1); n = 7 8282 (4) / 6874 (2) / 7809 us (1))
+#ifndef DG_BICGW_CELLS5
+#define DG_BICGW_CELLS5 1
+#endif
+#ifndef DG_BICGW_CELLS7
+#define DG_BICGW_CELLS7 2
+#endif
+template <int N> constexpr int bicgw_cells() {
+  return N == 5 ? DG_BICGW_CELLS5 : (N == 7 ? DG_BICGW_CELLS7 : Cells<N>::C);
+}
 #ifndef DG_CGW_CELLS
 #define DG_CGW_CELLS 1   // cells per CTA of the warp-per-cell CG at n = 5
 #endif
@@ -1684,14 +1695,14 @@ k_cg_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
 
 // Jacobi right-preconditioned BiCGStab with one warp per cell (n = 5), the same scheme as k_cg_w:
 // CTA-wide setup and defect, warp-local iterations without CTA barriers.
-template <int N, bool SWEEP>
-__global__ void __launch_bounds__(Geo<N>::NTW, 2)
+template <int N, bool SWEEP, int CC = Cells<N>::C>
+__global__ void __launch_bounds__(Geo<N, CC>::NTW, (CC == Cells<N>::C ? 2 : 0))
 k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
              double* __restrict__ out) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int C = G::C;
   extern __shared__ double sm[];
-  __shared__ Group<N> g;
+  __shared__ Group<N, CC> g;
   double* X = sm;
   double* R = X + G::TENSOR;
   double* RH = R + G::TENSOR;
@@ -1702,7 +1713,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   double* Dg = T + G::TENSOR;
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
-  double* FB = fb_alias<N>() ? T : SB + G::TENSOR;
+  double* FB = fb_alias<N, CC>() ? T : SB + G::TENSOR;
   const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
@@ -1714,14 +1725,16 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
   else self_face_ops<N, G::NTW>(kq, g);
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
-    cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+    auto defect = [&](int cs, int j, int k, const double* v) {
       double fl[N] = {};
       if (cs < nvalid) ld<N, 1>(fb + cs * G::N3 + k * G::N2 + j * N, fl);
       double r[N];
 #pragma unroll
       for (int e = 0; e < N; ++e) r[e] = (cs < nvalid) ? fl[e] - v[e] : 0.0;
       st<N, 1>(R + cs * G::CS + k * G::ZS + j * G::YS, r);
-    });
+    };
+    if constexpr (DG_NODAL_APPLY && G::LINES <= G::NTW) apply_nodal<N, G::NTW, true>(kq, g, P, SA, SB, FB, defect);
+    else cell_operator<N, true, false, false, G::NTW>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     for (int it = tid; it < C * 6; it += G::NTW) g.nb[it / 6][it % 6] = nullptr;
   }
@@ -1742,7 +1755,7 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
     if constexpr (NODAL) {
       dt_nodal_smem<N, true>(g, SA, SB, PS, dst);
     } else {
-      cell_operator<N, false, true, true>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
+      cell_operator<N, false, true, true, G::NT>(kq, g, PS, SA, SB, FB, true, [&](int c, int j, int k, const double* v) {
         st<N, 1>(dst + c * G::CS + k * G::ZS + j * G::YS, v);
       });
     }
@@ -2178,6 +2191,7 @@ template <class K> cudaError_t set_smem(K kernel, size_t smem) {
 template <class K>
 cudaError_t launch(K kernel, int grid, int block, size_t smem, cudaStream_t s, const KParams& kp,
                    const double* a, const double* b, double* c) {
+  if (grid <= 0) return cudaSuccess;   // an empty split launch (no interior / boundary groups)
   cudaError_t e = set_smem(kernel, smem);
   if (e != cudaSuccess) return e;
   kernel<<<grid, block, smem, s>>>(kp, a, b, c);
@@ -2422,18 +2436,27 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
       return launch(k_cg<N, SWEEP, CC>, grid1, G1::NT, sm1, s, kp, in, f, out);
     }
   }
+  // (each kernel below has its own group size and split; launch() skips an empty grid)
   using G = Geo<N>;
   const int grid = split_groups(kp, G::C);
-  if (grid == 0) return cudaSuccess;
   // line solvers per degree (measured after the D_T fold and the register-resident CTA CG,
   // profiles/r02_ab.md): CG one warp per cell at n = 5, CTA-wide at n = 6..8; BiCGStab one warp
   // per cell at n = 5 and 7, CTA-wide at n = 6 and 8; VAR_LINE_CG_CTA selects the other kernel
   constexpr bool warp_cg = N == 5, warp_bicg = N == 5 || N == 7;
   if constexpr (N >= 5 && N <= 7) {
     const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_bicg;
-    if (method == LM_BICGSTAB && !cta)
+    if (method == LM_BICGSTAB && !cta) {
+      if constexpr (bicgw_cells<N>() != Cells<N>::C) {   // its own group size, hence its own split
+        constexpr int CC = bicgw_cells<N>();
+        using G1 = Geo<N, CC>;
+        const int grid1 = split_groups(kp, CC);
+        if (grid1 == 0) return cudaSuccess;
+        const size_t sm1 = sizeof(double) * (10 * (size_t)G1::TENSOR + (fb_alias<N, CC>() ? 0 : (size_t)G1::FACE));
+        return launch(k_bicgstab_w<N, SWEEP, CC>, grid1, G1::NTW, sm1, s, kp, in, f, out);
+      }
       return launch(k_bicgstab_w<N, SWEEP>, grid, G::NTW,
                     fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
+    }
   }
   if (method == LM_BICGSTAB)
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
