@@ -1225,6 +1225,17 @@ template <int N> constexpr int line_cg_cells() {
 template <int N> constexpr int bicgw_cells() {
   return N == 5 ? DG_BICGW_CELLS5 : (N == 7 ? DG_BICGW_CELLS7 : Cells<N>::C);
 }
+// cells per CTA of the CTA-wide line BiCGStab at n = 6, 8 (Cells<N>::C = 4, 2); convection
+// sweeps, ~8M DoF: n = 6 4115 (4 cells) / 4537 (3) / 3881 (2) / 4487 us (1); n = 8 5520 (2) / 5270 us (1)
+#ifndef DG_BICG_CELLS6
+#define DG_BICG_CELLS6 2
+#endif
+#ifndef DG_BICG_CELLS8
+#define DG_BICG_CELLS8 1
+#endif
+template <int N> constexpr int bicg_cells() {
+  return N == 6 ? DG_BICG_CELLS6 : (N == 8 ? DG_BICG_CELLS8 : Cells<N>::C);
+}
 #ifndef DG_CGW_CELLS
 #define DG_CGW_CELLS 1   // cells per CTA of the warp-per-cell CG at n = 5
 #endif
@@ -1914,14 +1925,14 @@ k_bicgstab_w(KParams kp, const double* __restrict__ in, const double* __restrict
 }
 
 // Jacobi right-preconditioned BiCGStab per cell (nonsymmetric blocks, b != 0).
-template <int N, bool SWEEP>
-__global__ void __launch_bounds__(Geo<N>::NT, 2)   // two CTAs per SM (n = 7: <= 146 registers)
+template <int N, bool SWEEP, int CC = Cells<N>::C>
+__global__ void __launch_bounds__(Geo<N, CC>::NT, (CC == Cells<N>::C ? 2 : 0))   // two CTAs per SM (n = 7: <= 146 registers)
 k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__ f,
            double* __restrict__ out) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int C = G::C;
   extern __shared__ double sm[];
-  __shared__ Group<N> g;
+  __shared__ Group<N, CC> g;
   double* X = sm;
   double* R = X + G::TENSOR;
   double* RH = R + G::TENSOR;
@@ -1932,16 +1943,16 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
   double* Dg = T + G::TENSOR;
   double* SA = Dg + G::TENSOR;
   double* SB = SA + G::TENSOR;
-  double* FB = fb_alias<N>() ? T : SB + G::TENSOR;   // defect only: aliases T and Dg when it fits
+  double* FB = fb_alias<N, CC>() ? T : SB + G::TENSOR;   // defect only: aliases T and Dg when it fits
   const int cell0 = block_group(kp, false) * G::C;
   const int nvalid = min(C, kp.ncells - cell0);
   const int tid = threadIdx.x;
-  load_tile<N>(g, cell0, kp.ncells, in, SWEEP ? P : R);
+  load_tile<N, G::NT>(g, cell0, kp.ncells, in, SWEEP ? P : R);
   const KParams& kq = kp;   // launched with mask = 7 (launch_local_solve / launch_sweep)
-  group_setup<N>(kq, g, cell0, SWEEP ? in : nullptr);
+  group_setup<N, G::NT>(kq, g, cell0, SWEEP ? in : nullptr);
   constexpr bool NODAL = DG_NODAL_DT;   // D_T of the iterations in the nodal form
-  if constexpr (NODAL) nodal_face_ops<N>(kq, g);
-  else self_face_ops<N>(kq, g);   // D_T in the loop: self faces at the Gauss points
+  if constexpr (NODAL) nodal_face_ops<N, G::NT>(kq, g);
+  else self_face_ops<N, G::NT>(kq, g);   // D_T in the loop: self faces at the Gauss points
   if (SWEEP) {
     const double* fb = f + (size_t)cell0 * G::N3;
     auto defect = [&](int cs, int j, int k, const double* v) {
@@ -1954,11 +1965,11 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     };
     // d = f - A u: nodal form at n <= 6 (n = 7, 8: the Gauss-point passes measured faster)
     if constexpr (DG_NODAL_APPLY && N <= 6) apply_nodal<N, G::NT, true>(kq, g, P, SA, SB, FB, defect);
-    else cell_operator<N>(kq, g, P, SA, SB, FB, true, defect);
+    else cell_operator<N, true, false, false, G::NT>(kq, g, P, SA, SB, FB, true, defect);
     __syncthreads();
     for (int it = tid; it < C * 6; it += G::NT) g.nb[it / 6][it % 6] = nullptr;
   }
-  diag_setup<N>(kp, g, Dg);
+  diag_setup<N, G::NT>(kp, g, Dg);
   __syncthreads();
   DG_FOR_XLINES({
     double r[N], zero[N] = {};
@@ -2033,7 +2044,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     if constexpr (NODAL) {
       dt_nodal_smem<N, false>(g, SA, SB, PS, V);
     } else {
-      cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      cell_operator<N, false, true, false, G::NT>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
         st<N, 1>(V + cs * G::CS + k * G::ZS + j * G::YS, v);
       });
     }
@@ -2094,7 +2105,7 @@ k_bicgstab(KParams kp, const double* __restrict__ in, const double* __restrict__
     if constexpr (NODAL) {
       dt_nodal_smem<N, false>(g, SA, SB, PS, T);
     } else {
-      cell_operator<N, false, true>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
+      cell_operator<N, false, true, false, G::NT>(kq, g, PS, SA, SB, FB, true, [&](int cs, int j, int k, const double* v) {
         st<N, 1>(T + cs * G::CS + k * G::ZS + j * G::YS, v);
       });
     }
@@ -2458,9 +2469,17 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
                     fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
     }
   }
-  if (method == LM_BICGSTAB)
+  if (method == LM_BICGSTAB) {
+    if constexpr (bicg_cells<N>() != Cells<N>::C) {   // its own group size, hence its own split
+      constexpr int CC = bicg_cells<N>();
+      using G1 = Geo<N, CC>;
+      const int grid1 = split_groups(kp, CC);
+      const size_t sm1 = sizeof(double) * (10 * (size_t)G1::TENSOR + (fb_alias<N, CC>() ? 0 : (size_t)G1::FACE));
+      return launch(k_bicgstab<N, SWEEP, CC>, grid1, G1::NT, sm1, s, kp, in, f, out);
+    }
     return launch(k_bicgstab<N, SWEEP>, grid, G::NT,
                   fb_alias<N>() ? sizeof(double) * 10 * (size_t)G::TENSOR : smem_bytes<N>(10), s, kp, in, f, out);
+  }
   if constexpr (N >= 5 && N <= 7) {   // n = 8: 255 registers with spills, the CTA version is faster
     const bool cta = ((kp.variant & VAR_LINE_CG_CTA) != 0) == warp_cg;
     if (!cta)
