@@ -1317,6 +1317,117 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
   }
 }
 
+// ---- the volume terms alone, lean line kernel (dg_apply_parts mask = volume, n >= 6) ----------
+// The passes and arithmetic of cell_operator<N, FACES = false> (stage 1: A_x, A_y, A_z to the
+// Gauss points; stage 2: reaction and the x / y / z direction terms at the Gauss points; stage 3:
+// the transposed contractions), bit for bit, without its instruction overhead (ncu,
+// p = 5: DFMA were 25 % of the issued instructions; the passes recomputed the line indices per
+// loop, the tile copy spent ~45 instructions per 8-byte cp.async): one x-line per thread, its
+// three line offsets and Gauss weight computed once, the cell's scalars in registers (loaded
+// before the dependency wait), its own x-line read from global memory straight into registers
+// and the result written from registers, so only the two work tensors live in shared memory.
+template <int N, bool GEN>
+__global__ void __launch_bounds__(Geo<N>::NT)
+k_volume_line(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
+  using G = Geo<N>;
+  constexpr int N2 = G::N2, N3 = G::N3, C = G::C;
+  static_assert(G::LINES <= G::NT, "one x-line per thread");
+  extern __shared__ double sm[];
+  double* SA = sm;
+  double* SB = SA + G::TENSOR;
+  const int t = threadIdx.x;
+  const int cell0 = block_group(kp, false) * C;
+  const bool act = t < G::LINES;
+  const int cs = act ? t / N2 : 0, l = t % N2, a = l % N, b = l / N;
+  const int ox = cs * G::CS + b * G::ZS + a * G::YS;   // x-line (j = a, k = b)
+  const int oy = cs * G::CS + b * G::ZS + a;           // y-line (i = a, k = b)
+  const int oz = cs * G::CS + b * G::YS + a;           // z-line (i = a, j = b)
+  const int cell = cell0 + cs;
+  const bool valid = act && cell < kp.ncells;
+  asm volatile("griddepcontrol.launch_dependents;");
+  // the cell's scalings (cell_operator: g.vc, g.vb from setup_cells), independent of u
+  double sK[3] = {0.0, 0.0, 0.0}, sb[3] = {0.0, 0.0, 0.0}, sc = 0.0;
+  if (valid) {
+    const int nxy = kp.nx * kp.ny;
+    const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+    const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) sK[d] = Kc[d] * vol * kp.ih[d] * kp.ih[d];
+    if constexpr (GEN) {
+      sc = kp.c ? vol * kp.c[cell] : 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        sb[d] = vol * (kp.bc ? kp.bc[(size_t)(cell + nxy) * 3 + d] : kp.b[d]) * kp.ih[d];
+    }
+  }
+  const double Wl = c_tab[N].w[a] * c_tab[N].w[b];   // (the same product in every pass)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  double v[N], o[N];
+  if (valid) {
+    ld<N, 1>(u + (size_t)cell * N3 + b * N2 + a * N, v);
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) v[e] = 0.0;
+  }
+  // pass 1: x-lines, SA = A_x u
+  if (act) {
+    mv<N, 0>(v, o);
+    st<N, 1>(SA + ox, o);
+  }
+  __syncthreads();
+  // pass 2: y-lines, SB = A_y SA
+  if (act) {
+    ld<N, G::YS>(SA + oy, v);
+    mv<N, 0>(v, o);
+    st<N, G::YS>(SB + oy, o);
+  }
+  __syncthreads();
+  // pass 3: z-lines, U = A_z SB -> SA, R = reaction + z-term -> SB
+  if (act) {
+    double U[N], R[N];
+    ld<N, G::ZS>(SB + oz, v);
+    mv<N, 0>(v, U);
+#pragma unroll
+    for (int q = 0; q < N; ++q) R[q] = GEN ? Wl * c_tab[N].w[q] * sc * U[q] : 0.0;
+    dir_term<N, GEN>(U, R, Wl, sK[2], GEN ? sb[2] : 0.0);
+    st<N, G::ZS>(SA + oz, U);
+    st<N, G::ZS>(SB + oz, R);
+  }
+  __syncthreads();
+  // pass 4: x-lines, R += x-term
+  if (act) {
+    double U[N], R[N];
+    ld<N, 1>(SA + ox, U);
+    ld<N, 1>(SB + ox, R);
+    dir_term<N, GEN>(U, R, Wl, sK[0], GEN ? sb[0] : 0.0);
+    st<N, 1>(SB + ox, R);
+  }
+  __syncthreads();
+  // pass 5: y-lines, R += y-term, then A_y^T
+  if (act) {
+    double U[N], R[N];
+    ld<N, G::YS>(SA + oy, U);
+    ld<N, G::YS>(SB + oy, R);
+    dir_term<N, GEN>(U, R, Wl, sK[1], GEN ? sb[1] : 0.0);
+    mtv<N, 0>(R, o);
+    st<N, G::YS>(SB + oy, o);
+  }
+  __syncthreads();
+  // pass 6: z-lines, A_z^T
+  if (act) {
+    ld<N, G::ZS>(SB + oz, v);
+    mtv<N, 0>(v, o);
+    st<N, G::ZS>(SB + oz, o);
+  }
+  __syncthreads();
+  // pass 7: x-lines, A_x^T, straight to global memory
+  if (valid) {
+    ld<N, 1>(SB + ox, v);
+    mtv<N, 0>(v, o);
+    st<N, 1>(out + (size_t)cell * N3 + b * N2 + a * N, o);
+  }
+}
+
 // Jacobi-preconditioned CG on every cell of the group (SPD blocks, b = 0).
 // SWEEP: in = u (defect d = f - A u formed first), result u + omega du; else in = d, result du.
 template <int N, bool SWEEP, int CC = Cells<N>::C>
@@ -2341,6 +2452,26 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   using G = Geo<N>;
   const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
+#ifndef DG_VOLUME_LINE_N
+#define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 81 -> 111 us, kept off)
+#endif
+  if (kp.mask == 1u && ((DG_VOLUME_LINE_N >> N) & 1)) {
+    const size_t smem = sizeof(double) * 2 * (size_t)G::TENSOR;
+    auto kv = gen_terms(kp) ? k_volume_line<N, true> : k_volume_line<N, false>;
+    cudaError_t e = set_smem(kv, smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(G::NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kv, kp, u, out, with_nbr);
+  }
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point
   // operators. Neither has face passes, so neither gets the face buffer (more resident CTAs)
   const bool nofb = kp.mask == 1u || (!with_nbr && kp.mask == 7u);   // kernels without face passes

@@ -40,12 +40,12 @@ def vec(P, seed):
 # ---- persistent volume kernels, multi-wave ------------------------------------------------
 # more cell groups than the resident CTA slots (148 SMs x 16 CTAs at p <= 4) (an upper bound for every k_volume*): each
 # CTA walks several groups, so the register / cp.async prefetch of the next group runs
-# (p = 5, 6: the line kernels; with -DDG_PLANE_VOL67=1 the plane-per-lane k_volume_s)
+# (p = 5, 6, 7: the lean line kernel k_volume_line; with -DDG_PLANE_VOL67=1 the plane-per-lane k_volume_s)
 MULTIWAVE = {1: (47, 43, 38), 2: (41, 37, 31), 3: (44, 43, 41), 4: (31, 30, 31), 5: (21, 19, 17),
-             6: (19, 17, 16)}
+             6: (19, 17, 16), 7: (15, 13, 12)}
 
 
-@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6, 7])
 @pytest.mark.parametrize("variant", [0, dg.DG_VARIANT_VOLUME_PREFETCH], ids=["default", "prefetch"])
 @pytest.mark.parametrize("gen", [False, True], ids=["diffusion", "conv-reaction"])
 def test_volume_kernel_multiwave_every_dof(p, variant, gen):
