@@ -1182,14 +1182,42 @@ __device__ __forceinline__ void lcp_async8(double* dst, const double* src, bool 
 __device__ __forceinline__ void lcp_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
-// the group's own tile (contiguous in global) into the padded CS layout, zero past the end
+__device__ __forceinline__ void lcp_async16(double* dst, const double* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+}
+// the group's own tile (contiguous in global) into the padded CS layout, zero past the end.
+// Unpadded layouts (n = 3, 5: CS = n^3) are the global block itself: 16-byte copies (the group's
+// first DoF is 16-byte aligned); padded ones one x-line per thread, its indices computed once per
+// line (per element they cost ~45 instructions per 8-byte copy: 30 % of the C3 apply's issued
+// instructions, ncu)
 template <int N>
 __device__ __forceinline__ void async_tile(double* dst, const double* src, int nvalid) {
   using G = Geo<N>;
-  for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
-    const int cs = e / G::N3, r = e % G::N3;
-    const int i = r % N, j = (r / N) % N, k = r / G::N2;
-    lcp_async8(dst + cs * G::CS + k * G::ZS + j * G::YS + i, src + (cs < nvalid ? e : 0), cs < nvalid);
+  if constexpr (G::CS == G::N3 && G::ZS == G::N2 && G::YS == N && (G::C * G::N3) % 2 == 0) {
+    const int nel = nvalid * G::N3;
+    for (int c = threadIdx.x; c < G::C * G::N3 / 2; c += G::NT) {
+      const int e = 2 * c;
+      const int bytes = e + 2 <= nel ? 16 : (e < nel ? 8 : 0);
+      lcp_async16(dst + e, src + (bytes ? e : 0), bytes);
+    }
+  } else if constexpr (N == 8) {
+    // n = 8 (128 threads, one line each): consecutive lanes on consecutive elements (per-line
+    // copies: p = 7 volume 81 -> 87 us, apply 142 -> 147 us)
+    for (int e = threadIdx.x; e < G::C * G::N3; e += G::NT) {
+      const int cs = e / G::N3, r = e % G::N3;
+      const int i = r % N, j = (r / N) % N, k = r / G::N2;
+      lcp_async8(dst + cs * G::CS + k * G::ZS + j * G::YS + i, src + (cs < nvalid ? e : 0), cs < nvalid);
+    }
+  } else {
+    for (int ln = threadIdx.x; ln < G::C * G::N2; ln += G::NT) {
+      const int cs = ln / G::N2, l = ln % G::N2, j = l % N, k = l / N;
+      const bool v = cs < nvalid;
+      double* d = dst + cs * G::CS + k * G::ZS + j * G::YS;
+      const double* sp = src + (v ? cs * G::N3 + k * G::N2 + j * N : 0);
+#pragma unroll
+      for (int i = 0; i < N; ++i) lcp_async8(d + i, sp + (v ? i : 0), v);
+    }
   }
 }
 
@@ -1320,111 +1348,221 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out, int 
 // ---- the volume terms alone, lean line kernel (dg_apply_parts mask = volume, n >= 6) ----------
 // The passes and arithmetic of cell_operator<N, FACES = false> (stage 1: A_x, A_y, A_z to the
 // Gauss points; stage 2: reaction and the x / y / z direction terms at the Gauss points; stage 3:
-// the transposed contractions), bit for bit, without its instruction overhead (ncu,
-// p = 5: DFMA were 25 % of the issued instructions; the passes recomputed the line indices per
-// loop, the tile copy spent ~45 instructions per 8-byte cp.async): one x-line per thread, its
-// three line offsets and Gauss weight computed once, the cell's scalars in registers (loaded
-// before the dependency wait), its own x-line read from global memory straight into registers
-// and the result written from registers, so only the two work tensors live in shared memory.
-template <int N, bool GEN>
-__global__ void __launch_bounds__(Geo<N>::NT)
+// the transposed contractions), without its instruction overhead (ncu, p = 5: DFMA
+// were 25 % of the issued instructions; the passes recomputed the line indices per loop, the
+// tile copy spent ~45 instructions per 8-byte cp.async): each thread owns L x-lines with the same
+// (j, k) in the cells cs and cs + CC / L (so the three line offsets and the Gauss weight are
+// computed once and every constant-bank table entry loaded into a uniform register feeds L
+// DFMA), the cells' scalars live in registers (loaded before the dependency wait), the own
+// x-lines are read from global memory straight into registers and the result is written from
+// registers, so only the two work tensors live in shared memory. Per line the FMA order is that
+// of mv / mtv / dir_term (the results equal cell_operator's bit for bit).
+template <int N, int W, int L> __device__ __forceinline__ void mvL(const double (&in)[L][N], double (&out)[L][N]) {
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    double s[L];
+#pragma unroll
+    for (int m = 0; m < L; ++m) s[m] = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double c = tab<N, W>(q * N + j);
+#pragma unroll
+      for (int m = 0; m < L; ++m) s[m] = fma(c, in[m][j], s[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < L; ++m) out[m][q] = s[m];
+  }
+}
+template <int N, int W, int L> __device__ __forceinline__ void mtvL(const double (&in)[L][N], double (&out)[L][N]) {
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    double s[L];
+#pragma unroll
+    for (int m = 0; m < L; ++m) s[m] = 0.0;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const double c = tab<N, W>(q * N + j);
+#pragma unroll
+      for (int m = 0; m < L; ++m) s[m] = fma(c, in[m][q], s[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < L; ++m) out[m][j] = s[m];
+  }
+}
+// dir_term for L lines (per-line scalings sK[m], sb[m]; the same FMA order per line)
+template <int N, bool GEN, int L>
+__device__ __forceinline__ void dir_termL(const double (&U)[L][N], double (&R)[L][N], double Wl,
+                                          const double (&sK)[L], const double (&sb)[L]) {
+  if constexpr (!GEN) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double s[L];
+#pragma unroll
+      for (int m = 0; m < L; ++m) s[m] = 0.0;
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const double c = c_tab[N].SG[r * N + q];
+#pragma unroll
+        for (int m = 0; m < L; ++m) s[m] = fma(c, U[m][q], s[m]);
+      }
+#pragma unroll
+      for (int m = 0; m < L; ++m) R[m][r] = fma(Wl * sK[m], s[m], R[m][r]);
+    }
+    return;
+  }
+  double du[L][N], F[L][N], t[L][N];
+  mvL<N, 1, L>(U, du);
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int m = 0; m < L; ++m) F[m][q] = Wl * c_tab[N].w[q] * fma(sK[m], du[m][q], -sb[m] * U[m][q]);
+  mtvL<N, 1, L>(F, t);
+#pragma unroll
+  for (int r = 0; r < N; ++r)
+#pragma unroll
+    for (int m = 0; m < L; ++m) R[m][r] += t[m][r];
+}
+template <int N, int L, int CC> struct VolLine {
+  static_assert(CC % L == 0, "L lines per thread: cells cs + i CC / L");
+  static constexpr int LINES = CC / L * N * N;            // threads with lines
+  static constexpr int NT = ((LINES + 31) / 32) * 32;
+};
+template <int N, bool GEN, int L, int CC>
+__global__ void __launch_bounds__(VolLine<N, L, CC>::NT)
 k_volume_line(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
-  using G = Geo<N>;
-  constexpr int N2 = G::N2, N3 = G::N3, C = G::C;
-  static_assert(G::LINES <= G::NT, "one x-line per thread");
+  using G = Geo<N, CC>;
+  using V = VolLine<N, L, CC>;
+  constexpr int N2 = G::N2, N3 = G::N3, CL = CC / L;
   extern __shared__ double sm[];
   double* SA = sm;
   double* SB = SA + G::TENSOR;
   const int t = threadIdx.x;
-  const int cell0 = block_group(kp, false) * C;
-  const bool act = t < G::LINES;
+  const int cell0 = block_group(kp, false) * CC;
+  const bool act = t < V::LINES;
   const int cs = act ? t / N2 : 0, l = t % N2, a = l % N, b = l / N;
-  const int ox = cs * G::CS + b * G::ZS + a * G::YS;   // x-line (j = a, k = b)
+  const int ox = cs * G::CS + b * G::ZS + a * G::YS;   // x-line (j = a, k = b) of line 0
   const int oy = cs * G::CS + b * G::ZS + a;           // y-line (i = a, k = b)
   const int oz = cs * G::CS + b * G::YS + a;           // z-line (i = a, j = b)
-  const int cell = cell0 + cs;
-  const bool valid = act && cell < kp.ncells;
+  constexpr int LS = CL * G::CS;                        // line m: + m LS (cell cs + m CL)
+  bool valid[L];
+  int cell[L];
+#pragma unroll
+  for (int m = 0; m < L; ++m) {
+    cell[m] = cell0 + cs + m * CL;
+    valid[m] = act && cell[m] < kp.ncells;
+  }
   asm volatile("griddepcontrol.launch_dependents;");
-  // the cell's scalings (cell_operator: g.vc, g.vb from setup_cells), independent of u
-  double sK[3] = {0.0, 0.0, 0.0}, sb[3] = {0.0, 0.0, 0.0}, sc = 0.0;
-  if (valid) {
-    const int nxy = kp.nx * kp.ny;
-    const double vol = kp.h[0] * kp.h[1] * kp.h[2];
-    const double* Kc = kp.K + (size_t)(cell + nxy) * 3;
+  // the cells' scalings (cell_operator: g.vc, g.vb from setup_cells), independent of u
+  double sK[3][L], sb[3][L], sc[L];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) sK[d] = Kc[d] * vol * kp.ih[d] * kp.ih[d];
-    if constexpr (GEN) {
-      sc = kp.c ? vol * kp.c[cell] : 0.0;
+  for (int m = 0; m < L; ++m) {
+    sc[m] = 0.0;
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
-        sb[d] = vol * (kp.bc ? kp.bc[(size_t)(cell + nxy) * 3 + d] : kp.b[d]) * kp.ih[d];
+    for (int d = 0; d < 3; ++d) sK[d][m] = sb[d][m] = 0.0;
+    if (valid[m]) {
+      const int nxy = kp.nx * kp.ny;
+      const double vol = kp.h[0] * kp.h[1] * kp.h[2];
+      const double* Kc = kp.K + (size_t)(cell[m] + nxy) * 3;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) sK[d][m] = Kc[d] * vol * kp.ih[d] * kp.ih[d];
+      if constexpr (GEN) {
+        sc[m] = kp.c ? vol * kp.c[cell[m]] : 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          sb[d][m] = vol * (kp.bc ? kp.bc[(size_t)(cell[m] + nxy) * 3 + d] : kp.b[d]) * kp.ih[d];
+      }
     }
   }
   const double Wl = c_tab[N].w[a] * c_tab[N].w[b];   // (the same product in every pass)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  double v[N], o[N];
-  if (valid) {
-    ld<N, 1>(u + (size_t)cell * N3 + b * N2 + a * N, v);
-  } else {
+  double v[L][N], o[L][N];
 #pragma unroll
-    for (int e = 0; e < N; ++e) v[e] = 0.0;
+  for (int m = 0; m < L; ++m) {
+    if (valid[m]) {
+      ld<N, 1>(u + (size_t)cell[m] * N3 + b * N2 + a * N, v[m]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < N; ++e) v[m][e] = 0.0;
+    }
   }
   // pass 1: x-lines, SA = A_x u
   if (act) {
-    mv<N, 0>(v, o);
-    st<N, 1>(SA + ox, o);
+    mvL<N, 0, L>(v, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) st<N, 1>(SA + ox + m * LS, o[m]);
   }
   __syncthreads();
   // pass 2: y-lines, SB = A_y SA
   if (act) {
-    ld<N, G::YS>(SA + oy, v);
-    mv<N, 0>(v, o);
-    st<N, G::YS>(SB + oy, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) ld<N, G::YS>(SA + oy + m * LS, v[m]);
+    mvL<N, 0, L>(v, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) st<N, G::YS>(SB + oy + m * LS, o[m]);
   }
   __syncthreads();
   // pass 3: z-lines, U = A_z SB -> SA, R = reaction + z-term -> SB
   if (act) {
-    double U[N], R[N];
-    ld<N, G::ZS>(SB + oz, v);
-    mv<N, 0>(v, U);
+    double U[L][N], R[L][N];
 #pragma unroll
-    for (int q = 0; q < N; ++q) R[q] = GEN ? Wl * c_tab[N].w[q] * sc * U[q] : 0.0;
-    dir_term<N, GEN>(U, R, Wl, sK[2], GEN ? sb[2] : 0.0);
-    st<N, G::ZS>(SA + oz, U);
-    st<N, G::ZS>(SB + oz, R);
+    for (int m = 0; m < L; ++m) ld<N, G::ZS>(SB + oz + m * LS, v[m]);
+    mvL<N, 0, L>(v, U);
+#pragma unroll
+    for (int m = 0; m < L; ++m)
+#pragma unroll
+      for (int q = 0; q < N; ++q) R[m][q] = GEN ? Wl * c_tab[N].w[q] * sc[m] * U[m][q] : 0.0;
+    dir_termL<N, GEN, L>(U, R, Wl, sK[2], sb[2]);
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      st<N, G::ZS>(SA + oz + m * LS, U[m]);
+      st<N, G::ZS>(SB + oz + m * LS, R[m]);
+    }
   }
   __syncthreads();
   // pass 4: x-lines, R += x-term
   if (act) {
-    double U[N], R[N];
-    ld<N, 1>(SA + ox, U);
-    ld<N, 1>(SB + ox, R);
-    dir_term<N, GEN>(U, R, Wl, sK[0], GEN ? sb[0] : 0.0);
-    st<N, 1>(SB + ox, R);
+    double U[L][N], R[L][N];
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      ld<N, 1>(SA + ox + m * LS, U[m]);
+      ld<N, 1>(SB + ox + m * LS, R[m]);
+    }
+    dir_termL<N, GEN, L>(U, R, Wl, sK[0], sb[0]);
+#pragma unroll
+    for (int m = 0; m < L; ++m) st<N, 1>(SB + ox + m * LS, R[m]);
   }
   __syncthreads();
   // pass 5: y-lines, R += y-term, then A_y^T
   if (act) {
-    double U[N], R[N];
-    ld<N, G::YS>(SA + oy, U);
-    ld<N, G::YS>(SB + oy, R);
-    dir_term<N, GEN>(U, R, Wl, sK[1], GEN ? sb[1] : 0.0);
-    mtv<N, 0>(R, o);
-    st<N, G::YS>(SB + oy, o);
+    double U[L][N], R[L][N];
+#pragma unroll
+    for (int m = 0; m < L; ++m) {
+      ld<N, G::YS>(SA + oy + m * LS, U[m]);
+      ld<N, G::YS>(SB + oy + m * LS, R[m]);
+    }
+    dir_termL<N, GEN, L>(U, R, Wl, sK[1], sb[1]);
+    mtvL<N, 0, L>(R, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) st<N, G::YS>(SB + oy + m * LS, o[m]);
   }
   __syncthreads();
   // pass 6: z-lines, A_z^T
   if (act) {
-    ld<N, G::ZS>(SB + oz, v);
-    mtv<N, 0>(v, o);
-    st<N, G::ZS>(SB + oz, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) ld<N, G::ZS>(SB + oz + m * LS, v[m]);
+    mtvL<N, 0, L>(v, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m) st<N, G::ZS>(SB + oz + m * LS, o[m]);
   }
   __syncthreads();
   // pass 7: x-lines, A_x^T, straight to global memory
-  if (valid) {
-    ld<N, 1>(SB + ox, v);
-    mtv<N, 0>(v, o);
-    st<N, 1>(out + (size_t)cell * N3 + b * N2 + a * N, o);
+  if (act) {
+#pragma unroll
+    for (int m = 0; m < L; ++m) ld<N, 1>(SB + ox + m * LS, v[m]);
+    mtvL<N, 0, L>(v, o);
+#pragma unroll
+    for (int m = 0; m < L; ++m)
+      if (valid[m]) st<N, 1>(out + (size_t)cell[m] * N3 + b * N2 + a * N, o[m]);
   }
 }
 
@@ -2455,14 +2593,30 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_VOLUME_LINE_N
 #define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 81 -> 111 us, kept off)
 #endif
+#ifndef DG_VOLUME_LPT
+#define DG_VOLUME_LPT 1         // x-lines per thread of k_volume_line (the convective n = 7 kernel: 2)
+#endif
+#ifndef DG_VOLUME_CELLS
+#define DG_VOLUME_CELLS 4       // cells per CTA of k_volume_line
+#endif
+  // lines per thread x cells per CTA, ~8M DoF cubes, diffusion / convective-reaction us
+  // (scripts/vol_times.py): p = 5: 1 x 4 55.9 / 64.1, 2 x 4 55.7 / 78.9, 2 x 8 58.5 / 80.0,
+  // 2 x 16 104 / 128; p = 6: 1 x 4 72.9 / 111.7, 2 x 4 74.8 / 94.3, 2 x 8 85.9 / 152
   if (kp.mask == 1u && ((DG_VOLUME_LINE_N >> N) & 1)) {
-    const size_t smem = sizeof(double) * 2 * (size_t)G::TENSOR;
-    auto kv = gen_terms(kp) ? k_volume_line<N, true> : k_volume_line<N, false>;
+    constexpr int CC = DG_VOLUME_CELLS;
+    constexpr int LG = N == 7 ? 2 : DG_VOLUME_LPT;   // lines per thread, convective kernel
+    using GV = Geo<N, CC>;
+    KParams kv_p = kp0;
+    const int gridv = split_groups(kv_p, CC);
+    if (gridv == 0) return cudaSuccess;
+    const size_t smem = sizeof(double) * 2 * (size_t)GV::TENSOR;
+    const bool gen = gen_terms(kp);
+    auto kv = gen ? k_volume_line<N, true, LG, CC> : k_volume_line<N, false, DG_VOLUME_LPT, CC>;
     cudaError_t e = set_smem(kv, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(G::NT);
+    cfg.gridDim = dim3(gridv);
+    cfg.blockDim = dim3(gen ? VolLine<N, LG, CC>::NT : VolLine<N, DG_VOLUME_LPT, CC>::NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute at[1];
@@ -2470,7 +2624,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kv, kp, u, out, with_nbr);
+    return cudaLaunchKernelEx(&cfg, kv, kv_p, u, out, with_nbr);
   }
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point
   // operators. Neither has face passes, so neither gets the face buffer (more resident CTAs)
