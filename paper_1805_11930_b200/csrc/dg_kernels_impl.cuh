@@ -172,6 +172,27 @@ template <int N, int S> __device__ __forceinline__ void st(double* p, const doub
 #pragma unroll
   for (int e = 0; e < N; ++e) p[e * S] = v[e];
 }
+// global line access, 16-byte vectors where a line starts 16-byte aligned (n even)
+template <int N> __device__ __forceinline__ void ldg_line(const double* p, double* v) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < N; e += 2) {
+      const double2 t = *reinterpret_cast<const double2*>(p + e);
+      v[e] = t.x;
+      v[e + 1] = t.y;
+    }
+  } else {
+    ld<N, 1>(p, v);
+  }
+}
+template <int N> __device__ __forceinline__ void stg_line(double* p, const double* v) {
+  if constexpr (N % 2 == 0) {
+#pragma unroll
+    for (int e = 0; e < N; e += 2) *reinterpret_cast<double2*>(p + e) = make_double2(v[e], v[e + 1]);
+  } else {
+    st<N, 1>(p, v);
+  }
+}
 
 // Stage 2 + the derivative half of stage 3 along one line of direction k:
 // R += D^T ( Wl * w_q * (sK * (D U)_q - sb * U_q) )
@@ -511,7 +532,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       const int off = bb * G::ZS + a * G::YS, goff = bb * N2 + a * N;
       if (nlo) {
         double w[N];
-        if (cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, w); else ld<N, 1>(nlo + goff, w);
+        if (cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, w); else ldg_line<N>(nlo + goff, w);
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
@@ -520,7 +541,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       }
       if (nhi) {
         double w[N];
-        if (cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, w); else ld<N, 1>(nhi + goff, w);
+        if (cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, w); else ldg_line<N>(nhi + goff, w);
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
@@ -1315,13 +1336,13 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
   double* o = out + (size_t)cell0 * G::N3;
   if constexpr (NODAL) {
     apply_nodal<N, Geo<N>::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
-      if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, w);
+      if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, w);
     }, PRE ? &W : nullptr);
     return;
   }
   cell_operator<N, FACES, USEB, false, Geo<N>::NT, GEN>(kp, g, SRC, SA, SB, FB, (kp.mask & 1u) != 0,
                           [&](int cs, int j, int k, const double* v) {
-                            if (cs < nvalid) st<N, 1>(o + cs * G::N3 + k * G::N2 + j * N, v);
+                            if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, v);
                           });
 }
 
@@ -1427,7 +1448,9 @@ template <int N, int L, int CC> struct VolLine {
   static constexpr int LINES = CC / L * N * N;            // threads with lines
   static constexpr int NT = ((LINES + 31) / 32) * 32;
 };
-template <int N, bool GEN, int L, int CC>
+// TILE: the own x-lines from a tile staged in SA by coalesced cp.async (one element per lane)
+// instead of per-lane line loads
+template <int N, bool GEN, int L, int CC, bool TILE = false>
 __global__ void __launch_bounds__(VolLine<N, L, CC>::NT)
 k_volume_line(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
   using G = Geo<N, CC>;
@@ -1476,13 +1499,28 @@ k_volume_line(KParams kp, const double* __restrict__ u, double* __restrict__ out
   const double Wl = c_tab[N].w[a] * c_tab[N].w[b];   // (the same product in every pass)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   double v[L][N], o[L][N];
+  if constexpr (TILE) {
+    const int nvalid = min(CC, kp.ncells - cell0);
+    const double* src = u + (size_t)cell0 * N3;
+    for (int e = t; e < CC * N3; e += V::NT) {
+      const int c = e / N3, r = e % N3;
+      const int i = r % N, j = (r / N) % N, k = r / N2;
+      lcp_async8(SA + c * G::CS + k * G::ZS + j * G::YS + i, src + (c < nvalid ? e : 0), c < nvalid);
+    }
+    lcp_wait_all();
+    __syncthreads();
 #pragma unroll
-  for (int m = 0; m < L; ++m) {
-    if (valid[m]) {
-      ld<N, 1>(u + (size_t)cell[m] * N3 + b * N2 + a * N, v[m]);
-    } else {
+    for (int m = 0; m < L; ++m) ld<N, 1>(SA + ox + m * LS, v[m]);
+    __syncthreads();
+  } else {
 #pragma unroll
-      for (int e = 0; e < N; ++e) v[m][e] = 0.0;
+    for (int m = 0; m < L; ++m) {
+      if (valid[m]) {
+        ldg_line<N>(u + (size_t)cell[m] * N3 + b * N2 + a * N, v[m]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < N; ++e) v[m][e] = 0.0;
+      }
     }
   }
   // pass 1: x-lines, SA = A_x u
@@ -1562,7 +1600,7 @@ k_volume_line(KParams kp, const double* __restrict__ u, double* __restrict__ out
     mtvL<N, 0, L>(v, o);
 #pragma unroll
     for (int m = 0; m < L; ++m)
-      if (valid[m]) st<N, 1>(out + (size_t)cell[m] * N3 + b * N2 + a * N, o[m]);
+      if (valid[m]) stg_line<N>(out + (size_t)cell[m] * N3 + b * N2 + a * N, o[m]);
   }
 }
 
@@ -2591,7 +2629,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   const int grid = split_groups(kp, G::C);
   if (grid == 0) return cudaSuccess;
 #ifndef DG_VOLUME_LINE_N
-#define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 81 -> 111 us, kept off)
+#define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 80 -> 116 us, off)
 #endif
 #ifndef DG_VOLUME_LPT
 #define DG_VOLUME_LPT 1         // x-lines per thread of k_volume_line (the convective n = 7 kernel: 2)
@@ -2599,19 +2637,23 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_VOLUME_CELLS
 #define DG_VOLUME_CELLS 4       // cells per CTA of k_volume_line
 #endif
+#ifndef DG_VOLUME_TILE_N
+#define DG_VOLUME_TILE_N 0      // bit n: k_volume_line reads its lines from a cp.async tile (p = 5: 48 -> 56 us)
+#endif
   // lines per thread x cells per CTA, ~8M DoF cubes, diffusion / convective-reaction us
   // (scripts/vol_times.py): p = 5: 1 x 4 55.9 / 64.1, 2 x 4 55.7 / 78.9, 2 x 8 58.5 / 80.0,
   // 2 x 16 104 / 128; p = 6: 1 x 4 72.9 / 111.7, 2 x 4 74.8 / 94.3, 2 x 8 85.9 / 152
   if (kp.mask == 1u && ((DG_VOLUME_LINE_N >> N) & 1)) {
     constexpr int CC = DG_VOLUME_CELLS;
-    constexpr int LG = N == 7 ? 2 : DG_VOLUME_LPT;   // lines per thread, convective kernel
+    constexpr int LG = N == 7 ? 2 : (N == 8 ? 1 : DG_VOLUME_LPT);   // lines per thread, convective kernel
     using GV = Geo<N, CC>;
     KParams kv_p = kp0;
     const int gridv = split_groups(kv_p, CC);
     if (gridv == 0) return cudaSuccess;
     const size_t smem = sizeof(double) * 2 * (size_t)GV::TENSOR;
     const bool gen = gen_terms(kp);
-    auto kv = gen ? k_volume_line<N, true, LG, CC> : k_volume_line<N, false, DG_VOLUME_LPT, CC>;
+    constexpr bool TL = (DG_VOLUME_TILE_N >> N) & 1;
+    auto kv = gen ? k_volume_line<N, true, LG, CC, TL> : k_volume_line<N, false, DG_VOLUME_LPT, CC, TL>;
     cudaError_t e = set_smem(kv, smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
