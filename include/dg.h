@@ -123,6 +123,26 @@ dg_status dg_block_jacobi_sweep(dg_ctx* ctx, double* u, const double* f, double 
 dg_status dg_block_jacobi_sweep_to(dg_ctx* ctx, const double* u, const double* f, double* u_new,
                                    double omega, double local_tol, void* cuda_stream);
 
+/* z-layer ranges, for streaming (the host<->device copy of one chunk of layers under the compute
+ * of another). Single slab only (nranks == 1, else DG_ERR_INVALID).
+ * dg_range_granule: *layers = the smallest number of z-layers whose cells fill whole cell groups
+ * of every kernel of this context; range bounds must be multiples of it (or the last local layer).
+ * dg_apply_range: (A u)_T for the cells T of local z-layers [z_begin, z_end) only (the rows of
+ * dg_apply, bit for bit); reads u of layers z_begin-1 .. z_end (the face neighbours,
+ * P:345-350). Au elsewhere is untouched.
+ * dg_block_jacobi_sweep_range: the out-of-place sweep (Alg. 2) for the cells of
+ * [z_begin, z_end): u_new_T = u_T + omega D_T^{-1}(f - A u)_T, bit for bit the values of
+ * dg_block_jacobi_sweep_to; reads u of layers z_begin-1 .. z_end and f of the range; u_new
+ * elsewhere is untouched. dg_get_stats then reports, per cell, its last local solve.
+ * Errors: DG_ERR_INVALID for a NULL pointer, aliasing as above, bounds outside
+ * [0, local layers] or not multiples of the granule, nranks > 1; z_begin == z_end is a no-op. */
+dg_status dg_range_granule(const dg_ctx* ctx, int32_t* layers);
+dg_status dg_apply_range(dg_ctx* ctx, const double* u, double* Au, int32_t z_begin, int32_t z_end,
+                         void* cuda_stream);
+dg_status dg_block_jacobi_sweep_range(dg_ctx* ctx, const double* u, const double* f, double* u_new,
+                                      double omega, double local_tol, int32_t z_begin, int32_t z_end,
+                                      void* cuda_stream);
+
 /* Block SOR / SSOR in the red-black cell order (Alg. 3): colour
  * (cx + cy + cz) mod 2 (global indices), red = 0 first. A forward sweep updates all red cells
  * from the current u, then all black cells from the updated u, each cell by

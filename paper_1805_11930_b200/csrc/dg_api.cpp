@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <numeric>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -623,6 +624,78 @@ dg_status dg_block_jacobi_sweep_to(dg_ctx* c, const double* u, const double* f, 
   if (check_vec(u, "u") || check_vec(f, "f") || check_vec(u_new, "u_new")) return DG_ERR_INVALID;
   if (u_new == u || u_new == f) return fail(DG_ERR_INVALID, "u_new must not alias u or f");
   return sweep_impl(c, u, f, u_new, omega, tol, (cudaStream_t)stream);
+}
+
+// ---- z-layer ranges (streaming: host<->device copies of one chunk under the compute of another)
+dg_status dg_range_granule(const dg_ctx* c, int32_t* layers) {
+  if (!c || !layers) return fail(DG_ERR_INVALID, "ctx or layers is NULL");
+  const int64_t g = dg::range_group_cells(c->desc.p);
+  const int64_t nxy = (int64_t)c->desc.nx * c->desc.ny;
+  *layers = (int32_t)(g / std::gcd(g, nxy));
+  return DG_OK;
+}
+
+static dg_status range_check(dg_ctx* c, int32_t zb, int32_t ze) {
+  if (c->desc.nranks != 1) return fail(DG_ERR_INVALID, "range calls need a single slab (nranks == 1)");
+  if (zb < 0 || ze > c->nzl || zb > ze) return fail(DG_ERR_INVALID, "z range outside [0, local layers]");
+  int32_t g = 1;
+  dg_range_granule(c, &g);
+  if (zb % g != 0 || (ze % g != 0 && ze != c->nzl))
+    return fail(DG_ERR_INVALID, "z range bounds must be multiples of dg_range_granule (or the last layer)");
+  return DG_OK;
+}
+
+dg_status dg_apply_range(dg_ctx* c, const double* u, double* Au, int32_t z_begin, int32_t z_end,
+                         void* stream) {
+  NvtxRange nv("dg_apply_range");
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(Au, "Au")) return DG_ERR_INVALID;
+  if (u == Au) return fail(DG_ERR_INVALID, "u and Au must not alias");
+  dg_status st = range_check(c, z_begin, z_end);
+  if (st != DG_OK) return st;
+  c->launches = 0;
+  if (z_begin == z_end) return DG_OK;
+  const int64_t nxy = (int64_t)c->desc.nx * c->desc.ny;
+  dg::KParams kp = c->kp;
+  kp.mask = 7u;
+  kp.gsplit = 3;
+  kp.cfirst = (int32_t)(z_begin * nxy);
+  kp.clast = (int32_t)(z_end * nxy);
+  cudaError_t e = dg::launch_apply(c->desc.p, kp, u, Au, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "apply_range");
+  c->launches = 1;
+  return DG_OK;
+}
+
+dg_status dg_block_jacobi_sweep_range(dg_ctx* c, const double* u, const double* f, double* u_new,
+                                      double omega, double tol, int32_t z_begin, int32_t z_end,
+                                      void* stream) {
+  NvtxRange nv("dg_block_jacobi_sweep_range");
+  if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
+  if (check_vec(u, "u") || check_vec(f, "f") || check_vec(u_new, "u_new")) return DG_ERR_INVALID;
+  if (u_new == u || u_new == f) return fail(DG_ERR_INVALID, "u_new must not alias u or f");
+  if (!(tol >= 0) || !std::isfinite(tol)) return fail(DG_ERR_INVALID, "local_tol must be >= 0");
+  if (!std::isfinite(omega)) return fail(DG_ERR_INVALID, "omega must be finite");
+  dg_status st = range_check(c, z_begin, z_end);
+  if (st != DG_OK) return st;
+  c->launches = 0;
+  if (z_begin == z_end) return DG_OK;
+  const int64_t nxy = (int64_t)c->desc.nx * c->desc.ny;
+  dg::KParams kp = c->kp;
+  kp.tol2 = tol * tol;
+  kp.max_it = c->max_it;
+  kp.krestart = c->krestart;
+  kp.omega = omega;
+  kp.gsplit = 3;
+  kp.cfirst = (int32_t)(z_begin * nxy);
+  kp.clast = (int32_t)(z_end * nxy);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = dg::launch_sweep(c->desc.p, c->method, kp, u, f, u_new, s);
+  if (e != cudaSuccess) return cuda_fail(e, "sweep_range");
+  c->last_stream = s;
+  c->have_stats = true;
+  c->launches = 1;
+  return DG_OK;
 }
 
 dg_status dg_block_sor_sweep(dg_ctx* c, double* u, const double* f, double omega, double tol,

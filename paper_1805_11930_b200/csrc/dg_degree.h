@@ -11,6 +11,7 @@ template <int N> struct Deg {
   static cudaError_t solve(int method, bool sweep, const KParams& kp, const double* in,
                            const double* f, double* out, cudaStream_t s);
   static int solver_group_cells();   // cells per CTA of the plane solvers (0: line family)
+  static int group_lcm();            // lcm of the cells per CTA of its apply / sweep kernels
 };
 
 }  // namespace dg

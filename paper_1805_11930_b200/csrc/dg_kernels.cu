@@ -85,6 +85,19 @@ int solver_group_cells(int p) {
   }
 }
 
+int range_group_cells(int p) {
+  switch (p) {
+    case 1: return Deg<2>::group_lcm();
+    case 2: return Deg<3>::group_lcm();
+    case 3: return Deg<4>::group_lcm();
+    case 4: return Deg<5>::group_lcm();
+    case 5: return Deg<6>::group_lcm();
+    case 6: return Deg<7>::group_lcm();
+    case 7: return Deg<8>::group_lcm();
+    default: return 0;
+  }
+}
+
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
   switch (p) {
     case 1: return Deg<2>::upload(t, err);

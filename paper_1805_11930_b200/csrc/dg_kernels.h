@@ -44,6 +44,8 @@ struct KParams {
   int32_t gsplit;                // 0: every cell group; 1: the groups off the slab's ghost faces
                                  // (launched before the halo arrives); 2: the others (after it)
   int32_t gfirst, glast;         // the interior groups [gfirst, glast) of a split launch
+  int32_t cfirst, clast;         // gsplit = 3 (dg_apply_range / dg_block_jacobi_sweep_range): the
+                                 // cells [cfirst, clast), group-aligned (range_group_cells)
   int32_t cmap;                  // 1: the cell groups enumerate the cells of kp.colour only (nx even;
                                  // group_cell), the other colour is not touched
 };
@@ -68,7 +70,7 @@ __host__ __device__ inline bool skip_cell(const KParams& kp, int cell) {
 #ifdef __CUDACC__
 __device__ inline int block_group(const KParams& kp, bool perm) {
   const int b = blockIdx.x;
-  if (kp.gsplit == 1) return kp.gfirst + b;
+  if (kp.gsplit == 1 || kp.gsplit == 3) return kp.gfirst + b;
   if (kp.gsplit == 2) return b < kp.gfirst ? b : kp.glast + (b - kp.gfirst);
   return (perm && kp.gperm) ? kp.gperm[b] : b;
 }
@@ -79,6 +81,12 @@ __device__ inline int block_group(const KParams& kp, bool perm) {
 inline int split_groups(KParams& kp, int C) {
   const int items = kp.cmap ? kp.ncells / 2 : kp.ncells;
   const int ng = (items + C - 1) / C;
+  if (kp.gsplit == 3 && !kp.cmap) {   // the groups of the cell range [cfirst, clast)
+    kp.gfirst = kp.cfirst / C;
+    kp.glast = (kp.clast + C - 1) / C;
+    if (kp.glast > ng) kp.glast = ng;
+    return kp.glast > kp.gfirst ? kp.glast - kp.gfirst : 0;
+  }
   if (kp.gsplit == 0 || kp.cmap) {
     kp.gsplit = 0;
     return ng;
@@ -114,6 +122,9 @@ bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
 
 // cells per CTA of the plane local solvers for degree p (0 when the line family runs them)
 int solver_group_cells(int p);
+// least common multiple of the cells per CTA of every kernel an apply or a sweep of degree p can
+// launch (the granule of the cell ranges of dg_apply_range / dg_block_jacobi_sweep_range)
+int range_group_cells(int p);
 
 // Au (or selected parts) for all local cells.
 cudaError_t launch_apply(int p, const KParams& kp, const double* u, double* out, cudaStream_t s);

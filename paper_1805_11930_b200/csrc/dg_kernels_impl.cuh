@@ -2859,6 +2859,20 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
 
 }  // namespace
 
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+constexpr int lcm_c(int a, int b) { return a / gcd_c(a, b) * b; }
+// every group size split_groups is called with at degree N (plane kernels n <= 5, line apply /
+// solvers, the warp / CTA CG and BiCGStab variants, the lean volume kernel)
+template <int N> constexpr int group_lcm_n() {
+  int l = lcm_c(Cells<N>::C, line_cg_cells<N>());
+  l = lcm_c(l, bicgw_cells<N>());
+  l = lcm_c(l, bicg_cells<N>());
+  l = lcm_c(l, DG_CGW_CELLS);
+  l = lcm_c(l, DG_VOLUME_CELLS);
+  if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);
+  return l;
+}
+
 #define DG_INSTANTIATE_DEGREE(NN)                                                              \
   template <> bool Deg<NN>::upload(const Tables1D& t, cudaError_t* err) { return upload_n<NN>(t, err); } \
   template <> cudaError_t Deg<NN>::apply(const KParams& kp, const double* u, double* out,        \
@@ -2866,6 +2880,7 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
     return apply_n<NN>(kp, u, out, s, with_nbr);                                                 \
   }                                                                                              \
   template <> int Deg<NN>::solver_group_cells() { return NN <= 4 ? pk::Geo<(NN <= 5 ? NN : 5)>::C : 0; } \
+  template <> int Deg<NN>::group_lcm() { return group_lcm_n<NN>(); }                          \
   template <> cudaError_t Deg<NN>::solve(int method, bool sweep, const KParams& kp,              \
                                          const double* in, const double* f, double* out,         \
                                          cudaStream_t s) {                                       \

@@ -29,7 +29,8 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_last_launch_count", "dg_last_error", "dg_version", "dg_nccl_unique_id",
            "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
            "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep", "dg_pmf_setup",
-           "dg_pmf_sweep", "dg_pmf_block", "dg_block_jacobi_sweep_to", "dg_set_kernel_variant"]
+           "dg_pmf_sweep", "dg_pmf_block", "dg_block_jacobi_sweep_to", "dg_set_kernel_variant",
+           "dg_range_granule", "dg_apply_range", "dg_block_jacobi_sweep_range"]
 
 
 class DGError(RuntimeError):
@@ -108,6 +109,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_set_local_solver": ([P, i32, i32, i32], i32),
         "dg_set_kernel_variant": ([P, u32], i32),
         "dg_block_jacobi_sweep_to": ([P, P, P, P, dbl, dbl, P], i32),
+        "dg_range_granule": ([P, ctypes.POINTER(i32)], i32),
+        "dg_apply_range": ([P, P, P, i32, i32, P], i32),
+        "dg_block_jacobi_sweep_range": ([P, P, P, P, dbl, dbl, i32, i32, P], i32),
         "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
         "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
         "dg_fill_ghosts": ([P, P, P, P], i32),
@@ -301,6 +305,27 @@ class DGContext:
         """Out-of-place sweep: u_new = u + omega D^-1 (f - A u) (u_new must not alias u or f)."""
         _check(self.lib.dg_block_jacobi_sweep_to(self.h, self._v(u), self._v(f), self._v(u_new),
                                                  float(omega), float(tol), _stream(stream)))
+        return u_new
+
+    # ---- z-layer ranges (streaming chunks; single slab) ------------------------
+    def range_granule(self) -> int:
+        """Range bounds must be multiples of this many local z-layers (or the last layer)."""
+        g = ctypes.c_int32()
+        _check(self.lib.dg_range_granule(self.h, ctypes.byref(g)))
+        return g.value
+
+    def apply_range(self, u, out, z_begin: int, z_end: int, stream=None):
+        """(A u) for the cells of local z-layers [z_begin, z_end) only (reads layers z_begin-1..z_end)."""
+        _check(self.lib.dg_apply_range(self.h, self._v(u), self._v(out), int(z_begin), int(z_end),
+                                       _stream(stream)))
+        return out
+
+    def sweep_range_to(self, u, f, u_new, z_begin: int, z_end: int, omega: float = 1.0,
+                       tol: float = 1e-12, stream=None):
+        """Out-of-place sweep for the cells of local z-layers [z_begin, z_end) only."""
+        _check(self.lib.dg_block_jacobi_sweep_range(self.h, self._v(u), self._v(f), self._v(u_new),
+                                                    float(omega), float(tol), int(z_begin), int(z_end),
+                                                    _stream(stream)))
         return u_new
 
     def set_kernel_variant(self, variant: int = 0):
