@@ -520,6 +520,8 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     else return FZb[cs_ * 4 * N2 + q * N2 + j * N + i];
   };
   const int base = cs * G::CS;
+  // (the face sums are written as explicit fma: the ghost-record and in-slab branches then round
+  // alike whatever the compiler contracts, so slab partitions stay bit for bit)
   double sxl = 0.0, txl = 0.0, sxh = 0.0, txh = 0.0;
   // ---- stage 0: the neighbours' face data at this thread's face nodes
   if (act) {
@@ -536,7 +538,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
-        sxl = clo[2] * w[N - 1] + clo[3] * gn * kp.ih[0];
+        sxl = fma(clo[2], w[N - 1], (clo[3] * gn) * kp.ih[0]);
         txl = clo[5] * w[N - 1];
       }
       if (nhi) {
@@ -545,7 +547,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
-        sxh = chi[2] * w[0] + chi[3] * gn * kp.ih[0];
+        sxh = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[0]);
         txh = chi[5] * w[0];
       }
     }
@@ -568,7 +570,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
-        s0 = clo[2] * w[N - 1] + clo[3] * gn * kp.ih[1];
+        s0 = fma(clo[2], w[N - 1], (clo[3] * gn) * kp.ih[1]);
         t0 = clo[5] * w[N - 1];
       }
       if (nhi) {
@@ -582,7 +584,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
-        s1 = chi[2] * w[0] + chi[3] * gn * kp.ih[1];
+        s1 = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[1]);
         t1 = chi[5] * w[0];
       }
       double* fy = FY + cs * 4 * N2 + bb * N + a;
@@ -613,7 +615,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
           for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
           av = w[N - 1];
         }
-        s0 = clo[2] * av + clo[3] * gn * kp.ih[2];
+        s0 = fma(clo[2], av, (clo[3] * gn) * kp.ih[2]);
         t0 = clo[5] * av;
       }
       if (nhi) {
@@ -633,7 +635,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
           for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
           av = w[0];
         }
-        s1 = chi[2] * av + chi[3] * gn * kp.ih[2];
+        s1 = fma(chi[2], av, (chi[3] * gn) * kp.ih[2]);
         t1 = chi[5] * av;
       }
       double* fz = FZ + cs * 4 * N2 + bb * N + a;
@@ -1212,9 +1214,9 @@ __device__ __forceinline__ void lcp_async16(double* dst, const double* src, int 
 // first DoF is 16-byte aligned); padded ones one x-line per thread, its indices computed once per
 // line (per element they cost ~45 instructions per 8-byte copy: 30 % of the C3 apply's issued
 // instructions, ncu)
-template <int N>
+template <int N, int CC = Cells<N>::C>
 __device__ __forceinline__ void async_tile(double* dst, const double* src, int nvalid) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   if constexpr (G::CS == G::N3 && G::ZS == G::N2 && G::YS == N && (G::C * G::N3) % 2 == 0) {
     const int nel = nvalid * G::N3;
     for (int c = threadIdx.x; c < G::C * G::N3 / 2; c += G::NT) {
@@ -1344,6 +1346,40 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
                           [&](int cs, int j, int k, const double* v) {
                             if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, v);
                           });
+}
+
+// The nodal A u (apply_nodal) with CC cells per CTA: CC = 1 makes every barrier of the four
+// stages a one-warp barrier (no CTA-wide waits behind the slowest cell's neighbour loads), at
+// 25 of 32 lanes busy at n = 5
+template <int N, bool GEN, int CC>
+__global__ void __launch_bounds__(Geo<N, CC>::NT)
+k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
+  using G = Geo<N, CC>;
+  using GR = Group<N, CC>;
+  using GH = GroupHead<N, CC>;
+  static_assert(offsetof(GR, td1) == offsetof(GH, td1), "GroupHead is a prefix of Group");
+  __shared__ GH gh;
+  Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
+  extern __shared__ double sm[];
+  double* SRC = sm;
+  double* SA = SRC + G::TENSOR;
+  double* SB = SA + G::TENSOR;
+  double* FB = SB + G::TENSOR;
+  const int cell0 = block_group(kp, false) * CC;
+  const int nvalid = min(CC, kp.ncells - cell0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  async_tile<N, CC>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  group_setup<N, G::NT>(kp, g, cell0, u);  // ends with __syncthreads
+  lcp_wait_all();
+  __syncthreads();
+  double* o = out + (size_t)cell0 * G::N3;
+  apply_nodal<N, G::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
+    if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, w);
+  });
+}
+template <int N, int CC> constexpr size_t apply_nodal_smem() {
+  return sizeof(double) * (3 * (size_t)Geo<N, CC>::TENSOR + (DG_APPLY_INPLACE && N > 4 ? 8 : 12) * (size_t)CC * N * N);
 }
 
 // resident CTAs the line apply is compiled for (n = 5: five by shared memory after INPLACE,
@@ -2626,8 +2662,6 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     }
   }
   using G = Geo<N>;
-  const int grid = split_groups(kp, G::C);
-  if (grid == 0) return cudaSuccess;
 #ifndef DG_VOLUME_LINE_N
 #define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 80 -> 116 us, off)
 #endif
@@ -2668,6 +2702,39 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kv, kv_p, u, out, with_nbr);
   }
+#ifndef DG_APPLY_CELLS5
+// cells per CTA of the nodal A u at n = 5 (C3 apply: 8 567 us, 4 561, 2 574, 1 546; staging the
+// six neighbour cells of a one-cell CTA with cp.async before the setup: 769 us, 7 KB of L2 reads
+// and shared-memory writes per cell)
+#define DG_APPLY_CELLS5 1
+#endif
+  if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_CELLS5 != Cells<5>::C) {
+    if (kp.mask == 7u && with_nbr) {
+      constexpr int CC = DG_APPLY_CELLS5;
+      KParams ka = kp0;
+      const int grida = split_groups(ka, CC);
+      if (grida == 0) return cudaSuccess;
+      const size_t smem = apply_nodal_smem<N, CC>();
+      auto ke = gen_terms(kp) ? k_apply_nodal<N, true, CC> : k_apply_nodal<N, false, CC>;
+      cudaError_t e = set_smem(ke, smem);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grida);
+      cfg.blockDim = dim3(Geo<N, CC>::NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, ke, ka, u, out, with_nbr);
+    }
+  }
+  // (each kernel above splits the groups by its own group size: an early return on the group
+  // count of G::C would skip its launch when that count is 0)
+  const int grid = split_groups(kp, G::C);
+  if (grid == 0) return cudaSuccess;
   // mask = volume: no face passes; D_T (all parts, no neighbours): self faces as Gauss-point
   // operators. Neither has face passes, so neither gets the face buffer (more resident CTAs)
   const bool nofb = kp.mask == 1u || (!with_nbr && kp.mask == 7u);   // kernels without face passes
@@ -2869,6 +2936,7 @@ template <int N> constexpr int group_lcm_n() {
   l = lcm_c(l, bicg_cells<N>());
   l = lcm_c(l, DG_CGW_CELLS);
   l = lcm_c(l, DG_VOLUME_CELLS);
+  if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);
   return l;
 }
