@@ -499,7 +499,7 @@ def run_ours(args):
     if world == 1:
         g = ctx.range_granule()
         nzl = ctx.z_end - ctx.z_begin
-        per0 = -(-nzl // 8)                 # ~8 chunks, rounded up to the range granule
+        per0 = -(-nzl // args.e2e_chunks)   # chunks rounded up to the range granule
         per = -(-per0 // g) * g
         chunks = [(z, min(nzl, z + per)) for z in range(0, nzl, per)]
     lay = P.nx * P.ny * P.nd
@@ -684,6 +684,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=16, help="z-layer chunks of the streamed e2e step")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args.gpus)
