@@ -450,10 +450,10 @@ __device__ __forceinline__ void dt_nodal_smem(const Group<N, CC>& g, double* SA,
 // slab-boundary z face the ghost trace record's face value and derivative sum in w[.][0], w[.][1].
 // Which faces have a neighbour is still read from the setup's pointers (the same decision).
 template <int N> struct NbrLines { double w[4][N]; };
-template <int N>
+template <int N, int CC = Cells<N>::C>
 __device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const double* u, int cell0,
                                                    NbrLines<N>& W) {
-  using G = Geo<N>;
+  using G = Geo<N, CC>;
   constexpr int N2 = G::N2, N3 = G::N3;
   const int t = threadIdx.x;
   const int cs = t / N2, l = t % N2, a = l % N, bb = l / N;
@@ -766,24 +766,25 @@ __device__ void setup_cells(const KParams& kp, double (*vc_)[4], double (*vb_)[3
       int cx = c0x + cs, cy = c0y, cz = c0z;
       while (cx >= kp.nx) { cx -= kp.nx; ++cy; }
       while (cy >= kp.ny) { cy -= kp.ny; ++cz; }
-      const int coord[3] = {cx, cy, cz};
-      const int dims[3] = {kp.nx, kp.ny, kp.nzl};
-      const int dstep[3] = {1, kp.nx, nxy};
+      // (selects, not arrays indexed by the runtime axis: those went to local memory)
+      const int crd = axis == 0 ? cx : (axis == 1 ? cy : cz);
+      const int dim = axis == 0 ? kp.nx : (axis == 1 ? kp.ny : kp.nzl);
+      const int dst = axis == 0 ? 1 : (axis == 1 ? kp.nx : nxy);
       const double ihk = kp.ih[axis];
       const double KT = kp.K[(size_t)(cell + nxy) * 3 + axis];
-      const int ncoord = coord[axis] + (hi ? 1 : -1);
+      const int ncoord = crd + (hi ? 1 : -1);
       int kind;  // 0 interior, 1 Dirichlet, 2 Neumann
       long kidx = 0;
-      if (ncoord >= 0 && ncoord < dims[axis]) {
+      if (ncoord >= 0 && ncoord < dim) {
         kind = 0;
-        const long nb = cell + (hi ? dstep[axis] : -dstep[axis]);
+        const long nb = cell + (hi ? dst : -dst);
         kidx = nb + nxy;
         if (u) nbp = u + (size_t)nb * N3;
       } else {
         const int sk = kp.slab_face[f];
         if (sk == FK_GHOST) {
           kind = 0;
-          const int col = coord[0] + kp.nx * coord[1];
+          const int col = cx + kp.nx * cy;
           kidx = hi ? (long)(kp.nzl + 1) * nxy + col : col;
           if (u) nbp = (hi ? kp.ghost_hi : kp.ghost_lo) + (size_t)col * 2 * N * N;   // trace record
         } else {
@@ -1370,13 +1371,18 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   async_tile<N, CC>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+#ifndef DG_APPLY1_PREFETCH
+#define DG_APPLY1_PREFETCH 0   // the y / z neighbour lines loaded before the setup (registers; C3 530 -> 578 us)
+#endif
+  NbrLines<N> W;
+  if constexpr (DG_APPLY1_PREFETCH) nbr_lines_prefetch<N, CC>(kp, u, cell0, W);
   group_setup<N, G::NT>(kp, g, cell0, u);  // ends with __syncthreads
   lcp_wait_all();
   __syncthreads();
   double* o = out + (size_t)cell0 * G::N3;
   apply_nodal<N, G::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
     if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, w);
-  });
+  }, DG_APPLY1_PREFETCH ? &W : nullptr);
 }
 template <int N, int CC> constexpr size_t apply_nodal_smem() {
   return sizeof(double) * (3 * (size_t)Geo<N, CC>::TENSOR + (DG_APPLY_INPLACE && N > 4 ? 8 : 12) * (size_t)CC * N * N);
