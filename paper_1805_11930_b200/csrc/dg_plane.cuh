@@ -377,6 +377,47 @@ __device__ __forceinline__ void cp_async16(double* dst, const double* src, bool 
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
+// The own tile and the four y / z neighbour tiles of the apply's prologue in one loop, when every
+// neighbour tile is on the fast path (no ghost-layer neighbour) and none of them goes by 16-byte
+// pairs: the element's cell, plane and in-plane offset are computed once for the five copies
+// (separately they were ~30 % of the C5 apply's warp samples, ncu). Same copies, same order of
+// arrival per destination: the result is bitwise that of async_own + async_nbr.
+#ifndef DG_FUSED_TILES
+#define DG_FUSED_TILES 2   // 1: the four neighbour tiles fused, 2: the own tile too (C5 apply 742 / 700 / 643 us)
+#endif
+template <int N> __host__ __device__ constexpr bool fused_tiles() {
+  return !(N % 2 == 0 && Geo<N>::FS % 2 == 0) && N <= 3;
+}
+template <int N, bool OWN, bool WB>
+__device__ __forceinline__ void async_tiles5(double* TB, double* FY, double* FX, double* FZ,
+                                             const Cells<N, WB>& cl, const KParams& kp,
+                                             const double* tile, int nvalid) {
+  using G = Geo<N>;
+  const long sy = (long)kp.nx * G::N3, sz = (long)kp.nx * kp.ny * G::N3;
+  const double* s2 = tile - sy;
+  const double* s3 = tile + sy;
+  const double* s4 = tile - sz;
+  const double* s5 = tile + sz;
+  const unsigned m20 = cl.nbm[2][0], m21 = cl.nbm[2][1], m30 = cl.nbm[3][0], m31 = cl.nbm[3][1];
+  const unsigned m40 = cl.nbm[4][0], m41 = cl.nbm[4][1], m50 = cl.nbm[5][0], m51 = cl.nbm[5][1];
+#pragma unroll
+  for (int m = 0; m < G::PER; ++m) {
+    const int e = threadIdx.x + m * G::NT;
+    if (e < G::C * G::N3) {
+      const int cs = e / G::N3, r = e % G::N3;
+      const int oT = cs * G::CTB + (r / G::N2) * G::KS + (r % G::N2);
+      const int oF = cs * G::FS + r;
+      auto bit = [&](unsigned a, unsigned b) { return ((cs < 32 ? a >> cs : b >> (cs - 32)) & 1u) != 0; };
+      const bool own = cs < nvalid, k2 = bit(m20, m21), k3 = bit(m30, m31), k4 = bit(m40, m41), k5 = bit(m50, m51);
+      if (OWN) cp_async8(TB + oT, tile + (own ? e : 0), own);
+      cp_async8(TB + G::ARR + oT, k2 ? s2 + e : tile, k2);
+      cp_async8(FY + oF, k3 ? s3 + e : tile, k3);
+      cp_async8(FX + oF, k4 ? s4 + e : tile, k4);
+      cp_async8(FZ + oF, k5 ? s5 + e : tile, k5);
+    }
+  }
+}
+
 // own tile (contiguous in global) -> TB layout, half h
 template <int N, bool ROLL = false>
 __device__ __forceinline__ void async_own(double* TB, const double* __restrict__ src, int nvalid) {
@@ -1460,9 +1501,15 @@ k_apply(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   SetupRegs<N> sr;
   setup_issue<N>(kp, cl, sr, cell0, NBR ? u : nullptr);
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  async_own<N>(TB, tile, nvalid);
+  // DG_FUSED_TILES = 2: the own tile in the fused loop too (issued after the setup barrier)
+  constexpr bool FUSED = DG_FUSED_TILES && NBR && fused_tiles<N>();
+  constexpr bool FOWN = FUSED && DG_FUSED_TILES == 2;
+  if (!FOWN) async_own<N>(TB, tile, nvalid);
   __syncthreads();   // neighbour pointers and masks
-  if (NBR) {
+  if (FUSED && (cl.nbg[2] | cl.nbg[3] | cl.nbg[4] | cl.nbg[5]) == 0) {
+    async_tiles5<N, FOWN>(TB, FY, FX, FZ, cl, kp, tile, nvalid);
+  } else if (NBR) {
+    if (FOWN) async_own<N>(TB, tile, nvalid);
     async_nbr<N, G::KS, G::CTB>(TB + G::ARR, cl, 2, u, kp, tile);   // y-lo -> TB half 1
     async_nbr<N, G::N2, G::FS>(FY, cl, 3, u, kp, tile);             // y-hi, z-lo, z-hi -> FY, FX, FZ
     async_nbr<N, G::N2, G::FS>(FX, cl, 4, u, kp, tile);
@@ -1641,14 +1688,20 @@ __device__ __forceinline__ void solver_setup(const KParams& kp, Cells<N, WB>& cl
   // n = 4 solvers: the copy loops rolled (the fused sweep kernel's prologue code shrinks by
   // ~20 KB; C2 sweep 433 -> 416 us, C4 7.40 -> 7.33 ms; n = 3 and the applies lose with it)
   constexpr bool RL = N == 4;
-  if (!CMAP) async_own<N, RL>(TB, tile, nvalid);
+  // the fused staging of the apply's prologue (async_tiles5), for the sweeps' defect
+  constexpr bool FUSED = DG_FUSED_TILES && SWEEP && !CMAP && fused_tiles<N>();
+  constexpr bool FOWN = FUSED && DG_FUSED_TILES == 2;
+  if (!CMAP && !FOWN) async_own<N, RL>(TB, tile, nvalid);
   clear_masks<N>(cl);
   __syncthreads();
   SetupRegs<N> sr;
   setup_issue<N, CMAP>(kp, cl, sr, cell0, SWEEP ? in : nullptr);
   __syncthreads();   // neighbour pointers and masks
   if (CMAP) async_own_map<N>(TB, in, cl);
-  if (SWEEP) {
+  if (FUSED && (cl.nbg[2] | cl.nbg[3] | cl.nbg[4] | cl.nbg[5]) == 0) {
+    async_tiles5<N, FOWN>(TB, FY, FX, FZ, cl, kp, tile, nvalid);
+  } else if (SWEEP) {
+    if (FOWN) async_own<N, RL>(TB, tile, nvalid);
     async_nbr<N, G::KS, G::CTB, RL>(TB + G::ARR, cl, 2, in, kp, tile);
     async_nbr<N, G::N2, G::FS, RL>(FY, cl, 3, in, kp, tile);
     async_nbr<N, G::N2, G::FS, RL>(FX, cl, 4, in, kp, tile);
