@@ -501,7 +501,14 @@ def run_ours(args):
         nzl = ctx.z_end - ctx.z_begin
         per0 = -(-nzl // args.e2e_chunks)   # chunks rounded up to the range granule
         per = -(-per0 // g) * g
-        chunks = [(z, min(nzl, z + per)) for z in range(0, nzl, per)]
+        # the first two chunks (the first applies wait for both) and the last one (its read-back
+        # is not hidden) one granule each, the others `per` layers
+        bounds = [0]
+        while bounds[-1] < nzl:
+            z = bounds[-1]
+            small = len(bounds) <= 2 or nzl - z <= per + g
+            bounds.append(min(nzl, z + (g if small and args.e2e_taper else per)))
+        chunks = list(zip(bounds[:-1], bounds[1:]))
     lay = P.nx * P.ny * P.nd
 
     def e2e_streamed():
@@ -685,6 +692,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16, help="z-layer chunks of the streamed e2e step")
+    ap.add_argument("--e2e-taper", type=int, default=1, help="granule-sized first two and last chunks")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args.gpus)
