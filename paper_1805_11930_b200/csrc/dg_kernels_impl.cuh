@@ -502,7 +502,7 @@ __device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const doub
 template <int N, int NTH, bool GEN, bool INPLACE = false, class Out, int CC>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out,
-                                            const NbrLines<N>* W = nullptr) {
+                                            const NbrLines<N>* W = nullptr, const double* own = nullptr) {
   using G = Geo<N, CC>;
   constexpr int N2 = G::N2, C = G::C;
   static_assert(G::LINES <= NTH, "one x-line per thread");
@@ -646,7 +646,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
   // ---- x stage (x-line j = a, k = bb): b = Mhat u, c = Kx u + x faces; z faces: Mhat_x
   if (act) {
     double u[N], bv[N], cv[N];
-    ld<N, 1>(src + base + bb * G::ZS + a * G::YS, u);
+    if (own) {   // the thread's own x-line, loaded by the caller into registers
+#pragma unroll
+      for (int e = 0; e < N; ++e) u[e] = own[e];
+    } else {
+      ld<N, 1>(src + base + bb * G::ZS + a * G::YS, u);
+    }
     mv<N, 2>(u, bv);
     kfly<N, GEN>(kp, g, cs, 0, u, cv);
     const double fa = kp.fa[0];
@@ -1362,15 +1367,30 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
   __shared__ GH gh;
   Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
   extern __shared__ double sm[];
+#ifndef DG_APPLY1_REGSRC
+#define DG_APPLY1_REGSRC 1   // one cell per CTA: the own x-line straight into registers, no tile
+#endif
+  constexpr bool REGSRC = DG_APPLY1_REGSRC && CC == 1;
   double* SRC = sm;
-  double* SA = SRC + G::TENSOR;
+  double* SA = REGSRC ? sm : SRC + G::TENSOR;
   double* SB = SA + G::TENSOR;
   double* FB = SB + G::TENSOR;
   const int cell0 = block_group(kp, false) * CC;
   const int nvalid = min(CC, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  async_tile<N, CC>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  double ownl[N];
+  if constexpr (REGSRC) {
+    const int t = threadIdx.x;
+    if (t < G::LINES && nvalid > 0) {
+      ld<N, 1>(u + (size_t)cell0 * G::N3 + (t / N) * G::N2 + (t % N) * N, ownl);
+    } else {
+#pragma unroll
+      for (int e = 0; e < N; ++e) ownl[e] = 0.0;
+    }
+  } else {
+    async_tile<N, CC>(SRC, u + (size_t)cell0 * G::N3, nvalid);
+  }
 #ifndef DG_APPLY1_PREFETCH
 #define DG_APPLY1_PREFETCH 0   // the y / z neighbour lines loaded before the setup (registers; C3 530 -> 578 us)
 #endif
@@ -1380,12 +1400,14 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
   lcp_wait_all();
   __syncthreads();
   double* o = out + (size_t)cell0 * G::N3;
-  apply_nodal<N, G::NT, GEN, (DG_APPLY_INPLACE && N > 4)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
+  apply_nodal<N, G::NT, GEN, (DG_APPLY_INPLACE && N > 4 && !REGSRC)>(kp, g, SRC, SA, SB, FB, [&](int cs, int j, int k, const double* w) {
     if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, w);
-  }, DG_APPLY1_PREFETCH ? &W : nullptr);
+  }, DG_APPLY1_PREFETCH ? &W : nullptr, REGSRC ? ownl : nullptr);
 }
 template <int N, int CC> constexpr size_t apply_nodal_smem() {
-  return sizeof(double) * (3 * (size_t)Geo<N, CC>::TENSOR + (DG_APPLY_INPLACE && N > 4 ? 8 : 12) * (size_t)CC * N * N);
+  // REGSRC (one cell per CTA): no tile; the z-face arrays after Mhat_x in the face buffer
+  return CC == 1 && DG_APPLY1_REGSRC ? sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)N * N)
+                                     : sizeof(double) * (3 * (size_t)Geo<N, CC>::TENSOR + (DG_APPLY_INPLACE && N > 4 ? 8 : 12) * (size_t)CC * N * N);
 }
 
 // resident CTAs the line apply is compiled for (n = 5: five by shared memory after INPLACE,
