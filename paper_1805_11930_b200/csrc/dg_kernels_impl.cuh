@@ -499,7 +499,7 @@ __device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const doub
 // INPLACE: src may be overwritten (A u alone): after the x stage has read a thread's own line, the
 // z-face arrays after Mhat_x go there (4 < n entries per line) and FA shrinks to 8 C n^2
 // W (optional): the y / z neighbour lines prefetched by nbr_lines_prefetch
-template <int N, int NTH, bool GEN, bool INPLACE = false, class Out, int CC>
+template <int N, int NTH, bool GEN, bool INPLACE = false, bool WARP = false, class Out, int CC>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out,
                                             const NbrLines<N>* W = nullptr, const double* own = nullptr) {
@@ -507,8 +507,10 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
   constexpr int N2 = G::N2, C = G::C;
   static_assert(G::LINES <= NTH, "one x-line per thread");
   const int t = threadIdx.x;
-  const bool act = t < G::LINES;
-  const int cs = act ? t / N2 : 0, l = t % N2, a = l % N, bb = l / N;
+  // WARP: warp w owns cell w (lanes < n^2 one x-line each), the stages synchronise per warp
+  const bool act = WARP ? (t & 31) < N2 : t < G::LINES;
+  const int cs = WARP ? t >> 5 : (act ? t / N2 : 0), l = WARP ? (t & 31) : t % N2, a = l % N, bb = l / N;
+  auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
   double* FY = FA;                  // [C][4][n^2]: y faces S_lo, T_lo, S_hi, T_hi at (i, k)
   double* FZ = FA + 4 * C * N2;     // [C][4][n^2]: z faces at (i, j); reused after Mhat_y
   double* FZb = FA + 8 * C * N2;    // [C][4][n^2]: z faces after Mhat_x (not with INPLACE)
@@ -534,7 +536,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       const int off = bb * G::ZS + a * G::YS, goff = bb * N2 + a * N;
       if (nlo) {
         double w[N];
-        if (cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, w); else ldg_line<N>(nlo + goff, w);
+        if (!WARP && cs > 0) ld<N, 1>(src + (cs - 1) * G::CS + off, w); else ldg_line<N>(nlo + goff, w);
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
@@ -543,7 +545,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       }
       if (nhi) {
         double w[N];
-        if (cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, w); else ldg_line<N>(nhi + goff, w);
+        if (!WARP && cs < C - 1) ld<N, 1>(src + (cs + 1) * G::CS + off, w); else ldg_line<N>(nhi + goff, w);
         double gn = 0.0;
 #pragma unroll
         for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
@@ -642,7 +644,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       fz[0] = s0; fz[N2] = t0; fz[2 * N2] = s1; fz[3 * N2] = t1;
     }
   }
-  __syncthreads();
+  sync();
   // ---- x stage (x-line j = a, k = bb): b = Mhat u, c = Kx u + x faces; z faces: Mhat_x
   if (act) {
     double u[N], bv[N], cv[N];
@@ -669,7 +671,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
       fzb(cs, q, bb, a) = zs;
     }
   }
-  __syncthreads();
+  sync();
   // ---- y stage (y-line i = a, k = bb): d = Mhat b, g = Ky b + Mhat c + y faces (after Mhat_x);
   // z faces: Mhat_y
   if (act) {
@@ -705,7 +707,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     st<N, G::YS>(SA + off, dv);
     st<N, G::YS>(SB + off, ev);
   }
-  __syncthreads();
+  sync();
   // ---- z stage (z-line i = a, j = bb): q = Mhat g + Kz d + z faces (after Mhat_x, Mhat_y)
   if (act) {
     const int off = base + bb * G::YS + a;
@@ -723,7 +725,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
                              (e == N - 1 ? z2 : 0.0));
     st<N, G::ZS>(SA + off, o1);
   }
-  __syncthreads();
+  sync();
   if (act) {
     double v[N];
     ld<N, 1>(SA + base + bb * G::ZS + a * G::YS, v);
@@ -1357,8 +1359,11 @@ __device__ __forceinline__ void k_apply_body(const KParams& kp, const double* __
 // The nodal A u (apply_nodal) with CC cells per CTA: CC = 1 makes every barrier of the four
 // stages a one-warp barrier (no CTA-wide waits behind the slowest cell's neighbour loads), at
 // 25 of 32 lanes busy at n = 5
+#ifndef DG_APPLY1_MINB
+#define DG_APPLY1_MINB 0   // resident CTAs the one-cell apply is compiled for (0: no bound)
+#endif
 template <int N, bool GEN, int CC>
-__global__ void __launch_bounds__(Geo<N, CC>::NT)
+__global__ void __launch_bounds__(Geo<N, CC>::NT, (CC == 1 ? DG_APPLY1_MINB : 0))
 k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
   using G = Geo<N, CC>;
   using GR = Group<N, CC>;
@@ -1404,6 +1409,49 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
     if (cs < nvalid) stg_line<N>(o + cs * G::N3 + k * G::N2 + j * N, w);
   }, DG_APPLY1_PREFETCH ? &W : nullptr, REGSRC ? ownl : nullptr);
 }
+// Warp mode: CC independent cells per CTA, one warp each (apply_nodal<..., WARP = true>: the
+// stages synchronise per warp, the x neighbours come from global memory, the own x-line straight
+// into registers); the CTA barrier only after the coefficient setup. More resident warps than
+// the 32 one-warp CTAs an SM can hold.
+#ifndef DG_APPLYW_MINB
+#define DG_APPLYW_MINB 0
+#endif
+template <int N, bool GEN, int CC>
+__global__ void __launch_bounds__(CC * 32, DG_APPLYW_MINB)
+k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
+  using G = Geo<N, CC>;
+  using GR = Group<N, CC>;
+  using GH = GroupHead<N, CC>;
+  static_assert(offsetof(GR, td1) == offsetof(GH, td1), "GroupHead is a prefix of Group");
+  static_assert(G::N2 <= 32, "one warp per cell");
+  __shared__ GH gh;
+  Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
+  extern __shared__ double sm[];
+  double* SA = sm;
+  double* SB = SA + G::TENSOR;
+  double* FB = SB + G::TENSOR;
+  const int cell0 = block_group(kp, false) * CC;
+  const int nvalid = min(CC, kp.ncells - cell0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = threadIdx.x, cs = t >> 5, l = t & 31;
+  double ownl[N];
+  if (l < G::N2 && cs < nvalid) {
+    ld<N, 1>(u + (size_t)(cell0 + cs) * G::N3 + (l / N) * G::N2 + (l % N) * N, ownl);
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) ownl[e] = 0.0;
+  }
+  group_setup<N, CC * 32>(kp, g, cell0, u);  // ends with __syncthreads
+  double* o = out + (size_t)cell0 * G::N3;
+  apply_nodal<N, CC * 32, GEN, false, true>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
+    if (c < nvalid) stg_line<N>(o + c * G::N3 + k * G::N2 + j * N, w);
+  }, nullptr, ownl);
+}
+template <int N, int CC> constexpr size_t apply_warps_smem() {
+  return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)CC * N * N);
+}
+
 template <int N, int CC> constexpr size_t apply_nodal_smem() {
   // REGSRC (one cell per CTA): no tile; the z-face arrays after Mhat_x in the face buffer
   return CC == 1 && DG_APPLY1_REGSRC ? sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)N * N)
@@ -2736,6 +2784,32 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 // and shared-memory writes per cell)
 #define DG_APPLY_CELLS5 1
 #endif
+#ifndef DG_APPLY_WARPS5
+#define DG_APPLY_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal apply (0: off; C3 1 cell per CTA 515 us, 2 / 4 / 8 warps 500 / 490 / 504 us)
+#endif
+  if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_WARPS5 > 0) {
+    if (kp.mask == 7u && with_nbr) {
+      constexpr int CC = DG_APPLY_WARPS5;
+      KParams ka = kp0;
+      const int grida = split_groups(ka, CC);
+      if (grida == 0) return cudaSuccess;
+      const size_t smem = apply_warps_smem<N, CC>();
+      auto ke = gen_terms(kp) ? k_apply_warps<N, true, CC> : k_apply_warps<N, false, CC>;
+      cudaError_t e = set_smem(ke, smem);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grida);
+      cfg.blockDim = dim3(CC * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, ke, ka, u, out, with_nbr);
+    }
+  }
   if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_CELLS5 != Cells<5>::C) {
     if (kp.mask == 7u && with_nbr) {
       constexpr int CC = DG_APPLY_CELLS5;
@@ -2965,6 +3039,7 @@ template <int N> constexpr int group_lcm_n() {
   l = lcm_c(l, DG_CGW_CELLS);
   l = lcm_c(l, DG_VOLUME_CELLS);
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
+  if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
   if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);
   return l;
 }
