@@ -2634,6 +2634,17 @@ inline bool gen_terms(const KParams& kp) {
   return kp.c != nullptr || kp.bc != nullptr || kp.b[0] != 0.0 || kp.b[1] != 0.0 || kp.b[2] != 0.0;
 }
 
+#ifndef DG_VOLUME_LINE_N
+#define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 80 -> 116 us, off)
+#endif
+#ifndef DG_VOLUME_LINE_GEN_N
+// the same for the convective / reaction kernels: n = 5 too (p = 4 cube 77 -> 64 us: the plane
+// k_volume<5, true> spills; for diffusion the plane kernel stays, 55 vs 61 us)
+#define DG_VOLUME_LINE_GEN_N 0xe0
+#endif
+template <int N> inline bool volume_line(const KParams& kp) {
+  return (((gen_terms(kp) ? DG_VOLUME_LINE_GEN_N : DG_VOLUME_LINE_N) >> N) & 1) != 0;
+}
 template <int N>
 cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
   KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
@@ -2667,7 +2678,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     }
   }
   if constexpr (N <= 5) {
-    if (kp.mask == 1u && DG_VOL_PERSIST && N <= 5) {
+    if (kp.mask == 1u && DG_VOL_PERSIST && N <= 5 && !volume_line<N>(kp)) {
       using G = pk::Geo<N>;
       const int grid = (kp.ncells + G::C - 1) / G::C;
       if (grid == 0) return cudaSuccess;
@@ -2738,9 +2749,6 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     }
   }
   using G = Geo<N>;
-#ifndef DG_VOLUME_LINE_N
-#define DG_VOLUME_LINE_N 0xc0   // bit n: the volume terms alone by the lean k_volume_line (n = 8: 80 -> 116 us, off)
-#endif
 #ifndef DG_VOLUME_LPT
 #define DG_VOLUME_LPT 1         // x-lines per thread of k_volume_line (the convective n = 7 kernel: 2)
 #endif
@@ -2753,7 +2761,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   // lines per thread x cells per CTA, ~8M DoF cubes, diffusion / convective-reaction us
   // (scripts/vol_times.py): p = 5: 1 x 4 55.9 / 64.1, 2 x 4 55.7 / 78.9, 2 x 8 58.5 / 80.0,
   // 2 x 16 104 / 128; p = 6: 1 x 4 72.9 / 111.7, 2 x 4 74.8 / 94.3, 2 x 8 85.9 / 152
-  if (kp.mask == 1u && ((DG_VOLUME_LINE_N >> N) & 1)) {
+  if (kp.mask == 1u && volume_line<N>(kp)) {
     constexpr int CC = DG_VOLUME_CELLS;
     constexpr int LG = N == 7 ? 2 : (N == 8 ? 1 : DG_VOLUME_LPT);   // lines per thread, convective kernel
     using GV = Geo<N, CC>;
