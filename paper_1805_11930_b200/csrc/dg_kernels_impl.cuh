@@ -507,9 +507,11 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
   constexpr int N2 = G::N2, C = G::C;
   static_assert(G::LINES <= NTH, "one x-line per thread");
   const int t = threadIdx.x;
-  // WARP: warp w owns cell w (lanes < n^2 one x-line each), the stages synchronise per warp
-  const bool act = WARP ? (t & 31) < N2 : t < G::LINES;
-  const int cs = WARP ? t >> 5 : (act ? t / N2 : 0), l = WARP ? (t & 31) : t % N2, a = l % N, bb = l / N;
+  // WARP: warp w owns cell w (lanes < n^2 one x-line each; n <= 4: half-warps, two cells per
+  // warp), the stages synchronise per warp
+  constexpr int WL = N * N <= 16 ? 16 : 32;
+  const bool act = WARP ? (t % WL) < N2 : t < G::LINES;
+  const int cs = WARP ? t / WL : (act ? t / N2 : 0), l = WARP ? (t % WL) : t % N2, a = l % N, bb = l / N;
   auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
   double* FY = FA;                  // [C][4][n^2]: y faces S_lo, T_lo, S_hi, T_hi at (i, k)
   double* FZ = FA + 4 * C * N2;     // [C][4][n^2]: z faces at (i, j); reused after Mhat_y
@@ -1416,8 +1418,9 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
 #ifndef DG_APPLYW_MINB
 #define DG_APPLYW_MINB 0
 #endif
+template <int N> __host__ __device__ constexpr int warp_lanes() { return N * N <= 16 ? 16 : 32; }   // lanes per cell
 template <int N, bool GEN, int CC>
-__global__ void __launch_bounds__(CC * 32, DG_APPLYW_MINB)
+__global__ void __launch_bounds__(CC * warp_lanes<N>(), DG_APPLYW_MINB)
 k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
   using G = Geo<N, CC>;
   using GR = Group<N, CC>;
@@ -1434,7 +1437,9 @@ k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out
   const int nvalid = min(CC, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int t = threadIdx.x, cs = t >> 5, l = t & 31;
+  constexpr int WL = warp_lanes<N>();
+  static_assert((CC * WL) % 32 == 0, "whole warps");
+  const int t = threadIdx.x, cs = t / WL, l = t % WL;
   double ownl[N];
   if (l < G::N2 && cs < nvalid) {
     ld<N, 1>(u + (size_t)(cell0 + cs) * G::N3 + (l / N) * G::N2 + (l % N) * N, ownl);
@@ -1442,9 +1447,9 @@ k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out
 #pragma unroll
     for (int e = 0; e < N; ++e) ownl[e] = 0.0;
   }
-  group_setup<N, CC * 32>(kp, g, cell0, u);  // ends with __syncthreads
+  group_setup<N, CC * WL>(kp, g, cell0, u);  // ends with __syncthreads
   double* o = out + (size_t)cell0 * G::N3;
-  apply_nodal<N, CC * 32, GEN, false, true>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
+  apply_nodal<N, CC * WL, GEN, false, true>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
     if (c < nvalid) stg_line<N>(o + c * G::N3 + k * G::N2 + j * N, w);
   }, nullptr, ownl);
 }
@@ -2645,6 +2650,15 @@ inline bool gen_terms(const KParams& kp) {
 template <int N> inline bool volume_line(const KParams& kp) {
   return (((gen_terms(kp) ? DG_VOLUME_LINE_GEN_N : DG_VOLUME_LINE_N) >> N) & 1) != 0;
 }
+#ifndef DG_APPLY_WARPS4
+// n = 4: cells per CTA of the warp-mode nodal apply, two per warp (0: off), pure diffusion only
+// (C2 apply: plane 36.9 us, 4 / 8 / 16 cells 32.8 / 32.8 / 34.9; C4 with convection: plane 308,
+// warp mode 317 / 323 / 341 us)
+#define DG_APPLY_WARPS4 4
+#endif
+inline bool warp_apply4(const KParams& kp, int with_nbr) {
+  return DG_APPLY_WARPS4 > 0 && DG_NODAL_APPLY && kp.mask == 7u && with_nbr && !gen_terms(kp);
+}
 template <int N>
 cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
   KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
@@ -2722,7 +2736,8 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     }
   }
   if constexpr (plane_apply<N>()) {
-    if (!force_line(kp)) {
+    // (n = 4 with DG_APPLY_WARPS4: A u by the warp-mode line kernel below)
+    if (!force_line(kp) && !(N == 4 && warp_apply4(kp, with_nbr))) {
       using G = pk::Geo<N>;
       const int grid = split_groups(kp, G::C);
       if (grid == 0) return cudaSuccess;
@@ -2795,9 +2810,10 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_APPLY_WARPS5
 #define DG_APPLY_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal apply (0: off; C3 1 cell per CTA 515 us, 2 / 4 / 8 warps 500 / 490 / 504 us)
 #endif
-  if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_WARPS5 > 0) {
-    if (kp.mask == 7u && with_nbr) {
-      constexpr int CC = DG_APPLY_WARPS5;
+  constexpr int WCELLS = N == 5 ? DG_APPLY_WARPS5 : (N == 4 ? DG_APPLY_WARPS4 : 0);
+  if constexpr ((N == 5 || N == 4) && DG_NODAL_APPLY && WCELLS > 0) {
+    if (kp.mask == 7u && with_nbr && !force_line(kp) && (N == 5 || warp_apply4(kp, with_nbr))) {
+      constexpr int CC = WCELLS;
       KParams ka = kp0;
       const int grida = split_groups(ka, CC);
       if (grida == 0) return cudaSuccess;
@@ -2807,7 +2823,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grida);
-      cfg.blockDim = dim3(CC * 32);
+      cfg.blockDim = dim3(CC * warp_lanes<N>());
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
       cudaLaunchAttribute at[1];
@@ -3048,6 +3064,7 @@ template <int N> constexpr int group_lcm_n() {
   l = lcm_c(l, DG_VOLUME_CELLS);
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
+  if constexpr (N == 4 && DG_APPLY_WARPS4 > 0) l = lcm_c(l, DG_APPLY_WARPS4);
   if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);
   return l;
 }
