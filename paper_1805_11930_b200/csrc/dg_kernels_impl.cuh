@@ -2656,9 +2656,14 @@ template <int N> inline bool volume_line(const KParams& kp) {
 // warp mode 317 / 323 / 341 us)
 #define DG_APPLY_WARPS4 4
 #endif
-inline bool warp_apply4(const KParams& kp, int with_nbr) {
-  return DG_APPLY_WARPS4 > 0 && DG_NODAL_APPLY && kp.mask == 7u && with_nbr && !gen_terms(kp);
+#ifndef DG_APPLY_WARPS3
+#define DG_APPLY_WARPS3 0   // n = 3: the same (9 of 16 lanes; C5: plane 643 us, 4 / 8 cells 721 / 711 us: off)
+#endif
+template <int N> inline bool warp_apply(const KParams& kp, int with_nbr) {
+  constexpr int W = N == 4 ? DG_APPLY_WARPS4 : (N == 3 ? DG_APPLY_WARPS3 : 0);
+  return W > 0 && DG_NODAL_APPLY && kp.mask == 7u && with_nbr && !gen_terms(kp);
 }
+inline bool warp_apply4(const KParams& kp, int with_nbr) { return warp_apply<4>(kp, with_nbr); }
 template <int N>
 cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
   KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
@@ -2737,7 +2742,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   }
   if constexpr (plane_apply<N>()) {
     // (n = 4 with DG_APPLY_WARPS4: A u by the warp-mode line kernel below)
-    if (!force_line(kp) && !(N == 4 && warp_apply4(kp, with_nbr))) {
+    if (!force_line(kp) && !((N == 4 || N == 3) && warp_apply<N>(kp, with_nbr))) {
       using G = pk::Geo<N>;
       const int grid = split_groups(kp, G::C);
       if (grid == 0) return cudaSuccess;
@@ -2810,9 +2815,9 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_APPLY_WARPS5
 #define DG_APPLY_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal apply (0: off; C3 1 cell per CTA 515 us, 2 / 4 / 8 warps 500 / 490 / 504 us)
 #endif
-  constexpr int WCELLS = N == 5 ? DG_APPLY_WARPS5 : (N == 4 ? DG_APPLY_WARPS4 : 0);
-  if constexpr ((N == 5 || N == 4) && DG_NODAL_APPLY && WCELLS > 0) {
-    if (kp.mask == 7u && with_nbr && !force_line(kp) && (N == 5 || warp_apply4(kp, with_nbr))) {
+  constexpr int WCELLS = N == 5 ? DG_APPLY_WARPS5 : (N == 4 ? DG_APPLY_WARPS4 : (N == 3 ? DG_APPLY_WARPS3 : 0));
+  if constexpr ((N == 5 || N == 4 || N == 3) && DG_NODAL_APPLY && WCELLS > 0) {
+    if (kp.mask == 7u && with_nbr && !force_line(kp) && (N == 5 || warp_apply<N>(kp, with_nbr))) {
       constexpr int CC = WCELLS;
       KParams ka = kp0;
       const int grida = split_groups(ka, CC);
@@ -3065,6 +3070,7 @@ template <int N> constexpr int group_lcm_n() {
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
   if constexpr (N == 4 && DG_APPLY_WARPS4 > 0) l = lcm_c(l, DG_APPLY_WARPS4);
+  if constexpr (N == 3 && DG_APPLY_WARPS3 > 0) l = lcm_c(l, DG_APPLY_WARPS3);
   if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);
   return l;
 }
