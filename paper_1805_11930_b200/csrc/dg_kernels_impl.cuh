@@ -2740,35 +2740,6 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
       return cudaGetLastError();
     }
   }
-  if constexpr (plane_apply<N>()) {
-    // (n = 4 with DG_APPLY_WARPS4: A u by the warp-mode line kernel below)
-    if (!force_line(kp) && !((N == 4 || N == 3) && warp_apply<N>(kp, with_nbr))) {
-      using G = pk::Geo<N>;
-      const int grid = split_groups(kp, G::C);
-      if (grid == 0) return cudaSuccess;
-      const bool faces = kp.mask != 1u;   // mask = volume: the volume terms alone
-      const size_t smem = pk::smem_apply<N>(with_nbr, faces);
-      const bool gen = gen_terms(kp);
-      auto kern = with_nbr ? (gen ? pk::k_apply<N, true, true, true> : pk::k_apply<N, true, true, false>)
-                           : (gen ? pk::k_apply<N, false, true, true> : pk::k_apply<N, false, true, false>);
-      if (!faces) kern = gen ? pk::k_apply<N, false, false, true> : pk::k_apply<N, false, false, false>;
-      cudaError_t e = set_smem(kern, smem);
-      if (e != cudaSuccess) return e;
-      // programmatic dependent launch (the kernel waits on griddepcontrol before touching u)
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(G::NT);
-      cfg.dynamicSmemBytes = smem;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      return cudaLaunchKernelEx(&cfg, kern, kp, u, out);
-    }
-  }
-  using G = Geo<N>;
 #ifndef DG_VOLUME_LPT
 #define DG_VOLUME_LPT 1         // x-lines per thread of k_volume_line (the convective n = 7 kernel: 2)
 #endif
@@ -2806,6 +2777,35 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kv, kv_p, u, out, with_nbr);
   }
+  if constexpr (plane_apply<N>()) {
+    // (n = 4 with DG_APPLY_WARPS4: A u by the warp-mode line kernel below)
+    if (!force_line(kp) && !((N == 4 || N == 3) && warp_apply<N>(kp, with_nbr))) {
+      using G = pk::Geo<N>;
+      const int grid = split_groups(kp, G::C);
+      if (grid == 0) return cudaSuccess;
+      const bool faces = kp.mask != 1u;   // mask = volume: the volume terms alone
+      const size_t smem = pk::smem_apply<N>(with_nbr, faces);
+      const bool gen = gen_terms(kp);
+      auto kern = with_nbr ? (gen ? pk::k_apply<N, true, true, true> : pk::k_apply<N, true, true, false>)
+                           : (gen ? pk::k_apply<N, false, true, true> : pk::k_apply<N, false, true, false>);
+      if (!faces) kern = gen ? pk::k_apply<N, false, false, true> : pk::k_apply<N, false, false, false>;
+      cudaError_t e = set_smem(kern, smem);
+      if (e != cudaSuccess) return e;
+      // programmatic dependent launch (the kernel waits on griddepcontrol before touching u)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(G::NT);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kern, kp, u, out);
+    }
+  }
+  using G = Geo<N>;
 #ifndef DG_APPLY_CELLS5
 // cells per CTA of the nodal A u at n = 5 (C3 apply: 8 567 us, 4 561, 2 574, 1 546; staging the
 // six neighbour cells of a one-cell CTA with cp.async before the setup: 769 us, 7 KB of L2 reads
