@@ -29,7 +29,7 @@
 #define DG_APPLY_SETUP_FIRST 0   // line apply: coefficient setup before the PDL wait (A/B)
 #endif
 #ifndef DG_NODAL_FLY
-#define DG_NODAL_FLY 0   // local solvers: nodal factors from shared memory (1) or formed on the fly
+#define DG_NODAL_FLY 0   // local solvers: bit a = the nodal factor of direction a formed on the fly (else from shared memory)
 #endif
 #ifndef DG_NODAL_APPLY
 #define DG_NODAL_APPLY 1   // line-family A u in the nodal Kronecker-sum form (apply_nodal)
@@ -370,7 +370,7 @@ __device__ __forceinline__ void kfly(const KParams& kp, const CB& g, int cs, int
 // x-lines b = Mhat p, c = Kx p (registers) -> y-lines d = Mhat b, g = Ky b + Mhat c -> z-lines
 // q = Mhat g + Kz d -> back to the thread's x-line. 7 one-direction contractions and 3 transposes
 // (the Gauss-point form: 9 contractions, 6 transposes). pin: the thread's x-line of p.
-template <int N, bool WARP, bool FLY = false, bool GEN = true, int CC>
+template <int N, bool WARP, int FLY = 0, bool GEN = true, int CC>
 __device__ __forceinline__ void dt_nodal(const Group<N, CC>& g, double* SA, double* SB, const double* pin,
                                          double* q, const KParams* kpp = nullptr) {
   using G = Geo<N, CC>;
@@ -387,7 +387,7 @@ __device__ __forceinline__ void dt_nodal(const Group<N, CC>& g, double* SA, doub
   if (act) {   // x-lines (j = a, k = b)
     double bv[N], cv[N];
     mv<N, 2>(pin, bv);
-    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 0, pin, cv); else kmv<N>(Kx, pin, cv);
+    if constexpr (FLY & 1) kfly<N, GEN>(*kpp, g, cs, 0, pin, cv); else kmv<N>(Kx, pin, cv);
     st<N, 1>(SA + base + b * G::ZS + a * G::YS, bv);
     st<N, 1>(SB + base + b * G::ZS + a * G::YS, cv);
   }
@@ -398,7 +398,7 @@ __device__ __forceinline__ void dt_nodal(const Group<N, CC>& g, double* SA, doub
     ld<N, G::YS>(SA + off, bv);
     ld<N, G::YS>(SB + off, cv);
     mv<N, 2>(bv, dv);
-    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 1, bv, ev); else kmv<N>(Ky, bv, ev);
+    if constexpr (FLY & 2) kfly<N, GEN>(*kpp, g, cs, 1, bv, ev); else kmv<N>(Ky, bv, ev);
     mv<N, 2>(cv, fv);
 #pragma unroll
     for (int e = 0; e < N; ++e) ev[e] += fv[e];
@@ -412,7 +412,7 @@ __device__ __forceinline__ void dt_nodal(const Group<N, CC>& g, double* SA, doub
     ld<N, G::ZS>(SA + off, dv);
     ld<N, G::ZS>(SB + off, gv);
     mv<N, 2>(gv, o1);
-    if constexpr (FLY) kfly<N, GEN>(*kpp, g, cs, 2, dv, o2); else kmv<N>(Kz, dv, o2);
+    if constexpr (FLY & 4) kfly<N, GEN>(*kpp, g, cs, 2, dv, o2); else kmv<N>(Kz, dv, o2);
 #pragma unroll
     for (int e = 0; e < N; ++e) o1[e] += o2[e];
     st<N, G::ZS>(SA + off, o1);
