@@ -13,7 +13,8 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libdg_b200.so")
 # one translation unit per degree n = p+1 (compiled in parallel), the dispatch, the C ABI, tables
-SOURCES = [f"dg_kernels_n{n}.cu" for n in range(2, 9)] + ["dg_kernels.cu", "dg_hybrid.cu", "dg_pmf.cu", "dg_api.cpp", "dg_tables.cpp"]
+SOURCES = [f"dg_kernels_n{n}.cu" for n in range(2, 9)] + ["dg_kernels_gmres.cu", "dg_kernels.cu", "dg_hybrid.cu",
+                                                            "dg_pmf.cu", "dg_api.cpp", "dg_tables.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -85,7 +85,16 @@ int solver_group_cells(int p) {
   }
 }
 
+static int lcm_i(int a, int b) {
+  int x = a, y = b;
+  while (y) { const int t = x % y; x = y; y = t; }
+  return a / x * b;
+}
 int range_group_cells(int p) {
+  if (p >= 1 && p <= 3) {   // the GMRES translation unit's groups too
+    const int a = p == 1 ? Deg<2>::group_lcm() : (p == 2 ? Deg<3>::group_lcm() : Deg<4>::group_lcm());
+    return lcm_i(a, gmres_group_cells(p));
+  }
   switch (p) {
     case 1: return Deg<2>::group_lcm();
     case 2: return Deg<3>::group_lcm();
@@ -100,9 +109,9 @@ int range_group_cells(int p) {
 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err) {
   switch (p) {
-    case 1: return Deg<2>::upload(t, err);
-    case 2: return Deg<3>::upload(t, err);
-    case 3: return Deg<4>::upload(t, err);
+    case 1: return Deg<2>::upload(t, err) && upload_gmres(p, t, err);
+    case 2: return Deg<3>::upload(t, err) && upload_gmres(p, t, err);
+    case 3: return Deg<4>::upload(t, err) && upload_gmres(p, t, err);
     case 4: return Deg<5>::upload(t, err);
     case 5: return Deg<6>::upload(t, err);
     case 6: return Deg<7>::upload(t, err);

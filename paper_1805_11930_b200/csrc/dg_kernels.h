@@ -120,6 +120,13 @@ enum LocalMethod : int32_t { LM_CG = 1, LM_BICGSTAB = 2, LM_BICGSTAB_THOMAS = 3,
 
 bool upload_tables(int p, const Tables1D& t, cudaError_t* err);
 
+// local GMRES at p = 1..3 (n <= 4): kernels of their own translation unit with four-warp plane
+// CTAs (dg_kernels_gmres.cu); its table upload, launcher and cells per CTA
+bool upload_gmres(int p, const Tables1D& t, cudaError_t* err);
+cudaError_t solve_gmres(int p, int method, bool sweep, const KParams& kp, const double* in,
+                        const double* f, double* out, cudaStream_t s);
+int gmres_group_cells(int p);
+
 // cells per CTA of the plane local solvers for degree p (0 when the line family runs them)
 int solver_group_cells(int p);
 // least common multiple of the cells per CTA of every kernel an apply or a sweep of degree p can

@@ -2891,6 +2891,33 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   return cudaLaunchKernelEx(&cfg, kl, kp, u, out, with_nbr);
 }
 
+#ifndef DG_GMRES_TU
+#define DG_GMRES_TU 0
+#endif
+// restarted GMRES(KR) on the plane kernels, Krylov basis + diagonal in TMEM (compact colour maps
+// not supported: the SOR half-sweeps run masked). KR fills 256 TMEM columns at n = 2, 3 (two CTAs
+// per SM) and all 512 at n = 4 (one CTA per SM: GMRES(7) with two CTAs was faster on C4, 13.3 vs
+// 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_ab.md); n = 5: 9 basis vectors + the
+// diagonal = 500 of the 512 columns (one CTA per SM). The CTAs take the groups in order (the
+// longest-first permutation is made for the other solvers' group size).
+template <int N, bool SWEEP>
+cudaError_t gmres_n(int method, const KParams& kp0, const double* in, const double* f, double* out,
+                    cudaStream_t s) {
+  if constexpr (N <= 5) {
+    KParams kp = kp0;
+    kp.gperm = nullptr;
+    using G = pk::Geo<N>;
+    const int grid = split_groups(kp, G::C);
+    if (grid == 0) return cudaSuccess;
+    constexpr int KR = N == 5 ? 9 : N == 4 ? 15 : N == 3 ? 13 : 15;
+    if (method == LM_GMRES)
+      return launch(pk::k_gmres<N, SWEEP, false, KR>, grid, G::NT, pk::smem_gmres<N, KR>(false), s, kp, in, f, out);
+    if (method == LM_GMRES_THOMAS)
+      return launch(pk::k_gmres<N, SWEEP, true, KR>, grid, G::NT, pk::smem_gmres<N, KR>(true), s, kp, in, f, out);
+  }
+  return cudaErrorInvalidValue;
+}
+
 template <int N, bool SWEEP>
 cudaError_t solve_n(int method, const KParams& kp0, const double* in, const double* f, double* out,
                     cudaStream_t s) {
@@ -2923,17 +2950,12 @@ cudaError_t solve_n(int method, const KParams& kp0, const double* in, const doub
       }
       if (method == LM_BICGSTAB_THOMAS)
         return launch(pk::k_bicgstab<N, SWEEP, true>, grid, G::NT, pk::smem_solve<N>(7), s, kp, in, f, out);
-      {
-        // restarted GMRES(KR), Krylov basis + diagonal in TMEM (compact colour maps not
-        // supported: the SOR half-sweeps run masked). KR fills 256 TMEM columns at n = 2, 3
-        // (two CTAs per SM) and all 512 at n = 4 (one CTA per SM: GMRES(7) with two CTAs was
-        // faster on C4, 13.3 vs 14.8 ms, but stalls at cell Peclet 1.8e4; profiles/r01_ab.md);
-        // n = 5: 9 basis vectors + the diagonal = 500 of the 512 columns (one CTA per SM)
-        constexpr int KR = N == 5 ? 9 : N == 4 ? 15 : N == 3 ? 13 : 15;
-        if (method == LM_GMRES)
-          return launch(pk::k_gmres<N, SWEEP, false, KR>, grid, G::NT, pk::smem_gmres<N, KR>(false), s, kp, in, f, out);
-        if (method == LM_GMRES_THOMAS)
-          return launch(pk::k_gmres<N, SWEEP, true, KR>, grid, G::NT, pk::smem_gmres<N, KR>(true), s, kp, in, f, out);
+      if (method == LM_GMRES || method == LM_GMRES_THOMAS) {
+        // n <= 4: the GMRES kernels come from their own translation unit (dg_kernels_gmres.cu),
+        // compiled with four-warp plane CTAs: the basis fills 256 / 512 TMEM columns, and a
+        // CTA's warps reach only their own lane quadrants, so a CTA must span all four
+        if constexpr (N <= 4 && !DG_GMRES_TU) return solve_gmres(N - 1, method, SWEEP, kp0, in, f, out, s);
+        else return gmres_n<N, SWEEP>(method, kp0, in, f, out, s);
       }
       if constexpr (N <= 4) {
         if (method == LM_BICGSTAB) {

@@ -41,14 +41,18 @@ namespace pk {
 template <int N> struct PL;
 // KS/CTB: transpose-buffer plane / cell strides; QS/PS: plane / cell strides of the per-lane
 // plane storage (X, diag, ...). All chosen by an offline search for conflict-free lane patterns.
+// warps (cell groups of 32 / n cells each) per plane CTA: two (measured: C4 BiCGStab sweep
+// 5490 / 4306 / 4155 us with 4 / 3 / 2 warps, C2 CG sweep 340 / 304 / 276, C5 apply 644 / - / 587,
+// p = 1 apply 192 / - / 178; four warps needed 119 KB of shared memory per CTA at n = 4: one CTA,
+// 4 warps per SM); the local GMRES keeps four (dg_kernels_gmres.cu: tensor-memory lane quadrants)
 #ifndef DG_PL_WARPS2
-#define DG_PL_WARPS2 4
+#define DG_PL_WARPS2 2
 #endif
 #ifndef DG_PL_WARPS3
-#define DG_PL_WARPS3 4
+#define DG_PL_WARPS3 2
 #endif
 #ifndef DG_PL_WARPS4
-#define DG_PL_WARPS4 4
+#define DG_PL_WARPS4 2
 #endif
 #ifndef DG_PL_WARPS5
 #define DG_PL_WARPS5 2
