@@ -1786,8 +1786,13 @@ k_volume(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
 #ifndef DG_VOL4_MINB
 #define DG_VOL4_MINB 4
 #endif
+#ifndef DG_VOL4_MINB_GEN
+// the convective / reaction instantiation with two-warp CTAs: eight per SM (C4 volume 97.9 ->
+// 95.4 us, 0.51); the same bound for diffusion costs the L2-resident C2 (14.0 -> 17.6 us)
+#define DG_VOL4_MINB_GEN 8
+#endif
 template <int N, bool GEN = true>
-__global__ void __launch_bounds__(Geo<N>::NT, DG_VOL4_MINB)
+__global__ void __launch_bounds__(Geo<N>::NT, GEN ? DG_VOL4_MINB_GEN : DG_VOL4_MINB)
 k_volume_s(KParams kp, const double* __restrict__ u, double* __restrict__ out) {
   using G = Geo<N>;
   extern __shared__ double sm[];
