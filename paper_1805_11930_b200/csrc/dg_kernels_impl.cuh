@@ -255,23 +255,29 @@ template <int N> __host__ __device__ constexpr bool fold_volume() { return (DG_F
 // Needs g.fc, g.vc, g.vb; ends with a barrier.
 template <int N, int NTH = Geo<N>::NT, int CC> __device__ void self_face_ops(const KParams& kp, Group<N, CC>& g) {
   using G = Geo<N, CC>;
-  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
-    const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
-    const int q = (rem % (N * N)) / N, r = rem % N;
+  // one thread per row (cs, a, q), the row's entries unrolled (compile-time table columns: at
+  // most n distinct constant-bank addresses per warp-wide load, see nodal_face_ops)
+  for (int it = threadIdx.x; it < G::C * 3 * N; it += NTH) {
+    const int cs = it / (3 * N), rem = it % (3 * N), a = rem / N, q = rem % N;
     const double* lo = g.fc[cs][2 * a];
     const double* hi = g.fc[cs][2 * a + 1];
     const double ih = kp.ih[a];   // 1 / h_a (host-computed, identical IEEE quotient)
     const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
-    double b = c_tab[N].E0[q] * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) + c_tab[N].F0[q] * lo[4] * c_tab[N].E0[r];
-    b += c_tab[N].E1[q] * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) + c_tab[N].F1[q] * hi[4] * c_tab[N].E1[r];
-    double t = area * b;
-    if constexpr (fold_volume<N>()) {
-      t = fma(g.vc[cs][a], c_tab[N].SG[q * N + r], t);
-      t = fma(-g.vb[cs][a], c_tab[N].CG[q * N + r], t);
-      if (a == 2 && q == r) t = fma(g.vc[cs][3], c_tab[N].w[q], t);
+    const double e0q = c_tab[N].E0[q], f0q = c_tab[N].F0[q], e1q = c_tab[N].E1[q], f1q = c_tab[N].F1[q];
+    const double vk = g.vc[cs][a], vb = g.vb[cs][a], vr = g.vc[cs][3], wq = c_tab[N].w[q];
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      double b = e0q * (lo[0] * c_tab[N].E0[r] + lo[1] * ih * c_tab[N].F0[r]) + f0q * lo[4] * c_tab[N].E0[r];
+      b += e1q * (hi[0] * c_tab[N].E1[r] + hi[1] * ih * c_tab[N].F1[r]) + f1q * hi[4] * c_tab[N].E1[r];
+      double t = area * b;
+      if constexpr (fold_volume<N>()) {
+        t = fma(vk, c_tab[N].SG[q * N + r], t);
+        t = fma(-vb, c_tab[N].CG[q * N + r], t);
+        if (a == 2 && q == r) t = fma(vr, wq, t);
+      }
+      g.Bf[cs][a][q * Group<N, CC>::BR + r] = t;
     }
-    g.Bf[cs][a][q * Group<N, CC>::BR + r] = t;
-    if (r == N - 1 && (N & 1)) g.Bf[cs][a][q * Group<N, CC>::BR + N] = 0.0;   // the pad
+    if (N & 1) g.Bf[cs][a][q * Group<N, CC>::BR + N] = 0.0;   // the pad
   }
   __syncthreads();
 }
@@ -285,22 +291,30 @@ template <int N, int NTH = Geo<N>::NT, int CC> __device__ void self_face_ops(con
 // i.e. A^T Bf_a A of the Gauss-point line operators. Stored in g.Bf (rows of stride BR).
 template <int N, int NTH = Geo<N>::NT, int CC> __device__ void nodal_face_ops(const KParams& kp, Group<N, CC>& g) {
   using G = Geo<N, CC>;
-  for (int it = threadIdx.x; it < G::C * 3 * N * N; it += NTH) {
-    const int cs = it / (3 * N * N), rem = it % (3 * N * N), a = rem / (N * N);
-    const int i = (rem % (N * N)) / N, ip = rem % N;
+  // one thread per row (cs, a, i), the row's entries unrolled: the 1D tables are then read with
+  // a compile-time column, i.e. at most n distinct constant-bank addresses per warp-wide load
+  // (one thread per entry: up to 32, serialised by the constant cache; C3 D_T 490 -> 279 us)
+  for (int it = threadIdx.x; it < G::C * 3 * N; it += NTH) {
+    const int cs = it / (3 * N), rem = it % (3 * N), a = rem / N, i = rem % N;
     const double* lo = g.fc[cs][2 * a];
     const double* hi = g.fc[cs][2 * a + 1];
     const double ih = kp.ih[a];
     const double area = a == 0 ? kp.h[1] * kp.h[2] : (a == 1 ? kp.h[0] * kp.h[2] : kp.h[0] * kp.h[1]);
-    const double e0i = i == 0, e0p = ip == 0, e1i = i == N - 1, e1p = ip == N - 1;
-    double f = e0i * (lo[0] * e0p + lo[1] * ih * c_tab[N].d0[ip]) + lo[4] * c_tab[N].d0[i] * e0p;
-    f += e1i * (hi[0] * e1p + hi[1] * ih * c_tab[N].d1[ip]) + hi[4] * c_tab[N].d1[i] * e1p;
-    double t = area * f;
-    t = fma(g.vc[cs][a], c_tab[N].S[i * N + ip], t);
-    t = fma(-g.vb[cs][a], c_tab[N].Cm[i * N + ip], t);
-    if (a == 2) t = fma(g.vc[cs][3], c_tab[N].M[i * N + ip], t);
-    g.Bf[cs][a][i * Group<N, CC>::BR + ip] = t;
-    if (ip == N - 1 && (N & 1)) g.Bf[cs][a][i * Group<N, CC>::BR + N] = 0.0;
+    const double e0i = i == 0, e1i = i == N - 1;
+    const double d0i = c_tab[N].d0[i], d1i = c_tab[N].d1[i];
+    const double vk = g.vc[cs][a], vb = g.vb[cs][a], vr = g.vc[cs][3];
+#pragma unroll
+    for (int ip = 0; ip < N; ++ip) {
+      const double e0p = ip == 0, e1p = ip == N - 1;
+      double f = e0i * (lo[0] * e0p + lo[1] * ih * c_tab[N].d0[ip]) + lo[4] * d0i * e0p;
+      f += e1i * (hi[0] * e1p + hi[1] * ih * c_tab[N].d1[ip]) + hi[4] * d1i * e1p;
+      double t = area * f;
+      t = fma(vk, c_tab[N].S[i * N + ip], t);
+      t = fma(-vb, c_tab[N].Cm[i * N + ip], t);
+      if (a == 2) t = fma(vr, c_tab[N].M[i * N + ip], t);
+      g.Bf[cs][a][i * Group<N, CC>::BR + ip] = t;
+    }
+    if (N & 1) g.Bf[cs][a][i * Group<N, CC>::BR + N] = 0.0;   // the pad
   }
   __syncthreads();
 }
@@ -1455,6 +1469,39 @@ k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out
 }
 template <int N, int CC> constexpr size_t apply_warps_smem() {
   return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)CC * N * N);
+}
+
+// D_T u (dg_block_diag_apply: the volume and self-face terms of each cell) with one
+// warp per cell in the nodal Kronecker-sum form of the local CG's operator (dt_nodal, WARP mode;
+// the factors K_a of nodal_face_ops): the own x-line from global memory straight into registers,
+// the result from registers to global memory, two work tensors in shared memory. Replaces the
+// Gauss-point line kernel k_apply<N, false, true> at n = 5 (C3 D_T: 569 us, 0.29 of the fp64 peak).
+template <int N, bool GEN, int CC>
+__global__ void __launch_bounds__(CC * 32)
+k_dt_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
+  using G = Geo<N, CC>;
+  static_assert(G::N2 <= 32, "one warp per cell");
+  __shared__ Group<N, CC> g;
+  extern __shared__ double sm[];
+  double* SA = sm;
+  double* SB = SA + G::TENSOR;
+  const int cell0 = block_group(kp, false) * CC;
+  const int nvalid = min(CC, kp.ncells - cell0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = threadIdx.x, cs = t >> 5, l = t & 31;
+  const bool act = l < G::N2 && cs < nvalid;
+  double ownl[N], q[N];
+  if (act) {
+    ld<N, 1>(u + (size_t)(cell0 + cs) * G::N3 + (l / N) * G::N2 + (l % N) * N, ownl);
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) ownl[e] = 0.0;
+  }
+  group_setup<N, CC * 32>(kp, g, cell0, nullptr);   // coefficients only; ends with __syncthreads
+  nodal_face_ops<N, CC * 32>(kp, g);                // K_x, K_y, K_z per cell; ends with __syncthreads
+  dt_nodal<N, true, 0, GEN>(g, SA, SB, ownl, q, &kp);
+  if (act) stg_line<N>(out + (size_t)(cell0 + cs) * G::N3 + (l / N) * G::N2 + (l % N) * N, q);
 }
 
 template <int N, int CC> constexpr size_t apply_nodal_smem() {
@@ -2862,6 +2909,32 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
       return cudaLaunchKernelEx(&cfg, ke, ka, u, out, with_nbr);
     }
   }
+#ifndef DG_DT_WARPS5
+#define DG_DT_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal D_T (0: off)
+#endif
+  if constexpr (N == 5 && DG_DT_WARPS5 > 0) {
+    if (kp.mask == 7u && !with_nbr && !force_line(kp)) {
+      constexpr int CC = DG_DT_WARPS5;
+      KParams ka = kp0;
+      const int grida = split_groups(ka, CC);
+      if (grida == 0) return cudaSuccess;
+      const size_t smem = sizeof(double) * 2 * (size_t)Geo<N, CC>::TENSOR;
+      auto ke = gen_terms(kp) ? k_dt_warps<N, true, CC> : k_dt_warps<N, false, CC>;
+      cudaError_t e = set_smem(ke, smem);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grida);
+      cfg.blockDim = dim3(CC * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, ke, ka, u, out, with_nbr);
+    }
+  }
   // (each kernel above splits the groups by its own group size: an early return on the group
   // count of G::C would skip its launch when that count is 0)
   const int grid = split_groups(kp, G::C);
@@ -3091,6 +3164,7 @@ template <int N> constexpr int group_lcm_n() {
   l = lcm_c(l, DG_VOLUME_CELLS);
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
+  if constexpr (N == 5 && DG_DT_WARPS5 > 0) l = lcm_c(l, DG_DT_WARPS5);
   if constexpr (N == 4 && DG_APPLY_WARPS4 > 0) l = lcm_c(l, DG_APPLY_WARPS4);
   if constexpr (N == 3 && DG_APPLY_WARPS3 > 0) l = lcm_c(l, DG_APPLY_WARPS3);
   if constexpr (N <= 5) l = lcm_c(l, pk::Geo<N>::C);

@@ -152,3 +152,22 @@ def test_unknown_variant_rejected():
     with dg.DGContext(P) as ctx:
         with pytest.raises(dg.DGError):
             ctx.set_kernel_variant(1 << 8)
+
+
+# ---- the warp-mode nodal D_T at p = 4 (k_dt_warps): ragged last CTA, slab-free and both term sets
+@pytest.mark.parametrize("gen", [False, True], ids=["diffusion", "conv-reaction"])
+@pytest.mark.parametrize("mesh", [(5, 3, 3), (7, 5, 3)], ids=["45cells", "105cells"])
+def test_block_diag_warp_kernel_p4_every_dof(gen, mesh):
+    P = random_problem(*mesh, 4, seed=510, spread=1.5, b=(0.7, -0.4, 0.3) if gen else (0, 0, 0),
+                       c=gen, bc=MIXED if gen else (DIRICHLET,) * 6, L=(1.0, 0.7, 1.3))
+    if gen:
+        P.b_cells = np.random.default_rng(5).normal(size=(P.n_cells, 3))
+    u, _ = vec(P, 61)
+    ref = TierB(P).block_diag_apply(u).reshape(-1)
+    for variant in (0, dg.DG_VARIANT_LINE):
+        with dg.DGContext(P) as ctx:
+            ctx.set_kernel_variant(variant)
+            out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+            ctx.block_diag_apply(cuda(u), out)
+            got = host(out)
+        assert rel(got, ref) <= APPLY_TOL, variant
