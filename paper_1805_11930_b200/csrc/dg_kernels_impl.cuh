@@ -513,7 +513,22 @@ __device__ __forceinline__ void nbr_lines_prefetch(const KParams& kp, const doub
 // INPLACE: src may be overwritten (A u alone): after the x stage has read a thread's own line, the
 // z-face arrays after Mhat_x go there (4 < n entries per line) and FA shrinks to 8 C n^2
 // W (optional): the y / z neighbour lines prefetched by nbr_lines_prefetch
-template <int N, int NTH, bool GEN, bool INPLACE = false, bool WARP = false, class Out, int CC>
+// RS: row stride of the face arrays (N: the dense [n][n] layout; an even RS > N: 16-byte aligned
+// rows read as 128-bit pairs, and the z-face arrays after Mhat_x stored transposed so that the y
+// stage reads them as rows too)
+template <int N> __device__ __forceinline__ void ld_row(const double* p, double* v) {
+#pragma unroll
+  for (int e = 0; e < N; e += 2) {
+    if (e + 1 < N) {
+      const double2 t = *reinterpret_cast<const double2*>(p + e);
+      v[e] = t.x;
+      v[e + 1] = t.y;
+    } else {
+      v[e] = p[e];
+    }
+  }
+}
+template <int N, int NTH, bool GEN, bool INPLACE = false, bool WARP = false, int RS = N, class Out, int CC>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out,
                                             const NbrLines<N>* W = nullptr, const double* own = nullptr) {
@@ -527,14 +542,18 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
   const bool act = WARP ? (t % WL) < N2 : t < G::LINES;
   const int cs = WARP ? t / WL : (act ? t / N2 : 0), l = WARP ? (t % WL) : t % N2, a = l % N, bb = l / N;
   auto sync = [] { if constexpr (WARP) __syncwarp(); else __syncthreads(); };
-  double* FY = FA;                  // [C][4][n^2]: y faces S_lo, T_lo, S_hi, T_hi at (i, k)
-  double* FZ = FA + 4 * C * N2;     // [C][4][n^2]: z faces at (i, j); reused after Mhat_y
-  double* FZb = FA + 8 * C * N2;    // [C][4][n^2]: z faces after Mhat_x (not with INPLACE)
+  constexpr bool ROWS = RS != N;
+  static_assert(!ROWS || (RS % 2 == 0 && RS > N && !INPLACE), "padded rows: even, 16-byte aligned");
+  constexpr int AS = N * RS;        // one face array
+  double* FY = FA;                  // [C][4][n][RS]: y faces S_lo, T_lo, S_hi, T_hi at (i, k), row k
+  double* FZ = FA + 4 * C * AS;     // [C][4][n][RS]: z faces at (i, j), row j; reused after Mhat_y
+  double* FZb = FA + 8 * C * AS;    // [C][4][n][RS]: z faces after Mhat_x (not with INPLACE; ROWS: row i)
   static_assert(!INPLACE || N > 4, "INPLACE: the four face arrays fit in an x-line");
   // z-face entry (i, j) of array q after Mhat_x: in FZb, or (INPLACE) in the tile's x-line
   // (j' = i, k' = j), i.e. the line of the thread that produces the entry
   auto fzb = [&](int cs_, int q, int j, int i) -> double& {
     if constexpr (INPLACE) return const_cast<double*>(src)[cs_ * G::CS + j * G::ZS + i * G::YS + q];
+    else if constexpr (ROWS) return FZb[cs_ * 4 * AS + q * AS + i * RS + j];
     else return FZb[cs_ * 4 * N2 + q * N2 + j * N + i];
   };
   const int base = cs * G::CS;
@@ -605,8 +624,8 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         s1 = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[1]);
         t1 = chi[5] * w[0];
       }
-      double* fy = FY + cs * 4 * N2 + bb * N + a;
-      fy[0] = s0; fy[N2] = t0; fy[2 * N2] = s1; fy[3 * N2] = t1;
+      double* fy = FY + cs * 4 * AS + bb * RS + a;
+      fy[0] = s0; fy[AS] = t0; fy[2 * AS] = s1; fy[3 * AS] = t1;
     }
     // z faces at (i = a, j = bb); at a slab boundary the neighbour is a ghost trace record
     {
@@ -656,8 +675,8 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         s1 = fma(chi[2], av, (chi[3] * gn) * kp.ih[2]);
         t1 = chi[5] * av;
       }
-      double* fz = FZ + cs * 4 * N2 + bb * N + a;
-      fz[0] = s0; fz[N2] = t0; fz[2 * N2] = s1; fz[3 * N2] = t1;
+      double* fz = FZ + cs * 4 * AS + bb * RS + a;
+      fz[0] = s0; fz[AS] = t0; fz[2 * AS] = s1; fz[3 * AS] = t1;
     }
   }
   sync();
@@ -680,10 +699,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     st<N, 1>(SB + base + bb * G::ZS + a * G::YS, cv);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {   // z-face arrays along x: entry (i = a, j = bb)
-      const double* row = FZ + cs * 4 * N2 + q * N2 + bb * N;
+      const double* row = FZ + cs * 4 * AS + q * AS + bb * RS;
+      double rv[N];
+      if constexpr (ROWS) ld_row<N>(row, rv); else ld<N, 1>(row, rv);
       double zs = 0.0;
 #pragma unroll
-      for (int ip = 0; ip < N; ++ip) zs = fma(c_tab[N].M[a * N + ip], row[ip], zs);
+      for (int ip = 0; ip < N; ++ip) zs = fma(c_tab[N].M[a * N + ip], rv[ip], zs);
       fzb(cs, q, bb, a) = zs;
     }
   }
@@ -701,10 +722,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     double yq[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const double* row = FY + cs * 4 * N2 + q * N2 + bb * N;
+      const double* row = FY + cs * 4 * AS + q * AS + bb * RS;
+      double rv[N];
+      if constexpr (ROWS) ld_row<N>(row, rv); else ld<N, 1>(row, rv);
       double s = 0.0;
 #pragma unroll
-      for (int ip = 0; ip < N; ++ip) s = fma(c_tab[N].M[a * N + ip], row[ip], s);
+      for (int ip = 0; ip < N; ++ip) s = fma(c_tab[N].M[a * N + ip], rv[ip], s);
       yq[q] = s;
     }
     const double fa = kp.fa[1];
@@ -715,10 +738,17 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     // z-face arrays along y (entry (i = a, j = bb)) -> FZ (free again)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      double rv[N];
+      if constexpr (ROWS) {
+        ld_row<N>(FZb + cs * 4 * AS + q * AS + a * RS, rv);
+      } else {
+#pragma unroll
+        for (int jp = 0; jp < N; ++jp) rv[jp] = fzb(cs, q, jp, a);
+      }
       double s = 0.0;
 #pragma unroll
-      for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[bb * N + jp], fzb(cs, q, jp, a), s);
-      FZ[cs * 4 * N2 + q * N2 + bb * N + a] = s;
+      for (int jp = 0; jp < N; ++jp) s = fma(c_tab[N].M[bb * N + jp], rv[jp], s);
+      FZ[cs * 4 * AS + q * AS + bb * RS + a] = s;
     }
     st<N, G::YS>(SA + off, dv);
     st<N, G::YS>(SB + off, ev);
@@ -732,8 +762,8 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     ld<N, G::ZS>(SB + off, gv);
     mv<N, 2>(gv, o1);
     kfly<N, GEN>(kp, g, cs, 2, dv, o2);
-    const double* fz = FZ + cs * 4 * N2 + bb * N + a;
-    const double z0 = fz[0], z1 = fz[N2], z2 = fz[2 * N2], z3 = fz[3 * N2];
+    const double* fz = FZ + cs * 4 * AS + bb * RS + a;
+    const double z0 = fz[0], z1 = fz[AS], z2 = fz[2 * AS], z3 = fz[3 * AS];
     const double fa = kp.fa[2];
 #pragma unroll
     for (int e = 0; e < N; ++e)
@@ -1433,6 +1463,15 @@ k_apply_nodal(KParams kp, const double* __restrict__ u, double* __restrict__ out
 #define DG_APPLYW_MINB 0
 #endif
 template <int N> __host__ __device__ constexpr int warp_lanes() { return N * N <= 16 ? 16 : 32; }   // lanes per cell
+#ifndef DG_APPLYW_ROWS
+// bit n: the warp-mode apply's face arrays in padded 16-byte rows (apply_nodal RS). Off: the
+// row reads are 2-wavefront LDS.64 with 5 distinct addresses per warp either way, and the 128-bit
+// pairs did not halve them (C3 apply 493 -> 511 us; the face-row contractions are 36 % of the
+// kernel's shared-memory wavefronts, ncu)
+#define DG_APPLYW_ROWS 0
+#endif
+// face-array row stride of the warp-mode apply (N + 1 rounded up to even where enabled)
+template <int N> __host__ __device__ constexpr int apply_warps_rs() { return ((DG_APPLYW_ROWS >> N) & 1) ? ((N + 2) & ~1) : N; }
 template <int N, bool GEN, int CC>
 __global__ void __launch_bounds__(CC * warp_lanes<N>(), DG_APPLYW_MINB)
 k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
@@ -1463,12 +1502,12 @@ k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out
   }
   group_setup<N, CC * WL>(kp, g, cell0, u);  // ends with __syncthreads
   double* o = out + (size_t)cell0 * G::N3;
-  apply_nodal<N, CC * WL, GEN, false, true>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
+  apply_nodal<N, CC * WL, GEN, false, true, apply_warps_rs<N>()>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
     if (c < nvalid) stg_line<N>(o + c * G::N3 + k * G::N2 + j * N, w);
   }, nullptr, ownl);
 }
 template <int N, int CC> constexpr size_t apply_warps_smem() {
-  return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)CC * N * N);
+  return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)CC * N * apply_warps_rs<N>());
 }
 
 // D_T u (dg_block_diag_apply: the volume and self-face terms of each cell) with one

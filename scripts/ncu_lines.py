@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: python scripts/ncu_lines.py REPORT.ncu-rep LIB.so KERNEL_SUBSTRING [--launch N] [--top K]
+usage: python scripts/ncu_lines.py REPORT.ncu-rep LIB.so KERNEL_SUBSTRING [--launch N] [--top K] [--metric COLUMN]
 
 The SASS page of the report (per-instruction samples) is joined with the line table of the
 kernel's cubin (nvdisasm -gi, from the -lineinfo build) and summed per source line, both for
@@ -68,7 +68,9 @@ def main():
         if re.search(ksub, rows[st][1]):
             blocks.append((rows[st][1], rows[st + 1], [r for r in rows[st + 2:end] if r]))
     kname, h, data = blocks[launch]
-    iS = h.index("Warp Stall Sampling (All Samples)")
+    # --metric COLUMN: sum that SASS-page column instead of the stall samples (e.g. "L1 Wavefronts Shared")
+    metric = sys.argv[sys.argv.index("--metric") + 1] if "--metric" in sys.argv else "Warp Stall Sampling (All Samples)"
+    iS = h.index(metric)
     stall_cols = [i for i, x in enumerate(h) if x.startswith("stall_") and "Not Issued" not in x]
 
     # the mangled name is not in the report; match the cubin function by instruction count
