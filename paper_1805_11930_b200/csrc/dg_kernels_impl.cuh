@@ -528,7 +528,9 @@ template <int N> __device__ __forceinline__ void ld_row(const double* p, double*
     }
   }
 }
-template <int N, int NTH, bool GEN, bool INPLACE = false, bool WARP = false, int RS = N, class Out, int CC>
+// SHUF (WARP mode): the face arrays' tangential-mass contractions take the other face nodes' values
+// from their lanes by warp shuffles instead of shared memory (the face arrays are not used)
+template <int N, int NTH, bool GEN, bool INPLACE = false, bool WARP = false, int RS = N, bool SHUF = false, class Out, int CC>
 __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC>& g, const double* src,
                                             double* SA, double* SB, double* FA, Out out,
                                             const NbrLines<N>* W = nullptr, const double* own = nullptr) {
@@ -560,6 +562,11 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
   // (the face sums are written as explicit fma: the ghost-record and in-slab branches then round
   // alike whatever the compiler contracts, so slab partitions stay bit for bit)
   double sxl = 0.0, txl = 0.0, sxh = 0.0, txh = 0.0;
+  static_assert(!SHUF || WARP, "shuffles: one cell per (half-)warp");
+  // SHUF: this lane's y- and z-face values (S_lo, T_lo, S_hi, T_hi), the lane of face node
+  // (i, k) resp. (i, j) = (a, bb) being lb + bb n + a
+  double yf[4] = {0.0, 0.0, 0.0, 0.0}, zf[4] = {0.0, 0.0, 0.0, 0.0};
+  const int lb = (t & 31) & ~(WL - 1);
   // ---- stage 0: the neighbours' face data at this thread's face nodes
   if (act) {
     // x faces at (j = a, k = bb): the neighbours' x-lines (in the group: from the tile)
@@ -624,8 +631,12 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         s1 = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[1]);
         t1 = chi[5] * w[0];
       }
-      double* fy = FY + cs * 4 * AS + bb * RS + a;
-      fy[0] = s0; fy[AS] = t0; fy[2 * AS] = s1; fy[3 * AS] = t1;
+      if constexpr (SHUF) {
+        yf[0] = s0; yf[1] = t0; yf[2] = s1; yf[3] = t1;
+      } else {
+        double* fy = FY + cs * 4 * AS + bb * RS + a;
+        fy[0] = s0; fy[AS] = t0; fy[2 * AS] = s1; fy[3 * AS] = t1;
+      }
     }
     // z faces at (i = a, j = bb); at a slab boundary the neighbour is a ghost trace record
     {
@@ -675,11 +686,30 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
         s1 = fma(chi[2], av, (chi[3] * gn) * kp.ih[2]);
         t1 = chi[5] * av;
       }
-      double* fz = FZ + cs * 4 * AS + bb * RS + a;
-      fz[0] = s0; fz[AS] = t0; fz[2 * AS] = s1; fz[3 * AS] = t1;
+      if constexpr (SHUF) {
+        zf[0] = s0; zf[1] = t0; zf[2] = s1; zf[3] = t1;
+      } else {
+        double* fz = FZ + cs * 4 * AS + bb * RS + a;
+        fz[0] = s0; fz[AS] = t0; fz[2 * AS] = s1; fz[3 * AS] = t1;
+      }
     }
   }
   sync();
+  // SHUF: the z-face arrays after Mhat_x at (i = a, j = bb), all lanes taking part
+  double zx[4] = {0.0, 0.0, 0.0, 0.0};
+  if constexpr (SHUF) {
+    const int ia = act ? a : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double zs = 0.0;
+#pragma unroll
+      for (int ip = 0; ip < N; ++ip) {
+        const double v = __shfl_sync(0xffffffffu, zf[q], lb + bb * N + ip);
+        zs = fma(c_tab[N].M[ia * N + ip], v, zs);
+      }
+      zx[q] = zs;
+    }
+  }
   // ---- x stage (x-line j = a, k = bb): b = Mhat u, c = Kx u + x faces; z faces: Mhat_x
   if (act) {
     double u[N], bv[N], cv[N];
@@ -698,7 +728,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     st<N, 1>(SA + base + bb * G::ZS + a * G::YS, bv);
     st<N, 1>(SB + base + bb * G::ZS + a * G::YS, cv);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {   // z-face arrays along x: entry (i = a, j = bb)
+    for (int q = 0; q < 4 && !SHUF; ++q) {   // z-face arrays along x: entry (i = a, j = bb)
       const double* row = FZ + cs * 4 * AS + q * AS + bb * RS;
       double rv[N];
       if constexpr (ROWS) ld_row<N>(row, rv); else ld<N, 1>(row, rv);
@@ -709,6 +739,28 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     }
   }
   sync();
+  // SHUF: the y-face arrays after Mhat_x at (i = a, k = bb) and the z-face arrays after Mhat_x,
+  // Mhat_y at (i = a, j = bb)
+  double yqs[4] = {0.0, 0.0, 0.0, 0.0}, zy[4] = {0.0, 0.0, 0.0, 0.0};
+  if constexpr (SHUF) {
+    const int ia = act ? a : 0, ib = act ? bb : 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double s = 0.0, z = 0.0;
+#pragma unroll
+      for (int ip = 0; ip < N; ++ip) {
+        const double v = __shfl_sync(0xffffffffu, yf[q], lb + bb * N + ip);
+        s = fma(c_tab[N].M[ia * N + ip], v, s);
+      }
+#pragma unroll
+      for (int jp = 0; jp < N; ++jp) {
+        const double v = __shfl_sync(0xffffffffu, zx[q], lb + jp * N + a);
+        z = fma(c_tab[N].M[ib * N + jp], v, z);
+      }
+      yqs[q] = s;
+      zy[q] = z;
+    }
+  }
   // ---- y stage (y-line i = a, k = bb): d = Mhat b, g = Ky b + Mhat c + y faces (after Mhat_x);
   // z faces: Mhat_y
   if (act) {
@@ -722,6 +774,10 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     double yq[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      if constexpr (SHUF) {
+        yq[q] = yqs[q];
+        continue;
+      }
       const double* row = FY + cs * 4 * AS + q * AS + bb * RS;
       double rv[N];
       if constexpr (ROWS) ld_row<N>(row, rv); else ld<N, 1>(row, rv);
@@ -737,7 +793,7 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
                              (e == N - 1 ? yq[2] : 0.0));
     // z-face arrays along y (entry (i = a, j = bb)) -> FZ (free again)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < 4 && !SHUF; ++q) {
       double rv[N];
       if constexpr (ROWS) {
         ld_row<N>(FZb + cs * 4 * AS + q * AS + a * RS, rv);
@@ -763,7 +819,8 @@ __device__ __forceinline__ void apply_nodal(const KParams& kp, const Group<N, CC
     mv<N, 2>(gv, o1);
     kfly<N, GEN>(kp, g, cs, 2, dv, o2);
     const double* fz = FZ + cs * 4 * AS + bb * RS + a;
-    const double z0 = fz[0], z1 = fz[AS], z2 = fz[2 * AS], z3 = fz[3 * AS];
+    const double z0 = SHUF ? zy[0] : fz[0], z1 = SHUF ? zy[1] : fz[AS], z2 = SHUF ? zy[2] : fz[2 * AS],
+                 z3 = SHUF ? zy[3] : fz[3 * AS];
     const double fa = kp.fa[2];
 #pragma unroll
     for (int e = 0; e < N; ++e)
@@ -1471,6 +1528,13 @@ template <int N> __host__ __device__ constexpr int warp_lanes() { return N * N <
 #define DG_APPLYW_ROWS 0
 #endif
 // face-array row stride of the warp-mode apply (N + 1 rounded up to even where enabled)
+#ifndef DG_APPLYW_SHFL
+// bit n: the warp-mode apply's face contractions by shuffles (apply_nodal SHUF). Off: the
+// shuffles cost the same pipe as the shared-memory face arrays they replace and raise the
+// registers (C3 apply 493 -> 529 us at 80 registers, 503 us capped at 64; C2 32.9 -> 34.2 us)
+#define DG_APPLYW_SHFL 0
+#endif
+template <int N> __host__ __device__ constexpr bool apply_warps_shfl() { return (DG_APPLYW_SHFL >> N) & 1; }
 template <int N> __host__ __device__ constexpr int apply_warps_rs() { return ((DG_APPLYW_ROWS >> N) & 1) ? ((N + 2) & ~1) : N; }
 template <int N, bool GEN, int CC>
 __global__ void __launch_bounds__(CC * warp_lanes<N>(), DG_APPLYW_MINB)
@@ -1502,12 +1566,12 @@ k_apply_warps(KParams kp, const double* __restrict__ u, double* __restrict__ out
   }
   group_setup<N, CC * WL>(kp, g, cell0, u);  // ends with __syncthreads
   double* o = out + (size_t)cell0 * G::N3;
-  apply_nodal<N, CC * WL, GEN, false, true, apply_warps_rs<N>()>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
+  apply_nodal<N, CC * WL, GEN, false, true, apply_warps_rs<N>(), apply_warps_shfl<N>()>(kp, g, SA, SA, SB, FB, [&](int c, int j, int k, const double* w) {
     if (c < nvalid) stg_line<N>(o + c * G::N3 + k * G::N2 + j * N, w);
   }, nullptr, ownl);
 }
 template <int N, int CC> constexpr size_t apply_warps_smem() {
-  return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + 12 * (size_t)CC * N * apply_warps_rs<N>());
+  return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + (apply_warps_shfl<N>() ? 0 : 12 * (size_t)CC * N * apply_warps_rs<N>()));
 }
 
 // D_T u (dg_block_diag_apply: the volume and self-face terms of each cell) with one
