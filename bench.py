@@ -543,6 +543,40 @@ def run_ours(args):
                 out_pin[zb * lay:ze * lay].copy_(src[zb * lay:ze * lay], non_blocking=True)
         stream.wait_stream(out_stream)
 
+    copy_stream2 = torch.cuda.Stream(device=dev)
+
+    def e2e_interleaved():
+        """Per z-layer chunk k: upload u_k (copy stream) and f_k (a second copy stream with
+        --e2e-streams 2, else the same one), then chunk k's applies and its sweep (the sweep
+        writes the other vector, so the later chunks' applies still read the uploaded u; the
+        applies' and the sweep's face neighbours in chunk k + 1 are resident first), then its
+        read-back. The same work as the serial step, scheduled chunk by chunk (one sweep)."""
+        K = len(chunks)
+        ev_u = [torch.cuda.Event() for _ in range(K)]
+        ev_f = [torch.cuda.Event() for _ in range(K)]
+        ev_s = [torch.cuda.Event() for _ in range(K)]
+        fs = copy_stream2 if args.e2e_streams == 2 else copy_stream
+        copy_stream.wait_stream(stream)
+        fs.wait_stream(stream)
+        for k, (zb, ze) in enumerate(chunks):
+            with torch.cuda.stream(copy_stream):
+                ua[zb * lay:ze * lay].copy_(u_pin[zb * lay:ze * lay], non_blocking=True)
+                ev_u[k].record(copy_stream)
+            with torch.cuda.stream(fs):
+                f_dev[zb * lay:ze * lay].copy_(f_pin[zb * lay:ze * lay], non_blocking=True)
+                ev_f[k].record(fs)
+        for k, (zb, ze) in enumerate(chunks):
+            stream.wait_event(ev_u[min(k + 1, K - 1)])
+            for _ in range(n_apply):
+                ctx.apply_range(ua, Au, zb, ze)
+            stream.wait_event(ev_f[k])
+            ctx.sweep_range_to(ua, f_dev, ub, zb, ze, 1.0, 1e-12)
+            ev_s[k].record(stream)
+            out_stream.wait_event(ev_s[k])
+            with torch.cuda.stream(out_stream):
+                out_pin[zb * lay:ze * lay].copy_(ub[zb * lay:ze * lay], non_blocking=True)
+        stream.wait_stream(out_stream)
+
     def time_e2e(fn):
         ms = 0.0
         fn()   # warm-up (events, pinned staging)
@@ -570,11 +604,17 @@ def run_ours(args):
     e2e_ms = e2e_serial_ms
     e2e_mode = "serial: whole-vector H2D, step, D2H (f under the applies)"
     if chunks and len(chunks) > 1:
-        e2e_ms = time_e2e(e2e_streamed)
+        if args.e2e_schedule == "interleaved" and n_sweep == 1:
+            e2e_ms = time_e2e(e2e_interleaved)
+            e2e_mode = (f"streamed, chunk-interleaved: {len(chunks)} z-layer chunks, each uploaded (u, f on "
+                        f"{args.e2e_streams} copy stream(s)), applied 10x and swept (dg_apply_range / "
+                        "dg_block_jacobi_sweep_range) and read back under the transfers of the others")
+        else:
+            e2e_ms = time_e2e(e2e_streamed)
+            e2e_mode = (f"streamed: {len(chunks)} z-layer chunks (dg_apply_range / dg_block_jacobi_sweep_range), "
+                        "H2D and D2H of one chunk under the compute of another")
         if not torch.equal(out_pin, serial_out):
             raise SystemExit("streamed e2e step differs from the serial one")
-        e2e_mode = (f"streamed: {len(chunks)} z-layer chunks (dg_apply_range / dg_block_jacobi_sweep_range), "
-                    "H2D and D2H of one chunk under the compute of another")
 
     # ---- the volume kernel alone (a^v terms, Stages 1-3; north_star's >= 50 % target at p >= 3)
     vol_calls = 20
@@ -693,6 +733,9 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=16, help="z-layer chunks of the streamed e2e step")
     ap.add_argument("--e2e-taper", type=int, default=1, help="granule-sized first two and last chunks")
+    ap.add_argument("--e2e-schedule", default="phases", choices=["phases", "interleaved"],
+                    help="streamed e2e: all applies then the sweep (phases) or both per chunk (interleaved)")
+    ap.add_argument("--e2e-streams", type=int, default=1, choices=[1, 2], help="upload streams (interleaved)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         relaunch_under_torchrun(args.gpus)
