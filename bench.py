@@ -708,6 +708,11 @@ def run_ours(args):
                 "serial_value": dof * (n_apply + n_sweep) * e2e_steps / (e2e_serial_ms * 1e-3)},
         "gpu_launches": launches,
         "clocks": clk,
+        # context, not the target: the paper's only fraction-of-peak statement
+        "paper_context": {"frac_fp64_peak": 0.6, "peak_gflops": 486.4,
+                          "hardware": "Xeon E5-2698v3, 16-core Haswell, 243.2e9 FMA/s (P:93-96)",
+                          "statement": "matrix-free operator application 'close to 60 %' of peak "
+                                       "'in some cases' (P:888-890); no DoF/s figure published"},
     }
     if world == 1 and not args.no_extras:
         try:
