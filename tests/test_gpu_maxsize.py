@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 from oracle.tier_b import TierB                                    # noqa: E402
 from synth import Problem, normal, uniform_pm1                      # noqa: E402
 import paper_1805_11930_b200 as dg                                  # noqa: E402
+from stencil_sub import gather, sub_problem                        # noqa: E402
 
 APPLY_TOL = 1e-12
 SWEEP_TOL = 1e-9
@@ -35,37 +36,6 @@ def tiled(seed, n_dof):
     for s in range(0, n_dof, BLOCK):
         m = min(BLOCK, n_dof - s)
         out[s:s + m] = blk[:m]
-    return out
-
-
-def sub_problem(P, K, cell):
-    """The 3 x 3 x 3 problem around `cell` and the map sub-cell -> global cell (or -1)."""
-    dims = (P.nx, P.ny, P.nz)
-    co = (cell % P.nx, (cell // P.nx) % P.ny, cell // (P.nx * P.ny))
-    # position of T in the sub-mesh: on the boundary side it touches, else the centre
-    so = [0 if co[d] == 0 else (2 if co[d] == dims[d] - 1 else 1) for d in range(3)]
-    h = P.h
-    Ks = np.ones(27)
-    gmap = -np.ones(27, dtype=np.int64)
-    for sz in range(3):
-        for sy in range(3):
-            for sx in range(3):
-                g = [co[0] + sx - so[0], co[1] + sy - so[1], co[2] + sz - so[2]]
-                if all(0 <= g[d] < dims[d] for d in range(3)):
-                    gc = g[0] + P.nx * (g[1] + P.ny * g[2])
-                    gmap[sx + 3 * (sy + 3 * sz)] = gc
-                    Ks[sx + 3 * (sy + 3 * sz)] = K[gc]
-    Ps = Problem(3, 3, 3, P.p, Lx=3 * h[0], Ly=3 * h[1], Lz=3 * h[2], alpha=P.alpha, K=Ks)
-    return Ps, gmap, so[0] + 3 * (so[1] + 3 * so[2])
-
-
-def gather(t, gmap, nd):
-    """The sub-mesh vector: the device vector's cells where they exist (T and its face
-    neighbours are the ones that matter), zero elsewhere."""
-    out = np.zeros(27 * nd)
-    for s, g in enumerate(gmap):
-        if g >= 0:
-            out[s * nd:(s + 1) * nd] = t[g * nd:(g + 1) * nd].cpu().numpy()
     return out
 
 

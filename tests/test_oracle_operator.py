@@ -307,3 +307,27 @@ def test_volume_apply_equals_per_cell_volume_blocks(p):
     u = np.random.default_rng(p).uniform(-1, 1, P.n_dof)
     ref = tb.apply_parts_cells(u, range(P.n_cells), 1).reshape(-1)
     assert rel(tb.volume_apply(u), ref) < 1e-14
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_stencil_sub_problem_reproduces_cells(p):
+    """Minimal stencil: (A u)_T and the block-Jacobi update of T on a 3 x 3 x 3 problem
+    holding T and its face neighbours (tests/stencil_sub.py, the reference of the maximum-size GPU
+    parity) equal the full-mesh oracle, on every cell of a mesh with interior, face, edge and
+    corner cells."""
+    from stencil_sub import gather, sub_problem
+    nx, ny, nz = 5, 4, 3
+    rng = np.random.default_rng(40 + p)
+    K = np.exp(rng.normal(size=nx * ny * nz))
+    P = Problem(nx, ny, nz, p, Lx=1.0, Ly=0.7, Lz=1.3, K=K)
+    nd = P.nd
+    u, f = rng.uniform(-1, 1, P.n_dof), rng.uniform(-1, 1, P.n_dof)
+    tb = TierB(P)
+    A = tb.apply(u).reshape(-1, nd)
+    S = tb.sweep(u, f, 0.9).reshape(-1, nd)
+    for cell in range(P.n_cells):
+        Ps, gmap, sc = sub_problem(P, K, cell)
+        t = TierB(Ps)
+        us, fs = gather(u, gmap, nd), gather(f, gmap, nd)
+        assert rel(t.apply_cells(us, [sc])[0], A[cell]) < 1e-13
+        assert rel(t.sweep_cells(us, fs, 0.9, [sc])[0], S[cell]) < 1e-12
