@@ -175,6 +175,14 @@ dg_status dg_set_kernel_variant(dg_ctx* ctx, uint32_t variant);
 /* Synchronises the last sweep/solve stream and reduces its per-cell iteration counts. */
 dg_status dg_get_stats(dg_ctx* ctx, dg_stats* st);
 
+/* SURVEY 8(b)'s one-call forms: dg_block_jacobi_sweep / dg_local_block_solve followed by
+ * dg_get_stats (they synchronise cuda_stream; the asynchronous calls above do not). st: host,
+ * written on DG_OK; NULL = no statistics (then identical to the plain call). */
+dg_status dg_block_jacobi_sweep_stats(dg_ctx* ctx, double* u, const double* f, double omega,
+                                      double local_tol, dg_stats* st, void* cuda_stream);
+dg_status dg_local_block_solve_stats(dg_ctx* ctx, const double* d, double* du, double local_tol,
+                                     dg_stats* st, void* cuda_stream);
+
 /* Component hooks for parity tests:
  *  dg_apply_parts: mask 1 = volume terms a^v, 2 = interior-face terms a^if,
  *                  4 = boundary-face terms a^bf (sums of the selected parts of A u);

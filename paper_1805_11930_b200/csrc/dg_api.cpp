@@ -775,6 +775,18 @@ dg_status dg_get_stats(dg_ctx* c, dg_stats* st) {
   return DG_OK;
 }
 
+dg_status dg_block_jacobi_sweep_stats(dg_ctx* c, double* u, const double* f, double omega, double tol,
+                                      dg_stats* st, void* stream) {
+  const dg_status s = dg_block_jacobi_sweep(c, u, f, omega, tol, stream);
+  return (s != DG_OK || !st) ? s : dg_get_stats(c, st);
+}
+
+dg_status dg_local_block_solve_stats(dg_ctx* c, const double* d, double* du, double tol, dg_stats* st,
+                                     void* stream) {
+  const dg_status s = dg_local_block_solve(c, d, du, tol, stream);
+  return (s != DG_OK || !st) ? s : dg_get_stats(c, st);
+}
+
 int32_t dg_last_launch_count(const dg_ctx* c) { return c ? c->launches : 0; }
 
 dg_status dg_slab_range(int32_t nz, int32_t rank, int32_t nranks, int32_t* zb, int32_t* ze) {

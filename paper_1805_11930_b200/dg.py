@@ -30,7 +30,8 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_local_range", "dg_apply", "dg_block_ja
            "dg_microbench_dfma", "dg_slab_range", "dg_halo_plan", "dg_coarse_matrix",
            "dg_hybrid_vcycle", "dg_hybrid_solve", "dg_block_sor_sweep", "dg_pmf_setup",
            "dg_pmf_sweep", "dg_pmf_block", "dg_block_jacobi_sweep_to", "dg_set_kernel_variant",
-           "dg_range_granule", "dg_apply_range", "dg_block_jacobi_sweep_range"]
+           "dg_range_granule", "dg_apply_range", "dg_block_jacobi_sweep_range",
+           "dg_block_jacobi_sweep_stats", "dg_local_block_solve_stats"]
 
 
 class DGError(RuntimeError):
@@ -113,6 +114,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
         "dg_apply_range": ([P, P, P, i32, i32, P], i32),
         "dg_block_jacobi_sweep_range": ([P, P, P, P, dbl, dbl, i32, i32, P], i32),
         "dg_get_stats": ([P, ctypes.POINTER(dg_stats)], i32),
+        "dg_block_jacobi_sweep_stats": ([P, P, P, dbl, dbl, ctypes.POINTER(dg_stats), P], i32),
+        "dg_local_block_solve_stats": ([P, P, P, dbl, ctypes.POINTER(dg_stats), P], i32),
         "dg_ghost_layers": ([P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(i64)], i32),
         "dg_fill_ghosts": ([P, P, P, P], i32),
         "dg_tables": ([i32, ctypes.POINTER(dbl)], i32),
@@ -300,6 +303,19 @@ class DGContext:
         _check(self.lib.dg_block_jacobi_sweep(self.h, self._v(u), self._v(f), float(omega), float(tol),
                                               _stream(stream)))
         return u
+
+    def sweep_stats(self, u, f, omega: float = 1.0, tol: float = 1e-12, stream=None) -> dict:
+        """dg_block_jacobi_sweep_stats: the in-place sweep and its statistics in one (synchronising) call."""
+        st = dg_stats()
+        _check(self.lib.dg_block_jacobi_sweep_stats(self.h, self._v(u), self._v(f), float(omega), float(tol),
+                                                    ctypes.byref(st), _stream(stream)))
+        return st.as_dict()
+
+    def local_block_solve_stats(self, d, du, tol: float, stream=None) -> dict:
+        st = dg_stats()
+        _check(self.lib.dg_local_block_solve_stats(self.h, self._v(d), self._v(du), float(tol),
+                                                   ctypes.byref(st), _stream(stream)))
+        return st.as_dict()
 
     def sweep_to(self, u, f, u_new, omega: float = 1.0, tol: float = 1e-12, stream=None):
         """Out-of-place sweep: u_new = u + omega D^-1 (f - A u) (u_new must not alias u or f)."""

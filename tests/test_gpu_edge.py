@@ -113,3 +113,23 @@ def test_isotropic_scalar_k_input():
     Au, us, _ = run(P, u, f)
     assert rel(Au, tb.apply(u)) <= 1e-12
     assert rel(us, tb.sweep(u, f, 1.0)) <= 1e-9
+
+
+def test_one_call_stats_forms_equal_the_two_call_forms():
+    """dg_block_jacobi_sweep_stats / dg_local_block_solve_stats (SURVEY 8(b)'s signatures) give
+    the bits of the plain calls and the statistics dg_get_stats reports after them."""
+    P = random_problem(4, 3, 3, 3, seed=61, spread=1.0)
+    u, f = uniform_pm1(62, 0, P.n_dof), uniform_pm1(63, 0, P.n_dof)
+    with dg.DGContext(P) as ctx:
+        a, b = cuda(u), cuda(u)
+        ft = cuda(f)
+        ctx.sweep(a, ft, 0.9, 1e-12)
+        st_two = ctx.stats()
+        st_one = ctx.sweep_stats(b, ft, 0.9, 1e-12)
+        assert torch.equal(a, b) and st_one == st_two and st_one["n_cells"] == P.n_cells
+        assert st_one["it_min"] >= 1 and st_one["n_nonconverged"] == 0
+        da, db = torch.empty_like(a), torch.empty_like(a)
+        ctx.local_block_solve(ft, da, 1e-12)
+        st_two = ctx.stats()
+        st_one = ctx.local_block_solve_stats(ft, db, 1e-12)
+        assert torch.equal(da, db) and st_one == st_two
