@@ -63,9 +63,10 @@ enum { DG_HALO_NCCL = 0, DG_HALO_EXTERNAL = 1 };
  * degree; DG_VARIANT_NO_TMEM: shared-memory p = 3 BiCGStab (default: Krylov vectors in tensor
  * memory); DG_VARIANT_LINE_CG_CTA: the other line-solver kernel at p = 4..6 (defaults: CG one
  * warp per cell at p = 4, CTA-wide at p = 5, 6; BiCGStab one warp per cell at p = 4, 6, CTA-wide
- * at p = 5; the flag swaps them). */
+ * at p = 5; the flag swaps them); DG_VARIANT_APPLY_NOFOLD: dg_apply at p = 4 through the warp-mode
+ * nodal kernel with face arrays (default: the mass-folded kernel k_apply_fold). */
 enum { DG_VARIANT_VOLUME_PREFETCH = 1, DG_VARIANT_LINE = 2, DG_VARIANT_NO_TMEM = 4,
-       DG_VARIANT_LINE_CG_CTA = 8 };
+       DG_VARIANT_LINE_CG_CTA = 8, DG_VARIANT_APPLY_NOFOLD = 16 };
 
 typedef struct {
   int32_t nx, ny, nz;        /* GLOBAL cells per axis (uniform cells, D2 of SURVEY §2.1) */

@@ -401,6 +401,7 @@ dg_status dg_create(const dg_desc* desc, dg_ctx** out) {
   }
   if (getenv_flag("DG_NO_TMEM")) kp.variant |= dg::VAR_NO_TMEM;
   if (getenv_flag("DG_LINE_CG_CTA")) kp.variant |= dg::VAR_LINE_CG_CTA;
+  if (getenv_flag("DG_APPLY_NOFOLD")) kp.variant |= dg::VAR_APPLY_NOFOLD;
   if (const int C = dg::solver_group_cells(desc->p); C > 0 && !getenv_flag("DG_NO_GPERM")) {
     // Longest-processing-time-first order for the local-solver CTAs: cells with Dirichlet faces
     // take more local iterations (the penalty stiffens their block), so the groups holding them
@@ -521,7 +522,7 @@ dg_status dg_set_local_solver(dg_ctx* c, int32_t method, int32_t max_it, int32_t
 
 dg_status dg_set_kernel_variant(dg_ctx* c, uint32_t variant) {
   if (!c) return fail(DG_ERR_INVALID, "ctx is NULL");
-  if (variant & ~15u) return fail(DG_ERR_INVALID, "unknown kernel variant bits");
+  if (variant & ~31u) return fail(DG_ERR_INVALID, "unknown kernel variant bits");
   c->kp.variant = variant;
   return DG_OK;
 }

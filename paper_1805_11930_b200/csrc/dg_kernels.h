@@ -9,7 +9,8 @@ namespace dg {
 
 enum FaceKind : int32_t { FK_DIRICHLET = 0, FK_NEUMANN = 1, FK_GHOST = 2 };
 // kernel variant bits (= DG_VARIANT_* of dg.h)
-enum : uint32_t { VAR_VOLUME_PREFETCH = 1u, VAR_LINE = 2u, VAR_NO_TMEM = 4u, VAR_LINE_CG_CTA = 8u };
+enum : uint32_t { VAR_VOLUME_PREFETCH = 1u, VAR_LINE = 2u, VAR_NO_TMEM = 4u, VAR_LINE_CG_CTA = 8u,
+                  VAR_APPLY_NOFOLD = 16u };
 
 // Everything a kernel needs about the local slab (passed by value).
 struct KParams {

@@ -62,6 +62,14 @@ struct DevTab {
   double SGW[64];                     // SG[r][s] / w_r: the plane kernels' unweighted residual form
 };
 __constant__ DevTab c_tab[kMaxN + 1];
+// mass-folded forms (k_apply_fold): Mhat^-1 Shat, Mhat^-1 Chat and Mhat^-1 applied to the face
+// injection profiles e0, e1, d0, d1; one instance per translation unit (= per degree: the
+// constant bank has no room for one per entry of c_tab)
+struct FoldTab {
+  double MiS[64], MiC[64];
+  double mie0[8], mie1[8], mid0[8], mid1[8];
+};
+__constant__ FoldTab c_fold;
 
 // Padded tensor layout per n: element (i,j,k) of cell slot cs at cs*CS + k*ZS + j*YS + i.
 // Chosen offline to minimise shared-memory bank conflicts of x/y/z line passes.
@@ -1574,6 +1582,230 @@ template <int N, int CC> constexpr size_t apply_warps_smem() {
   return sizeof(double) * (2 * (size_t)Geo<N, CC>::TENSOR + (apply_warps_shfl<N>() ? 0 : 12 * (size_t)CC * N * apply_warps_rs<N>()));
 }
 
+// Mass-folded nodal A u, one warp per cell (n^2 <= 32 lanes, one line each). With exact 1D masses
+// every term of (A u)_T carries Mhat in the directions it does not act on, so
+//   (A u)_T = (Mhat (x) Mhat (x) Mhat) w,
+//   w = sum_a [ vc_a Mhat^-1 Shat - vb_a Mhat^-1 Chat ]_a u + vc_3 u
+//       + sum_a |F_a| [ (Mhat^-1 e0) S_lo + (Mhat^-1 d0) T_lo + (Mhat^-1 e1) S_hi + (Mhat^-1 d1) T_hi ]_a
+// with S, T the value-test and derivative-test face sums (self and neighbour, the fc coefficients
+// of group_setup) at the face node, which the lane that owns the normal line through
+// that node forms in registers: no face arrays, no tangential-mass contractions of face data, no
+// per-cell factor matrices (the 1D tables are constant-bank operands). Six line products
+// (three derivative, three mass) instead of seven plus twelve face-array contractions.
+// Stages: own x-line -> shared; z-lines: w_z; y-lines: += w_y; x-lines: += w_x, Mhat_x; y-lines:
+// Mhat_y; z-lines: Mhat_z, stored to global memory as z-lines (n^2 consecutive doubles per k).
+#ifndef DG_APPLY_FOLD5
+#define DG_APPLY_FOLD5 4   // n = 5: cells (= warps) per CTA of the mass-folded apply (0: off)
+#endif
+template <int N, bool GEN>
+__device__ __forceinline__ void fold_line(const KParams& kp, int a, const double* vc, const double* vb,
+                                          const double* lo, const double* hi, const double (&u)[N],
+                                          double sl, double tl, double sh, double th, double (&w)[N]) {
+  double g0 = 0.0, g1 = 0.0;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    g0 = fma(c_tab[N].d0[e], u[e], g0);
+    g1 = fma(c_tab[N].d1[e], u[e], g1);
+  }
+  const double ih = kp.ih[a], fa = kp.fa[a];
+  const double Sl = fa * (sl + fma(lo[0], u[0], (lo[1] * g0) * ih));
+  const double Tl = fa * fma(lo[4], u[0], tl);
+  const double Sh = fa * (sh + fma(hi[0], u[N - 1], (hi[1] * g1) * ih));
+  const double Th = fa * fma(hi[4], u[N - 1], th);
+  const double vk = vc[a], vbb = GEN ? vb[a] : 0.0;
+#pragma unroll
+  for (int e = 0; e < N; ++e) {
+    double s = 0.0, c = 0.0;
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+      s = fma(c_fold.MiS[e * N + r], u[r], s);
+      if constexpr (GEN) c = fma(c_fold.MiC[e * N + r], u[r], c);
+    }
+    double acc = fma(vk, s, w[e]);
+    if constexpr (GEN) acc = fma(-vbb, c, acc);
+    acc = fma(c_fold.mie0[e], Sl, acc);
+    acc = fma(c_fold.mid0[e], Tl, acc);
+    acc = fma(c_fold.mie1[e], Sh, acc);
+    acc = fma(c_fold.mid1[e], Th, acc);
+    w[e] = acc;
+  }
+}
+template <int N, bool GEN, int CC>
+__global__ void __launch_bounds__(CC * 32)
+k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
+  using G = Geo<N, CC>;
+  using GR = Group<N, CC>;
+  using GH = GroupHead<N, CC>;
+  static_assert(offsetof(GR, td1) == offsetof(GH, td1), "GroupHead is a prefix of Group");
+  static_assert(G::N2 <= 32 && G::N2 > 16, "one warp per cell");
+  __shared__ GH gh;
+  Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
+  extern __shared__ double sm[];
+  double* SU = sm;
+  double* SA = SU + G::TENSOR;
+  constexpr int N2 = G::N2;
+  const int cell0 = block_group(kp, false) * CC;
+  const int nvalid = min(CC, kp.ncells - cell0);
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int t = threadIdx.x, cs = t >> 5, l = t & 31, a = l % N, bb = l / N;
+  const bool act = l < N2 && cs < nvalid;
+  double own[N];
+  if (act) {
+    ld<N, 1>(u + (size_t)(cell0 + cs) * G::N3 + bb * N2 + a * N, own);
+  } else {
+#pragma unroll
+    for (int e = 0; e < N; ++e) own[e] = 0.0;
+  }
+  group_setup<N, CC * 32>(kp, g, cell0, u);  // ends with __syncthreads
+  const int base = cs * G::CS;
+  // ---- stage 0: the neighbours' parts of the face sums at this lane's face nodes (as apply_nodal)
+  double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0}, sz[4] = {0.0, 0.0, 0.0, 0.0};
+  if (act) {
+    st<N, 1>(SU + base + bb * G::ZS + a * G::YS, own);
+    {
+      const double* nlo = g.nb[cs][0];
+      const double* nhi = g.nb[cs][1];
+      const double* clo = g.fc[cs][0];
+      const double* chi = g.fc[cs][1];
+      const int goff = bb * N2 + a * N;
+      if (nlo) {
+        double w[N];
+        ldg_line<N>(nlo + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+        sx[0] = fma(clo[2], w[N - 1], (clo[3] * gn) * kp.ih[0]);
+        sx[1] = clo[5] * w[N - 1];
+      }
+      if (nhi) {
+        double w[N];
+        ldg_line<N>(nhi + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+        sx[2] = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[0]);
+        sx[3] = chi[5] * w[0];
+      }
+    }
+    {
+      const double* nlo = g.nb[cs][2];
+      const double* nhi = g.nb[cs][3];
+      const double* clo = g.fc[cs][2];
+      const double* chi = g.fc[cs][3];
+      const int goff = bb * N2 + a;
+      if (nlo) {
+        double w[N];
+        ld<N, N>(nlo + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+        sy[0] = fma(clo[2], w[N - 1], (clo[3] * gn) * kp.ih[1]);
+        sy[1] = clo[5] * w[N - 1];
+      }
+      if (nhi) {
+        double w[N];
+        ld<N, N>(nhi + goff, w);
+        double gn = 0.0;
+#pragma unroll
+        for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+        sy[2] = fma(chi[2], w[0], (chi[3] * gn) * kp.ih[1]);
+        sy[3] = chi[5] * w[0];
+      }
+    }
+    {
+      const double* nlo = g.nb[cs][4];
+      const double* nhi = g.nb[cs][5];
+      const double* clo = g.fc[cs][4];
+      const double* chi = g.fc[cs][5];
+      const int goff = bb * N + a;
+      if (nlo) {
+        double av, gn = 0.0;
+        if (ghost_trace(kp, g.cell[cs], 0)) {
+          av = nlo[goff];
+          gn = nlo[N2 + goff];
+        } else {
+          double w[N];
+          ld<N, N2>(nlo + goff, w);
+#pragma unroll
+          for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d1[e], w[e], gn);
+          av = w[N - 1];
+        }
+        sz[0] = fma(clo[2], av, (clo[3] * gn) * kp.ih[2]);
+        sz[1] = clo[5] * av;
+      }
+      if (nhi) {
+        double av, gn = 0.0;
+        if (ghost_trace(kp, g.cell[cs], 1)) {
+          av = nhi[goff];
+          gn = nhi[N2 + goff];
+        } else {
+          double w[N];
+          ld<N, N2>(nhi + goff, w);
+#pragma unroll
+          for (int e = 0; e < N; ++e) gn = fma(c_tab[N].d0[e], w[e], gn);
+          av = w[0];
+        }
+        sz[2] = fma(chi[2], av, (chi[3] * gn) * kp.ih[2]);
+        sz[3] = chi[5] * av;
+      }
+    }
+  }
+  __syncwarp();
+  const double* vc = g.vc[cs];
+  const double* vb = g.vb[cs];
+  // ---- z-lines (i = a, j = bb): w = w_z (+ reaction)
+  if (act) {
+    const int off = base + bb * G::YS + a;
+    double v[N], w[N];
+    ld<N, G::ZS>(SU + off, v);
+#pragma unroll
+    for (int e = 0; e < N; ++e) w[e] = GEN ? vc[3] * v[e] : 0.0;
+    fold_line<N, GEN>(kp, 2, vc, vb, g.fc[cs][4], g.fc[cs][5], v, sz[0], sz[1], sz[2], sz[3], w);
+    st<N, G::ZS>(SA + off, w);
+  }
+  __syncwarp();
+  // ---- y-lines (i = a, k = bb): w += w_y
+  if (act) {
+    const int off = base + bb * G::ZS + a;
+    double v[N], w[N];
+    ld<N, G::YS>(SU + off, v);
+    ld<N, G::YS>(SA + off, w);
+    fold_line<N, GEN>(kp, 1, vc, vb, g.fc[cs][2], g.fc[cs][3], v, sy[0], sy[1], sy[2], sy[3], w);
+    st<N, G::YS>(SA + off, w);
+  }
+  __syncwarp();
+  // ---- x-lines (j = a, k = bb): w += w_x, then Mhat_x
+  if (act) {
+    const int off = base + bb * G::ZS + a * G::YS;
+    double w[N], c[N];
+    ld<N, 1>(SA + off, w);
+    fold_line<N, GEN>(kp, 0, vc, vb, g.fc[cs][0], g.fc[cs][1], own, sx[0], sx[1], sx[2], sx[3], w);
+    mv<N, 2>(w, c);
+    st<N, 1>(SA + off, c);
+  }
+  __syncwarp();
+  // ---- y-lines: Mhat_y
+  if (act) {
+    const int off = base + bb * G::ZS + a;
+    double c[N], d[N];
+    ld<N, G::YS>(SA + off, c);
+    mv<N, 2>(c, d);
+    st<N, G::YS>(SA + off, d);
+  }
+  __syncwarp();
+  // ---- z-lines: Mhat_z, to global memory (lane (i, j): n^2 consecutive doubles per k)
+  if (act) {
+    double d[N], o[N];
+    ld<N, G::ZS>(SA + base + bb * G::YS + a, d);
+    mv<N, 2>(d, o);
+    double* op = out + (size_t)(cell0 + cs) * G::N3 + bb * N + a;
+#pragma unroll
+    for (int k = 0; k < N; ++k) op[k * N2] = o[k];
+  }
+}
+template <int N, int CC> constexpr size_t apply_fold_smem() { return sizeof(double) * 2 * (size_t)Geo<N, CC>::TENSOR; }
+
 // D_T u (dg_block_diag_apply: the volume and self-face terms of each cell) with one
 // warp per cell in the nodal Kronecker-sum form of the local CG's operator (dt_nodal, WARP mode;
 // the factors K_a of nodal_face_ops): the own x-line from global memory straight into registers,
@@ -2965,6 +3197,29 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_APPLY_WARPS5
 #define DG_APPLY_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal apply (0: off; C3 1 cell per CTA 515 us, 2 / 4 / 8 warps 500 / 490 / 504 us)
 #endif
+  if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_FOLD5 > 0) {
+    if (kp.mask == 7u && with_nbr && !force_line(kp) && !(kp.variant & VAR_APPLY_NOFOLD)) {
+      constexpr int CC = DG_APPLY_FOLD5;
+      KParams ka = kp0;
+      const int grida = split_groups(ka, CC);
+      if (grida == 0) return cudaSuccess;
+      const size_t smem = apply_fold_smem<N, CC>();
+      auto ke = gen_terms(kp) ? k_apply_fold<N, true, CC> : k_apply_fold<N, false, CC>;
+      cudaError_t e = set_smem(ke, smem);
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grida);
+      cfg.blockDim = dim3(CC * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = DG_PDL;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, ke, ka, u, out, with_nbr);
+    }
+  }
   constexpr int WCELLS = N == 5 ? DG_APPLY_WARPS5 : (N == 4 ? DG_APPLY_WARPS4 : (N == 3 ? DG_APPLY_WARPS3 : 0));
   if constexpr ((N == 5 || N == 4 || N == 3) && DG_NODAL_APPLY && WCELLS > 0) {
     if (kp.mask == 7u && with_nbr && !force_line(kp) && (N == 5 || warp_apply<N>(kp, with_nbr))) {
@@ -3249,6 +3504,51 @@ template <int N> bool upload_n(const Tables1D& t, cudaError_t* err) {
       d.S[i * n + j] = sv;
       d.Cm[i * n + j] = cv;
     }
+  {
+    // Mhat^-1 [Shat | Chat | e0 | e1 | d0 | d1] by Gauss-Jordan with partial pivoting (long double)
+    const int m = 2 * n + 4;
+    FoldTab ft{};
+    long double a[8][8], b[8][20];
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) {
+        a[i][j] = t.M[i * n + j];
+        b[i][j] = d.S[i * n + j];
+        b[i][n + j] = d.Cm[i * n + j];
+      }
+      b[i][2 * n] = i == 0;
+      b[i][2 * n + 1] = i == n - 1;
+      b[i][2 * n + 2] = t.d0[i];
+      b[i][2 * n + 3] = t.d1[i];
+    }
+    for (int c = 0; c < n; ++c) {
+      int pv = c;
+      for (int r = c + 1; r < n; ++r)
+        if (fabsl(a[r][c]) > fabsl(a[pv][c])) pv = r;
+      for (int j = 0; j < n; ++j) { const long double x = a[c][j]; a[c][j] = a[pv][j]; a[pv][j] = x; }
+      for (int j = 0; j < m; ++j) { const long double x = b[c][j]; b[c][j] = b[pv][j]; b[pv][j] = x; }
+      const long double ip = 1.0L / a[c][c];
+      for (int j = 0; j < n; ++j) a[c][j] *= ip;
+      for (int j = 0; j < m; ++j) b[c][j] *= ip;
+      for (int r = 0; r < n; ++r) {
+        if (r == c) continue;
+        const long double f = a[r][c];
+        for (int j = 0; j < n; ++j) a[r][j] -= f * a[c][j];
+        for (int j = 0; j < m; ++j) b[r][j] -= f * b[c][j];
+      }
+    }
+    for (int i = 0; i < n; ++i) {
+      for (int j = 0; j < n; ++j) {
+        ft.MiS[i * n + j] = (double)b[i][j];
+        ft.MiC[i * n + j] = (double)b[i][n + j];
+      }
+      ft.mie0[i] = (double)b[i][2 * n];
+      ft.mie1[i] = (double)b[i][2 * n + 1];
+      ft.mid0[i] = (double)b[i][2 * n + 2];
+      ft.mid1[i] = (double)b[i][2 * n + 3];
+    }
+    *err = cudaMemcpyToSymbol(c_fold, &ft, sizeof(FoldTab));
+    if (*err != cudaSuccess) return false;
+  }
   *err = cudaMemcpyToSymbol(c_tab, &d, sizeof(DevTab), sizeof(DevTab) * N);
   return *err == cudaSuccess;
 }
@@ -3267,6 +3567,7 @@ template <int N> constexpr int group_lcm_n() {
   l = lcm_c(l, DG_VOLUME_CELLS);
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
+  if constexpr (N == 5 && DG_APPLY_FOLD5 > 0) l = lcm_c(l, DG_APPLY_FOLD5);
   if constexpr (N == 5 && DG_DT_WARPS5 > 0) l = lcm_c(l, DG_DT_WARPS5);
   if constexpr (N == 4 && DG_APPLY_WARPS4 > 0) l = lcm_c(l, DG_APPLY_WARPS4);
   if constexpr (N == 3 && DG_APPLY_WARPS3 > 0) l = lcm_c(l, DG_APPLY_WARPS3);

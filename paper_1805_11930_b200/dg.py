@@ -20,6 +20,7 @@ DG_LOCAL_AUTO, DG_LOCAL_CG, DG_LOCAL_BICGSTAB, DG_LOCAL_BICGSTAB_THOMAS = 0, 1, 
 DG_LOCAL_GMRES, DG_LOCAL_GMRES_THOMAS = 4, 5
 DG_HALO_NCCL, DG_HALO_EXTERNAL = 0, 1
 DG_VARIANT_VOLUME_PREFETCH, DG_VARIANT_LINE, DG_VARIANT_NO_TMEM, DG_VARIANT_LINE_CG_CTA = 1, 2, 4, 8
+DG_VARIANT_APPLY_NOFOLD = 16
 MASK_VOLUME, MASK_INTERIOR_FACES, MASK_BOUNDARY_FACES = 1, 2, 4
 
 # every symbol include/dg.h declares (checked by the CPU tests)
