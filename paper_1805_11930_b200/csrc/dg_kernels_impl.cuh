@@ -1597,6 +1597,12 @@ template <int N, int CC> constexpr size_t apply_warps_smem() {
 #ifndef DG_APPLY_FOLD5
 #define DG_APPLY_FOLD5 4   // n = 5: cells (= warps) per CTA of the mass-folded apply (0: off)
 #endif
+#ifndef DG_APPLY_FOLD4
+#define DG_APPLY_FOLD4 8   // n = 4: cells (half-warps) per CTA (0: off)
+#endif
+#ifndef DG_APPLY_FOLD3
+#define DG_APPLY_FOLD3 8   // n = 3: cells (half-warps, 9 of 16 lanes busy) per CTA (0: off)
+#endif
 template <int N, bool GEN>
 __device__ __forceinline__ void fold_line(const KParams& kp, int a, const double* vc, const double* vb,
                                           const double* lo, const double* hi, const double (&u)[N],
@@ -1630,14 +1636,19 @@ __device__ __forceinline__ void fold_line(const KParams& kp, int a, const double
     w[e] = acc;
   }
 }
+#ifndef DG_APPLYF_MINB
+#define DG_APPLYF_MINB 0   // resident CTAs the mass-folded apply is compiled for (0: no bound)
+#endif
 template <int N, bool GEN, int CC>
-__global__ void __launch_bounds__(CC * 32)
+__global__ void __launch_bounds__(CC * warp_lanes<N>(), DG_APPLYF_MINB)
 k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
   using G = Geo<N, CC>;
   using GR = Group<N, CC>;
   using GH = GroupHead<N, CC>;
   static_assert(offsetof(GR, td1) == offsetof(GH, td1), "GroupHead is a prefix of Group");
-  static_assert(G::N2 <= 32 && G::N2 > 16, "one warp per cell");
+  static_assert(G::N2 <= 32, "one warp (n^2 <= 16: half-warp) per cell");
+  constexpr int WL = warp_lanes<N>();
+  static_assert((CC * WL) % 32 == 0, "whole warps");
   __shared__ GH gh;
   Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
   extern __shared__ double sm[];
@@ -1648,7 +1659,7 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
   const int nvalid = min(CC, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int t = threadIdx.x, cs = t >> 5, l = t & 31, a = l % N, bb = l / N;
+  const int t = threadIdx.x, cs = t / WL, l = t % WL, a = l % N, bb = l / N;
   const bool act = l < N2 && cs < nvalid;
   double own[N];
   if (act) {
@@ -1657,7 +1668,7 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
 #pragma unroll
     for (int e = 0; e < N; ++e) own[e] = 0.0;
   }
-  group_setup<N, CC * 32>(kp, g, cell0, u);  // ends with __syncthreads
+  group_setup<N, CC * WL>(kp, g, cell0, u);  // ends with __syncthreads
   const int base = cs * G::CS;
   // ---- stage 0: the neighbours' parts of the face sums at this lane's face nodes (as apply_nodal)
   double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0}, sz[4] = {0.0, 0.0, 0.0, 0.0};
@@ -3046,6 +3057,11 @@ template <int N> inline bool warp_apply(const KParams& kp, int with_nbr) {
   return W > 0 && DG_NODAL_APPLY && kp.mask == 7u && with_nbr && !gen_terms(kp);
 }
 inline bool warp_apply4(const KParams& kp, int with_nbr) { return warp_apply<4>(kp, with_nbr); }
+// the full A u goes through the mass-folded kernel k_apply_fold (n = 3, 4, 5; any term set)
+template <int N> inline bool fold_apply(const KParams& kp, int with_nbr) {
+  constexpr int F = N == 5 ? DG_APPLY_FOLD5 : (N == 4 ? DG_APPLY_FOLD4 : (N == 3 ? DG_APPLY_FOLD3 : 0));
+  return F > 0 && DG_NODAL_APPLY && kp.mask == 7u && with_nbr && !force_line(kp) && !(kp.variant & VAR_APPLY_NOFOLD);
+}
 template <int N>
 cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream_t s, int with_nbr) {
   KParams kp = kp0;   // split_groups fills the split range of this kernel's group size
@@ -3161,7 +3177,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
   }
   if constexpr (plane_apply<N>()) {
     // (n = 4 with DG_APPLY_WARPS4: A u by the warp-mode line kernel below)
-    if (!force_line(kp) && !((N == 4 || N == 3) && warp_apply<N>(kp, with_nbr))) {
+    if (!force_line(kp) && !((N == 4 || N == 3) && warp_apply<N>(kp, with_nbr)) && !fold_apply<N>(kp, with_nbr)) {
       using G = pk::Geo<N>;
       const int grid = split_groups(kp, G::C);
       if (grid == 0) return cudaSuccess;
@@ -3197,9 +3213,10 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
 #ifndef DG_APPLY_WARPS5
 #define DG_APPLY_WARPS5 4   // n = 5: cells (= warps) per CTA of the warp-mode nodal apply (0: off; C3 1 cell per CTA 515 us, 2 / 4 / 8 warps 500 / 490 / 504 us)
 #endif
-  if constexpr (N == 5 && DG_NODAL_APPLY && DG_APPLY_FOLD5 > 0) {
-    if (kp.mask == 7u && with_nbr && !force_line(kp) && !(kp.variant & VAR_APPLY_NOFOLD)) {
-      constexpr int CC = DG_APPLY_FOLD5;
+  constexpr int FCELLS = N == 5 ? DG_APPLY_FOLD5 : (N == 4 ? DG_APPLY_FOLD4 : (N == 3 ? DG_APPLY_FOLD3 : 0));
+  if constexpr (DG_NODAL_APPLY && FCELLS > 0) {
+    if (fold_apply<N>(kp, with_nbr)) {
+      constexpr int CC = FCELLS;
       KParams ka = kp0;
       const int grida = split_groups(ka, CC);
       if (grida == 0) return cudaSuccess;
@@ -3209,7 +3226,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grida);
-      cfg.blockDim = dim3(CC * 32);
+      cfg.blockDim = dim3(CC * warp_lanes<N>());
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
       cudaLaunchAttribute at[1];
@@ -3568,6 +3585,8 @@ template <int N> constexpr int group_lcm_n() {
   if constexpr (N == 5) l = lcm_c(l, DG_APPLY_CELLS5);
   if constexpr (N == 5 && DG_APPLY_WARPS5 > 0) l = lcm_c(l, DG_APPLY_WARPS5);
   if constexpr (N == 5 && DG_APPLY_FOLD5 > 0) l = lcm_c(l, DG_APPLY_FOLD5);
+  if constexpr (N == 4 && DG_APPLY_FOLD4 > 0) l = lcm_c(l, DG_APPLY_FOLD4);
+  if constexpr (N == 3 && DG_APPLY_FOLD3 > 0) l = lcm_c(l, DG_APPLY_FOLD3);
   if constexpr (N == 5 && DG_DT_WARPS5 > 0) l = lcm_c(l, DG_DT_WARPS5);
   if constexpr (N == 4 && DG_APPLY_WARPS4 > 0) l = lcm_c(l, DG_APPLY_WARPS4);
   if constexpr (N == 3 && DG_APPLY_WARPS3 > 0) l = lcm_c(l, DG_APPLY_WARPS3);

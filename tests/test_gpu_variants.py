@@ -171,3 +171,27 @@ def test_block_diag_warp_kernel_p4_every_dof(gen, mesh):
             ctx.block_diag_apply(cuda(u), out)
             got = host(out)
         assert rel(got, ref) <= APPLY_TOL, variant
+
+
+# ---- dg_apply at p = 4: the mass-folded kernel (default) and the face-array warp kernel ------
+@pytest.mark.parametrize("variant", [0, dg.DG_VARIANT_APPLY_NOFOLD], ids=["fold", "face-arrays"])
+@pytest.mark.parametrize("gen", [False, True], ids=["diffusion", "conv-reaction"])
+@pytest.mark.parametrize("mesh", [(5, 3, 3), (7, 5, 3)], ids=["45cells", "105cells"])
+def test_apply_p4_kernels_every_dof(variant, gen, mesh):
+    """Both p = 4 apply kernels on meshes with a ragged last CTA (4 cells per CTA), mixed
+    Dirichlet / Neumann faces, anisotropic cells and K; every DoF against the oracle, and the two
+    kernels against each other."""
+    nx, ny, nz = mesh
+    P = random_problem(nx, ny, nz, 4, seed=760 + nx, spread=1.5, bc=MIXED, L=(1.0, 0.6, 1.4),
+                       b=(0.7, -0.4, 0.3) if gen else (0.0, 0.0, 0.0), c=gen)
+    if gen:
+        P.b_cells = np.random.default_rng(nx).normal(size=(P.n_cells, 3))
+    u, _ = vec(P, 61)
+    ref = TierB(P).apply(u)
+    with dg.DGContext(P) as ctx:
+        ctx.set_kernel_variant(variant)
+        out = torch.empty(P.n_dof, dtype=torch.float64, device="cuda")
+        ctx.apply(cuda(u), out)
+        got = host(out)
+    assert rel(got, ref) <= 1e-12
+    assert np.abs(got - ref).max() <= 1e-11 * np.abs(ref).max()
