@@ -1601,7 +1601,10 @@ template <int N, int CC> constexpr size_t apply_warps_smem() {
 #define DG_APPLY_FOLD4 8   // n = 4: cells (half-warps) per CTA (0: off)
 #endif
 #ifndef DG_APPLY_FOLD3
-#define DG_APPLY_FOLD3 8   // n = 3: cells (half-warps, 9 of 16 lanes busy) per CTA (0: off)
+// n = 3: cells per CTA, three per warp (27 of 32 lanes busy; half-warp cells: C5 580 us; 12 cells
+// in 4 warps: 459 us, but a group size with a factor 3 triples the range granule). 20 cells in 7
+// warps divide the other kernels' groups. (0: off)
+#define DG_APPLY_FOLD3 20
 #endif
 template <int N, bool GEN>
 __device__ __forceinline__ void fold_line(const KParams& kp, int a, const double* vc, const double* vb,
@@ -1639,16 +1642,22 @@ __device__ __forceinline__ void fold_line(const KParams& kp, int a, const double
 #ifndef DG_APPLYF_MINB
 #define DG_APPLYF_MINB 0   // resident CTAs the mass-folded apply is compiled for (0: no bound)
 #endif
+// lanes per cell: a warp at n = 5 (25 busy), a half-warp at n = 4, 9 lanes at n = 3 (three cells per
+// warp, 27 of 32 lanes busy)
+template <int N> __host__ __device__ constexpr int fold_wl() { return N == 3 ? 9 : warp_lanes<N>(); }
+template <int N, int CC> __host__ __device__ constexpr int fold_threads() {
+  constexpr int CPW = 32 / fold_wl<N>();
+  return (CC + CPW - 1) / CPW * 32;   // the last warp may hold fewer cells
+}
 template <int N, bool GEN, int CC>
-__global__ void __launch_bounds__(CC * warp_lanes<N>(), DG_APPLYF_MINB)
+__global__ void __launch_bounds__(fold_threads<N, CC>(), DG_APPLYF_MINB)
 k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out, int) {
   using G = Geo<N, CC>;
   using GR = Group<N, CC>;
   using GH = GroupHead<N, CC>;
   static_assert(offsetof(GR, td1) == offsetof(GH, td1), "GroupHead is a prefix of Group");
   static_assert(G::N2 <= 32, "one warp (n^2 <= 16: half-warp) per cell");
-  constexpr int WL = warp_lanes<N>();
-  static_assert((CC * WL) % 32 == 0, "whole warps");
+  constexpr int WL = fold_wl<N>(), CPW = 32 / WL, NTH = fold_threads<N, CC>();
   __shared__ GH gh;
   Group<N, CC>& g = *reinterpret_cast<Group<N, CC>*>(&gh);
   extern __shared__ double sm[];
@@ -1659,8 +1668,8 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
   const int nvalid = min(CC, kp.ncells - cell0);
   asm volatile("griddepcontrol.launch_dependents;");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int t = threadIdx.x, cs = t / WL, l = t % WL, a = l % N, bb = l / N;
-  const bool act = l < N2 && cs < nvalid;
+  const int t = threadIdx.x, ln = t & 31, cs = (t >> 5) * CPW + ln / WL, l = ln % WL, a = l % N, bb = l / N;
+  const bool act = ln < CPW * WL && l < N2 && cs < nvalid;
   double own[N];
   if (act) {
     ld<N, 1>(u + (size_t)(cell0 + cs) * G::N3 + bb * N2 + a * N, own);
@@ -1668,7 +1677,7 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
 #pragma unroll
     for (int e = 0; e < N; ++e) own[e] = 0.0;
   }
-  group_setup<N, CC * WL>(kp, g, cell0, u);  // ends with __syncthreads
+  group_setup<N, NTH>(kp, g, cell0, u);  // ends with __syncthreads
   const int base = cs * G::CS;
   // ---- stage 0: the neighbours' parts of the face sums at this lane's face nodes (as apply_nodal)
   double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0}, sz[4] = {0.0, 0.0, 0.0, 0.0};
@@ -3226,7 +3235,7 @@ cudaError_t apply_n(const KParams& kp0, const double* u, double* out, cudaStream
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grida);
-      cfg.blockDim = dim3(CC * warp_lanes<N>());
+      cfg.blockDim = dim3(fold_threads<N, CC>());
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
       cudaLaunchAttribute at[1];
