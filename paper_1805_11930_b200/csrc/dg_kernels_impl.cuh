@@ -1639,6 +1639,11 @@ __device__ __forceinline__ void fold_line(const KParams& kp, int a, const double
     w[e] = acc;
   }
 }
+#ifndef DG_APPLYF_PRE
+// 1: the neighbours' traces loaded and reduced before the coefficient setup (12 scalars live across
+// its barrier). Measured slower (72 registers, 7 CTAs per SM): C3 367 -> 380 us, C4 193 -> 199, C5 490 -> 513
+#define DG_APPLYF_PRE 0
+#endif
 #ifndef DG_APPLYF_MINB
 #define DG_APPLYF_MINB 0   // resident CTAs the mass-folded apply is compiled for (0: no bound)
 #endif
@@ -1677,6 +1682,90 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
 #pragma unroll
     for (int e = 0; e < N; ++e) own[e] = 0.0;
   }
+#if DG_APPLYF_PRE
+  // the neighbours' face values and normal-derivative sums at this lane's face nodes, loaded and
+  // reduced before the coefficient setup (their latency runs under the setup's own loads; 12
+  // scalars live across the barrier). The neighbour of face f: the in-slab cell, the ghost trace
+  // record at a slab boundary (FK_GHOST), or none (as setup_cells decides).
+  double nav[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0}, ngn[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  unsigned nmask = 0;
+  if (act) {
+    const int cell = cell0 + cs, nxy = kp.nx * kp.ny;
+    const int cx = cell % kp.nx, cy = (cell / kp.nx) % kp.ny, cz = cell / nxy;
+    const double* uc = u + (size_t)cell * G::N3;
+    if (cx > 0) {
+      double w[N];
+      ldg_line<N>(uc - G::N3 + bb * N2 + a * N, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d1[e], w[e], gsum);
+      nav[0] = w[N - 1]; ngn[0] = gsum; nmask |= 1u;
+    }
+    if (cx < kp.nx - 1) {
+      double w[N];
+      ldg_line<N>(uc + G::N3 + bb * N2 + a * N, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d0[e], w[e], gsum);
+      nav[1] = w[0]; ngn[1] = gsum; nmask |= 2u;
+    }
+    if (cy > 0) {
+      double w[N];
+      ld<N, N>(uc - (size_t)kp.nx * G::N3 + bb * N2 + a, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d1[e], w[e], gsum);
+      nav[2] = w[N - 1]; ngn[2] = gsum; nmask |= 4u;
+    }
+    if (cy < kp.ny - 1) {
+      double w[N];
+      ld<N, N>(uc + (size_t)kp.nx * G::N3 + bb * N2 + a, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d0[e], w[e], gsum);
+      nav[3] = w[0]; ngn[3] = gsum; nmask |= 8u;
+    }
+    const int col = cx + kp.nx * cy;
+    if (cz > 0) {
+      double w[N];
+      ld<N, N2>(uc - (size_t)nxy * G::N3 + bb * N + a, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d1[e], w[e], gsum);
+      nav[4] = w[N - 1]; ngn[4] = gsum; nmask |= 16u;
+    } else if (kp.slab_face[4] == FK_GHOST) {
+      const double* rec = kp.ghost_lo + (size_t)col * 2 * N2;
+      nav[4] = rec[bb * N + a]; ngn[4] = rec[N2 + bb * N + a]; nmask |= 16u;
+    }
+    if (cz < kp.nzl - 1) {
+      double w[N];
+      ld<N, N2>(uc + (size_t)nxy * G::N3 + bb * N + a, w);
+      double gsum = 0.0;
+#pragma unroll
+      for (int e = 0; e < N; ++e) gsum = fma(c_tab[N].d0[e], w[e], gsum);
+      nav[5] = w[0]; ngn[5] = gsum; nmask |= 32u;
+    } else if (kp.slab_face[5] == FK_GHOST) {
+      const double* rec = kp.ghost_hi + (size_t)col * 2 * N2;
+      nav[5] = rec[bb * N + a]; ngn[5] = rec[N2 + bb * N + a]; nmask |= 32u;
+    }
+  }
+  group_setup<N, NTH>(kp, g, cell0, u);  // ends with __syncthreads
+  const int base = cs * G::CS;
+  double sx[4] = {0.0, 0.0, 0.0, 0.0}, sy[4] = {0.0, 0.0, 0.0, 0.0}, sz[4] = {0.0, 0.0, 0.0, 0.0};
+  if (act) {
+    st<N, 1>(SU + base + bb * G::ZS + a * G::YS, own);
+#pragma unroll
+    for (int f = 0; f < 6; ++f) {
+      if (!((nmask >> f) & 1u)) continue;
+      const double* cf = g.fc[cs][f];
+      const double sv = fma(cf[2], nav[f], (cf[3] * ngn[f]) * kp.ih[f >> 1]);
+      const double tv = cf[5] * nav[f];
+      double* dst = (f >> 1) == 0 ? sx : ((f >> 1) == 1 ? sy : sz);
+      dst[2 * (f & 1)] = sv;
+      dst[2 * (f & 1) + 1] = tv;
+    }
+  }
+#else
   group_setup<N, NTH>(kp, g, cell0, u);  // ends with __syncthreads
   const int base = cs * G::CS;
   // ---- stage 0: the neighbours' parts of the face sums at this lane's face nodes (as apply_nodal)
@@ -1771,6 +1860,7 @@ k_apply_fold(KParams kp, const double* __restrict__ u, double* __restrict__ out,
       }
     }
   }
+#endif
   __syncwarp();
   const double* vc = g.vc[cs];
   const double* vb = g.vb[cs];
